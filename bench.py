@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- Flash-LoRA-Attention batched decode on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload cfg2|cfg1|cfg4|cfg5]
+
+One "step" = one decode step of the whole agent batch: every agent's query attends to the shared
+trajectory through ALL layers of the model (32 for the Llama-3.1-8B shape), i.e. one pass of the hot
+path gqa_attention (reference: proj/include/lorakv/attention.hpp:332, called per agent per layer by
+engine.hpp:440-443).  Metric: agent-tokens per second (= agents / step time).
+
+  value     inputs (paged K/V/V_lr cache, B tables, q) resident in HBM, CUDA-event timed
+  e2e       the same step through the C ABI with HOST buffers: q pinned host -> device, kernels,
+            output device -> host, inside the timed region (wall clock, synchronised both sides)
+  roofline  dominant kernel's algorithmic bytes / its CUDA-event duration vs MEASURED_PEAKS.json
+  cpu_baseline  the reference CPU path (oracle/_ref when built, else the oracle port) on the host
+            cores, bounded sample (rank 0, N = 1 only)
+
+N > 1 (torchrun, one rank per GPU): KV heads are sharded across ranks (north star: no communication
+inside attention); the only collective is the end-of-step all-gather of the output slab (NCCL).
+The total work is fixed, so scaling is "strong".
+
+--impl reference times the reference's own CPU implementation of the path on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (description, n_layers, n_q, n_kv, d_head, rank, agents, L, d_model)
+    "cfg1": ("tiny single-layer: 4q/2kv heads, d=64, r=8, 2 agents, 512-token context, decode", 1, 4, 2, 64, 8, 2, 512, 256),
+    "cfg2": ("Llama-3.1-8B attention shape (32q/8kv, d=128), r=16, 3 agents, 32K shared trajectory, batched decode", 32, 32, 8, 128, 16, 3, 32768, 4096),
+    "cfg4": ("Mistral-7B shape (32q/8kv, d=128), r=64, 8 agents, 64K shared trajectory, decode", 32, 32, 8, 128, 64, 8, 65536, 4096),
+    "cfg5": ("long-context stress: 128K shared context, 16 agents, r=32, 32-layer sweep", 32, 32, 8, 128, 32, 16, 131072, 4096),
+}
+
+
+def algorithmic_bytes(n_layers, n_q, n_kv_local, n_kv, d, r, A, L, e):
+    """per layer 2*L*n_kv'*d*e [K+V] + L*r*e [V_lr] + 2*A*g*n_kv'*d*4 [q,out fp32] + A*r*n_kv'*d*4 [B]."""
+    g = n_q // n_kv
+    per_layer = 2 * L * n_kv_local * d * e + L * r * e + 2 * A * g * n_kv_local * d * 4 + A * r * n_kv_local * d * 4
+    return n_layers * per_layer
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.path = device, None, None
+
+    def start(self):
+        try:
+            f = tempfile.NamedTemporaryFile("w", suffix=".csv", delete=False)
+            self.path = f.name
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "100"], stdout=f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if not self.proc:
+            return out
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.path):
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 9:
+                    continue
+                try:
+                    sm.append(float(p[1])); mx.append(float(p[2]))
+                except ValueError:
+                    continue
+                for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), p[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_time(chk, q_list, k, v, v_lr, b_list, lr_scale, L, n_q, n_kv, threads):
+    """One layer x all agents through the reference CPU path; returns seconds."""
+    t0 = time.perf_counter()
+    outs = []
+    for a in range(len(q_list)):
+        outs.append(chk.gqa_attention(q_list[a], k, v, v_lr, b_list[a], lr_scale, L - 1, n_q, n_kv, threads=threads))
+    return time.perf_counter() - t0, outs
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference's own CPU implementation of the path on the host cores."""
+    from oracle import checker
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    desc, n_layers, n_q, n_kv, d, r, A, L, d_model = wl
+    chk = checker.best()
+    threads = host_threads()
+    rng = np.random.default_rng(0)
+    sc = float(1.0 / np.sqrt(d))
+    k = (rng.standard_normal((L, n_kv * d), dtype=np.float32) * sc)
+    v = rng.standard_normal((L, n_kv * d), dtype=np.float32)
+    v_lr = rng.standard_normal((L, r), dtype=np.float32)
+    q = [(rng.standard_normal((1, n_q * d), dtype=np.float32) * sc) for _ in range(A)]
+    b = [(rng.standard_normal((r, n_kv * d), dtype=np.float32) * float(0.02 / np.sqrt(max(r, 1)))) for _ in range(A)]
+    k, v, v_lr = (np.ascontiguousarray(x, dtype=np.float32) for x in (k, v, v_lr))
+    q = [np.ascontiguousarray(x, dtype=np.float32) for x in q]
+    b = [np.ascontiguousarray(x, dtype=np.float32) for x in b]
+    lr_scale = 16.0 / r if r else 1.0
+    for _ in range(args.warmup):
+        cpu_reference_time(chk, q, k, v, v_lr, b, lr_scale, L, n_q, n_kv, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_reference_time(chk, q, k, v, v_lr, b, lr_scale, L, n_q, n_kv, threads)
+    per_layer = (time.perf_counter() - t0) / args.steps
+    step_s = per_layer * n_layers
+    value = A / step_s
+    sample = f"each step times 1 of {n_layers} layers x {A} agents (gqa_attention<float>, {threads} threads over q heads) and scales by {n_layers}"
+    line = {
+        "impl": "reference", "metric": "flash_lora_attn_decode_agent_tokens_per_s", "value": value, "unit": "tok/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "description": desc, "n_layers": n_layers, "agents": A, "context": L, "rank": r},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": threads, "kind": chk.kind, "sample": sample},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--per-layer-launch", action="store_true", help="one launch per layer instead of one per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--policy", type=int, default=0, help="0 auto (tcgen05 where supported), 1 CUDA-core kernels")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2602_01053_b200 as pkg
+    from paper_2602_01053_b200 import abi
+
+    desc, n_layers, n_q, n_kv, d, r, A, L, d_model = wl
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if n_kv % world != 0:
+        raise SystemExit(f"n_kv_heads {n_kv} not divisible by {world} ranks")
+    n_kv_local = n_kv // world
+    kv_begin = rank * n_kv_local
+    g = n_q // n_kv
+    n_q_local = n_kv_local * g
+    dtype = abi.BF16 if args.dtype == "bf16" else abi.F32
+    e = 2 if dtype == abi.BF16 else 4
+
+    # a non-default torch stream shared with the library, so torch.cuda.Event brackets exactly the
+    # launches the C ABI makes (a NULL stream would make lorakv_ctx_create open a private one)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
+    ctx = pkg.Context(local_rank, stream=stream.cuda_stream)
+    ctx.set_kernel_policy(args.policy)
+    pool = pkg.Pool(ctx, "BaseLRShared", n_layers, n_kv, d, d_model, r, A, max_tokens=L, dtype=dtype,
+                    kv_head_begin=kv_begin, n_kv_local=n_kv_local)
+    ad = pkg.Adapters(ctx, n_layers, A, d_model, r, n_kv, d, kv_head_begin=kv_begin, n_kv_local=n_kv_local, dtype=dtype)
+
+    # ---- synthetic cache of the named shape, generated on the device (same seed on every rank so
+    # that head shards are slices of one logical cache) ----------------------------------------
+    gen = torch.Generator(device=dev)
+    sc = float(1.0 / np.sqrt(d))
+    pool.append_tokens(L)
+    rows_per_chunk = 8192
+    for layer in range(n_layers):
+        gen.manual_seed(1000 + layer)
+        for c0 in range(0, L, rows_per_chunk):
+            n = min(rows_per_chunk, L - c0)
+            kbuf = torch.randn((n, n_kv * d), generator=gen, device=dev, dtype=torch.float32) * sc
+            vbuf = torch.randn((n, n_kv * d), generator=gen, device=dev, dtype=torch.float32)
+            lbuf = torch.randn((n, max(r, 1)), generator=gen, device=dev, dtype=torch.float32)
+            pool.append_device(abi.KEY, layer, 0, c0, kbuf.data_ptr(), n, n_kv * d)
+            pool.append_device(abi.VALUE, layer, 0, c0, vbuf.data_ptr(), n, n_kv * d)
+            if r > 0:
+                pool.append_device(abi.LR, layer, 0, c0, lbuf.data_ptr(), n, max(r, 1))
+        torch.cuda.synchronize()
+    host_rng = np.random.default_rng(7)
+    b_host = [[(host_rng.standard_normal((r, n_kv * d)).astype(np.float32) * (0.02 / np.sqrt(max(r, 1)))) for _ in range(A)]
+              for _ in range(n_layers)]
+    bf16_round = (lambda x: torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()) if dtype == abi.BF16 else (lambda x: x)
+    for layer in range(n_layers):
+        for a in range(A):
+            b_host[layer][a] = bf16_round(b_host[layer][a])
+            ad.set_b(layer, a, b_host[layer][a], 16.0)
+    q_full = bf16_round((host_rng.standard_normal((n_layers, A, n_q * d)).astype(np.float32) * sc))
+    q_local_host = np.ascontiguousarray(q_full.reshape(n_layers, A, n_q, d)[:, :, kv_begin * g:(kv_begin + n_kv_local) * g, :]
+                                        .reshape(n_layers, A, n_q_local * d))
+    q_dev = torch.from_numpy(q_local_host).to(dev)
+    out_dev = torch.zeros((n_layers, A, n_q_local * d), device=dev, dtype=torch.float32)
+    gathered = torch.zeros((world, n_layers, A, n_q_local * d), device=dev, dtype=torch.float32) if world > 1 else None
+    agent_ids = list(range(A))
+
+    def step_device():
+        if args.per_layer_launch:
+            for layer in range(n_layers):
+                pool.decode_device(ad, layer, layer + 1, agent_ids, n_q,
+                                   q_dev[layer].data_ptr(), out_dev[layer].data_ptr())
+        else:
+            pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
+        if world > 1:   # the end-of-step output gather, the only collective on the path
+            dist.all_gather_into_tensor(gathered, out_dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timing --------------------------------------------------------------------
+    for _ in range(max(args.warmup, 3)):
+        step_device()
+    barrier()
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+    launches0 = ctx.launch_count
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record()
+    for _ in range(args.steps):
+        step_device()
+    ev1.record()
+    barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = ctx.launch_count - launches0
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = A / (ms * 1e-3)
+
+    # ---- dominant-kernel duration for the roofline: events around the attention launch only ----------
+    k_ms = []
+    for _ in range(min(args.steps, 10)):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
+        a1.record()
+        torch.cuda.synchronize()
+        k_ms.append(a0.elapsed_time(a1))
+    kernel_ms = statistics.median(k_ms)
+    clocks = sampler.stop() if rank == 0 else None
+
+    # ---- end to end through the C ABI with host buffers ------------------------------------------------
+    q_pin = ctx.pinned_array(q_local_host.shape)
+    q_pin[...] = q_local_host
+    out_pin = ctx.pinned_array(q_local_host.shape)
+    for _ in range(3):
+        pool.decode(ad, 0, n_layers, agent_ids, n_q, q_pin, out=out_pin)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        pool.decode(ad, 0, n_layers, agent_ids, n_q, q_pin, out=out_pin)   # H2D + kernels + D2H + sync
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, out_dev)
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = A / (e2e_ms * 1e-3)
+    io_bytes = int(q_local_host.nbytes)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = load_peaks()
+    alg = algorithmic_bytes(n_layers, n_q, n_kv_local, n_kv, d, r, A, L, e)
+    achieved = alg / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.workload}_{args.dtype}_{ctx.last_kernel()}")
+    except Exception:
+        pass
+    line = {
+        "metric": "flash_lora_attn_decode_agent_tokens_per_s", "value": value, "unit": "tok/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.dtype if args.dtype != "f32" else "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "description": desc, "n_layers": n_layers, "agents": A, "context": L,
+                   "rank": r, "page_tokens": int(pool.dims.page_tokens), "scheme": "BaseLRShared",
+                   "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                   "launch": "per-layer" if args.per_layer_launch else "one launch per step over all layers",
+                   "l2": f"inputs ({alg / 1e9:.2f} GB per step) larger than L2; no flush needed",
+                   "kernel": ctx.last_kernel()},
+        "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+                "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+                     "kernel_ms": kernel_ms, "kernel": ctx.last_kernel()},
+    }
+
+    # ---- CPU baseline + parity at full size on layer 0 (rank 0, N = 1 only) -----------------------------
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import checker
+        chk = checker.best()
+        threads = host_threads()
+        k0 = pool.key_view(0, 0); v0 = pool.value_view(0, 0); lr0 = pool.lr_view(0, 0)
+        qs = [np.ascontiguousarray(q_full[0, a][None, :]) for a in range(A)]
+        reps, total, outs = 0, 0.0, None
+        while reps < 8 and total < 10.0:      # bounded sample: ~10 s of CPU work
+            s_, outs = cpu_reference_time(chk, qs, k0, v0, lr0, b_host[0], 16.0 / r if r else 1.0, L, n_q, n_kv, threads)
+            total += s_; reps += 1
+        secs = total / reps
+        got = out_pin
+        errs = [chk.max_rel_error(got[0, a][None, :], outs[a]) for a in range(A)]
+        cpu_step = secs * n_layers
+        line["cpu_baseline"] = {"value": A / cpu_step, "unit": "tok/s", "cores": threads, "kind": chk.kind,
+                                "sample": f"1 of {n_layers} layers x {A} agents timed {reps}x (mean {secs:.2f} s, gqa_attention<float> over "
+                                          f"{threads} threads) and scaled by {n_layers}; same cache contents as the GPU"}
+        line["parity"] = {"layer0_max_rel_error": max(errs), "tolerance": 2e-2 if dtype == abi.BF16 else 1e-4,
+                          "oracle": chk.kind}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,228 @@
+/*
+ * lorakv_b200.h -- C ABI of the B200-native Flash-LoRA-Attention path (liblorakv_b200.so).
+ *
+ * This is the drop-in boundary.  The reference (lorakv, arXiv 2602.01053) has no FFI layer: its
+ * operator API is the C++ header surface in proj/include/lorakv/.  Every entry point below names
+ * the reference symbol (file:line under /root/reference) it stands in for; the source-compatible
+ * C++ headers in include/lorakv/ are thin wrappers over exactly these functions, and
+ * INTEGRATION.md shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; opaque handles for device-resident state;
+ *   - every function returns 0 on success, non-zero on failure; the message (same wording as the
+ *     reference's std::runtime_error text where one exists, matrix.hpp:17-19) is returned by
+ *     lorakv_last_error() for the calling thread;
+ *   - matrices are row-major with an explicit row stride in ELEMENTS (Span2D, matrix.hpp:31-38);
+ *   - there is no CPU fallback: without a CUDA device every compute entry point fails loudly.
+ */
+#ifndef LORAKV_B200_H
+#define LORAKV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LORAKV_ABI_VERSION 1
+
+typedef struct lorakv_ctx lorakv_ctx;           /* device + stream + scratch */
+typedef struct lorakv_pool lorakv_pool;         /* paged cache of one trajectory (KvStore<T>) */
+typedef struct lorakv_adapters lorakv_adapters; /* shared A per layer, B per (layer, agent) */
+
+enum { LORAKV_OK = 0, LORAKV_ERR = 1 };
+
+/* storage / arithmetic modes */
+enum { LORAKV_F32 = 0, LORAKV_BF16 = 1 };
+/* where a caller buffer lives */
+enum { LORAKV_HOST = 0, LORAKV_DEVICE = 1 };
+/* SchemeKind, kvcache.hpp:15-21 (SelectiveRecompute is outside the hot path) */
+enum { LORAKV_NONSHARED = 0, LORAKV_FULLSHARED = 1, LORAKV_BASESHARED = 2, LORAKV_BASELRSHARED = 3,
+       LORAKV_SELECTIVE = 4 };
+/* which cache */
+enum { LORAKV_KEY = 0, LORAKV_VALUE = 1, LORAKV_LR = 2 };
+
+int lorakv_abi_version(void);
+const char* lorakv_last_error(void);
+
+/* ---- context ------------------------------------------------------------------------------- */
+/* stream: a cudaStream_t to launch on (borrowed), or NULL to create a private one. */
+int lorakv_ctx_create(int device, void* stream, lorakv_ctx** out);
+void lorakv_ctx_destroy(lorakv_ctx* ctx);
+int lorakv_ctx_synchronize(lorakv_ctx* ctx);
+void* lorakv_ctx_stream(lorakv_ctx* ctx);
+int lorakv_ctx_sm_count(lorakv_ctx* ctx);
+/* number of kernels this library has launched on ctx since creation (bench.py's gpu_launches) */
+int64_t lorakv_ctx_launch_count(lorakv_ctx* ctx);
+
+/* device / pinned-host buffers for callers that do not link the CUDA runtime themselves */
+int lorakv_dev_alloc(lorakv_ctx* ctx, int64_t bytes, void** out);
+int lorakv_dev_free(lorakv_ctx* ctx, void* p);
+int lorakv_host_alloc(lorakv_ctx* ctx, int64_t bytes, void** out); /* pinned */
+int lorakv_host_free(lorakv_ctx* ctx, void* p);
+int lorakv_copy_h2d(lorakv_ctx* ctx, void* dst_dev, const void* src_host, int64_t bytes); /* async on ctx stream */
+int lorakv_copy_d2h(lorakv_ctx* ctx, void* dst_host, const void* src_dev, int64_t bytes); /* async on ctx stream */
+/* writes `bytes` of a scratch buffer (> L2) so that the next kernel starts with a cold L2 */
+int lorakv_flush_l2(lorakv_ctx* ctx);
+
+/* ---- per-head operators over caller memory (HOST pointers) ----------------------------------
+ * flash_lora_attention<T>, attention.hpp:210-268.  q: L_c x d, k/v_base: L x d, v_lr: L x r,
+ * b_up: r x d, out: L_c x d dense.  row_max / row_denom (OnlineSoftmaxStats, :116-119) may be NULL.
+ * Result is independent of any tiling, so BlockConfig only needs validating by the caller. */
+int lorakv_fla_forward_f32(lorakv_ctx* ctx, const float* q, int64_t ldq, const float* k, int64_t ldk,
+                           const float* v_base, int64_t ldv, const float* v_lr, int64_t ldlr,
+                           const float* b_up, int64_t ldb, float lr_scale, int64_t L_c, int64_t L,
+                           int64_t d, int64_t r, int64_t query_offset, float* out, float* row_max,
+                           float* row_denom);
+int lorakv_fla_forward_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const double* k, int64_t ldk,
+                           const double* v_base, int64_t ldv, const double* v_lr, int64_t ldlr,
+                           const double* b_up, int64_t ldb, double lr_scale, int64_t L_c, int64_t L,
+                           int64_t d, int64_t r, int64_t query_offset, double* out, double* row_max,
+                           double* row_denom);
+/* expand_first_attention<T>, attention.hpp:274-326: materialises lr_scale*(V_lr*B) (L x d) on the
+ * device, then attends with a second d-wide accumulator.  The baseline the paper compares with. */
+int lorakv_expand_first_forward_f32(lorakv_ctx* ctx, const float* q, int64_t ldq, const float* k,
+                                    int64_t ldk, const float* v_base, int64_t ldv, const float* v_lr,
+                                    int64_t ldlr, const float* b_up, int64_t ldb, float lr_scale,
+                                    int64_t L_c, int64_t L, int64_t d, int64_t r,
+                                    int64_t query_offset, float* out);
+int lorakv_expand_first_forward_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const double* k,
+                                    int64_t ldk, const double* v_base, int64_t ldv,
+                                    const double* v_lr, int64_t ldlr, const double* b_up, int64_t ldb,
+                                    double lr_scale, int64_t L_c, int64_t L, int64_t d, int64_t r,
+                                    int64_t query_offset, double* out);
+/* naive_attention<T>, attention.hpp:81-112: full score matrix, row softmax, expanded values --
+ * the materialising algorithm, kept as an independent device implementation for cross-checks. */
+int lorakv_naive_forward_f32(lorakv_ctx* ctx, const float* q, int64_t ldq, const float* k, int64_t ldk,
+                             const float* v_base, int64_t ldv, const float* v_lr, int64_t ldlr,
+                             const float* b_up, int64_t ldb, float lr_scale, int64_t L_c, int64_t L,
+                             int64_t d, int64_t r, int64_t query_offset, float* out);
+int lorakv_naive_forward_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const double* k,
+                             int64_t ldk, const double* v_base, int64_t ldv, const double* v_lr,
+                             int64_t ldlr, const double* b_up, int64_t ldb, double lr_scale,
+                             int64_t L_c, int64_t L, int64_t d, int64_t r, int64_t query_offset,
+                             double* out);
+/* gqa_attention<T>, attention.hpp:332-363: all q heads in one launch.  q: L_c x (n_q*d_head),
+ * k/v_base: L x (n_kv*d_head), v_lr: L x r (shared by all heads), b_up: r x (n_kv*d_head). */
+int lorakv_gqa_forward_f32(lorakv_ctx* ctx, const float* q, int64_t ldq, const float* k, int64_t ldk,
+                           const float* v_base, int64_t ldv, const float* v_lr, int64_t ldlr,
+                           const float* b_up, int64_t ldb, float lr_scale, int64_t L_c, int64_t L,
+                           int64_t n_q_heads, int64_t n_kv_heads, int64_t d_head, int64_t r,
+                           int64_t query_offset, float* out);
+int lorakv_gqa_forward_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const double* k, int64_t ldk,
+                           const double* v_base, int64_t ldv, const double* v_lr, int64_t ldlr,
+                           const double* b_up, int64_t ldb, double lr_scale, int64_t L_c, int64_t L,
+                           int64_t n_q_heads, int64_t n_kv_heads, int64_t d_head, int64_t r,
+                           int64_t query_offset, double* out);
+
+/* lr_mac_counts, attention.hpp:35-41, and the dense AttnMacs closed forms (:229-243):
+ * macs[0]=qk, [1]=pv, [2]=lr (reordered).  Pure integer arithmetic on the host. */
+void lorakv_lr_mac_counts(int64_t total_len, int64_t cur_len, int64_t rank, int64_t d_head,
+                          uint64_t* no_reorder, uint64_t* reorder);
+void lorakv_attn_macs(int64_t L_c, int64_t L, int64_t d, int64_t r, int expand_first,
+                      uint64_t macs[3]);
+
+/* ---- planning (pure integers) --------------------------------------------------------------
+ * plan_core, kvcache.hpp:112-142.  out[0..1]=hidden_pass, [2..3]=kv_project, [4..5]=lr_project,
+ * [6..7]=kv_recompute, [8]=skip_layers_below. */
+int lorakv_plan_core(int scheme, int64_t first_recompute, int64_t length, int64_t seen,
+                     int64_t new_tokens, int64_t out[9]);
+
+/* ---- paged cache pool: KvStore<T>, kvcache.hpp:213-420 ---------------------------------------- */
+typedef struct {
+  int32_t scheme;        /* LORAKV_NONSHARED .. LORAKV_BASELRSHARED */
+  int32_t dtype;         /* LORAKV_F32 or LORAKV_BF16 storage in HBM */
+  int64_t n_layers;
+  int64_t n_kv_heads;    /* kv heads of the whole model */
+  int64_t d_head;
+  int64_t d_model;
+  int64_t rank;          /* 0 = no low-rank cache */
+  int64_t n_agents;
+  int64_t page_tokens;   /* tokens per page; 0 = default (64) */
+  int64_t max_tokens;    /* capacity of the trajectory, rounded up to whole pages */
+  int64_t kv_head_begin; /* this pool stores kv heads [kv_head_begin, kv_head_begin + n_kv_local) */
+  int64_t n_kv_local;    /* 0 = all heads (single GPU) */
+} lorakv_pool_dims;
+
+int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_pool** out);
+void lorakv_pool_destroy(lorakv_pool* pool);
+int lorakv_pool_dims_get(const lorakv_pool* pool, lorakv_pool_dims* out);
+
+int lorakv_pool_append_tokens(lorakv_pool* pool, int64_t n);            /* :254-257 */
+int64_t lorakv_pool_length(const lorakv_pool* pool);                    /* :251 */
+int lorakv_pool_seen(const lorakv_pool* pool, int64_t agent, int64_t* out); /* :259 */
+int lorakv_pool_mark_seen(lorakv_pool* pool, int64_t agent);            /* :260-264 */
+int lorakv_pool_plan_step(const lorakv_pool* pool, int64_t agent, int64_t new_tokens,
+                          int64_t out[9]);                              /* plan_step :423-425 */
+
+/* append_key / append_value / append_lr, :268-288, with first-writer-wins (:400-407) resolved on
+ * the host before any launch.  rows: n_rows x cols(which) float32, row stride ld, in HOST or
+ * DEVICE memory; cols = n_kv_heads*d_head for key/value (the FULL width -- the pool keeps its own
+ * head slice) and rank for lr.  *appended (may be NULL) receives the rows actually written. */
+int lorakv_pool_append(lorakv_pool* pool, int which, int64_t layer, int64_t agent,
+                       int64_t row_begin, const float* rows, int64_t n_rows, int64_t ld,
+                       int mem_kind, int64_t* appended);
+/* The append path of engine.hpp:414-418: V_lr rows = X * A (unscaled) computed on the device and
+ * written straight into the LR pages.  x: n_rows x d_model float32. */
+int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* adapters, int64_t layer,
+                                  int64_t agent, int64_t row_begin, const float* x, int64_t n_rows,
+                                  int64_t ld, int mem_kind, int64_t* appended);
+/* rows currently materialised in the buffer (layer, agent) resolves to (GrowMat::rows) */
+int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows);
+/* key_view / value_view / lr_view, :307-324: de-paginate rows [row_begin, row_begin+n_rows) into a
+ * dense float32 HOST matrix (n_rows x cols, cols = n_kv_local*d_head or rank). */
+int lorakv_pool_read(const lorakv_pool* pool, int which, int64_t layer, int64_t agent,
+                     int64_t row_begin, int64_t n_rows, float* out);
+/* CacheBytes / bytes(), :144-150,330-344: {key, value, lr, hidden} = logical elements*sizeof(T);
+ * allocated_elements(), :346-358. */
+int lorakv_pool_bytes(const lorakv_pool* pool, uint64_t out[4]);
+uint64_t lorakv_pool_allocated_elements(const lorakv_pool* pool);
+/* bytes of HBM actually reserved for pages (capacity, not occupancy) */
+uint64_t lorakv_pool_reserved_bytes(const lorakv_pool* pool);
+/* logical page -> physical page of the page set that (which, agent) resolves to.  Pages are handed
+ * out in first-touch order.  Writes min(cap, n_pages) entries, *n_pages = pages in use. */
+int lorakv_pool_page_table(const lorakv_pool* pool, int which, int64_t agent, int32_t* out,
+                           int64_t cap, int64_t* n_pages);
+
+/* ---- adapter tables: LoraAdapter / MultiLoraSet, lora.hpp:13-87 -------------------------------- */
+int lorakv_adapters_create(lorakv_ctx* ctx, int64_t n_layers, int64_t n_agents, int64_t d_model,
+                           int64_t rank, int64_t n_kv_heads, int64_t d_head, int64_t kv_head_begin,
+                           int64_t n_kv_local, int dtype, lorakv_adapters** out);
+void lorakv_adapters_destroy(lorakv_adapters* ad);
+/* shared down-projection A (d_model x rank, HOST float32, dense) of one layer: shared-A multi-LoRA,
+ * lora.hpp:69-73 -- one A for every agent, so X*A is computed once */
+int lorakv_adapters_set_a(lorakv_adapters* ad, int64_t layer, const float* a);
+/* per-agent up-projection B (rank x n_kv_heads*d_head, HOST float32, dense, FULL width) and alpha;
+ * the effective scale alpha/rank travels with B (lora.hpp:9-11,34) */
+int lorakv_adapters_set_b(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* b,
+                          double alpha);
+
+/* ---- device-resident fast paths --------------------------------------------------------------
+ * Batched decode = one gqa_attention call (attention.hpp:332) per (layer, batch entry), every
+ * entry attending to the whole shared cache (query_offset = L-1, engine.hpp:440-443), fused into
+ * one launch over layers [layer_begin, layer_end).
+ *   agent_ids: n_batch HOST int32 (which B table each query row group uses)
+ *   q:   [layer_end-layer_begin][n_batch][n_q_local*d_head] float32
+ *   out: same shape, float32                (n_q_local = n_kv_local * n_q_heads/n_kv_heads)
+ * q/out live in HOST or DEVICE memory as mem_kind says (HOST: copies ride the ctx stream). */
+int lorakv_fla_decode_batched(lorakv_pool* pool, const lorakv_adapters* adapters,
+                              int64_t layer_begin, int64_t layer_end, const int32_t* agent_ids,
+                              int64_t n_batch, int64_t n_q_heads, const float* q, float* out,
+                              int mem_kind);
+/* Prefill / append-step attention of one agent on one layer: q rows cover positions
+ * [query_offset, query_offset+L_c) of the cached trajectory (causal rule attention.hpp:44-46).
+ *   q/out: L_c x (n_q_local*d_head) float32, dense. */
+int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* adapters, int64_t layer,
+                       int64_t agent, int64_t n_q_heads, const float* q, int64_t L_c,
+                       int64_t query_offset, float* out, int mem_kind);
+
+/* selects the kernel family for the fast paths: 0 = auto (tcgen05/TMA where the shape allows),
+ * 1 = force the CUDA-core kernels.  Returns the previous value. */
+int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy);
+/* name of the kernel family the last fast-path call on this ctx dispatched to */
+const char* lorakv_last_kernel(lorakv_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

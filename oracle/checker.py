@@ -277,10 +277,20 @@ class Checker:
         return a.value, b.value
 
     def round_bf16(self, x):
+        """Round-to-nearest-even to bf16 and back to float32 (numpy; same bits as orc_round_bf16)."""
         x = np.ascontiguousarray(x, dtype=np.float32)
-        out = np.empty_like(x)
-        P = C.POINTER(C.c_float)
-        self._round_bf16_array(x.ctypes.data_as(P), out.ctypes.data_as(P), x.size)
+        u = x.view(np.uint32).astype(np.uint64)
+        c = lambda v: np.uint64(v)
+        special = (u & c(0x7F800000)) == c(0x7F800000)
+        r = (u + c(0x7FFF) + ((u >> c(16)) & c(1))) & c(0xFFFF0000)
+        quiet = np.where((u & c(0x007FFFFF)) != c(0), c(0x00400000), c(0))
+        r = np.where(special, (u | quiet) & c(0xFFFF0000), r)
+        out = r.astype(np.uint32).view(np.float32).reshape(x.shape)
+        if self.prefix == "orc_":   # keep the C helper honest
+            chk = np.empty_like(x)
+            P = C.POINTER(C.c_float)
+            self._round_bf16_array(x.ctypes.data_as(P), chk.ctypes.data_as(P), x.size)
+            assert np.array_equal(chk.view(np.uint32), out.view(np.uint32))
         return out
 
     def store(self, scheme, n_layers, d_kv, d_model, rank, n_agents, dtype=np.float64):

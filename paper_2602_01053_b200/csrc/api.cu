@@ -1,0 +1,741 @@
+// api.cu -- the C ABI (include/lorakv_b200.h): context, memory helpers, the integer bookkeeping of
+// the reference's KvStore (proj/include/lorakv/kvcache.hpp:112-142, 213-420) kept on the host, the
+// adapter tables (proj/include/lorakv/lora.hpp:13-87) and the dispatch into the kernels.
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "kernels.hpp"
+#include "state.hpp"
+
+namespace lk {
+
+std::string& err_slot() {
+  thread_local std::string s;
+  return s;
+}
+
+int fail(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  err_slot() = buf;
+  return LORAKV_ERR;
+}
+
+int scratch_reserve(lorakv_ctx* ctx, Scratch& s, size_t bytes) {
+  if (bytes <= s.bytes) return LORAKV_OK;
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (s.ptr) LK_CUDA(cudaFree(s.ptr));
+  s.ptr = nullptr; s.bytes = 0;
+  size_t want = std::max(bytes, (size_t)1 << 20);
+  want = (want + ((size_t)1 << 20) - 1) & ~(((size_t)1 << 20) - 1);
+  LK_CUDA(cudaMalloc(&s.ptr, want));
+  s.bytes = want;
+  return LORAKV_OK;
+}
+
+int pinned_reserve(lorakv_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->pinned_bytes) return LORAKV_OK;
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->pinned) LK_CUDA(cudaFreeHost(ctx->pinned));
+  ctx->pinned = nullptr; ctx->pinned_bytes = 0;
+  LK_CUDA(cudaMallocHost(&ctx->pinned, bytes));
+  ctx->pinned_bytes = bytes;
+  return LORAKV_OK;
+}
+
+static const char* kSchemeName[5] = {"NonShared", "FullShared", "BaseShared", "BaseLRShared",
+                                     "SelectiveRecompute"};
+static const char* kWhat[3] = {"key", "value", "lr"};
+
+// resolve (which, layer, agent) -> (set, row counter) the way append_* / *_view do
+// (kvcache.hpp:268-288, 307-324); *none is set for the LR cache of a scheme that keeps none
+static int resolve(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* set,
+                   bool* none) {
+  *none = false; *set = 0;
+  if (which < LORAKV_KEY || which > LORAKV_LR) return fail("bad cache selector %d", which);
+  const bool per_agent = (which != LORAKV_LR && pool->dims.scheme == LORAKV_NONSHARED) ||
+                         (which == LORAKV_LR && pool->dims.scheme == LORAKV_BASESHARED);
+  if (which == LORAKV_LR && pool->lr_sets() == 0) {
+    *none = true;
+    return LORAKV_OK;
+  }
+  if (per_agent) {
+    if (agent < 0 || agent >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)agent);
+    *set = agent;
+  }
+  if (layer < 0 || layer >= pool->dims.n_layers) return fail("layer %lld out of range", (long long)layer);
+  return LORAKV_OK;
+}
+
+static std::vector<std::vector<int64_t>>& rows_of(lorakv_pool* pool, int which) {
+  return which == LORAKV_KEY ? pool->key_rows : which == LORAKV_VALUE ? pool->value_rows : pool->lr_rows;
+}
+static const std::vector<std::vector<int64_t>>& rows_of(const lorakv_pool* pool, int which) {
+  return which == LORAKV_KEY ? pool->key_rows : which == LORAKV_VALUE ? pool->value_rows : pool->lr_rows;
+}
+
+// make sure logical pages covering rows [0, row_end) of `set` exist; ids in first-touch order
+static int ensure_pages(lorakv_pool* pool, PageSpace& sp, int64_t set, int64_t row_end) {
+  const int64_t need = (row_end + pool->P - 1) / pool->P;
+  auto& tab = sp.table[(size_t)set];
+  if ((int64_t)tab.size() >= need) return LORAKV_OK;
+  if (need > sp.max_pages)
+    return fail("KvStore: trajectory of %lld rows exceeds the pool capacity of %lld tokens",
+                (long long)row_end, (long long)(sp.max_pages * pool->P));
+  const size_t first = tab.size();
+  while ((int64_t)tab.size() < need) tab.push_back(sp.next_free++);
+  LK_CUDA(cudaMemcpyAsync(sp.dev_table + set * sp.max_pages + first, tab.data() + first,
+                          (tab.size() - first) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                          pool->ctx->stream));
+  // the host vector may be reallocated by a later push_back before the copy runs
+  LK_CUDA(cudaStreamSynchronize(pool->ctx->stream));
+  return LORAKV_OK;
+}
+
+static int stage_rows(lorakv_ctx* ctx, const float* rows, int64_t n, int64_t cols, int64_t ld,
+                      int mem_kind, const float** dev, int64_t* dev_ld) {
+  if (mem_kind == LORAKV_DEVICE) { *dev = rows; *dev_ld = ld; return LORAKV_OK; }
+  if (mem_kind != LORAKV_HOST) return fail("bad mem_kind %d", mem_kind);
+  LK_TRY(scratch_reserve(ctx, ctx->in, (size_t)std::max<int64_t>(n * cols, 1) * sizeof(float)));
+  if (n > 0 && cols > 0)
+    LK_CUDA(cudaMemcpy2DAsync(ctx->in.ptr, cols * sizeof(float), rows, ld * sizeof(float),
+                              cols * sizeof(float), n, cudaMemcpyHostToDevice, ctx->stream));
+  *dev = static_cast<const float*>(ctx->in.ptr);
+  *dev_ld = cols;
+  return LORAKV_OK;
+}
+
+}  // namespace lk
+
+using namespace lk;
+
+extern "C" {
+
+int lorakv_abi_version(void) { return LORAKV_ABI_VERSION; }
+const char* lorakv_last_error(void) { return err_slot().c_str(); }
+
+// ---- context -------------------------------------------------------------------------------
+int lorakv_ctx_create(int device, void* stream, lorakv_ctx** out) {
+  if (!out) return fail("ctx_create: null out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail("lorakv_b200 needs a CUDA device (there is no CPU fallback): %s",
+                e != cudaSuccess ? cudaGetErrorString(e) : "no device found");
+  if (device < 0 || device >= n) return fail("ctx_create: device %d out of range [0,%d)", device, n);
+  LK_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  LK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail("lorakv_b200 is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major,
+                prop.minor);
+  lorakv_ctx* ctx = new (std::nothrow) lorakv_ctx();
+  if (!ctx) return fail("ctx_create: out of host memory");
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t se = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (se != cudaSuccess) { delete ctx; return fail("ctx_create: %s", cudaGetErrorString(se)); }
+    ctx->owns_stream = true;
+  }
+  *out = ctx;
+  return LORAKV_OK;
+}
+
+void lorakv_ctx_destroy(lorakv_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush})
+    if (s->ptr) cudaFree(s->ptr);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int lorakv_ctx_synchronize(lorakv_ctx* ctx) {
+  if (!ctx) return fail("null context");
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LORAKV_OK;
+}
+void* lorakv_ctx_stream(lorakv_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+int lorakv_ctx_sm_count(lorakv_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
+int64_t lorakv_ctx_launch_count(lorakv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int lorakv_dev_alloc(lorakv_ctx* ctx, int64_t bytes, void** out) {
+  if (!ctx || !out || bytes < 0) return fail("dev_alloc: bad arguments");
+  LK_CUDA(cudaSetDevice(ctx->device));
+  LK_CUDA(cudaMalloc(out, (size_t)std::max<int64_t>(bytes, 1)));
+  return LORAKV_OK;
+}
+int lorakv_dev_free(lorakv_ctx* ctx, void* p) {
+  if (!ctx) return fail("null context");
+  if (p) LK_CUDA(cudaFree(p));
+  return LORAKV_OK;
+}
+int lorakv_host_alloc(lorakv_ctx* ctx, int64_t bytes, void** out) {
+  if (!ctx || !out || bytes < 0) return fail("host_alloc: bad arguments");
+  LK_CUDA(cudaMallocHost(out, (size_t)std::max<int64_t>(bytes, 1)));
+  return LORAKV_OK;
+}
+int lorakv_host_free(lorakv_ctx* ctx, void* p) {
+  if (!ctx) return fail("null context");
+  if (p) LK_CUDA(cudaFreeHost(p));
+  return LORAKV_OK;
+}
+int lorakv_copy_h2d(lorakv_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+  if (!ctx) return fail("null context");
+  LK_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return LORAKV_OK;
+}
+int lorakv_copy_d2h(lorakv_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+  if (!ctx) return fail("null context");
+  LK_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return LORAKV_OK;
+}
+int lorakv_flush_l2(lorakv_ctx* ctx) {
+  if (!ctx) return fail("null context");
+  const size_t bytes = (size_t)256 << 20;   // 2x the 126 MB L2
+  LK_TRY(scratch_reserve(ctx, ctx->flush, bytes));
+  LK_CUDA(cudaMemsetAsync(ctx->flush.ptr, 0, bytes, ctx->stream));
+  return LORAKV_OK;
+}
+
+int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy) {
+  if (!ctx) return 0;
+  const int old = ctx->policy;
+  ctx->policy = policy;
+  return old;
+}
+const char* lorakv_last_kernel(lorakv_ctx* ctx) { return ctx ? ctx->last_kernel : "none"; }
+
+// ---- per-head operators ------------------------------------------------------------------------
+#define LK_OPS(SUF, T)                                                                              \
+  int lorakv_fla_forward_##SUF(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t ldk,   \
+                               const T* v, int64_t ldv, const T* vlr, int64_t ldlr, const T* b,     \
+                               int64_t ldb, T s, int64_t Lc, int64_t L, int64_t d, int64_t r,       \
+                               int64_t off, T* out, T* row_max, T* row_denom) {                     \
+    return generic_forward<T>(ctx, "flash_lora_attention", 0, q, ldq, k, ldk, v, ldv, vlr, ldlr, b, \
+                              ldb, s, Lc, L, 1, 1, d, r, off, out, row_max, row_denom);             \
+  }                                                                                                 \
+  int lorakv_expand_first_forward_##SUF(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k,       \
+                                        int64_t ldk, const T* v, int64_t ldv, const T* vlr,         \
+                                        int64_t ldlr, const T* b, int64_t ldb, T s, int64_t Lc,     \
+                                        int64_t L, int64_t d, int64_t r, int64_t off, T* out) {     \
+    return generic_forward<T>(ctx, "expand_first_attention", 1, q, ldq, k, ldk, v, ldv, vlr, ldlr,  \
+                              b, ldb, s, Lc, L, 1, 1, d, r, off, out, nullptr, nullptr);            \
+  }                                                                                                 \
+  int lorakv_naive_forward_##SUF(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t ldk, \
+                                 const T* v, int64_t ldv, const T* vlr, int64_t ldlr, const T* b,   \
+                                 int64_t ldb, T s, int64_t Lc, int64_t L, int64_t d, int64_t r,     \
+                                 int64_t off, T* out) {                                             \
+    return naive_forward<T>(ctx, q, ldq, k, ldk, v, ldv, vlr, ldlr, b, ldb, s, Lc, L, d, r, off,    \
+                            out);                                                                   \
+  }                                                                                                 \
+  int lorakv_gqa_forward_##SUF(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t ldk,   \
+                               const T* v, int64_t ldv, const T* vlr, int64_t ldlr, const T* b,     \
+                               int64_t ldb, T s, int64_t Lc, int64_t L, int64_t n_q, int64_t n_kv,  \
+                               int64_t d, int64_t r, int64_t off, T* out) {                         \
+    if (n_q < 1 || n_kv < 1 || n_q % n_kv != 0)                                                     \
+      return fail("gqa_attention: n_q_heads %lld not divisible by n_kv_heads %lld", (long long)n_q, \
+                  (long long)n_kv);                                                                 \
+    return generic_forward<T>(ctx, "flash_lora_attention", 0, q, ldq, k, ldk, v, ldv, vlr, ldlr, b, \
+                              ldb, s, Lc, L, (int)n_q, (int)n_kv, d, r, off, out, nullptr, nullptr);\
+  }
+LK_OPS(f32, float)
+LK_OPS(f64, double)
+
+void lorakv_lr_mac_counts(int64_t total_len, int64_t cur_len, int64_t rank, int64_t d_head,
+                          uint64_t* no_reorder, uint64_t* reorder) {
+  const uint64_t L = (uint64_t)total_len, Lc = (uint64_t)cur_len, r = (uint64_t)rank, d = (uint64_t)d_head;
+  if (no_reorder) *no_reorder = L * r * d + Lc * L * d;
+  if (reorder) *reorder = Lc * L * r + Lc * r * d;
+}
+
+void lorakv_attn_macs(int64_t L_c, int64_t L, int64_t d, int64_t r, int expand_first, uint64_t macs[3]) {
+  // Dense tile accounting of attention.hpp:229-243 / :286-307 summed over any tiling.
+  const uint64_t Lc = (uint64_t)L_c, Lu = (uint64_t)L, du = (uint64_t)d, ru = (uint64_t)r;
+  macs[0] = Lc * Lu * du;
+  macs[1] = Lc * Lu * du;
+  macs[2] = expand_first ? Lu * ru * du + Lc * Lu * (ru > 0 ? du : 0) : Lc * Lu * ru + Lc * ru * du;
+}
+
+// ---- planning ---------------------------------------------------------------------------------
+int lorakv_plan_core(int scheme, int64_t first_recompute, int64_t length, int64_t seen,
+                     int64_t new_tokens, int64_t out[9]) {
+  if (new_tokens < 0) return fail("plan_core: new_tokens must be >= 0");
+  if (seen < 0 || seen > length) return fail("plan_core: seen out of range");
+  if (scheme < LORAKV_NONSHARED || scheme > LORAKV_SELECTIVE) return fail("plan_core: unknown scheme %d", scheme);
+  const int64_t total = length + new_tokens;
+  // every range starts as `fresh` = [length, total); the schemes that cannot reuse another
+  // agent's work widen some of them to `unseen` = [seen, total)
+  for (int i = 0; i < 3; ++i) { out[2 * i] = length; out[2 * i + 1] = total; }
+  out[6] = out[7] = out[8] = 0;
+  const bool widen_hidden = scheme == LORAKV_NONSHARED || scheme == LORAKV_BASESHARED || scheme == LORAKV_SELECTIVE;
+  const bool widen_kv = scheme == LORAKV_NONSHARED;
+  const bool widen_lr = scheme == LORAKV_NONSHARED || scheme == LORAKV_BASESHARED;
+  if (widen_hidden) out[0] = seen;
+  if (widen_kv) out[2] = seen;
+  if (widen_lr) out[4] = seen;
+  if (scheme == LORAKV_SELECTIVE) { out[6] = seen; out[7] = total; out[8] = first_recompute; }
+  return LORAKV_OK;
+}
+
+// ---- pool ----------------------------------------------------------------------------------------
+int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_pool** out) {
+  if (!ctx || !dims || !out) return fail("pool_create: null argument");
+  *out = nullptr;
+  if (dims->n_layers < 1 || dims->n_kv_heads < 1 || dims->d_head < 1 || dims->d_model < 1 || dims->n_agents < 1)
+    return fail("KvStore: invalid dims");
+  if (dims->rank < 0) return fail("KvStore: negative rank");
+  if (dims->scheme < LORAKV_NONSHARED || dims->scheme > LORAKV_BASELRSHARED)
+    return fail("KvStore: scheme %s is outside the B200 hot path",
+                dims->scheme == LORAKV_SELECTIVE ? kSchemeName[4] : "?");
+  if (dims->dtype != LORAKV_F32 && dims->dtype != LORAKV_BF16) return fail("KvStore: unknown dtype %d", dims->dtype);
+  if (dims->max_tokens < 1) return fail("KvStore: max_tokens must be >= 1");
+  lorakv_pool* p = new (std::nothrow) lorakv_pool();
+  if (!p) return fail("pool_create: out of host memory");
+  p->ctx = ctx;
+  p->dims = *dims;
+  p->P = dims->page_tokens > 0 ? dims->page_tokens : 64;
+  p->dims.page_tokens = p->P;
+  p->n_kv_local = dims->n_kv_local > 0 ? dims->n_kv_local : dims->n_kv_heads - dims->kv_head_begin;
+  p->dims.n_kv_local = p->n_kv_local;
+  if (dims->kv_head_begin < 0 || p->n_kv_local < 1 || dims->kv_head_begin + p->n_kv_local > dims->n_kv_heads) {
+    delete p;
+    return fail("KvStore: kv head shard [%lld,+%lld) outside [0,%lld)", (long long)dims->kv_head_begin,
+                (long long)dims->n_kv_local, (long long)dims->n_kv_heads);
+  }
+  p->elem = dims->dtype == LORAKV_BF16 ? 2 : 4;
+  const bool has_lr = p->lr_sets() > 0 && dims->rank > 0;
+  p->r_pad = has_lr ? (dims->rank + 7) / 8 * 8 : 0;
+  p->seen.assign((size_t)dims->n_agents, 0);
+  const int64_t max_pages = (dims->max_tokens + p->P - 1) / p->P;
+  p->dims.max_tokens = max_pages * p->P;
+  auto init_space = [&](PageSpace& sp, int64_t sets) {
+    sp.n_sets = sets; sp.max_pages = max_pages; sp.next_free = 0;
+    sp.table.assign((size_t)sets, {});
+  };
+  init_space(p->kv_space, p->kv_sets());
+  init_space(p->lr_space, p->lr_sets());
+  p->key_rows.assign((size_t)p->kv_sets(), std::vector<int64_t>((size_t)dims->n_layers, 0));
+  p->value_rows = p->key_rows;
+  p->lr_rows.assign((size_t)std::max<int64_t>(p->lr_sets(), 1), std::vector<int64_t>((size_t)dims->n_layers, 0));
+
+  auto cleanup = [&](int rc) { lorakv_pool_destroy(p); return rc; };
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cleanup(fail("pool_create: %s", cudaGetErrorString(e)));
+  const size_t kv_bytes = (size_t)(dims->n_layers * p->kv_layer_stride()) * (size_t)p->elem;
+  const size_t lr_bytes = (size_t)(dims->n_layers * p->lr_layer_stride()) * (size_t)p->elem;
+  auto alloc_zero = [&](void** ptr, size_t bytes) -> int {
+    if (bytes == 0) return LORAKV_OK;
+    LK_CUDA(cudaMalloc(ptr, bytes));
+    // pages are zero-filled so that the unused tail of the last page multiplies as exact zeros
+    LK_CUDA(cudaMemsetAsync(*ptr, 0, bytes, ctx->stream));
+    p->reserved_bytes += bytes;
+    return LORAKV_OK;
+  };
+  int rc = alloc_zero(&p->k_pages, kv_bytes);
+  if (rc == LORAKV_OK) rc = alloc_zero(&p->v_pages, kv_bytes);
+  if (rc == LORAKV_OK) rc = alloc_zero(&p->lr_pages, lr_bytes);
+  auto alloc_table = [&](PageSpace& sp) -> int {
+    if (sp.total_pages() == 0) return LORAKV_OK;
+    LK_CUDA(cudaMalloc(&sp.dev_table, (size_t)sp.total_pages() * sizeof(int32_t)));
+    LK_CUDA(cudaMemsetAsync(sp.dev_table, 0, (size_t)sp.total_pages() * sizeof(int32_t), ctx->stream));
+    return LORAKV_OK;
+  };
+  if (rc == LORAKV_OK) rc = alloc_table(p->kv_space);
+  if (rc == LORAKV_OK) rc = alloc_table(p->lr_space);
+  if (rc != LORAKV_OK) return cleanup(rc);
+  *out = p;
+  return LORAKV_OK;
+}
+
+void lorakv_pool_destroy(lorakv_pool* p) {
+  if (!p) return;
+  cudaSetDevice(p->ctx->device);
+  cudaStreamSynchronize(p->ctx->stream);
+  for (void* q : {p->k_pages, p->v_pages, p->lr_pages, (void*)p->kv_space.dev_table, (void*)p->lr_space.dev_table})
+    if (q) cudaFree(q);
+  delete p;
+}
+
+int lorakv_pool_dims_get(const lorakv_pool* pool, lorakv_pool_dims* out) {
+  if (!pool || !out) return fail("null argument");
+  *out = pool->dims;
+  return LORAKV_OK;
+}
+
+int lorakv_pool_append_tokens(lorakv_pool* pool, int64_t n) {
+  if (!pool) return fail("null pool");
+  if (n < 0) return fail("append_tokens: negative count");
+  pool->length += n;
+  return LORAKV_OK;
+}
+int64_t lorakv_pool_length(const lorakv_pool* pool) { return pool ? pool->length : -1; }
+
+int lorakv_pool_seen(const lorakv_pool* pool, int64_t agent, int64_t* out) {
+  if (!pool || !out) return fail("null argument");
+  if (agent < 0 || agent >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)agent);
+  *out = pool->seen[(size_t)agent];
+  return LORAKV_OK;
+}
+int lorakv_pool_mark_seen(lorakv_pool* pool, int64_t agent) {
+  if (!pool) return fail("null pool");
+  if (agent < 0 || agent >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)agent);
+  if (pool->length < pool->seen[(size_t)agent]) return fail("KvStore: seen_upto may not decrease");
+  pool->seen[(size_t)agent] = pool->length;
+  return LORAKV_OK;
+}
+int lorakv_pool_plan_step(const lorakv_pool* pool, int64_t agent, int64_t new_tokens, int64_t out[9]) {
+  int64_t seen = 0;
+  LK_TRY(lorakv_pool_seen(pool, agent, &seen));
+  return lorakv_plan_core(pool->dims.scheme, 0, pool->length, seen, new_tokens, out);
+}
+
+// first-writer-wins arithmetic of append_fww (kvcache.hpp:400-407)
+static int fww(const char* what, int64_t rows, int64_t row_begin, int64_t n, int64_t* skip, int64_t* add) {
+  if (row_begin > rows) return fail("KvStore: %s append leaves a gap at row %lld", what, (long long)rows);
+  const int64_t present = rows - row_begin;
+  if (present >= n) { *skip = n; *add = 0; return LORAKV_OK; }
+  *skip = present;
+  *add = n - present;
+  return LORAKV_OK;
+}
+
+int lorakv_pool_append(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin,
+                       const float* rows, int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended) {
+  if (!pool) return fail("null pool");
+  if (appended) *appended = 0;
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, which, layer, agent, &set, &none));
+  if (none) return fail("KvStore: scheme %s has no LR cache", kSchemeName[pool->dims.scheme]);
+  if (n_rows < 0) return fail("append: negative row count");
+  int64_t& have = rows_of(pool, which)[(size_t)set][(size_t)layer];
+  int64_t skip, add;
+  LK_TRY(fww(kWhat[which], have, row_begin, n_rows, &skip, &add));
+  if (add == 0) return LORAKV_OK;
+  const bool is_lr = which == LORAKV_LR;
+  const int64_t full_cols = is_lr ? pool->dims.rank : pool->dims.n_kv_heads * pool->dims.d_head;
+  if (full_cols > 0) {
+    if (!rows) return fail("append: null rows");
+    lorakv_ctx* ctx = pool->ctx;
+    LK_CUDA(cudaSetDevice(ctx->device));
+    LK_TRY(ensure_pages(pool, is_lr ? pool->lr_space : pool->kv_space, set, have + add));
+    const float* dev; int64_t dev_ld;
+    LK_TRY(stage_rows(ctx, rows + skip * ld, add, full_cols, ld, mem_kind, &dev, &dev_ld));
+    const int64_t col0 = is_lr ? 0 : pool->dims.kv_head_begin * pool->dims.d_head;
+    LK_TRY(launch_append_scatter(pool, which, layer, set, have, dev + col0, add, dev_ld));
+    if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));  // staging is reused
+  }
+  have += add;
+  if (appended) *appended = add;
+  return LORAKV_OK;
+}
+
+int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer,
+                                  int64_t agent, int64_t row_begin, const float* x, int64_t n_rows,
+                                  int64_t ld, int mem_kind, int64_t* appended) {
+  if (!pool || !ad) return fail("null argument");
+  if (appended) *appended = 0;
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, LORAKV_LR, layer, agent, &set, &none));
+  if (none) return fail("KvStore: scheme %s has no LR cache", kSchemeName[pool->dims.scheme]);
+  if (ad->rank != pool->dims.rank || ad->d_model != pool->dims.d_model || layer >= ad->n_layers)
+    return fail("lr_append_project: adapter table does not match the pool (rank %lld vs %lld)",
+                (long long)ad->rank, (long long)pool->dims.rank);
+  if (pool->dims.rank > 0 && !ad->a_set[(size_t)layer]) return fail("lr_append_project: A of layer %lld was never uploaded", (long long)layer);
+  int64_t& have = pool->lr_rows[(size_t)set][(size_t)layer];
+  int64_t skip, add;
+  LK_TRY(fww("lr", have, row_begin, n_rows, &skip, &add));
+  if (add == 0) return LORAKV_OK;
+  if (pool->dims.rank > 0) {
+    lorakv_ctx* ctx = pool->ctx;
+    LK_CUDA(cudaSetDevice(ctx->device));
+    LK_TRY(ensure_pages(pool, pool->lr_space, set, have + add));
+    const float* dev; int64_t dev_ld;
+    LK_TRY(stage_rows(ctx, x + skip * ld, add, pool->dims.d_model, ld, mem_kind, &dev, &dev_ld));
+    LK_TRY(launch_lr_project(pool, ad, layer, set, have, dev, add, dev_ld));
+    if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  have += add;
+  if (appended) *appended = add;
+  return LORAKV_OK;
+}
+
+int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows) {
+  if (!pool || !rows) return fail("null argument");
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, which, layer, agent, &set, &none));
+  if (none) {   // lr_view on a scheme without LR: L x 0 with L = key rows (kvcache.hpp:323)
+    LK_TRY(resolve(pool, LORAKV_KEY, layer, agent, &set, &none));
+    *rows = pool->key_rows[(size_t)set][(size_t)layer];
+    return LORAKV_OK;
+  }
+  *rows = rows_of(pool, which)[(size_t)set][(size_t)layer];
+  return LORAKV_OK;
+}
+
+int lorakv_pool_read(const lorakv_pool* pool, int which, int64_t layer, int64_t agent,
+                     int64_t row_begin, int64_t n_rows, float* out) {
+  if (!pool) return fail("null pool");
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, which, layer, agent, &set, &none));
+  if (none) return LORAKV_OK;   // zero columns
+  const int64_t have = rows_of(pool, which)[(size_t)set][(size_t)layer];
+  if (row_begin < 0 || n_rows < 0 || row_begin + n_rows > have)
+    return fail("row_range [%lld,%lld) out of bounds for %lld rows", (long long)row_begin,
+                (long long)(row_begin + n_rows), (long long)have);
+  const int64_t cols = which == LORAKV_LR ? pool->dims.rank : pool->d_kv_local();
+  if (n_rows == 0 || cols == 0) return LORAKV_OK;
+  if (!out) return fail("read: null out");
+  lorakv_ctx* ctx = pool->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  LK_TRY(scratch_reserve(ctx, ctx->out, (size_t)(n_rows * cols) * sizeof(float)));
+  LK_TRY(launch_gather_rows(pool, which, layer, set, row_begin, n_rows, static_cast<float*>(ctx->out.ptr)));
+  LK_CUDA(cudaMemcpyAsync(out, ctx->out.ptr, (size_t)(n_rows * cols) * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LORAKV_OK;
+}
+
+int lorakv_pool_bytes(const lorakv_pool* pool, uint64_t out[4]) {
+  if (!pool || !out) return fail("null argument");
+  // elements x sizeof(T), exactly as CacheBytes counts them (kvcache.hpp:330-344): logical rows,
+  // not page capacity; a kv-head shard counts its own columns
+  const uint64_t sz = (uint64_t)pool->elem, dkv = (uint64_t)pool->d_kv_local(), r = (uint64_t)pool->dims.rank;
+  uint64_t k = 0, v = 0, l = 0;
+  for (const auto& per : pool->key_rows) for (int64_t n : per) k += (uint64_t)n * dkv;
+  for (const auto& per : pool->value_rows) for (int64_t n : per) v += (uint64_t)n * dkv;
+  if (pool->lr_sets() > 0)
+    for (const auto& per : pool->lr_rows) for (int64_t n : per) l += (uint64_t)n * r;
+  out[0] = k * sz; out[1] = v * sz; out[2] = l * sz; out[3] = 0;
+  return LORAKV_OK;
+}
+uint64_t lorakv_pool_allocated_elements(const lorakv_pool* pool) {
+  uint64_t b[4];
+  if (lorakv_pool_bytes(pool, b) != LORAKV_OK) return 0;
+  return (b[0] + b[1] + b[2]) / (uint64_t)pool->elem;
+}
+uint64_t lorakv_pool_reserved_bytes(const lorakv_pool* pool) { return pool ? pool->reserved_bytes : 0; }
+
+int lorakv_pool_page_table(const lorakv_pool* pool, int which, int64_t agent, int32_t* out, int64_t cap,
+                           int64_t* n_pages) {
+  if (!pool) return fail("null pool");
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, which, 0, agent, &set, &none));
+  if (none) { if (n_pages) *n_pages = 0; return LORAKV_OK; }
+  const auto& tab = (which == LORAKV_LR ? pool->lr_space : pool->kv_space).table[(size_t)set];
+  if (n_pages) *n_pages = (int64_t)tab.size();
+  for (int64_t i = 0; i < cap && i < (int64_t)tab.size(); ++i) out[i] = tab[(size_t)i];
+  return LORAKV_OK;
+}
+
+// ---- adapters ---------------------------------------------------------------------------------------
+int lorakv_adapters_create(lorakv_ctx* ctx, int64_t n_layers, int64_t n_agents, int64_t d_model,
+                           int64_t rank, int64_t n_kv_heads, int64_t d_head, int64_t kv_head_begin,
+                           int64_t n_kv_local, int dtype, lorakv_adapters** out) {
+  if (!ctx || !out) return fail("adapters_create: null argument");
+  *out = nullptr;
+  if (n_layers < 1 || n_agents < 1 || d_model < 1 || n_kv_heads < 1 || d_head < 1) return fail("adapters: invalid dims");
+  if (rank < 1) return fail("LoraAdapter: rank must be >= 1, got %lld", (long long)rank);
+  if (rank > std::min(d_model, n_kv_heads * d_head))
+    return fail("LoraAdapter: rank %lld exceeds min(d_in, d_out)", (long long)rank);
+  if (n_kv_local <= 0) n_kv_local = n_kv_heads - kv_head_begin;
+  if (kv_head_begin < 0 || kv_head_begin + n_kv_local > n_kv_heads) return fail("adapters: bad kv head shard");
+  lorakv_adapters* ad = new (std::nothrow) lorakv_adapters();
+  if (!ad) return fail("adapters_create: out of host memory");
+  ad->ctx = ctx; ad->n_layers = n_layers; ad->n_agents = n_agents; ad->d_model = d_model; ad->rank = rank;
+  ad->n_kv_heads = n_kv_heads; ad->d_head = d_head; ad->kv_head_begin = kv_head_begin; ad->n_kv_local = n_kv_local;
+  ad->dtype = dtype;
+  ad->scale_host.assign((size_t)(n_layers * n_agents), 0.f);
+  ad->a_set.assign((size_t)n_layers, 0);
+  ad->b_set.assign((size_t)(n_layers * n_agents), 0);
+  cudaSetDevice(ctx->device);
+  const size_t a_bytes = (size_t)(n_layers * d_model * rank) * sizeof(float);
+  const size_t b_bytes = (size_t)(n_layers * n_agents * rank * n_kv_local * d_head) * sizeof(float);
+  cudaError_t e = cudaMalloc(&ad->a, a_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&ad->b, b_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&ad->scale, (size_t)(n_layers * n_agents) * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemsetAsync(ad->a, 0, a_bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ad->b, 0, b_bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ad->scale, 0, (size_t)(n_layers * n_agents) * sizeof(float), ctx->stream);
+  if (e != cudaSuccess) {
+    lorakv_adapters_destroy(ad);
+    return fail("adapters_create: %s", cudaGetErrorString(e));
+  }
+  *out = ad;
+  return LORAKV_OK;
+}
+
+void lorakv_adapters_destroy(lorakv_adapters* ad) {
+  if (!ad) return;
+  cudaSetDevice(ad->ctx->device);
+  cudaStreamSynchronize(ad->ctx->stream);
+  if (ad->a) cudaFree(ad->a);
+  if (ad->b) cudaFree(ad->b);
+  if (ad->scale) cudaFree(ad->scale);
+  delete ad;
+}
+
+int lorakv_adapters_set_a(lorakv_adapters* ad, int64_t layer, const float* a) {
+  if (!ad || !a) return fail("null argument");
+  if (layer < 0 || layer >= ad->n_layers) return fail("layer %lld out of range", (long long)layer);
+  LK_CUDA(cudaSetDevice(ad->ctx->device));
+  LK_CUDA(cudaMemcpyAsync(ad->a + layer * ad->d_model * ad->rank, a, (size_t)(ad->d_model * ad->rank) * sizeof(float),
+                          cudaMemcpyHostToDevice, ad->ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
+  ad->a_set[(size_t)layer] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_adapters_set_b(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* b, double alpha) {
+  if (!ad || !b) return fail("null argument");
+  if (layer < 0 || layer >= ad->n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (agent < 0 || agent >= ad->n_agents)
+    return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)ad->n_agents);
+  const double s = alpha / (double)ad->rank;
+  if (!(std::isfinite(s) && s > 0.0)) return fail("LoraAdapter: effective scale alpha/rank must be finite and positive");
+  LK_CUDA(cudaSetDevice(ad->ctx->device));
+  const int64_t dkv_full = ad->n_kv_heads * ad->d_head, dkv = ad->n_kv_local * ad->d_head;
+  float* dst = ad->b + ((layer * ad->n_agents + agent) * ad->rank) * dkv;
+  LK_CUDA(cudaMemcpy2DAsync(dst, dkv * sizeof(float), b + ad->kv_head_begin * ad->d_head, dkv_full * sizeof(float),
+                            dkv * sizeof(float), ad->rank, cudaMemcpyHostToDevice, ad->ctx->stream));
+  const float sf = (float)s;
+  ad->scale_host[(size_t)(layer * ad->n_agents + agent)] = sf;
+  LK_CUDA(cudaMemcpyAsync(ad->scale + layer * ad->n_agents + agent, &ad->scale_host[(size_t)(layer * ad->n_agents + agent)],
+                          sizeof(float), cudaMemcpyHostToDevice, ad->ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
+  ad->b_set[(size_t)(layer * ad->n_agents + agent)] = 1;
+  return LORAKV_OK;
+}
+
+// ---- fast paths ---------------------------------------------------------------------------------------
+static int check_adapters(const lorakv_pool* pool, const lorakv_adapters* ad) {
+  if (pool->r_pad == 0) return LORAKV_OK;
+  if (!ad) return fail("attention: the pool keeps a rank-%lld cache but no adapter tables were given", (long long)pool->dims.rank);
+  if (ad->rank != pool->dims.rank || ad->n_layers != pool->dims.n_layers || ad->n_kv_local != pool->n_kv_local ||
+      ad->kv_head_begin != pool->dims.kv_head_begin || ad->d_head != pool->dims.d_head)
+    return fail("attention: adapter tables do not match the pool");
+  return LORAKV_OK;
+}
+
+// rows every buffer the call reads has materialised (K, V and -- when present -- LR)
+static int visible_rows(const lorakv_pool* pool, int64_t layer, int64_t kv_set, int64_t lr_set, int64_t* L) {
+  int64_t n = std::min(pool->key_rows[(size_t)kv_set][(size_t)layer], pool->value_rows[(size_t)kv_set][(size_t)layer]);
+  if (pool->r_pad > 0) n = std::min(n, pool->lr_rows[(size_t)lr_set][(size_t)layer]);
+  *L = n;
+  return LORAKV_OK;
+}
+
+static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer_begin, int64_t layer_end,
+                     int64_t kv_set, int64_t lr_set, const int32_t* agent_ids, int64_t n_batch,
+                     int64_t rows_per_entry, int64_t query_offset, int64_t n_q_heads, const float* q,
+                     float* out, int mem_kind) {
+  lorakv_ctx* ctx = pool->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  if (layer_begin < 0 || layer_end > pool->dims.n_layers || layer_begin >= layer_end) return fail("attention: bad layer range");
+  if (n_q_heads < 1 || n_q_heads % pool->dims.n_kv_heads != 0)
+    return fail("gqa_attention: n_q_heads %lld not divisible by n_kv_heads %lld", (long long)n_q_heads, (long long)pool->dims.n_kv_heads);
+  LK_TRY(check_adapters(pool, ad));
+  const int64_t group = n_q_heads / pool->dims.n_kv_heads;
+  const int64_t n_q_local = group * pool->n_kv_local;
+  int64_t L = -1;
+  for (int64_t l = layer_begin; l < layer_end; ++l) {
+    int64_t Ll;
+    LK_TRY(visible_rows(pool, l, kv_set, lr_set, &Ll));
+    if (L >= 0 && Ll != L) return fail("attention: layers %lld..%lld hold different row counts", (long long)layer_begin, (long long)layer_end);
+    L = Ll;
+  }
+  if (query_offset < 0 || query_offset + rows_per_entry > L)
+    return fail("attention: query_offset %lld with L_c %lld exceeds L %lld", (long long)query_offset,
+                (long long)rows_per_entry, (long long)L);
+  const int64_t n_layers = layer_end - layer_begin;
+  const int64_t n_elems = n_layers * n_batch * rows_per_entry * n_q_local * pool->dims.d_head;
+  if (n_elems == 0) return LORAKV_OK;
+
+  // agent ids -> device (tiny), staged through pinned memory
+  LK_TRY(pinned_reserve(ctx, 4096 + (size_t)n_batch * sizeof(int32_t)));
+  int32_t* ids_host = static_cast<int32_t*>(ctx->pinned);
+  for (int64_t i = 0; i < n_batch; ++i) {
+    const int32_t a = agent_ids ? agent_ids[i] : 0;
+    if (a < 0 || a >= pool->dims.n_agents) return fail("unknown agent %d", a);
+    if (ad && pool->r_pad > 0)
+      for (int64_t l = layer_begin; l < layer_end; ++l)
+        if (!ad->b_set[(size_t)(l * ad->n_agents + a)]) return fail("attention: B of layer %lld agent %d was never uploaded", (long long)l, a);
+    ids_host[i] = a;
+  }
+  const size_t ids_bytes = ((size_t)n_batch * sizeof(int32_t) + 255) / 256 * 256;
+  const size_t q_bytes = (size_t)n_elems * sizeof(float);
+  const bool host = mem_kind == LORAKV_HOST;
+  if (!host && mem_kind != LORAKV_DEVICE) return fail("bad mem_kind %d", mem_kind);
+  LK_TRY(scratch_reserve(ctx, ctx->out, ids_bytes + (host ? 2 * ((q_bytes + 255) / 256 * 256) : 0)));
+  char* base = static_cast<char*>(ctx->out.ptr);
+  int32_t* ids_dev = reinterpret_cast<int32_t*>(base);
+  LK_CUDA(cudaMemcpyAsync(ids_dev, ids_host, (size_t)n_batch * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  const float* q_dev = q;
+  float* out_dev = out;
+  if (host) {
+    float* qd = reinterpret_cast<float*>(base + ids_bytes);
+    out_dev = reinterpret_cast<float*>(base + ids_bytes + (q_bytes + 255) / 256 * 256);
+    LK_CUDA(cudaMemcpyAsync(qd, q, q_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    q_dev = qd;
+  }
+
+  PagedAttnCall call;
+  call.pool = pool; call.adapters = ad; call.layer_begin = layer_begin; call.layer_end = layer_end;
+  call.kv_set = kv_set; call.lr_set = lr_set; call.agent_ids_dev = ids_dev; call.n_batch = n_batch;
+  call.rows_per_entry = rows_per_entry; call.query_offset = query_offset; call.n_q_local = n_q_local;
+  call.L = L; call.q_dev = q_dev; call.out_dev = out_dev;
+  if (ctx->policy == 0 && decode_umma_supported(call)) LK_TRY(launch_decode_umma(call));
+  else LK_TRY(launch_paged_simt(call));
+
+  if (host) {
+    LK_CUDA(cudaMemcpyAsync(out, out_dev, q_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return LORAKV_OK;
+}
+
+int lorakv_fla_decode_batched(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer_begin,
+                              int64_t layer_end, const int32_t* agent_ids, int64_t n_batch,
+                              int64_t n_q_heads, const float* q, float* out, int mem_kind) {
+  if (!pool || !q || !out) return fail("fla_decode_batched: null argument");
+  if (n_batch < 1) return fail("fla_decode_batched: empty batch");
+  // per-agent caches (NonShared K/V, BaseShared LR) can only serve one agent per launch
+  int64_t kv_set = 0, lr_set = 0;
+  const bool per_agent = pool->dims.scheme == LORAKV_NONSHARED || (pool->dims.scheme == LORAKV_BASESHARED && pool->r_pad > 0);
+  if (per_agent) {
+    for (int64_t i = 1; i < n_batch; ++i)
+      if (agent_ids && agent_ids[i] != agent_ids[0])
+        return fail("fla_decode_batched: scheme %s keeps per-agent caches; batch one agent per call", kSchemeName[pool->dims.scheme]);
+    const int64_t a = agent_ids ? agent_ids[0] : 0;
+    if (a < 0 || a >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)a);
+    if (pool->dims.scheme == LORAKV_NONSHARED) kv_set = a; else lr_set = a;
+  }
+  int64_t L;
+  LK_TRY(visible_rows(pool, layer_begin, kv_set, lr_set, &L));
+  if (L < 1) return fail("attention: query_offset 0 with L_c 1 exceeds L 0");
+  return run_paged(pool, ad, layer_begin, layer_end, kv_set, lr_set, agent_ids, n_batch, 1, L - 1, n_q_heads, q, out, mem_kind);
+}
+
+int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer, int64_t agent,
+                       int64_t n_q_heads, const float* q, int64_t L_c, int64_t query_offset, float* out,
+                       int mem_kind) {
+  if (!pool || !q || !out) return fail("fla_prefill: null argument");
+  if (agent < 0 || agent >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)agent);
+  if (L_c < 0) return fail("fla_prefill: negative L_c");
+  if (L_c == 0) return LORAKV_OK;
+  int64_t kv_set = pool->dims.scheme == LORAKV_NONSHARED ? agent : 0;
+  int64_t lr_set = pool->dims.scheme == LORAKV_BASESHARED ? agent : 0;
+  const int32_t id = (int32_t)agent;
+  return run_paged(pool, ad, layer, layer + 1, kv_set, lr_set, &id, 1, L_c, query_offset, n_q_heads, q, out, mem_kind);
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// kernels.hpp -- host-callable launchers implemented in the .cu files of this directory.
+#pragma once
+
+#include <cstdint>
+
+#include "lorakv_b200.h"
+
+struct lorakv_ctx;
+struct lorakv_pool;
+struct lorakv_adapters;
+
+namespace lk {
+
+// fla_generic.cu ------------------------------------------------------------------------------
+template <class T>
+int generic_forward(lorakv_ctx* ctx, const char* op, int mode, const T* q, int64_t ldq, const T* k,
+                    int64_t ldk, const T* v, int64_t ldv, const T* vlr, int64_t ldlr, const T* b,
+                    int64_t ldb, T lr_scale, int64_t Lc, int64_t L, int n_q, int n_kv, int64_t d,
+                    int64_t r, int64_t off, T* out, T* row_max, T* row_denom);
+template <class T>
+int naive_forward(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t ldk, const T* v,
+                  int64_t ldv, const T* vlr, int64_t ldlr, const T* b, int64_t ldb, T lr_scale,
+                  int64_t Lc, int64_t L, int64_t d, int64_t r, int64_t off, T* out);
+
+// cache_kernels.cu ----------------------------------------------------------------------------
+// Copy `n_rows` float32 rows (device, row stride ld, already offset to the pool's first column)
+// into pages, starting at logical row `row0` of the page set `set`.
+int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
+                          const float* src_dev, int64_t n_rows, int64_t ld);
+// V_lr rows = X * A for one layer, written into the LR pages of `set` from logical row `row0`.
+int launch_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer, int64_t set,
+                      int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld);
+// De-paginate rows [row0, row0+n_rows) into a dense float32 device matrix.
+int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
+                       int64_t n_rows, float* dst_dev);
+
+// fla_paged_simt.cu ---------------------------------------------------------------------------
+struct PagedAttnCall {
+  lorakv_pool* pool;
+  const lorakv_adapters* adapters;  // may be null when rank == 0
+  int64_t layer_begin, layer_end;
+  int64_t kv_set, lr_set;           // page sets to read (0 for the shared schemes)
+  const int32_t* agent_ids_dev;     // [n_batch] which B table / scale each batch entry uses
+  int64_t n_batch;                  // decode: batch entries; prefill: 1
+  int64_t rows_per_entry;           // decode: 1; prefill: L_c
+  int64_t query_offset;             // position of row 0 of every entry
+  int64_t n_q_local;                // q heads held by this pool
+  int64_t L;                        // cached rows visible to the kernel (min over K, V, LR buffers)
+  const float* q_dev;               // [layers][n_batch][rows_per_entry][n_q_local*d]
+  float* out_dev;                   // same shape
+};
+int launch_paged_simt(const PagedAttnCall& call);
+
+// fla_decode_umma.cu (tcgen05 / TMA) -------------------------------------------------------------
+bool decode_umma_supported(const PagedAttnCall& call);
+int launch_decode_umma(const PagedAttnCall& call);
+
+}  // namespace lk

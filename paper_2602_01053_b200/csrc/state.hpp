@@ -1,0 +1,123 @@
+// state.hpp -- host-side state behind the C ABI (include/lorakv_b200.h).
+//
+// lorakv_ctx      : device, stream, scratch buffers, launch counter
+// lorakv_pool     : paged HBM cache of one trajectory + the integer bookkeeping of the reference's
+//                   KvStore<T> (proj/include/lorakv/kvcache.hpp:213-420), kept on the host
+// lorakv_adapters : shared A per layer, per-agent B tables (proj/include/lorakv/lora.hpp:13-87)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "lorakv_b200.h"
+
+namespace lk {
+
+// ---- errors: status code + thread-local message (the reference throws, matrix.hpp:17-19) ----
+std::string& err_slot();
+int fail(const char* fmt, ...);
+
+#define LK_CUDA(expr)                                                                      \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return lk::fail("CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__, __LINE__, \
+                      cudaGetErrorString(e_));                                             \
+  } while (0)
+
+#define LK_TRY(expr)            \
+  do {                          \
+    int rc_ = (expr);           \
+    if (rc_ != LORAKV_OK) return rc_; \
+  } while (0)
+
+struct Scratch {            // grow-only device buffer
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace lk
+
+struct lorakv_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  int sm_count = 0;
+  int64_t launches = 0;
+  int policy = 0;
+  const char* last_kernel = "none";
+  lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
+  void* pinned = nullptr;             // small pinned staging buffer
+  size_t pinned_bytes = 0;
+  void* tma_encode = nullptr;         // cuTensorMapEncodeTiled, resolved through the runtime
+};
+
+namespace lk {
+
+int scratch_reserve(lorakv_ctx* ctx, Scratch& s, size_t bytes);
+int pinned_reserve(lorakv_ctx* ctx, size_t bytes);
+
+// One page space: page ids handed out in first-touch order to the logical pages of its sets.
+struct PageSpace {
+  int64_t n_sets = 0, max_pages = 0;          // logical pages per set
+  int32_t next_free = 0;
+  std::vector<std::vector<int32_t>> table;    // [set][logical page] -> physical page
+  int32_t* dev_table = nullptr;               // [n_sets][max_pages], mirrors `table`
+  int64_t total_pages() const { return n_sets * max_pages; }
+};
+
+}  // namespace lk
+
+struct lorakv_pool {
+  lorakv_ctx* ctx = nullptr;
+  lorakv_pool_dims dims{};
+  int64_t P = 64;            // page_tokens
+  int64_t r_pad = 0;         // LR row width in HBM (rank rounded up to 8 elements; 0 when rank == 0)
+  int64_t elem = 4;          // bytes per stored element
+  int64_t n_kv_local = 0;
+  int64_t length = 0;        // KvStore::length_
+  std::vector<int64_t> seen; // KvStore::seen_
+  // row counts of every logical buffer (GrowMat::rows): [set][layer]
+  std::vector<std::vector<int64_t>> key_rows, value_rows, lr_rows;
+  lk::PageSpace kv_space, lr_space;
+  void* k_pages = nullptr;   // [n_layers][n_kv_local][kv_total_pages][P][d]
+  void* v_pages = nullptr;
+  void* lr_pages = nullptr;  // [n_layers][lr_total_pages][P][r_pad]
+  uint64_t reserved_bytes = 0;
+  // cached TMA descriptors (built lazily by the tcgen05 paths); opaque 128-byte blobs
+  alignas(64) unsigned char tmap_k[128];
+  alignas(64) unsigned char tmap_v[128];
+  alignas(64) unsigned char tmap_lr[128];
+  bool tmaps_ready = false;
+
+  int64_t kv_sets() const { return dims.scheme == LORAKV_NONSHARED ? dims.n_agents : 1; }
+  int64_t lr_sets() const {
+    if (dims.scheme == LORAKV_BASESHARED) return dims.n_agents;
+    if (dims.scheme == LORAKV_BASELRSHARED) return 1;
+    return 0;
+  }
+  int64_t d_kv_local() const { return n_kv_local * dims.d_head; }
+  // element strides of the page arrays
+  int64_t kv_page_stride() const { return P * dims.d_head; }
+  int64_t kv_head_stride() const { return kv_space.total_pages() * kv_page_stride(); }
+  int64_t kv_layer_stride() const { return n_kv_local * kv_head_stride(); }
+  int64_t lr_page_stride() const { return P * r_pad; }
+  int64_t lr_layer_stride() const { return lr_space.total_pages() * lr_page_stride(); }
+};
+
+struct lorakv_adapters {
+  lorakv_ctx* ctx = nullptr;
+  int64_t n_layers = 0, n_agents = 0, d_model = 0, rank = 0, n_kv_heads = 0, d_head = 0;
+  int64_t kv_head_begin = 0, n_kv_local = 0;
+  int dtype = LORAKV_F32;
+  float* a = nullptr;      // [n_layers][d_model][rank] float32 (values already representable in dtype)
+  float* b = nullptr;      // [n_layers][n_agents][rank][n_kv_local*d_head] float32
+  float* scale = nullptr;  // [n_layers][n_agents] device copy of alpha/rank
+  std::vector<float> scale_host;
+  std::vector<uint8_t> a_set, b_set;
+};

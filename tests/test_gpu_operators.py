@@ -1,0 +1,170 @@
+"""Parity of the CUDA per-head operators (called through the C ABI) with the CPU oracle.
+Mirrors the reference's tests/test_attention.cpp and the kernel fuzz (fuzz.hpp).  Needs a B200."""
+import numpy as np
+import pytest
+
+from tests.cases import BLOCKS, fuzz_cases, random_case
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-4, np.float64: 1e-10}   # cli.cpp:94,103 / acceptance.cpp:70-83
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2602_01053_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("dtype,seed,n_cases", [(np.float64, 7001, 40), (np.float32, 7002, 40),
+                                                (np.float64, 20250810, 120), (np.float32, 20250811, 120)])
+def test_kernel_fuzz_against_oracle(ctx, orc, dtype, seed, n_cases):
+    """fuzz.hpp:25-72 with the device kernels in place of the blocked CPU kernels.  The device result
+    does not depend on (b_r, b_c); the oracle side still sweeps tilings for one case in eight."""
+    worst = 0.0
+    for n, c in enumerate(fuzz_cases(orc, seed, n_cases, 64, dtype)):
+        expected = orc.naive_attention(*c)
+        got = ctx.flash_lora_attention(*c)
+        worst = max(worst, orc.max_rel_error(got, expected))
+        worst = max(worst, orc.max_rel_error(ctx.expand_first_attention(*c), expected))
+        worst = max(worst, orc.max_rel_error(ctx.naive_attention(*c), expected))
+        if n % 8 == 0:
+            for br in BLOCKS:
+                for bc in BLOCKS:
+                    assert orc.max_rel_error(got, orc.flash_lora_attention(*c, br, bc)) <= TOL[dtype]
+    assert worst <= TOL[dtype], worst
+
+
+@pytest.mark.parametrize("tag,dtype", [("f64", np.float64), ("f32", np.float32)])
+def test_known_answers_from_reference(ctx, orc, golden, tag, dtype):
+    att = golden["attention"]
+    for c in golden["tables"]["attention_cases"]:
+        args = random_case(orc, c["L"], c["L_c"], c["d"], c["r"], c["offset"], c["seed"], dtype)
+        key = f"{c['name']}_{tag}"
+        out, rmax, rden = ctx.flash_lora_attention(*args, stats=True)
+        assert orc.max_rel_error(out, att[key + "_naive"]) <= TOL[dtype]
+        assert orc.max_rel_error(out, att[key + "_flash"]) <= TOL[dtype]
+        assert orc.max_rel_error(ctx.expand_first_attention(*args), att[key + "_expand"]) <= TOL[dtype]
+        # OnlineSoftmaxStats (test_attention.cpp:196-215)
+        np.testing.assert_allclose(rmax, att[key + "_rowmax"], rtol=1e-5 if dtype == np.float32 else 1e-12, atol=1e-6 if dtype == np.float32 else 1e-13)
+        np.testing.assert_allclose(rden, att[key + "_rowdenom"], rtol=1e-4 if dtype == np.float32 else 1e-10)
+
+
+def test_single_token_and_first_row(ctx, orc):
+    """test_attention.cpp:75-85,120-128."""
+    c = random_case(orc, 1, 1, 8, 2, 0, 31, np.float64)
+    got = ctx.flash_lora_attention(*c)
+    want = c[2][0] + 0.5 * (c[3][0] @ c[4])
+    np.testing.assert_allclose(got[0], want, rtol=1e-13)
+    c = random_case(orc, 4, 4, 4, 2, 0, 53, np.float64)
+    got = ctx.flash_lora_attention(*c)
+    np.testing.assert_allclose(got[0], c[2][0] + 0.5 * (c[3][0] @ c[4]), rtol=1e-13)
+
+
+def test_uniform_weights(ctx, orc):
+    """test_attention.cpp:101-118: zero query -> row mean of the expanded values."""
+    L, d, r = 4, 4, 2
+    c = random_case(orc, L, 1, d, r, L - 1, 47, np.float64)
+    c[0][:] = 0.0
+    got = ctx.flash_lora_attention(*c)
+    want = (c[2] + 0.5 * (c[3] @ c[4])).mean(axis=0)
+    np.testing.assert_allclose(got[0], want, rtol=1e-13)
+
+
+def test_masked_positions_contribute_exactly_zero(ctx, orc):
+    """test_attention.cpp:144-175: keys past the causal boundary carry 1e6; the result must be
+    bit-identical to the same inputs truncated to the visible prefix."""
+    L, L_c, d, r, off = 24, 6, 8, 2, 9
+    for dtype in (np.float64, np.float32):
+        c = random_case(orc, L, L_c, d, r, off, 977, dtype)
+        c[1][off + L_c:, :] = 1e6
+        c[2][off + L_c:, :] = 1e6
+        vis = off + L_c
+        full = ctx.flash_lora_attention(*c)
+        trunc = ctx.flash_lora_attention(c[0], c[1][:vis].copy(), c[2][:vis].copy(), c[3][:vis].copy(), c[4], 0.5, off)
+        assert orc.max_abs_diff(full, trunc) == 0.0
+        assert orc.max_rel_error(full, orc.naive_attention(c[0], c[1][:vis], c[2][:vis], c[3][:vis], c[4], 0.5, off)) <= TOL[dtype]
+
+
+def test_rank_zero_is_plain_attention(ctx, orc):
+    """test_attention.cpp:266-272."""
+    from paper_2602_01053_b200 import abi
+    c = random_case(orc, 16, 6, 8, 0, 10, 127, np.float64)
+    assert orc.max_rel_error(ctx.flash_lora_attention(*c), orc.naive_attention(*c)) <= 1e-12
+    assert abi.attn_macs(6, 16, 8, 0)[2] == 0
+
+
+def test_mac_counters_match_reference_instrumentation(orc):
+    """test_attention.cpp:217-257: AttnMacs are tiling-independent closed forms; the C ABI computes
+    them on the host.  Checked against the oracle's instrumented counters on random tilings."""
+    from paper_2602_01053_b200 import abi
+    assert abi.lr_mac_counts(4096, 1, 8, 128) == (4718592, 33792)
+    u = orc.u64(97, 24 * 6)
+    for t in range(24):
+        L = 1 + int(u[6 * t] % np.uint64(50)); L_c = 1 + int(u[6 * t + 1] % np.uint64(L))
+        d = 4 + int(u[6 * t + 2] % np.uint64(12)); r = 1 + int(u[6 * t + 3] % np.uint64(6))
+        br = 1 + int(u[6 * t + 4] % np.uint64(16)); bc = 1 + int(u[6 * t + 5] % np.uint64(16))
+        c = random_case(orc, L, L_c, d, r, L - L_c, 1000 + t, np.float64)
+        _, macs = orc.flash_lora_attention(*c, br, bc, want_macs=True)
+        _, emacs = orc.expand_first_attention(*c, br, bc, want_macs=True)
+        assert abi.attn_macs(L_c, L, d, r) == macs
+        assert abi.attn_macs(L_c, L, d, r, expand_first=True) == emacs
+        assert abi.lr_mac_counts(L, L_c, r, d) == (emacs[2], macs[2])
+
+
+def test_bad_shapes_are_rejected(ctx, orc):
+    """test_attention.cpp:274-284."""
+    from paper_2602_01053_b200 import LorakvError
+    bad = random_case(orc, 8, 4, 4, 2, 5, 137, np.float64)   # offset + L_c > L
+    with pytest.raises(LorakvError, match="exceeds L"):
+        ctx.flash_lora_attention(*bad)
+    mism = random_case(orc, 8, 4, 4, 2, 4, 139, np.float64)
+    mism[3] = np.zeros((7, 2))
+    with pytest.raises(LorakvError):
+        ctx.flash_lora_attention(*mism)
+    with pytest.raises(LorakvError, match="not divisible"):
+        z = lambda r_, c_: np.zeros((r_, c_))
+        ctx.gqa_attention(z(2, 12), z(4, 8), z(4, 8), z(4, 0), z(0, 8), 1.0, 2, 3, 2)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_gqa_head_mapping(ctx, orc, golden, dtype):
+    """test_attention.cpp:286-363."""
+    L, L_c, d_head, r = 12, 5, 4, 2
+    tag = "f64" if dtype == np.float64 else "f32"
+    for seed, n_q, n_kv in ((149, 3, 3), (151, 4, 2)):
+        g = lambda rows, cols, key: orc.gaussian(rows, cols, orc.child(seed, key), 1.0, dtype)
+        q, k, v = g(L_c, n_q * d_head, 1), g(L, n_kv * d_head, 2), g(L, n_kv * d_head, 3)
+        v_lr, b_up = g(L, r, 4), g(r, n_kv * d_head, 5)
+        got = ctx.gqa_attention(q, k, v, v_lr, b_up, 0.5, L - L_c, n_q, n_kv)
+        assert orc.max_rel_error(got, golden["attention"][f"gqa_{seed}_{tag}"]) <= TOL[dtype]
+        # per-head calls on column slices give the same bits as the fused launch
+        group = n_q // n_kv
+        for h in range(n_q):
+            kv = h // group
+            head = ctx.flash_lora_attention(q[:, h * d_head:(h + 1) * d_head], k[:, kv * d_head:(kv + 1) * d_head],
+                                            v[:, kv * d_head:(kv + 1) * d_head], v_lr,
+                                            b_up[:, kv * d_head:(kv + 1) * d_head], 0.5, L - L_c)
+            assert np.array_equal(got[:, h * d_head:(h + 1) * d_head], head)
+        # grouped heads == kv-duplication oracle, exactly
+        if n_q != n_kv:
+            rep = lambda m: np.concatenate([m[:, (h // group) * d_head:(h // group + 1) * d_head] for h in range(n_q)], axis=1)
+            mha = ctx.gqa_attention(q, rep(k), rep(v), v_lr, rep(b_up), 0.5, L - L_c, n_q, n_q)
+            assert orc.max_abs_diff(got, mha) == 0.0
+
+
+def test_larger_shapes_and_split_keys(ctx, orc):
+    """Shapes beyond the reference's fuzz range (d=128, r=16, thousands of keys) so that the
+    split-key path and the merge are exercised; oracle = naive_attention in float64."""
+    for (L, L_c, d, r, off, seed) in ((4096, 1, 128, 16, 4095, 1), (3000, 7, 128, 16, 2993, 2),
+                                      (2500, 300, 64, 8, 1100, 3), (1537, 64, 256, 128, 1000, 4)):
+        c64 = random_case(orc, L, L_c, d, r, off, seed, np.float64)
+        c64[0] *= 1.0 / np.sqrt(d) ** 0.5
+        want = orc.naive_attention(*c64)
+        got64 = ctx.flash_lora_attention(*c64)
+        assert orc.max_rel_error(got64, want) <= 1e-10
+        c32 = [a.astype(np.float32) if isinstance(a, np.ndarray) else a for a in c64]
+        got32 = ctx.flash_lora_attention(*c32)
+        assert orc.max_rel_error(got32.astype(np.float64), want) <= 1e-4

@@ -276,14 +276,15 @@ def main():
     if rank == 0:
         sampler.start()
     launches0 = ctx.launch_count
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # events are recorded by the library on the stream its kernels launch on (lorakv_event_record)
+    ev0, ev1 = ctx.event(), ctx.event()
     barrier()
     ev0.record()
     for _ in range(args.steps):
         step_device()
     ev1.record()
+    ms = ev0.elapsed_ms(ev1) / args.steps
     barrier()
-    ms = ev0.elapsed_time(ev1) / args.steps
     launches = ctx.launch_count - launches0
     if world > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -294,12 +295,11 @@ def main():
     # ---- dominant-kernel duration for the roofline: events around the attention launch only ----------
     k_ms = []
     for _ in range(min(args.steps, 10)):
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0, a1 = ctx.event(), ctx.event()
         a0.record()
         pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
         a1.record()
-        torch.cuda.synchronize()
-        k_ms.append(a0.elapsed_time(a1))
+        k_ms.append(a0.elapsed_ms(a1))
     kernel_ms = statistics.median(k_ms)
     clocks = sampler.stop() if rank == 0 else None
 

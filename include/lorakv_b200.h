@@ -64,6 +64,14 @@ int lorakv_copy_h2d(lorakv_ctx* ctx, void* dst_dev, const void* src_host, int64_
 int lorakv_copy_d2h(lorakv_ctx* ctx, void* dst_host, const void* src_dev, int64_t bytes); /* async on ctx stream */
 /* writes `bytes` of a scratch buffer (> L2) so that the next kernel starts with a cold L2 */
 int lorakv_flush_l2(lorakv_ctx* ctx);
+/* CUDA events recorded on the ctx stream -- the stream every kernel of this library launches on --
+ * so a caller can time the library on the device without linking the CUDA runtime.
+ * lorakv_event_elapsed_ms waits for `stop` and returns the device time between the two records. */
+typedef struct lorakv_event lorakv_event;
+int lorakv_event_create(lorakv_ctx* ctx, lorakv_event** out);
+int lorakv_event_record(lorakv_ctx* ctx, lorakv_event* ev);
+int lorakv_event_elapsed_ms(lorakv_event* start, lorakv_event* stop, float* ms);
+void lorakv_event_destroy(lorakv_event* ev);
 
 /* ---- per-head operators over caller memory (HOST pointers) ----------------------------------
  * flash_lora_attention<T>, attention.hpp:210-268.  q: L_c x d, k/v_base: L x d, v_lr: L x r,

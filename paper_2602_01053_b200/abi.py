@@ -75,6 +75,10 @@ SIGNATURES = {
     "lorakv_copy_h2d": (C.c_int, [_vp, _vp, _vp, _i64]),
     "lorakv_copy_d2h": (C.c_int, [_vp, _vp, _vp, _i64]),
     "lorakv_flush_l2": (C.c_int, [_vp]),
+    "lorakv_event_create": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "lorakv_event_record": (C.c_int, [_vp, _vp]),
+    "lorakv_event_elapsed_ms": (C.c_int, [_vp, _vp, C.POINTER(C.c_float)]),
+    "lorakv_event_destroy": (None, [_vp]),
     "lorakv_fla_forward_f32": (C.c_int, _attn_sig(_f, _pf, True)),
     "lorakv_fla_forward_f64": (C.c_int, _attn_sig(_d, _pd, True)),
     "lorakv_expand_first_forward_f32": (C.c_int, _attn_sig(_f, _pf, False)),
@@ -195,6 +199,10 @@ class Context:
     def flush_l2(self):
         _check(self.lib.lorakv_flush_l2(self.h))
 
+    # device timing on the ctx stream -----------------------------------------------------------
+    def event(self) -> "Event":
+        return Event(self)
+
     # raw buffers -----------------------------------------------------------------------------
     def dev_alloc(self, nbytes: int) -> int:
         p = _vp()
@@ -278,6 +286,33 @@ class Context:
             self.h, *args, T(lr_scale), q.shape[0], L, n_q, n_kv, d, r, query_offset,
             out.ctypes.data_as(C.POINTER(T))))
         return out
+
+
+class Event:
+    """lorakv_event: a CUDA event recorded on the ctx stream (the stream the kernels launch on)."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+        h = _vp()
+        _check(ctx.lib.lorakv_event_create(ctx.h, C.byref(h)))
+        self.h = h
+
+    def record(self):
+        _check(self.ctx.lib.lorakv_event_record(self.ctx.h, self.h))
+        return self
+
+    def elapsed_ms(self, stop: "Event") -> float:
+        ms = C.c_float()
+        _check(self.ctx.lib.lorakv_event_elapsed_ms(self.h, stop.h, C.byref(ms)))
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.lorakv_event_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
 
 
 def lr_mac_counts(L, L_c, r, d):

@@ -208,6 +208,34 @@ int lorakv_flush_l2(lorakv_ctx* ctx) {
   return LORAKV_OK;
 }
 
+struct lorakv_event { cudaEvent_t ev; };
+int lorakv_event_create(lorakv_ctx* ctx, lorakv_event** out) {
+  if (!ctx || !out) return fail("event_create: null argument");
+  LK_CUDA(cudaSetDevice(ctx->device));
+  lorakv_event* e = new (std::nothrow) lorakv_event();
+  if (!e) return fail("event_create: out of host memory");
+  cudaError_t ce = cudaEventCreate(&e->ev);
+  if (ce != cudaSuccess) { delete e; return fail("event_create: %s", cudaGetErrorString(ce)); }
+  *out = e;
+  return LORAKV_OK;
+}
+int lorakv_event_record(lorakv_ctx* ctx, lorakv_event* ev) {
+  if (!ctx || !ev) return fail("event_record: null argument");
+  LK_CUDA(cudaEventRecord(ev->ev, ctx->stream));
+  return LORAKV_OK;
+}
+int lorakv_event_elapsed_ms(lorakv_event* start, lorakv_event* stop, float* ms) {
+  if (!start || !stop || !ms) return fail("event_elapsed_ms: null argument");
+  LK_CUDA(cudaEventSynchronize(stop->ev));
+  LK_CUDA(cudaEventElapsedTime(ms, start->ev, stop->ev));
+  return LORAKV_OK;
+}
+void lorakv_event_destroy(lorakv_event* ev) {
+  if (!ev) return;
+  cudaEventDestroy(ev->ev);
+  delete ev;
+}
+
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy) {
   if (!ctx) return 0;
   const int old = ctx->policy;

@@ -343,7 +343,14 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   }
   p->elem = dims->dtype == LORAKV_BF16 ? 2 : 4;
   const bool has_lr = p->lr_sets() > 0 && dims->rank > 0;
-  p->r_pad = has_lr ? (dims->rank + 7) / 8 * 8 : 0;
+  // LR row width in HBM: the rank padded with zero columns (exact) to 8/16/32/64 or a multiple of
+  // 64, the widths page_layout.cuh can swizzle
+  p->r_pad = 0;
+  if (has_lr) {
+    p->r_pad = 8;
+    while (p->r_pad < dims->rank && p->r_pad < 64) p->r_pad *= 2;
+    if (p->r_pad < dims->rank) p->r_pad = (dims->rank + 63) / 64 * 64;
+  }
   p->seen.assign((size_t)dims->n_agents, 0);
   const int64_t max_pages = (dims->max_tokens + p->P - 1) / p->P;
   p->dims.max_tokens = max_pages * p->P;
@@ -721,7 +728,7 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   call.kv_set = kv_set; call.lr_set = lr_set; call.agent_ids_dev = ids_dev; call.n_batch = n_batch;
   call.rows_per_entry = rows_per_entry; call.query_offset = query_offset; call.n_q_local = n_q_local;
   call.L = L; call.q_dev = q_dev; call.out_dev = out_dev;
-  if (ctx->policy == 0 && decode_umma_supported(call)) LK_TRY(launch_decode_umma(call));
+  if (ctx->policy == 0 && decode_tma_supported(call)) LK_TRY(launch_decode_tma(call));
   else LK_TRY(launch_paged_simt(call));
 
   if (host) {

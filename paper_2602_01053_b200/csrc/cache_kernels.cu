@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 
 #include "kernels.hpp"
+#include "page_layout.cuh"
 #include "state.hpp"
 
 namespace lk {
@@ -25,6 +26,7 @@ struct PageAddr {
   int P, width;             // tokens per page; elements per row within one head (d or r_pad)
   int n_heads;              // heads in a source row (1 for LR)
   int src_cols;             // valid source columns per head (d or rank); the rest is zero padding
+  PageLayout lay;           // element placement inside one page (page_layout.cuh)
 };
 
 template <class S> __device__ __forceinline__ S to_store(float x);
@@ -58,7 +60,7 @@ __global__ void kv_append_scatter_kernel(PageAddr a, int64_t row0, const float* 
   const int64_t row = row0 + i;
   const int64_t phys = a.table[row / a.P];
   S* dst = static_cast<S*>(a.base) + (int64_t)head * a.head_stride + phys * a.page_stride +
-           (row % a.P) * a.width + c;
+           page_offset(a.lay, (int)(row % a.P), c);
   if (sizeof(S) == 2) {
     __nv_bfloat162 p0 = __floats2bfloat162_rn(x[0], x[1]), p1 = __floats2bfloat162_rn(x[2], x[3]);
     __nv_bfloat162 p2 = __floats2bfloat162_rn(x[4], x[5]), p3 = __floats2bfloat162_rn(x[6], x[7]);
@@ -86,7 +88,7 @@ __global__ void kv_append_scatter_scalar_kernel(PageAddr a, int64_t row0, const 
   const float x = c < a.src_cols ? src[i * ld + (int64_t)head * a.src_cols + c] : 0.f;
   const int64_t row = row0 + i;
   const int64_t phys = a.table[row / a.P];
-  static_cast<S*>(a.base)[(int64_t)head * a.head_stride + phys * a.page_stride + (row % a.P) * a.width + c] = to_store<S>(x);
+  static_cast<S*>(a.base)[(int64_t)head * a.head_stride + phys * a.page_stride + page_offset(a.lay, (int)(row % a.P), c)] = to_store<S>(x);
 }
 
 template <class S>
@@ -100,7 +102,7 @@ __global__ void gather_rows_kernel(PageAddr a, int64_t row0, int64_t n_rows, flo
   const int64_t row = row0 + i;
   const int64_t phys = a.table[row / a.P];
   dst[idx] = from_store<S>(static_cast<const S*>(a.base)[(int64_t)head * a.head_stride + phys * a.page_stride +
-                                                        (row % a.P) * a.width + c]);
+                                                        page_offset(a.lay, (int)(row % a.P), c)]);
 }
 
 // V_lr = X * A on CUDA cores: a 64-row x r_pad tile per CTA, K staged through shared memory in
@@ -150,11 +152,12 @@ __global__ void __launch_bounds__(kProjThreads) lr_append_project_kernel(
   if (i >= n_rows) return;
   const int64_t row = row0 + i;
   const int64_t phys = a.table[row / a.P];
-  S* dst = static_cast<S*>(a.base) + phys * a.page_stride + (row % a.P) * rp;
+  S* dst = static_cast<S*>(a.base) + phys * a.page_stride;
+  const int t = (int)(row % a.P);
 #pragma unroll
   for (int u = 0; u < 32; ++u) {
     const int c = cg + 4 * u;
-    if (c < rp) dst[c] = to_store<S>(c < rank ? acc[u] : 0.f);
+    if (c < rp) dst[page_offset(a.lay, t, c)] = to_store<S>(c < rank ? acc[u] : 0.f);
   }
 }
 
@@ -180,6 +183,7 @@ PageAddr make_addr(const lorakv_pool* pool, int which, int64_t layer, int64_t se
     a.src_cols = (int)pool->dims.d_head;
   }
   a.P = (int)pool->P;
+  a.lay = make_page_layout(a.P, a.width, (int)elem);
   return a;
 }
 

@@ -1,0 +1,548 @@
+// fla_decode_tma.cu -- batched Flash-LoRA-Attention decode over the paged bf16 cache, tuned for HBM
+// bandwidth: K / V_base / V_lr tiles are streamed from HBM into shared memory by the TMA engine
+// (cp.async.bulk + mbarrier rings, one ring per worker), the contractions run on the tensor cores
+// (mma.sync m16n8k16 bf16 -> fp32) and the softmax bookkeeping uses warp-level reductions.
+//
+// What it computes: one gqa_attention call (proj/include/lorakv/attention.hpp:332-363) per (layer,
+// batch entry) with query_offset = L-1 (engine.hpp:440-443), i.e. per q head the blocked
+// flash_lora_attention of attention.hpp:210-268 -- but reordered so that the cache is read ONCE:
+// the g q heads of a kv head and all batch entries (agents) are rows of the same MMA tile, where the
+// reference's per-head loop (:347-361) re-streams K/V for every q head and every agent.
+//
+//   worker   = MW warps (MW = 1/2/4/8 for <= 16/32/64/128 query rows per kv head); warp i of a worker
+//              owns rows [16 i, 16 i + 16) and every worker owns its own ring of shared-memory stages
+//   work     = the (unit, 16-key tile) pairs in unit-major order, cut into equal contiguous ranges,
+//              one per worker (unit = layer x kv head [x 128-row block]); a worker emits one partial
+//              (m, l, O, O_lr) per unit its range touches and fla_decode_merge combines them
+//   per tile = S = Q K^T (8 k-steps), online softmax in the exp2 domain with lazy rescaling,
+//              O += P V_base and O_lr += P V_lr with the same P (attention.hpp:185-198)
+//   epilogue = fla_decode_merge: split merge, o += (lr_scale * o_lr[p]) * B[agent][p,:], out = o / l
+//              (attention.hpp:244-259)
+//
+// Pages arrive pre-swizzled (page_layout.cuh), so a contiguous bulk copy of 16 tokens lands as a
+// bank-conflict-free ldmatrix tile.  Masking: key j contributes iff j < L; masked scores are never
+// exponentiated (p = 0 exactly), matching attention.hpp:154-171.
+#include <cuda_bf16.h>
+
+#include <limits>
+
+#include "kernels.hpp"
+#include "page_layout.cuh"
+#include "state.hpp"
+#include "umma.cuh"
+
+namespace lk {
+
+namespace {
+
+constexpr int kWarps = 8;           // warps per CTA
+constexpr int kTK = 16;             // keys per tile
+constexpr int kMaxStages = 24;      // ring depth limit per worker
+constexpr int kRingBudget = 216 * 1024;   // of the 227 KB a CTA may own
+constexpr float kRescaleThreshold = 8.0f;   // log2 units: p stays <= 2^8 between rescales
+
+struct DecodeParams {
+  const __nv_bfloat16 *k_pages, *v_pages, *lr_pages;
+  const int32_t *kv_table, *lr_table;
+  int64_t kv_layer_stride, kv_head_stride, kv_page_stride, lr_layer_stride, lr_page_stride;  // elements
+  int P, group, n_kv_local, n_batch, rows_total, row_blocks, n_pages;
+  int64_t L, layer_begin, n_q_local;
+  int64_t T;             // tiles per unit
+  int64_t total_tiles;   // units * T
+  int64_t G;             // tiles per worker
+  int max_seg, n_stages;
+  float scale_log2;      // (1/sqrt(d)) * log2(e)
+  const float* q;        // [layers][n_batch][n_q_local * d]
+  float* part;           // [workers * max_seg][16 * MW][4 + D + RP]
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// D = d_head (64 / 128), RP = padded rank (0 / 8 / 16 / 32 / 64), MW = warps per worker
+template <int D, int RP, int MW>
+__global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
+  constexpr int kWorkers = kWarps / MW;
+  constexpr int kBlocks = D / 64;                       // 64-column blocks of a K / V page
+  constexpr uint32_t kBlockBytes = kTK * 128;           // one block of one tile
+  constexpr uint32_t kKvBytes = kBlocks * kBlockBytes;  // K (or V) tile
+  constexpr uint32_t kLrBytes = kTK * RP * 2;
+  constexpr uint32_t kStageBytes = 2 * kKvBytes + kLrBytes;
+  constexpr int kNO = D / 8, kNL = RP / 8;              // n8 tiles of O and O_lr
+  constexpr int PS = 4 + D + RP;                        // floats per partial row
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full_bar[kWorkers][kMaxStages];
+  __shared__ uint64_t empty_bar[kWorkers][kMaxStages];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wk = warp / MW, wi = warp % MW;
+  const int g = lane >> 2, t = lane & 3;
+  const int NS = p.n_stages;
+
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < kWorkers; ++a)
+      for (int s = 0; s < NS; ++s) {
+        ptx::mbar_init(&full_bar[a][s], 1);
+        ptx::mbar_init(&empty_bar[a][s], MW);
+      }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int64_t w = (int64_t)blockIdx.x * kWorkers + wk;
+  const int64_t g0 = w * p.G;
+  const int64_t g1 = min(g0 + p.G, p.total_tiles);
+  const int n = g1 > g0 ? (int)(g1 - g0) : 0;
+  if (n == 0) return;
+
+  const uint32_t ring = ptx::smem_u32(smem) + (uint32_t)wk * (uint32_t)NS * kStageBytes;
+  uint64_t* full = full_bar[wk];
+  uint64_t* empty = empty_bar[wk];
+  const bool producer = wi == 0;
+  const int units_per_layer = p.n_kv_local * p.row_blocks;
+
+  // page-table window held across the lanes of the producer warp: lane i caches logical page base + i
+  int win_base = -(1 << 30), win_kv = 0, win_lr = 0;
+
+  auto issue = [&](int i) {       // whole producer warp; lane 0 talks to the TMA engine
+    const int64_t gt = g0 + i;
+    const int64_t u = gt / p.T;
+    const int tl = (int)(gt - u * p.T);
+    const int layer_rel = (int)(u / units_per_layer);
+    const int kvh = (int)((u / p.row_blocks) % p.n_kv_local);
+    const int key0 = tl * kTK;
+    const int page = key0 / p.P, tok0 = key0 % p.P;
+    if (page < win_base || page >= win_base + 32) {
+      win_base = page;
+      const int pg = page + lane;
+      win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
+      if (RP > 0) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
+    }
+    const int phys_kv = __shfl_sync(0xffffffffu, win_kv, page - win_base);
+    const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, page - win_base) : 0;
+    if (lane == 0) {
+      const int s = i % NS;
+      const uint32_t dst = ring + (uint32_t)s * kStageBytes;
+      const int64_t layer = p.layer_begin + layer_rel;
+      const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)kvh * p.kv_head_stride +
+                             (int64_t)phys_kv * p.kv_page_stride + (int64_t)tok0 * 64;
+      ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
+#pragma unroll
+      for (int b = 0; b < kBlocks; ++b) {
+        bulk_g2s(dst + b * kBlockBytes, p.k_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[s]);
+        bulk_g2s(dst + kKvBytes + b * kBlockBytes, p.v_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[s]);
+      }
+      if (RP > 0) {
+        const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)tok0 * RP;
+        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[s]);
+      }
+    }
+  };
+
+  if (producer) {
+    const int pre = n < NS ? n : NS;
+    for (int i = 0; i < pre; ++i) issue(i);
+  }
+
+  const float ninf = -std::numeric_limits<float>::infinity();
+  uint32_t qa[D / 16][4];
+  float o[kNO][4];
+  float olr[kNL > 0 ? kNL : 1][4];
+  float m_used[2], l_run[2];
+  int64_t cur_unit = -1;
+
+  auto flush = [&]() {            // partial of the unit just finished
+    const int64_t first_unit = g0 / p.T;
+    const int64_t slot = w * p.max_seg + (cur_unit - first_unit);
+    float* base = p.part + (slot * (16 * MW) + wi * 16) * PS;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float l = l_run[h];
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      float* row = base + (g + 8 * h) * PS;
+      if (t == 0) { row[0] = m_used[h]; row[1] = l; }
+#pragma unroll
+      for (int nt = 0; nt < kNO; ++nt)
+        *reinterpret_cast<float2*>(row + 4 + 8 * nt + 2 * t) = make_float2(o[nt][2 * h], o[nt][2 * h + 1]);
+#pragma unroll
+      for (int nt = 0; nt < kNL; ++nt)
+        *reinterpret_cast<float2*>(row + 4 + D + 8 * nt + 2 * t) = make_float2(olr[nt][2 * h], olr[nt][2 * h + 1]);
+    }
+  };
+
+  // ldmatrix lane roles
+  const int mi = lane >> 3, rr = lane & 7;
+
+  for (int i = 0; i < n; ++i) {
+    const int64_t gt = g0 + i;
+    const int64_t u = gt / p.T;
+    const int tl = (int)(gt - u * p.T);
+    if (u != cur_unit) {
+      if (cur_unit >= 0) flush();
+      cur_unit = u;
+      const int layer_rel = (int)(u / units_per_layer);
+      const int kvh = (int)((u / p.row_blocks) % p.n_kv_local);
+      const int rb = (int)(u % p.row_blocks);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rho = rb * 16 * MW + wi * 16 + g + 8 * h;
+        const bool real = rho < p.rows_total;
+        const int entry = real ? rho / p.group : 0, gi = real ? rho % p.group : 0;
+        const float* src = p.q + (((int64_t)layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
+          if (real) {
+            lo = __ldg(reinterpret_cast<const float2*>(src + 16 * kk + 2 * t));
+            hi = __ldg(reinterpret_cast<const float2*>(src + 16 * kk + 8 + 2 * t));
+          }
+          qa[kk][h] = pack_bf16(lo.x, lo.y);
+          qa[kk][2 + h] = pack_bf16(hi.x, hi.y);
+        }
+        m_used[h] = ninf; l_run[h] = 0.f;
+      }
+#pragma unroll
+      for (int nt = 0; nt < kNO; ++nt) { o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f; }
+#pragma unroll
+      for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
+    }
+
+    // refill the stage released one iteration ago
+    if (producer && i >= 1 && i - 1 + NS < n) {
+      ptx::mbar_wait(&empty[(i - 1) % NS], (uint32_t)(((i - 1) / NS) & 1));
+      issue(i - 1 + NS);
+    }
+    const int s = i % NS;
+    ptx::mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+
+    const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
+
+    // ---- S = Q K^T : 16 rows x 16 keys ------------------------------------------------------
+    float sc[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+    {
+      const int key = (mi >> 1) * 8 + rr;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const int chunk = 2 * kk + (mi & 1);
+        const uint32_t addr = sK + (uint32_t)(chunk >> 3) * kBlockBytes + (uint32_t)key * 128u +
+                              (uint32_t)(((chunk & 7) ^ rr) << 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(addr, b0, b1, b2, b3);
+        mma_bf16(sc[0], qa[kk], b0, b1);
+        mma_bf16(sc[1], qa[kk], b2, b3);
+      }
+    }
+
+    // ---- online softmax (exp2 domain), rows g and g + 8 ------------------------------------------
+    const int64_t key_base = (int64_t)tl * kTK + 2 * t;
+    bool valid[2][2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) valid[nt][e] = key_base + 8 * nt + e < p.L;
+    float tmax[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float mx = ninf;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float v = valid[nt][e] ? sc[nt][2 * h + e] * p.scale_log2 : ninf;
+          sc[nt][2 * h + e] = v;
+          mx = fmaxf(mx, v);
+        }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      tmax[h] = mx;
+    }
+    const bool grow = tmax[0] > m_used[0] + kRescaleThreshold || tmax[1] > m_used[1] + kRescaleThreshold;
+    if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float m_new = fmaxf(m_used[h], tmax[h]);
+        const float alpha = (m_used[h] == ninf) ? 0.f : ex2(m_used[h] - m_new);
+        m_used[h] = m_new;
+        l_run[h] *= alpha;
+#pragma unroll
+        for (int nt = 0; nt < kNO; ++nt) { o[nt][2 * h] *= alpha; o[nt][2 * h + 1] *= alpha; }
+#pragma unroll
+        for (int nt = 0; nt < kNL; ++nt) { olr[nt][2 * h] *= alpha; olr[nt][2 * h + 1] *= alpha; }
+      }
+    }
+    uint32_t pa[4];
+    {
+      float pv[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float x = valid[nt][e] ? ex2(sc[nt][2 * h + e] - m_used[h]) : 0.f;
+            pv[nt][2 * h + e] = x;
+            l_run[h] += x;
+          }
+      pa[0] = pack_bf16(pv[0][0], pv[0][1]);
+      pa[1] = pack_bf16(pv[0][2], pv[0][3]);
+      pa[2] = pack_bf16(pv[1][0], pv[1][1]);
+      pa[3] = pack_bf16(pv[1][2], pv[1][3]);
+    }
+
+    // ---- O += P V_base, O_lr += P V_lr ---------------------------------------------------------------
+    {
+      const int key = (mi & 1) * 8 + rr;
+#pragma unroll
+      for (int np = 0; np < D / 16; ++np) {
+        const int chunk = 2 * np + (mi >> 1);
+        const uint32_t addr = sV + (uint32_t)(chunk >> 3) * kBlockBytes + (uint32_t)key * 128u +
+                              (uint32_t)(((chunk & 7) ^ rr) << 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(addr, b0, b1, b2, b3);
+        mma_bf16(o[2 * np], pa, b0, b1);
+        mma_bf16(o[2 * np + 1], pa, b2, b3);
+      }
+      if (RP >= 16) {
+#pragma unroll
+        for (int np = 0; np < RP / 16; ++np) {
+          const int chunk = 2 * np + (mi >> 1);
+          uint32_t off = (uint32_t)key * (2u * RP) + (uint32_t)chunk * 16u;
+          off ^= ((off >> 7) & (uint32_t)(RP / 8 - 1)) << 4;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(sLR + off, b0, b1, b2, b3);
+          mma_bf16(olr[2 * np], pa, b0, b1);
+          mma_bf16(olr[2 * np + 1], pa, b2, b3);
+        }
+      } else if (RP == 8) {
+        uint32_t b0, b1;
+        ldsm_x2_t(sLR + (uint32_t)key * 16u, b0, b1);     // lanes 16..31 pass valid, unused addresses
+        mma_bf16(olr[0], pa, b0, b1);
+      }
+    }
+
+    // this warp is done with the stage
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+  }
+  flush();
+}
+
+// ---- merge of the per-worker partials + up-projection epilogue -----------------------------------
+struct DecodeMergeParams {
+  const float* part;
+  int D, RP, r, MW, group, n_kv_local, n_batch, rows_total, row_blocks;
+  int64_t T, G, layer_begin, n_q_local;
+  int max_seg;
+  const int32_t* agent_ids;
+  const float* b;        // [n_layers][n_agents][r][n_kv_local * d]
+  const float* scale;    // [n_layers][n_agents]
+  int64_t n_agents;
+  float* out;            // [layers][n_batch][n_q_local * d]
+};
+
+__global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMergeParams p) {
+  extern __shared__ float sm[];          // [ns] weights, then [r] merged O_lr
+  __shared__ float l_total;
+  const int rho = blockIdx.x;
+  const int kvh = blockIdx.y % p.n_kv_local;
+  const int64_t layer_rel = blockIdx.y / p.n_kv_local;
+  const int rows_blk = 16 * p.MW;
+  const int rb = rho / rows_blk, r_in = rho % rows_blk;
+  const int64_t u = (layer_rel * p.n_kv_local + kvh) * p.row_blocks + rb;
+  const int64_t w_lo = (u * p.T) / p.G, w_hi = ((u + 1) * p.T - 1) / p.G;
+  const int ns = (int)(w_hi - w_lo + 1);
+  const int PS = 4 + p.D + p.RP;
+  float* w_s = sm;
+  float* olr_s = sm + ns;
+  const float ninf = -std::numeric_limits<float>::infinity();
+  auto row_of = [&](int s) -> const float* {
+    const int64_t w = w_lo + s;
+    const int64_t slot = w * p.max_seg + (u - (w * p.G) / p.T);
+    return p.part + (slot * rows_blk + r_in) * PS;
+  };
+  if (threadIdx.x < 32) {
+    float mx = ninf;
+    for (int s = threadIdx.x; s < ns; s += 32) mx = fmaxf(mx, row_of(s)[0]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float l = 0.f;
+    for (int s = threadIdx.x; s < ns; s += 32) {
+      const float* row = row_of(s);
+      const float wgt = (row[0] == ninf) ? 0.f : exp2f(row[0] - mx);
+      w_s[s] = wgt;
+      l += wgt * row[1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (threadIdx.x == 0) l_total = l;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < p.r; c += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < ns; ++s) acc = fmaf(w_s[s], row_of(s)[4 + p.D + c], acc);
+    olr_s[c] = acc;
+  }
+  __syncthreads();
+  const int gi = rho % p.group, entry = rho / p.group;
+  const int64_t layer = p.layer_begin + layer_rel;
+  const int64_t dkv = (int64_t)p.n_kv_local * p.D;
+  const int agent = p.agent_ids ? p.agent_ids[entry] : 0;
+  const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
+  const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
+  float* dst = p.out + ((layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * p.D;
+  const float inv_l = 1.0f / l_total;
+  for (int c = threadIdx.x; c < p.D; c += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < ns; ++s) acc = fmaf(w_s[s], row_of(s)[4 + c], acc);
+    for (int k = 0; k < p.r; ++k) acc = fmaf(scale * olr_s[k], b[k * dkv + c], acc);
+    dst[c] = acc * inv_l;
+  }
+}
+
+template <int D, int RP, int MW>
+int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
+  auto kern = fla_decode_tma_kernel<D, RP, MW>;
+  LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kWarps * 32, smem, ctx->stream>>>(dp);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+template <int D, int RP>
+int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw) {
+  switch (mw) {
+    case 1: return launch_t<D, RP, 1>(ctx, dp, grid, smem);
+    case 2: return launch_t<D, RP, 2>(ctx, dp, grid, smem);
+    case 4: return launch_t<D, RP, 4>(ctx, dp, grid, smem);
+    default: return launch_t<D, RP, 8>(ctx, dp, grid, smem);
+  }
+}
+
+template <int D>
+int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int rp) {
+  switch (rp) {
+    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw);
+    case 8: return launch_mw<D, 8>(ctx, dp, grid, smem, mw);
+    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw);
+    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw);
+    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw);
+  }
+}
+
+}  // namespace
+
+bool decode_tma_supported(const PagedAttnCall& c) {
+  const lorakv_pool* pool = c.pool;
+  const int64_t d = pool->dims.d_head, rp = pool->r_pad;
+  if (pool->dims.dtype != LORAKV_BF16) return false;       // fp32 pages keep the 1e-4 contract on FFMA
+  if (c.rows_per_entry != 1 || c.query_offset != c.L - 1) return false;   // decode only
+  if (d != 64 && d != 128) return false;
+  if (!(rp == 0 || rp == 8 || rp == 16 || rp == 32 || rp == 64)) return false;
+  if (pool->P % kTK != 0) return false;
+  if (c.L < 1 || c.n_batch < 1) return false;
+  return true;
+}
+
+int launch_decode_tma(const PagedAttnCall& c) {
+  lorakv_pool* pool = c.pool;
+  lorakv_ctx* ctx = pool->ctx;
+  const int d = (int)pool->dims.d_head, r = (int)pool->dims.rank, rp = (int)pool->r_pad;
+  const int64_t n_layers = c.layer_end - c.layer_begin;
+  const int group = (int)(c.n_q_local / pool->n_kv_local);
+  const int64_t rows_total = c.n_batch * group;
+  if (r > 0 && !c.adapters) return fail("paged attention: rank %lld cache needs adapter tables", (long long)r);
+
+  int mw = 1;
+  while (16 * mw < rows_total && mw < 8) mw *= 2;
+  const int rows_blk = 16 * mw;
+  const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
+  const int workers_per_cta = kWarps / mw;
+  const uint32_t stage_bytes = kTK * (4 * d + 2 * rp);
+  int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
+  if (n_stages > kMaxStages) n_stages = kMaxStages;
+  const size_t smem = (size_t)workers_per_cta * n_stages * stage_bytes;
+
+  const int64_t T = (c.L + kTK - 1) / kTK;
+  const int64_t units = n_layers * pool->n_kv_local * row_blocks;
+  const int64_t total = units * T;
+  const int64_t max_workers = (int64_t)ctx->sm_count * workers_per_cta;
+  int64_t G = (total + max_workers - 1) / max_workers;
+  if (G < 4) G = 4;
+  const int64_t n_workers = (total + G - 1) / G;
+  const unsigned grid = (unsigned)((n_workers + workers_per_cta - 1) / workers_per_cta);
+  const int max_seg = (int)((G + T - 2) / T + 1);
+  const int PS = 4 + d + rp;
+  const size_t part_bytes = (size_t)grid * workers_per_cta * max_seg * rows_blk * PS * sizeof(float);
+  LK_TRY(scratch_reserve(ctx, ctx->work, part_bytes));
+
+  DecodeParams dp;
+  dp.k_pages = static_cast<const __nv_bfloat16*>(pool->k_pages);
+  dp.v_pages = static_cast<const __nv_bfloat16*>(pool->v_pages);
+  dp.lr_pages = static_cast<const __nv_bfloat16*>(pool->lr_pages);
+  dp.kv_table = pool->kv_space.dev_table + c.kv_set * pool->kv_space.max_pages;
+  dp.lr_table = rp > 0 ? pool->lr_space.dev_table + c.lr_set * pool->lr_space.max_pages : nullptr;
+  dp.kv_layer_stride = pool->kv_layer_stride(); dp.kv_head_stride = pool->kv_head_stride();
+  dp.kv_page_stride = pool->kv_page_stride();
+  dp.lr_layer_stride = pool->lr_layer_stride(); dp.lr_page_stride = pool->lr_page_stride();
+  dp.P = (int)pool->P; dp.group = group; dp.n_kv_local = (int)pool->n_kv_local; dp.n_batch = (int)c.n_batch;
+  dp.rows_total = (int)rows_total; dp.row_blocks = row_blocks;
+  dp.n_pages = (int)((c.L + pool->P - 1) / pool->P);
+  dp.L = c.L; dp.layer_begin = c.layer_begin; dp.n_q_local = c.n_q_local;
+  dp.T = T; dp.total_tiles = total; dp.G = G; dp.max_seg = max_seg; dp.n_stages = n_stages;
+  dp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
+  dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
+  if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, rp));
+  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, rp));
+
+  DecodeMergeParams mp;
+  mp.part = dp.part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;
+  mp.n_kv_local = (int)pool->n_kv_local; mp.n_batch = (int)c.n_batch; mp.rows_total = (int)rows_total;
+  mp.row_blocks = row_blocks; mp.T = T; mp.G = G; mp.layer_begin = c.layer_begin; mp.n_q_local = c.n_q_local;
+  mp.max_seg = max_seg; mp.agent_ids = c.agent_ids_dev;
+  mp.b = c.adapters ? c.adapters->b : nullptr; mp.scale = c.adapters ? c.adapters->scale : nullptr;
+  mp.n_agents = c.adapters ? c.adapters->n_agents : 1;
+  mp.out = c.out_dev;
+  const int ns_max = (int)((T - 1) / G + 2);
+  dim3 mgrid((unsigned)rows_total, (unsigned)(n_layers * pool->n_kv_local));
+  fla_decode_merge_kernel<<<mgrid, 128, (size_t)(ns_max + r + 1) * sizeof(float), ctx->stream>>>(mp);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  ctx->last_kernel = "fla_decode_tma";
+  return LORAKV_OK;
+}
+
+}  // namespace lk

@@ -17,6 +17,7 @@
 #include <limits>
 
 #include "kernels.hpp"
+#include "page_layout.cuh"
 #include "state.hpp"
 
 namespace lk {
@@ -32,6 +33,7 @@ struct SimtParams {
   const int32_t *kv_table, *lr_table;      // logical -> physical page of the selected sets
   int64_t kv_layer_stride, kv_head_stride, kv_page_stride, lr_layer_stride, lr_page_stride;
   int P, d, r_pad, group, n_kv_local;
+  PageLayout kv_lay, lr_lay;                // element placement inside a page (page_layout.cuh)
   int64_t L;                                // cached rows
   int64_t layer_begin;
   int64_t n_batch, rows_per_entry, query_offset;
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
       float tmp_k[EPC], tmp_v[EPC];
       if (j < j_end) {
         const int64_t phys = p.kv_table[j / p.P];
-        const int64_t off = phys * p.kv_page_stride + (j % p.P) * d + c * EPC;
+        const int64_t off = phys * p.kv_page_stride + page_offset(p.kv_lay, (int)(j % p.P), c * EPC);
         Elem<S>::load_chunk(kp + off, tmp_k);
         Elem<S>::load_chunk(vp + off, tmp_v);
       } else {
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
       float tmp[EPC];
       if (j < j_end) {
         const int64_t phys = p.lr_table[j / p.P];
-        Elem<S>::load_chunk(lp + phys * p.lr_page_stride + (j % p.P) * rp + c * EPC, tmp);
+        Elem<S>::load_chunk(lp + phys * p.lr_page_stride + page_offset(p.lr_lay, (int)(j % p.P), c * EPC), tmp);
       } else {
 #pragma unroll
         for (int u = 0; u < EPC; ++u) tmp[u] = 0.f;
@@ -425,6 +427,8 @@ int launch_paged_simt(const PagedAttnCall& c) {
   sp.kv_page_stride = pool->kv_page_stride();
   sp.lr_layer_stride = pool->lr_layer_stride(); sp.lr_page_stride = pool->lr_page_stride();
   sp.P = (int)pool->P; sp.d = (int)d; sp.r_pad = (int)rp; sp.group = group; sp.n_kv_local = (int)pool->n_kv_local;
+  sp.kv_lay = make_page_layout((int)pool->P, (int)d, (int)pool->elem);
+  sp.lr_lay = make_page_layout((int)pool->P, (int)rp, (int)pool->elem);
   sp.L = c.L; sp.layer_begin = c.layer_begin;
   sp.n_batch = c.n_batch; sp.rows_per_entry = c.rows_per_entry; sp.query_offset = c.query_offset;
   sp.rows_total = rows_total; sp.splits = splits; sp.chunk = chunk;

@@ -51,8 +51,8 @@ struct PagedAttnCall {
 };
 int launch_paged_simt(const PagedAttnCall& call);
 
-// fla_decode_umma.cu (tcgen05 / TMA) -------------------------------------------------------------
-bool decode_umma_supported(const PagedAttnCall& call);
-int launch_decode_umma(const PagedAttnCall& call);
+// fla_decode_tma.cu (TMA bulk-copy rings + tensor-core MMA; bf16 pages, decode) -------------------
+bool decode_tma_supported(const PagedAttnCall& call);
+int launch_decode_tma(const PagedAttnCall& call);
 
 }  // namespace lk

@@ -77,7 +77,7 @@ struct lorakv_pool {
   lorakv_ctx* ctx = nullptr;
   lorakv_pool_dims dims{};
   int64_t P = 64;            // page_tokens
-  int64_t r_pad = 0;         // LR row width in HBM (rank rounded up to 8 elements; 0 when rank == 0)
+  int64_t r_pad = 0;         // LR row width in HBM (rank zero-padded to 8/16/32/64/k*64; 0 when rank == 0)
   int64_t elem = 4;          // bytes per stored element
   int64_t n_kv_local = 0;
   int64_t length = 0;        // KvStore::length_
@@ -85,7 +85,7 @@ struct lorakv_pool {
   // row counts of every logical buffer (GrowMat::rows): [set][layer]
   std::vector<std::vector<int64_t>> key_rows, value_rows, lr_rows;
   lk::PageSpace kv_space, lr_space;
-  void* k_pages = nullptr;   // [n_layers][n_kv_local][kv_total_pages][P][d]
+  void* k_pages = nullptr;   // [n_layers][n_kv_local][kv_total_pages] pages; inside a page: page_layout.cuh
   void* v_pages = nullptr;
   void* lr_pages = nullptr;  // [n_layers][lr_total_pages][P][r_pad]
   uint64_t reserved_bytes = 0;

@@ -55,15 +55,54 @@ def algorithmic_bytes(n_layers, n_q, n_kv_local, n_kv, d, r, A, L, e):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md)."""
+    """SM clocks and throttle reasons DURING the timed region (B200_PROFILING.md).  The region lasts
+    milliseconds, so a thread polls NVML directly (about every millisecond) instead of parsing
+    `nvidia-smi -lms`; nvidia-smi remains the fallback when the NVML binding is missing."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device):
         self.device, self.proc, self.path = device, None, None
+        self.thread, self.stop_flag, self.samples, self.reasons = None, threading.Event(), [], set()
+        self.max_mhz, self.nvml = None, None
+
+    def _visible_index(self):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                return int(vis.split(",")[self.device])
+            except Exception:
+                pass
+        return self.device
+
+    def _poll(self, h):
+        n = self.nvml
+        bits = {"hw_slowdown": n.nvmlClocksEventReasonHwSlowdown, "hw_thermal_slowdown": n.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": n.nvmlClocksEventReasonSwThermalSlowdown, "sw_power_cap": n.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop_flag.is_set():
+            try:
+                self.samples.append(float(n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)))
+                r = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, bit in bits.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                break
+            time.sleep(0.0005)
 
     def start(self):
+        try:
+            import pynvml as n
+            n.nvmlInit()
+            h = n.nvmlDeviceGetHandleByIndex(self._visible_index())
+            self.max_mhz = float(n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM))
+            self.nvml = n
+            self.thread = threading.Thread(target=self._poll, args=(h,), daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             f = tempfile.NamedTemporaryFile("w", suffix=".csv", delete=False)
             self.path = f.name
@@ -74,6 +113,13 @@ class ClockSampler:
 
     def stop(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.thread:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            if self.samples:
+                out.update(sm_mhz=statistics.median(self.samples), sm_max_mhz=self.max_mhz, reasons=sorted(self.reasons),
+                           samples=len(self.samples), source="nvml")
+            return out
         if not self.proc:
             return out
         self.proc.terminate()
@@ -98,7 +144,8 @@ class ClockSampler:
         except Exception:
             pass
         if sm:
-            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm))
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm),
+                       source="nvidia-smi")
         return out
 
 
@@ -273,17 +320,18 @@ def main():
         step_device()
     barrier()
     sampler = ClockSampler(local_rank)
-    if rank == 0:
-        sampler.start()
     launches0 = ctx.launch_count
     # events are recorded by the library on the stream its kernels launch on (lorakv_event_record)
     ev0, ev1 = ctx.event(), ctx.event()
     barrier()
+    if rank == 0:
+        sampler.start()
     ev0.record()
     for _ in range(args.steps):
         step_device()
     ev1.record()
     ms = ev0.elapsed_ms(ev1) / args.steps
+    clocks = sampler.stop() if rank == 0 else None
     barrier()
     launches = ctx.launch_count - launches0
     if world > 1:
@@ -292,16 +340,15 @@ def main():
         ms = float(t.item())
     value = A / (ms * 1e-3)
 
-    # ---- dominant-kernel duration for the roofline: events around the attention launch only ----------
+    # ---- dominant-kernel duration for the roofline: the library brackets the attention kernel alone
+    # (not the merge epilogue) with events on its launch stream; averaged over the same K steps ----
+    ctx.set_profiling(True)
     k_ms = []
-    for _ in range(min(args.steps, 10)):
-        a0, a1 = ctx.event(), ctx.event()
-        a0.record()
-        pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
-        a1.record()
-        k_ms.append(a0.elapsed_ms(a1))
-    kernel_ms = statistics.median(k_ms)
-    clocks = sampler.stop() if rank == 0 else None
+    for _ in range(args.steps):
+        step_device()
+        k_ms.append(ctx.last_kernel_ms())
+    ctx.set_profiling(False)
+    kernel_ms = sum(k_ms) / len(k_ms)
 
     # ---- end to end through the C ABI with host buffers ------------------------------------------------
     q_pin = ctx.pinned_array(q_local_host.shape)
@@ -331,7 +378,8 @@ def main():
 
     peak, peak_src = load_peaks()
     alg = algorithmic_bytes(n_layers, n_q, n_kv_local, n_kv, d, r, A, L, e)
-    achieved = alg / (kernel_ms * 1e-3) / 1e9
+    alg_launch = alg / n_layers if args.per_layer_launch else alg   # last_kernel_ms covers one launch
+    achieved = alg_launch / (kernel_ms * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -353,7 +401,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": alg,
+                     "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": int(alg_launch),
                      "kernel_ms": kernel_ms, "kernel": ctx.last_kernel()},
     }
 

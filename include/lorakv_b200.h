@@ -224,6 +224,12 @@ int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* adapters, int64
                        int64_t agent, int64_t n_q_heads, const float* q, int64_t L_c,
                        int64_t query_offset, float* out, int mem_kind);
 
+/* Device time of the dominant kernel alone.  With profiling on, every fast-path call brackets its
+ * main attention kernel (not the merge epilogue, not the staging copies) with two events on the ctx
+ * stream; lorakv_ctx_last_kernel_ms waits for the second and returns the time between them. */
+int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled);
+int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms);
+
 /* selects the kernel family for the fast paths: 0 = auto (tcgen05/TMA where the shape allows),
  * 1 = force the CUDA-core kernels.  Returns the previous value. */
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy);

@@ -112,6 +112,8 @@ SIGNATURES = {
     "lorakv_adapters_set_b": (C.c_int, [_vp, _i64, _i64, _pf, C.c_double]),
     "lorakv_fla_decode_batched": (C.c_int, [_vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, _vp, C.c_int]),
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
+    "lorakv_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
+    "lorakv_ctx_last_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "lorakv_set_kernel_policy": (C.c_int, [_vp, C.c_int]),
     "lorakv_last_kernel": (C.c_char_p, [_vp]),
 }
@@ -192,6 +194,14 @@ class Context:
 
     def set_kernel_policy(self, policy: int) -> int:
         return self.lib.lorakv_set_kernel_policy(self.h, policy)
+
+    def set_profiling(self, enabled: bool):
+        _check(self.lib.lorakv_ctx_set_profiling(self.h, int(enabled)))
+
+    def last_kernel_ms(self) -> float:
+        ms = C.c_float()
+        _check(self.lib.lorakv_ctx_last_kernel_ms(self.h, C.byref(ms)))
+        return float(ms.value)
 
     def last_kernel(self) -> str:
         return self.lib.lorakv_last_kernel(self.h).decode()

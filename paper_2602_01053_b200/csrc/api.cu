@@ -156,6 +156,7 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
   for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush})
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (cudaEvent_t e : ctx->prof_ev) if (e) cudaEventDestroy(e);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -234,6 +235,25 @@ void lorakv_event_destroy(lorakv_event* ev) {
   if (!ev) return;
   cudaEventDestroy(ev->ev);
   delete ev;
+}
+
+int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled) {
+  if (!ctx) return fail("null context");
+  LK_CUDA(cudaSetDevice(ctx->device));
+  if (enabled && !ctx->prof_ev[0]) {
+    LK_CUDA(cudaEventCreate(&ctx->prof_ev[0]));
+    LK_CUDA(cudaEventCreate(&ctx->prof_ev[1]));
+  }
+  ctx->profiling = enabled != 0;
+  ctx->prof_valid = false;
+  return LORAKV_OK;
+}
+int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return fail("null argument");
+  if (!ctx->prof_valid) return fail("last_kernel_ms: no profiled fast-path call yet");
+  LK_CUDA(cudaEventSynchronize(ctx->prof_ev[1]));
+  LK_CUDA(cudaEventElapsedTime(ms, ctx->prof_ev[0], ctx->prof_ev[1]));
+  return LORAKV_OK;
 }
 
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy) {

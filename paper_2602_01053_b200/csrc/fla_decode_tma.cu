@@ -436,7 +436,9 @@ template <int D, int RP, int MW>
 int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
   auto kern = fla_decode_tma_kernel<D, RP, MW>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  prof_mark(ctx, 0);
   kern<<<grid, kWarps * 32, smem, ctx->stream>>>(dp);
+  prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;

@@ -372,7 +372,9 @@ static int launch_simt_t(lorakv_ctx* ctx, const SimtParams& sp, dim3 grid) {
   const size_t smem = sizeof(float) * ((size_t)8 * RW * d + 2 * kTile * (d + 4) + kTile * (rp + 4) + (size_t)8 * RW * kTile);
   auto kern = fla_paged_simt_kernel<S, RW, QD>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  prof_mark(ctx, 0);
   kern<<<grid, kThreads, smem, ctx->stream>>>(sp);
+  prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;

@@ -55,7 +55,19 @@ struct lorakv_ctx {
   void* pinned = nullptr;             // small pinned staging buffer
   size_t pinned_bytes = 0;
   void* tma_encode = nullptr;         // cuTensorMapEncodeTiled, resolved through the runtime
+  bool profiling = false;             // bracket the dominant kernel of fast-path calls with events
+  cudaEvent_t prof_ev[2] = {nullptr, nullptr};
+  bool prof_valid = false;
 };
+
+namespace lk {
+// record the start (which = 0) / end (which = 1) of the dominant kernel when profiling is on
+inline void prof_mark(lorakv_ctx* ctx, int which) {
+  if (!ctx->profiling) return;
+  cudaEventRecord(ctx->prof_ev[which], ctx->stream);
+  if (which == 1) ctx->prof_valid = true;
+}
+}  // namespace lk
 
 namespace lk {
 

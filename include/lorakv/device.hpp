@@ -1,0 +1,85 @@
+// lorakv/device.hpp -- device-resident fast paths over the paged cache.  NOT part of the reference's
+// header set: the reference attends over host views (engine.hpp:429-443 hands key_view / value_view /
+// lr_view to gqa_attention); here the cache already lives in HBM, so the engine-level call becomes
+//
+//   decode_batched(store, tables, layer_begin, layer_end, agents, n_q_heads, q)
+//       == for every layer, for every batch entry: gqa_attention(q_row, key_view, value_view, lr_view,
+//          B[agent], alpha/rank, query_offset = L-1, n_q, n_kv)            (attention.hpp:332-363)
+//   prefill(store, tables, layer, agent, n_q_heads, q, query_offset)
+//       == gqa_attention(q, key_view, value_view, lr_view, B[agent], alpha/rank, query_offset, ...)
+//   append_lr_project(store, tables, layer, agent, row_begin, x)
+//       == store.append_lr(layer, agent, row_begin, matmul(x, A))           (engine.hpp:414-418)
+//
+// AdapterTable keeps the shared down-projection A per layer and B / alpha per (layer, agent) in HBM
+// (lora.hpp:13-87; shared-A multi-LoRA, lora.hpp:69-73).
+#pragma once
+
+#include <vector>
+
+#include "lorakv/kvcache.hpp"
+#include "lorakv/lora.hpp"
+
+namespace lorakv {
+
+class AdapterTable {
+ public:
+  AdapterTable(const KvStore<float>& store, idx n_q_heads)
+      : n_q_heads_(n_q_heads), n_kv_heads_(store.device_options().n_kv_heads) {
+    const StoreDims& d = store.dims();
+    const DeviceOptions& o = store.device_options();
+    b200::check(lorakv_adapters_create(b200::Runtime::ctx(), d.n_layers, d.n_agents, d.d_model, d.rank, o.n_kv_heads,
+                                       d.d_kv / o.n_kv_heads, o.kv_head_begin, o.n_kv_local,
+                                       o.bf16 ? LORAKV_BF16 : LORAKV_F32, &h_));
+  }
+  ~AdapterTable() { lorakv_adapters_destroy(h_); }
+  AdapterTable(const AdapterTable&) = delete;
+  AdapterTable& operator=(const AdapterTable&) = delete;
+
+  // one adapter of one layer; under shared-A every agent's `a` is the same matrix and is uploaded once
+  void set(idx layer, idx agent, const LoraAdapter<float>& adapter, bool upload_a = true) {
+    if (upload_a) b200::check(lorakv_adapters_set_a(h_, layer, adapter.a.data.data()));
+    b200::check(lorakv_adapters_set_b(h_, layer, agent, adapter.b.data.data(), adapter.alpha));
+  }
+  void set_layer(idx layer, const MultiLoraSet<float>& set) {
+    for (idx a = 0; a < set.num_agents(); ++a) this->set(layer, a, set.adapter(a), a == 0);
+  }
+  lorakv_adapters* handle() const { return h_; }
+  idx n_q_heads() const { return n_q_heads_; }
+
+ private:
+  lorakv_adapters* h_ = nullptr;
+  idx n_q_heads_, n_kv_heads_;
+};
+
+// q: [(layer_end - layer_begin) * agents.size()] rows x (n_q_local * d_head); same-shaped result
+inline Matrix<float> decode_batched(KvStore<float>& store, const AdapterTable* tables, idx layer_begin, idx layer_end,
+                                    const std::vector<std::int32_t>& agents, idx n_q_heads, const Matrix<float>& q) {
+  const idx n_batch = static_cast<idx>(agents.size());
+  if (q.rows != (layer_end - layer_begin) * n_batch)
+    fail("decode_batched: q has " + std::to_string(q.rows) + " rows, expected layers x batch = " +
+         std::to_string((layer_end - layer_begin) * n_batch));
+  Matrix<float> out(q.rows, q.cols);
+  b200::check(lorakv_fla_decode_batched(store.handle(), tables ? tables->handle() : nullptr, layer_begin, layer_end,
+                                        agents.data(), n_batch, n_q_heads, q.data.data(), out.data.data(), LORAKV_HOST));
+  return out;
+}
+
+inline Matrix<float> prefill(KvStore<float>& store, const AdapterTable* tables, idx layer, idx agent, idx n_q_heads,
+                             const Matrix<float>& q, idx query_offset) {
+  Matrix<float> out(q.rows, q.cols);
+  b200::check(lorakv_fla_prefill(store.handle(), tables ? tables->handle() : nullptr, layer, agent, n_q_heads,
+                                 q.data.data(), q.rows, query_offset, out.data.data(), LORAKV_HOST));
+  return out;
+}
+
+// V_lr rows = x * A computed on the device once for all agents, written straight into the LR pages;
+// returns the rows actually appended (first writer wins)
+inline idx append_lr_project(KvStore<float>& store, const AdapterTable& tables, idx layer, idx agent, idx row_begin,
+                             Span2D<const float> x) {
+  std::int64_t added = 0;
+  b200::check(lorakv_pool_append_lr_project(store.handle(), tables.handle(), layer, agent, row_begin, x.data, x.rows,
+                                            x.stride, LORAKV_HOST, &added));
+  return added;
+}
+
+}  // namespace lorakv

@@ -123,6 +123,15 @@ int lorakv_gqa_forward_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const 
                            int64_t n_q_heads, int64_t n_kv_heads, int64_t d_head, int64_t r,
                            int64_t query_offset, double* out);
 
+/* matmul, matrix.hpp:101-135: out (M x N, dense) = a (M x K, stride lda) * b (K x N, stride ldb) over
+ * HOST pointers.  Ascending-k accumulation with separately rounded multiply and add, i.e. the bits the
+ * reference's triple loop produces under -ffp-contract=off.  Used by expand_lr / forward_decomposed
+ * (lora.hpp:39-47,97-108). */
+int lorakv_matmul_f32(lorakv_ctx* ctx, const float* a, int64_t lda, const float* b, int64_t ldb,
+                      int64_t M, int64_t K, int64_t N, float* out);
+int lorakv_matmul_f64(lorakv_ctx* ctx, const double* a, int64_t lda, const double* b, int64_t ldb,
+                      int64_t M, int64_t K, int64_t N, double* out);
+
 /* lr_mac_counts, attention.hpp:35-41, and the dense AttnMacs closed forms (:229-243):
  * macs[0]=qk, [1]=pv, [2]=lr (reordered).  Pure integer arithmetic on the host. */
 void lorakv_lr_mac_counts(int64_t total_len, int64_t cur_len, int64_t rank, int64_t d_head,

@@ -87,6 +87,8 @@ SIGNATURES = {
     "lorakv_naive_forward_f64": (C.c_int, _attn_sig(_d, _pd, False)),
     "lorakv_gqa_forward_f32": (C.c_int, _gqa_sig(_f, _pf)),
     "lorakv_gqa_forward_f64": (C.c_int, _gqa_sig(_d, _pd)),
+    "lorakv_matmul_f32": (C.c_int, [_vp, _pf, _i64, _pf, _i64, _i64, _i64, _i64, _pf]),
+    "lorakv_matmul_f64": (C.c_int, [_vp, _pd, _i64, _pd, _i64, _i64, _i64, _i64, _pd]),
     "lorakv_lr_mac_counts": (None, [_i64, _i64, _i64, _i64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "lorakv_attn_macs": (None, [_i64, _i64, _i64, _i64, C.c_int, C.POINTER(C.c_uint64)]),
     "lorakv_plan_core": (C.c_int, [C.c_int, _i64, _i64, _i64, _i64, C.POINTER(_i64)]),
@@ -279,6 +281,15 @@ class Context:
 
     def naive_attention(self, q, k, v, v_lr, b_up, lr_scale, query_offset):
         return self._attn("naive_forward", q, k, v, v_lr, b_up, lr_scale, query_offset)
+
+    def matmul(self, a, b):
+        suf, T = ("f32", _f) if a.dtype == np.float32 else ("f64", _d)
+        assert a.dtype == b.dtype and a.shape[1] == b.shape[0]
+        out = np.zeros((a.shape[0], b.shape[1]), dtype=a.dtype)
+        (pa, lda), (pb, ldb) = _span(a, T), _span(b, T)
+        _check(getattr(self.lib, f"lorakv_matmul_{suf}")(self.h, pa, lda, pb, ldb, a.shape[0], a.shape[1],
+                                                        b.shape[1], out.ctypes.data_as(C.POINTER(T))))
+        return out
 
     def gqa_attention(self, q, k, v, v_lr, b_up, lr_scale, query_offset, n_q, n_kv):
         suf, T = ("f32", _f) if q.dtype == np.float32 else ("f64", _d)

@@ -300,6 +300,15 @@ const char* lorakv_last_kernel(lorakv_ctx* ctx) { return ctx ? ctx->last_kernel 
 LK_OPS(f32, float)
 LK_OPS(f64, double)
 
+int lorakv_matmul_f32(lorakv_ctx* ctx, const float* a, int64_t lda, const float* b, int64_t ldb, int64_t M,
+                      int64_t K, int64_t N, float* out) {
+  return matmul_forward<float>(ctx, a, lda, b, ldb, M, K, N, out);
+}
+int lorakv_matmul_f64(lorakv_ctx* ctx, const double* a, int64_t lda, const double* b, int64_t ldb, int64_t M,
+                      int64_t K, int64_t N, double* out) {
+  return matmul_forward<double>(ctx, a, lda, b, ldb, M, K, N, out);
+}
+
 void lorakv_lr_mac_counts(int64_t total_len, int64_t cur_len, int64_t rank, int64_t d_head,
                           uint64_t* no_reorder, uint64_t* reorder) {
   const uint64_t L = (uint64_t)total_len, Lc = (uint64_t)cur_len, r = (uint64_t)rank, d = (uint64_t)d_head;

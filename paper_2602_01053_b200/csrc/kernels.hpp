@@ -22,6 +22,11 @@ int naive_forward(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t 
                   int64_t ldv, const T* vlr, int64_t ldlr, const T* b, int64_t ldb, T lr_scale,
                   int64_t Lc, int64_t L, int64_t d, int64_t r, int64_t off, T* out);
 
+// linalg_kernels.cu ---------------------------------------------------------------------------
+template <class T>
+int matmul_forward(lorakv_ctx* ctx, const T* a, int64_t lda, const T* b, int64_t ldb, int64_t M, int64_t K,
+                   int64_t N, T* out);
+
 // cache_kernels.cu ----------------------------------------------------------------------------
 // Copy `n_rows` float32 rows (device, row stride ld, already offset to the pool's first column)
 // into pages, starting at logical row `row0` of the page set `set`.

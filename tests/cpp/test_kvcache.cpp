@@ -1,0 +1,165 @@
+// The scheme-aware cache store behind include/lorakv/kvcache.hpp (paged HBM pool + host bookkeeping).
+// Mirrors proj/tests/test_kvcache.cpp: planner intervals, first-writer-wins, the gap / forbidden
+// errors, exact byte identities, monotone seen_upto -- all integer results bit-exact -- plus the page
+// table, which the reference does not have (first-touch order, checked against the oracle's page model).
+#include <cstdint>
+#include <vector>
+
+#include "check.hpp"
+#include "lorakv/kvcache.hpp"
+#include "oracle_glue.hpp"
+
+using namespace lorakv;
+
+namespace {
+
+Matrix<float> fill_rows(idx rows, idx cols, float tag) {   // small integers: exact in fp32 and bf16-free
+  Matrix<float> m(rows, cols);
+  for (idx i = 0; i < rows; ++i)
+    for (idx j = 0; j < cols; ++j) m(i, j) = tag + float(i * cols + j);
+  return m;
+}
+
+bool same(Span2D<const float> a, const Matrix<float>& b) {
+  if (a.rows != b.rows || a.cols != b.cols) return false;
+  for (idx i = 0; i < a.rows; ++i)
+    for (idx j = 0; j < a.cols; ++j)
+      if (a(i, j) != b(i, j)) return false;
+  return true;
+}
+
+CacheScheme scheme(SchemeKind k) { return CacheScheme{k, {}}; }
+
+}  // namespace
+
+TEST_CASE("plan_core: cold start plans the fresh range under every scheme") {
+  for (SchemeKind k : {SchemeKind::NonShared, SchemeKind::FullShared, SchemeKind::BaseShared, SchemeKind::BaseLRShared}) {
+    const PrefillPlan p = plan_core(scheme(k), 0, 0, 128);
+    CHECK(p.hidden_pass == (Interval{0, 128}));
+    CHECK(p.kv_project == (Interval{0, 128}));
+    CHECK(p.lr_project == (Interval{0, 128}));
+  }
+  CHECK_THROWS_AS(plan_core(scheme(SchemeKind::FullShared), 10, 11, 1), std::runtime_error);
+  CHECK_THROWS_AS(plan_core(scheme(SchemeKind::FullShared), 10, 0, -1), std::runtime_error);
+}
+
+TEST_CASE("plan_core: an agent switch after 1000 tokens") {
+  // the agent last saw 200 tokens, the trajectory holds 1000 and 16 new tokens arrive
+  const Interval fresh{1000, 1016}, unseen{200, 1016};
+  PrefillPlan p = plan_core(scheme(SchemeKind::NonShared), 1000, 200, 16);
+  CHECK(p.hidden_pass == unseen); CHECK(p.kv_project == unseen); CHECK(p.lr_project == unseen);
+  p = plan_core(scheme(SchemeKind::FullShared), 1000, 200, 16);
+  CHECK(p.hidden_pass == fresh); CHECK(p.kv_project == fresh); CHECK(p.lr_project == fresh);
+  p = plan_core(scheme(SchemeKind::BaseShared), 1000, 200, 16);
+  CHECK(p.hidden_pass == unseen); CHECK(p.kv_project == fresh); CHECK(p.lr_project == unseen);
+  p = plan_core(scheme(SchemeKind::BaseLRShared), 1000, 200, 16);
+  CHECK(p.hidden_pass == fresh); CHECK(p.kv_project == fresh); CHECK(p.lr_project == fresh);
+  // the oracle's restatement of plan_core agrees on every field
+  for (int k = 0; k < 4; ++k) {
+    std::int64_t want[9];
+    oracle::ok(orc_plan_core(k, 0, 1000, 200, 16, want));
+    const PrefillPlan g = plan_core(scheme(static_cast<SchemeKind>(k)), 1000, 200, 16);
+    CHECK(g.hidden_pass.begin == want[0]); CHECK(g.hidden_pass.end == want[1]);
+    CHECK(g.kv_project.begin == want[2]); CHECK(g.lr_project.begin == want[4]);
+  }
+}
+
+TEST_CASE("first writer wins; a gap is an error") {
+  KvStore<float> st(scheme(SchemeKind::BaseLRShared), StoreDims{2, 8, 16, 4, 3}, DeviceOptions{2, 256});
+  const Matrix<float> k0 = fill_rows(10, 8, 0.f), k1 = fill_rows(10, 8, 500.f);
+  st.append_tokens(std::vector<std::int32_t>(10, 7));
+  st.append_key(0, 0, 0, k0.view());
+  st.append_key(0, 1, 0, k1.view());                 // second writer: content unchanged
+  CHECK(same(st.key_view(0, 2), k0));
+  const Matrix<float> tail = fill_rows(6, 8, 900.f);  // rows 8..13: only 10..13 are new
+  st.append_key(0, 1, 8, tail.view());
+  const Span2D<const float> kv = st.key_view(0, 0);
+  REQUIRE(kv.rows == 14);
+  CHECK(kv(9, 0) == k0(9, 0));
+  CHECK(kv(10, 0) == tail(2, 0));
+  CHECK_THROWS_WITH_AS(st.append_key(0, 0, 20, k0.view()), "gap", std::runtime_error);
+  CHECK_THROWS_WITH_AS(st.append_value(1, 0, 1, k0.view()), "gap at row 0", std::runtime_error);
+  CHECK_THROWS_AS(st.append_key(2, 0, 0, k0.view()), std::runtime_error);     // layer out of range
+  CHECK_NOTHROW(st.key_view(0, 3));   // shared caches ignore the agent index (kvcache.hpp:307-311)
+}
+
+TEST_CASE("FullShared: a second writer adds no bytes; NonShared keeps disjoint caches") {
+  KvStore<float> fs(scheme(SchemeKind::FullShared), StoreDims{1, 8, 16, 0, 2}, DeviceOptions{1, 128});
+  const Matrix<float> rows = fill_rows(5, 8, 1.f);
+  fs.append_key(0, 0, 0, rows.view()); fs.append_value(0, 0, 0, rows.view());
+  const CacheBytes before = fs.bytes();
+  fs.append_key(0, 1, 0, rows.view()); fs.append_value(0, 1, 0, rows.view());
+  CHECK(fs.bytes().total() == before.total());
+  CHECK(before.key == 5u * 8u * sizeof(float));
+  CHECK(fs.lr_view(0, 0).rows == 5); CHECK(fs.lr_view(0, 0).cols == 0);
+  CHECK_THROWS_WITH_AS(fs.append_lr(0, 0, 0, Matrix<float>(5, 0).view()), "has no LR cache", std::runtime_error);
+
+  KvStore<float> ns(scheme(SchemeKind::NonShared), StoreDims{1, 8, 16, 0, 2}, DeviceOptions{1, 128});
+  const Matrix<float> other = fill_rows(3, 8, 100.f);
+  ns.append_key(0, 0, 0, rows.view()); ns.append_key(0, 1, 0, other.view());
+  CHECK(same(ns.key_view(0, 0), rows)); CHECK(same(ns.key_view(0, 1), other));
+  CHECK(ns.bytes().key == (5u + 3u) * 8u * sizeof(float));
+  CHECK_THROWS_WITH_AS(ns.key_view(0, 2), "unknown agent", std::runtime_error);
+}
+
+TEST_CASE("overwrites are forbidden; schemes without a hidden cache say so") {
+  KvStore<float> st(scheme(SchemeKind::BaseShared), StoreDims{1, 8, 16, 2, 2}, DeviceOptions{1, 64});
+  const Matrix<float> rows = fill_rows(2, 8, 0.f);
+  CHECK_THROWS_WITH_AS(st.recompute_overwrite(0, 0, rows.view(), rows.view()), "forbidden", std::runtime_error);
+  CHECK_THROWS_WITH_AS(st.append_hidden(0, rows.view()), "no hidden-state cache", std::runtime_error);
+  CHECK_THROWS_AS(KvStore<float>(CacheScheme{SchemeKind::SelectiveRecompute, {0}}, StoreDims{1, 8, 16, 2, 2}), std::runtime_error);
+  CHECK_THROWS_WITH_AS(CacheScheme::parse("Shared"), "unknown cache scheme", std::runtime_error);
+  CHECK(CacheScheme::parse("BaseLRShared").kind == SchemeKind::BaseLRShared);
+}
+
+TEST_CASE("byte ratios are the exact rationals 1/N + r/d_out, 1/N + r/(N d_out) and 1/N") {
+  for (idx r : {4, 8, 16, 32})
+    for (idx d_out : {256, 1024}) {
+      const idx N = 3, L = 40, layers = 2;
+      auto fill = [&](SchemeKind k) {
+        KvStore<float> st(scheme(k), StoreDims{layers, d_out, 64, r, N}, DeviceOptions{d_out / 64, 64});
+        const Matrix<float> kv = fill_rows(L, d_out, 0.f), lr = fill_rows(L, r, 0.f);
+        for (idx a = 0; a < N; ++a)
+          for (idx l = 0; l < layers; ++l) {
+            st.append_key(l, a, 0, kv.view()); st.append_value(l, a, 0, kv.view());
+            if (k == SchemeKind::BaseShared || k == SchemeKind::BaseLRShared) st.append_lr(l, a, 0, lr.view());
+          }
+        CHECK(st.bytes().total() == st.allocated_elements() * sizeof(float));
+        return st.bytes();
+      };
+      const CacheBytes ns = fill(SchemeKind::NonShared), bs = fill(SchemeKind::BaseShared), bl = fill(SchemeKind::BaseLRShared);
+      const std::uint64_t n = N, d = std::uint64_t(d_out), rr = std::uint64_t(r);
+      CHECK(bs.key * n == ns.key); CHECK(bl.key * n == ns.key);
+      CHECK((bs.value + bs.lr) * n * d == ns.value * (d + n * rr));     // 1/N + r/d_out
+      CHECK((bl.value + bl.lr) * n * d == ns.value * (d + rr));         // 1/N + r/(N d_out)
+    }
+}
+
+TEST_CASE("seen_upto is monotone; plan_step reads the store") {
+  KvStore<float> st(scheme(SchemeKind::BaseShared), StoreDims{1, 8, 16, 2, 2}, DeviceOptions{1, 64});
+  st.append_tokens(std::vector<std::int32_t>(12, 1));
+  st.mark_seen(0);
+  CHECK(st.seen(0) == 12); CHECK(st.seen(1) == 0);
+  st.append_tokens(std::vector<std::int32_t>(3, 2));
+  CHECK(st.length() == 15); CHECK(st.tokens().size() == 15u);
+  const PrefillPlan p = plan_step(st, 1, 4);
+  CHECK(p.hidden_pass == (Interval{0, 19})); CHECK(p.kv_project == (Interval{15, 19})); CHECK(p.lr_project == (Interval{0, 19}));
+  st.mark_seen(1);
+  CHECK(st.seen(1) == 15);
+  CHECK_THROWS_AS(st.seen(2), std::runtime_error);
+}
+
+TEST_CASE("pages are handed out in first-touch order (logical row -> row / P, row % P)") {
+  const idx P = 16;
+  KvStore<float> st(scheme(SchemeKind::NonShared), StoreDims{1, 8, 16, 0, 2}, DeviceOptions{1, 256, false, P});
+  const Matrix<float> a = fill_rows(20, 8, 0.f), b = fill_rows(40, 8, 0.f);
+  st.append_key(0, 1, 0, a.view());       // agent 1 touches logical pages 0,1 first -> physical 0,1
+  st.append_key(0, 0, 0, b.view());       // agent 0: logical 0,1,2 -> physical 2,3,4
+  st.append_key(0, 1, 20, a.view());      // agent 1 grows to 40 rows: logical 2 -> physical 5
+  std::int64_t page, slot;
+  orc_page_of(39, P, &page, &slot);
+  CHECK(page == 2); CHECK(slot == 7);
+  CHECK(st.page_table(LORAKV_KEY, 1) == (std::vector<std::int32_t>{0, 1, 5}));
+  CHECK(st.page_table(LORAKV_KEY, 0) == (std::vector<std::int32_t>{2, 3, 4}));
+  CHECK(same(st.key_view(0, 0), b));
+}

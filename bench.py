@@ -246,12 +246,12 @@ def main():
     else:
         torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if n_kv % world != 0:
-        raise SystemExit(f"n_kv_heads {n_kv} not divisible by {world} ranks")
-    n_kv_local = n_kv // world
-    kv_begin = rank * n_kv_local
-    g = n_q // n_kv
-    n_q_local = n_kv_local * g
+    from paper_2602_01053_b200.sharding import HeadShard
+    try:
+        shard = HeadShard(rank, world, n_q, n_kv)      # kv heads of this rank (no communication inside attention)
+    except ValueError as e:
+        raise SystemExit(str(e))
+    n_kv_local, kv_begin, g, n_q_local = shard.n_kv_local, shard.kv_begin, shard.group, shard.n_q_local
     dtype = abi.BF16 if args.dtype == "bf16" else abi.F32
     e = 2 if dtype == abi.BF16 else 4
 
@@ -293,8 +293,7 @@ def main():
             b_host[layer][a] = bf16_round(b_host[layer][a])
             ad.set_b(layer, a, b_host[layer][a], 16.0)
     q_full = bf16_round((host_rng.standard_normal((n_layers, A, n_q * d)).astype(np.float32) * sc))
-    q_local_host = np.ascontiguousarray(q_full.reshape(n_layers, A, n_q, d)[:, :, kv_begin * g:(kv_begin + n_kv_local) * g, :]
-                                        .reshape(n_layers, A, n_q_local * d))
+    q_local_host = shard.slice_q(q_full, d)
     q_dev = torch.from_numpy(q_local_host).to(dev)
     out_dev = torch.zeros((n_layers, A, n_q_local * d), device=dev, dtype=torch.float32)
     gathered = torch.zeros((world, n_layers, A, n_q_local * d), device=dev, dtype=torch.float32) if world > 1 else None
@@ -308,7 +307,7 @@ def main():
         else:
             pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
         if world > 1:   # the end-of-step output gather, the only collective on the path
-            dist.all_gather_into_tensor(gathered, out_dev)
+            dist.all_gather_into_tensor(gathered.view(-1), out_dev.view(-1))
 
     def barrier():
         if world > 1:
@@ -361,7 +360,7 @@ def main():
     for _ in range(args.steps):
         pool.decode(ad, 0, n_layers, agent_ids, n_q, q_pin, out=out_pin)   # H2D + kernels + D2H + sync
         if world > 1:
-            dist.all_gather_into_tensor(gathered, out_dev)
+            dist.all_gather_into_tensor(gathered.view(-1), out_dev.view(-1))
     barrier()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     if world > 1:

@@ -239,6 +239,14 @@ int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* adapters, int64
 int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled);
 int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms);
 
+/* One-tile tcgen05 self-test (diagnostics): D (128 x N) = A (128 x K) * B on the tensor cores with the
+ * shared-memory operand layouts the prefill kernel uses; B is N x K row-major (b_mn_major = 0, the
+ * K-page convention) or K x N row-major (b_mn_major = 1, the V / V_lr page convention).  HOST pointers,
+ * operands rounded to bf16, fp32 accumulation in TMEM.  rescale != 0 additionally scales the
+ * accumulator by alpha through tcgen05.ld/st and accumulates a second pass: D = (alpha + 1) * A B. */
+int lorakv_selftest_umma(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major,
+                         float alpha, int rescale, float* d);
+
 /* selects the kernel family for the fast paths: 0 = auto (tcgen05/TMA where the shape allows),
  * 1 = force the CUDA-core kernels.  Returns the previous value. */
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy);

@@ -256,6 +256,11 @@ int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms) {
   return LORAKV_OK;
 }
 
+int lorakv_selftest_umma(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha,
+                         int rescale, float* d) {
+  return umma_selftest(ctx, a, b, N, K, b_mn_major, alpha, rescale, d);
+}
+
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy) {
   if (!ctx) return 0;
   const int old = ctx->policy;

@@ -60,4 +60,8 @@ int launch_paged_simt(const PagedAttnCall& call);
 bool decode_tma_supported(const PagedAttnCall& call);
 int launch_decode_tma(const PagedAttnCall& call);
 
+// umma_selftest.cu ------------------------------------------------------------------------------------
+int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
+                  float* d);
+
 }  // namespace lk

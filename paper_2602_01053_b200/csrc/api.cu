@@ -377,11 +377,11 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   }
   p->elem = dims->dtype == LORAKV_BF16 ? 2 : 4;
   const bool has_lr = p->lr_sets() > 0 && dims->rank > 0;
-  // LR row width in HBM: the rank padded with zero columns (exact) to 8/16/32/64 or a multiple of
+  // LR row width in HBM: the rank padded with zero columns (exact) to 16/32/64 or a multiple of
   // 64, the widths page_layout.cuh can swizzle
   p->r_pad = 0;
   if (has_lr) {
-    p->r_pad = 8;
+    p->r_pad = 16;   // one tcgen05 N-tile / one 32-byte swizzled row at least
     while (p->r_pad < dims->rank && p->r_pad < 64) p->r_pad *= 2;
     if (p->r_pad < dims->rank) p->r_pad = (dims->rank + 63) / 64 * 64;
   }
@@ -762,7 +762,9 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   call.kv_set = kv_set; call.lr_set = lr_set; call.agent_ids_dev = ids_dev; call.n_batch = n_batch;
   call.rows_per_entry = rows_per_entry; call.query_offset = query_offset; call.n_q_local = n_q_local;
   call.L = L; call.q_dev = q_dev; call.out_dev = out_dev;
+  call.agent_host = ids_host[0];
   if (ctx->policy == 0 && decode_tma_supported(call)) LK_TRY(launch_decode_tma(call));
+  else if (ctx->policy == 0 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
   else LK_TRY(launch_paged_simt(call));
 
   if (host) {

@@ -49,6 +49,7 @@ struct PagedAttnCall {
   int64_t n_batch;                  // decode: batch entries; prefill: 1
   int64_t rows_per_entry;           // decode: 1; prefill: L_c
   int64_t query_offset;             // position of row 0 of every entry
+  int64_t agent_host;               // agent of batch entry 0 (host copy; prefill has exactly one entry)
   int64_t n_q_local;                // q heads held by this pool
   int64_t L;                        // cached rows visible to the kernel (min over K, V, LR buffers)
   const float* q_dev;               // [layers][n_batch][rows_per_entry][n_q_local*d]
@@ -59,6 +60,10 @@ int launch_paged_simt(const PagedAttnCall& call);
 // fla_decode_tma.cu (TMA bulk-copy rings + tensor-core MMA; bf16 pages, decode) -------------------
 bool decode_tma_supported(const PagedAttnCall& call);
 int launch_decode_tma(const PagedAttnCall& call);
+
+// fla_prefill_umma.cu (tcgen05 / TMEM / TMA; bf16 pages, prefill blocks) ---------------------------------
+bool prefill_umma_supported(const PagedAttnCall& call);
+int launch_prefill_umma(const PagedAttnCall& call);
 
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,

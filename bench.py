@@ -214,6 +214,83 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def load_tensor_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+    except Exception:
+        return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s)"
+
+
+def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L, d_model):
+    """TTFT of one layer: X*A projection of the L_c new rows (the V_lr append of engine.hpp:414-418, timed
+    on a scratch pool so the trajectory is untouched) + Flash-LoRA-Attention of the L_c query rows at
+    query_offset = L - L_c over the cached trajectory (lorakv_fla_prefill), device-resident operands."""
+    import paper_2602_01053_b200 as pkg
+    from paper_2602_01053_b200 import abi
+    L_c = L // 2
+    off = L - L_c
+    gen = torch.Generator(device=dev); gen.manual_seed(77)
+    sc = float(1.0 / np.sqrt(d))
+    q = (torch.randn((L_c, n_q * d), generator=gen, device=dev, dtype=torch.float32) * sc).to(torch.bfloat16).to(torch.float32)
+    out = torch.empty_like(q)
+    steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        pool.prefill_device(ad, 0, 1, n_q, q.data_ptr(), L_c, off, out.data_ptr())
+    ev0, ev1 = ctx.event(), ctx.event()
+    ev0.record()
+    for i in range(steps):
+        pool.prefill_device(ad, i % n_layers, 1, n_q, q.data_ptr(), L_c, off, out.data_ptr())
+    ev1.record()
+    attn_ms = ev0.elapsed_ms(ev1) / steps
+    kernel = ctx.last_kernel()
+    pairs = L_c * off + L_c * (L_c + 1) // 2
+    flops = 2 * n_q * pairs * (2 * d + r) + 2 * n_q * L_c * r * d
+    peak, peak_src = load_tensor_peak()
+    res = {"workload": "cfg3", "L_c": L_c, "query_offset": off, "attention_ms_per_layer": attn_ms,
+           "attention_tflops": flops / (attn_ms * 1e-3) / 1e12, "algorithmic_flops": flops, "kernel": kernel,
+           "roofline": {"bound": "tensor", "achieved": flops / (attn_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                        "frac": flops / (attn_ms * 1e-3) / 1e12 / peak, "peak_source": peak_src}}
+    # parity: a seeded sample of query rows against the reference CPU path (SURVEY 8d: rows via L_c = 1)
+    if not args.no_cpu_baseline:
+        from oracle import checker
+        chk = checker.best()
+        k0 = pool.key_view(0, 0); v0 = pool.value_view(0, 0); lr0 = pool.lr_view(0, 0)
+        pool.prefill_device(ad, 0, 1, n_q, q.data_ptr(), L_c, off, out.data_ptr())
+        torch.cuda.synchronize()
+        rows = [0, 1, L_c // 3, L_c - 1]
+        got = out[rows].cpu().numpy(); qh = q[rows].cpu().numpy()
+        b1 = bench_prefill.b_host[0][1]
+        worst = 0.0
+        for i, row in enumerate(rows):
+            pos = off + row
+            want = chk.gqa_attention(np.ascontiguousarray(qh[i][None, :]), k0[:pos + 1], v0[:pos + 1], lr0[:pos + 1], b1,
+                                     16.0 / r if r else 1.0, pos, n_q, n_kv, threads=host_threads())
+            worst = max(worst, chk.max_rel_error(got[i][None, :], want))
+        res["parity"] = {"sampled_rows": rows, "max_rel_error": worst, "tolerance": 2e-2, "oracle": chk.kind}
+    # the X*A projection + LR append of the same L_c rows (scratch pool, one layer)
+    try:
+        x = torch.randn((L_c, d_model), generator=gen, device=dev, dtype=torch.float32)
+        sp = pkg.Pool(ctx, "BaseLRShared", 1, n_kv, d, d_model, r, 1, max_tokens=4 * L_c, dtype=pool.dims.dtype)
+        sa = pkg.Adapters(ctx, 1, 1, d_model, r, n_kv, d, dtype=pool.dims.dtype)
+        sa.set_a(0, (np.random.default_rng(5).standard_normal((d_model, r)) / np.sqrt(d_model)).astype(np.float32))
+        sp.append_tokens(4 * L_c)
+        sp.append_lr_project(sa, 0, 0, 0, dev_ptr=x.data_ptr(), n_rows=L_c, ld=d_model)        # warm-up (module load)
+        p0, p1 = ctx.event(), ctx.event()
+        p0.record()
+        for i in range(1, 4):
+            sp.append_lr_project(sa, 0, 0, i * L_c, dev_ptr=x.data_ptr(), n_rows=L_c, ld=d_model)
+        p1.record()
+        res["xa_project_ms"] = p0.elapsed_ms(p1) / 3
+        res["xa_project_gbs"] = L_c * d_model * 4 / (res["xa_project_ms"] * 1e-3) / 1e9
+        res["ttft_ms_per_layer"] = attn_ms + res["xa_project_ms"]
+        sp.close(); sa.close()
+    except Exception as e:
+        res["xa_project_error"] = str(e)[:200]
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -224,6 +301,7 @@ def main():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--per-layer-launch", action="store_true", help="one launch per layer instead of one per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the prefill / TTFT leg")
     ap.add_argument("--policy", type=int, default=0, help="0 auto (tcgen05 where supported), 1 CUDA-core kernels")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -292,6 +370,7 @@ def main():
         for a in range(A):
             b_host[layer][a] = bf16_round(b_host[layer][a])
             ad.set_b(layer, a, b_host[layer][a], 16.0)
+    bench_prefill.b_host = b_host
     q_full = bf16_round((host_rng.standard_normal((n_layers, A, n_q * d)).astype(np.float32) * sc))
     q_local_host = shard.slice_q(q_full, d)
     q_dev = torch.from_numpy(q_local_host).to(dev)
@@ -415,6 +494,14 @@ def main():
                      "traffic": traffic, "peak_source": peak_src, "algorithmic_bytes_per_launch": int(alg_launch),
                      "kernel_ms": kernel_ms, "kernel": ctx.last_kernel()},
     }
+
+    # ---- prefill / TTFT leg (BASELINE configs[2]): L_c new rows appended onto the first half of the same
+    # trajectory, one agent, one layer per call; tensor-core roofline --------------------------------------
+    if world == 1 and not args.no_prefill and L >= 256:
+        try:
+            line["prefill"] = bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L, d_model)
+        except Exception as e:   # the decode line must survive a prefill failure
+            line["prefill"] = {"error": str(e)[:300]}
 
     # ---- CPU baseline + parity at full size on layer 0 (rank 0, N = 1 only) -----------------------------
     if world == 1 and not args.no_cpu_baseline:

@@ -105,60 +105,114 @@ __global__ void gather_rows_kernel(PageAddr a, int64_t row0, int64_t n_rows, flo
                                                         page_offset(a.lay, (int)(row % a.P), c)]);
 }
 
-// V_lr = X * A on CUDA cores: a 64-row x r_pad tile per CTA, K staged through shared memory in
-// slices of 32.  X is streamed once from HBM (the bound: d_model*4 bytes per row against 2*r flops
-// per element); A (d_model x r) stays L2 resident.  Accumulation order over k is ascending, like
-// matmul_accumulate (matrix.hpp:101-111).
-constexpr int kProjRows = 64, kProjK = 32, kProjThreads = 256;
-template <class S>
-__global__ void __launch_bounds__(kProjThreads) lr_append_project_kernel(
+// V_lr = X * A (engine.hpp:414-418 through matmul_accumulate, matrix.hpp:101-111), bound by the one
+// pass over X in HBM (d_model * 4 bytes per row against 2 * r flops per element).
+//
+// A warp owns R rows (R * RP = 128 accumulators per lane) and its lanes split the reduction
+// dimension: per 128-wide k chunk lane l takes k = 4l .. 4l+3, so every X row is read as one fully
+// coalesced 512-byte line per chunk and never revisited.  The matching A chunk (128 x RP) is staged
+// once per CTA in shared memory in a [k % 4][column quad][lane] order that makes the per-lane float4
+// reads conflict-free.  The 32 partial sums per output are combined by a halving butterfly
+// (124 shuffles for 128 outputs, not 640) that leaves four consecutive columns of one row per lane.
+constexpr int kProjWarps = 4, kProjChunk = 128;
+
+template <class S, int RP>
+__global__ void __launch_bounds__(kProjWarps * 32) lr_append_project_kernel(
     PageAddr a, int64_t row0, const float* __restrict__ x, int64_t n_rows, int64_t ld,
-    const float* __restrict__ A, int d_model, int rank, bool round_inputs) {
-  __shared__ float x_s[kProjRows][kProjK + 1];
-  extern __shared__ float a_s[];                 // [kProjK][r_pad]
-  const int rp = a.width;
-  const int tid = threadIdx.x;
-  const int r_local = tid / 4;                   // row within the tile
-  const int cg = tid % 4;                        // column group: columns cg, cg+4, ... (<= 32 per thread)
-  const int64_t tile0 = (int64_t)blockIdx.x * kProjRows;
-  float acc[32];
+    const float* __restrict__ A, int d_model, int rank, bool round_inputs, bool vec_ok) {
+  constexpr int R = 128 / RP;                      // rows per warp
+  constexpr int Q4 = RP / 4;                       // column quads
+  extern __shared__ float4 a_dyn[];                // [buffer][i][quad][lane]
+  float4 (*a_s)[4 * Q4 * 32] = reinterpret_cast<float4 (*)[4 * Q4 * 32]>(a_dyn);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t r_first = ((int64_t)blockIdx.x * kProjWarps + warp) * R;
+
+  float acc[R * RP];
 #pragma unroll
-  for (int u = 0; u < 32; ++u) acc[u] = 0.f;
-  for (int k0 = 0; k0 < d_model; k0 += kProjK) {
-    for (int idx = tid; idx < kProjRows * kProjK; idx += kProjThreads) {
-      const int rr = idx / kProjK, kk = idx % kProjK;
-      const int64_t row = tile0 + rr;
-      float v = (row < n_rows && k0 + kk < d_model) ? x[row * ld + k0 + kk] : 0.f;
-      if (round_inputs) v = __bfloat162float(__float2bfloat16_rn(v));
-      x_s[rr][kk] = v;
-    }
-    for (int idx = tid; idx < kProjK * rp; idx += kProjThreads) {
-      const int kk = idx / rp, c = idx % rp;
-      a_s[idx] = (k0 + kk < d_model && c < rank) ? A[(int64_t)(k0 + kk) * rank + c] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < kProjK; ++kk) {
-      const float xv = x_s[r_local][kk];
+  for (int i = 0; i < R * RP; ++i) acc[i] = 0.f;
+
+  auto stage_a = [&](int buf, int k0) {            // A[k0 .. k0+127][0 .. RP) -> a_s[buf]
+    for (int idx = tid; idx < 4 * Q4 * 32; idx += kProjWarps * 32) {
+      const int l = idx % 32, qd = (idx / 32) % Q4, i = idx / (32 * Q4);
+      const int k = k0 + 4 * l + i;
+      float v[4];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) {
-        const int c = cg + 4 * u;
-        if (c < rp) acc[u] = fmaf(xv, a_s[kk * rp + c], acc[u]);
+      for (int u = 0; u < 4; ++u) {
+        const int c = 4 * qd + u;
+        v[u] = (k < d_model && c < rank) ? A[(int64_t)k * rank + c] : 0.f;
+      }
+      a_s[buf][idx] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  };
+
+  const int n_chunks = (d_model + kProjChunk - 1) / kProjChunk;
+  stage_a(0, 0);
+  __syncthreads();
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int buf = ch & 1, k0 = ch * kProjChunk;
+    if (ch + 1 < n_chunks) stage_a(buf ^ 1, k0 + kProjChunk);
+    float xv[R][4];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const int64_t row = r_first + rr;
+      const int k = k0 + 4 * lane;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row < n_rows) {
+        const float* src = x + row * ld + k;
+        if (vec_ok && k + 3 < d_model) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          if (k < d_model) v.x = src[0];
+          if (k + 1 < d_model) v.y = src[1];
+          if (k + 2 < d_model) v.z = src[2];
+          if (k + 3 < d_model) v.w = src[3];
+        }
+      }
+      if (round_inputs) {
+        v.x = __bfloat162float(__float2bfloat16_rn(v.x)); v.y = __bfloat162float(__float2bfloat16_rn(v.y));
+        v.z = __bfloat162float(__float2bfloat16_rn(v.z)); v.w = __bfloat162float(__float2bfloat16_rn(v.w));
+      }
+      xv[rr][0] = v.x; xv[rr][1] = v.y; xv[rr][2] = v.z; xv[rr][3] = v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int qd = 0; qd < Q4; ++qd) {
+        const float4 av = a_s[buf][(i * Q4 + qd) * 32 + lane];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          acc[rr * RP + 4 * qd + 0] = fmaf(xv[rr][i], av.x, acc[rr * RP + 4 * qd + 0]);
+          acc[rr * RP + 4 * qd + 1] = fmaf(xv[rr][i], av.y, acc[rr * RP + 4 * qd + 1]);
+          acc[rr * RP + 4 * qd + 2] = fmaf(xv[rr][i], av.z, acc[rr * RP + 4 * qd + 2]);
+          acc[rr * RP + 4 * qd + 3] = fmaf(xv[rr][i], av.w, acc[rr * RP + 4 * qd + 3]);
+        }
       }
     }
-    __syncthreads();
+    __syncthreads();     // the next chunk of A is staged; the current one may be overwritten after this
   }
-  const int64_t i = tile0 + r_local;
-  if (i >= n_rows) return;
-  const int64_t row = row0 + i;
-  const int64_t phys = a.table[row / a.P];
-  S* dst = static_cast<S*>(a.base) + phys * a.page_stride;
-  const int t = (int)(row % a.P);
+
+  // halving butterfly: after the step with stride s a lane keeps the half of its values selected by
+  // its bit s; at the end lane l holds outputs [4 * bitrev-weighted(l), +4) fully reduced
+  int first = 0;
 #pragma unroll
-  for (int u = 0; u < 32; ++u) {
-    const int c = cg + 4 * u;
-    if (c < rp) dst[page_offset(a.lay, t, c)] = to_store<S>(c < rank ? acc[u] : 0.f);
+  for (int s = 16, n = (R * RP) / 2; s >= 1; s >>= 1, n >>= 1) {
+    const bool upper = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const float send = upper ? acc[i] : acc[i + n];
+      const float keep = upper ? acc[i + n] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+    if (upper) first += n;
   }
+  const int rr = first / RP, c0 = first % RP;       // four consecutive columns of one row
+  const int64_t i_row = r_first + rr;
+  if (i_row >= n_rows) return;
+  const int64_t row = row0 + i_row;
+  const int64_t phys = a.table[row / a.P];
+  S* dst = static_cast<S*>(a.base) + phys * a.page_stride + page_offset(a.lay, (int)(row % a.P), c0);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) dst[u] = to_store<S>(c0 + u < rank ? acc[u] : 0.f);
 }
 
 PageAddr make_addr(const lorakv_pool* pool, int which, int64_t layer, int64_t set) {
@@ -235,15 +289,22 @@ int launch_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t laye
   if (a.width == 0) return LORAKV_OK;
   if (a.width > 128) return fail("lr_append_project: rank %lld > 128 is not supported", (long long)pool->dims.rank);
   const float* A = ad->a + layer * ad->d_model * ad->rank;
-  const unsigned blocks = (unsigned)((n_rows + kProjRows - 1) / kProjRows);
-  const size_t smem = sizeof(float) * kProjK * a.width;
   const bool bf16 = pool->dims.dtype == LORAKV_BF16;
-  if (bf16)
-    lr_append_project_kernel<__nv_bfloat16><<<blocks, kProjThreads, smem, ctx->stream>>>(
-        a, row0, x_dev, n_rows, ld, A, (int)ad->d_model, (int)ad->rank, true);
-  else
-    lr_append_project_kernel<float><<<blocks, kProjThreads, smem, ctx->stream>>>(
-        a, row0, x_dev, n_rows, ld, A, (int)ad->d_model, (int)ad->rank, false);
+  const bool vec_ok = (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x_dev) & 15) == 0);
+  auto launch = [&](auto kern, int rp) {
+    const int rows_per_cta = kProjWarps * (128 / rp);
+    const unsigned blocks = (unsigned)((n_rows + rows_per_cta - 1) / rows_per_cta);
+    const size_t smem = (size_t)2 * rp * 512;       // two [4][rp/4][32] float4 buffers
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<blocks, kProjWarps * 32, smem, ctx->stream>>>(a, row0, x_dev, n_rows, ld, A, (int)ad->d_model, (int)ad->rank, bf16, vec_ok);
+  };
+  switch (a.width) {
+    case 16: bf16 ? launch(lr_append_project_kernel<__nv_bfloat16, 16>, 16) : launch(lr_append_project_kernel<float, 16>, 16); break;
+    case 32: bf16 ? launch(lr_append_project_kernel<__nv_bfloat16, 32>, 32) : launch(lr_append_project_kernel<float, 32>, 32); break;
+    case 64: bf16 ? launch(lr_append_project_kernel<__nv_bfloat16, 64>, 64) : launch(lr_append_project_kernel<float, 64>, 64); break;
+    case 128: bf16 ? launch(lr_append_project_kernel<__nv_bfloat16, 128>, 128) : launch(lr_append_project_kernel<float, 128>, 128); break;
+    default: return fail("lr_append_project: padded rank %d is not one of 16/32/64/128", a.width);
+  }
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;

@@ -243,9 +243,11 @@ int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms);
  * shared-memory operand layouts the prefill kernel uses; B is N x K row-major (b_mn_major = 0, the
  * K-page convention) or K x N row-major (b_mn_major = 1, the V / V_lr page convention).  HOST pointers,
  * operands rounded to bf16, fp32 accumulation in TMEM.  rescale != 0 additionally scales the
- * accumulator by alpha through tcgen05.ld/st and accumulates a second pass: D = (alpha + 1) * A B. */
+ * accumulator by alpha through tcgen05.ld/st and accumulates a second pass: D = (alpha + 1) * A B.
+ * a_in_tmem != 0 feeds A from tensor memory (packed bf16 pairs written with tcgen05.st), the way the
+ * prefill kernel feeds Q and P. */
 int lorakv_selftest_umma(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major,
-                         float alpha, int rescale, float* d);
+                         float alpha, int rescale, int a_in_tmem, float* d);
 
 /* selects the kernel family for the fast paths: 0 = auto (tcgen05/TMA where the shape allows),
  * 1 = force the CUDA-core kernels.  Returns the previous value. */

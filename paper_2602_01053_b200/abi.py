@@ -116,7 +116,7 @@ SIGNATURES = {
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
     "lorakv_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "lorakv_ctx_last_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
-    "lorakv_selftest_umma": (C.c_int, [_vp, _pf, _pf, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, _pf]),
+    "lorakv_selftest_umma": (C.c_int, [_vp, _pf, _pf, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int, _pf]),
     "lorakv_set_kernel_policy": (C.c_int, [_vp, C.c_int]),
     "lorakv_last_kernel": (C.c_char_p, [_vp]),
 }
@@ -206,13 +206,13 @@ class Context:
         _check(self.lib.lorakv_ctx_last_kernel_ms(self.h, C.byref(ms)))
         return float(ms.value)
 
-    def selftest_umma(self, a, b, b_mn_major: bool, alpha: float = 1.0, rescale: bool = False):
+    def selftest_umma(self, a, b, b_mn_major: bool, alpha: float = 1.0, rescale: bool = False, a_in_tmem: bool = False):
         a = np.ascontiguousarray(a, dtype=np.float32); b = np.ascontiguousarray(b, dtype=np.float32)
         K = a.shape[1]
         N = b.shape[1] if b_mn_major else b.shape[0]
         out = np.zeros((128, N), dtype=np.float32)
         _check(self.lib.lorakv_selftest_umma(self.h, a.ctypes.data_as(_pf), b.ctypes.data_as(_pf), N, K, int(b_mn_major),
-                                             alpha, int(rescale), out.ctypes.data_as(_pf)))
+                                             alpha, int(rescale), int(a_in_tmem), out.ctypes.data_as(_pf)))
         return out
 
     def last_kernel(self) -> str:

@@ -257,8 +257,8 @@ int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms) {
 }
 
 int lorakv_selftest_umma(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha,
-                         int rescale, float* d) {
-  return umma_selftest(ctx, a, b, N, K, b_mn_major, alpha, rescale, d);
+                         int rescale, int a_in_tmem, float* d) {
+  return umma_selftest(ctx, a, b, N, K, b_mn_major, alpha, rescale, a_in_tmem, d);
 }
 
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy) {

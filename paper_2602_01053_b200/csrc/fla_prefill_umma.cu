@@ -13,16 +13,22 @@
 // (the reference re-reads it per q head, :347-361).  Key tiles of 128 are visited up to the causal
 // boundary of the CTA's last row; only the boundary tiles pay for the mask.
 //
-// Roles (192 threads):
-//   warps 0-3  softmax + correction + epilogue; thread t owns MMA row t == TMEM lane t
-//   warp 4     TMA producer: bulk copies of K (2 stages) and V_base + V_lr (2 stages), mbarrier tracked
-//   warp 5     MMA issuer (one thread): S(j) = Q K_j^T into one of two TMEM S buffers, then
+// Roles (352 threads):
+//   warps 0-7  softmax + correction + epilogue; warps w and w+4 share MMA rows 32(w%4)..+31 (= TMEM
+//              lanes) and split the 128 key columns of a tile in halves (row max exchanged through smem)
+//   warp 8/10  TMA producers: bulk copies of K (warp 8) and of V_base + V_lr (warp 10) into 3-stage rings,
+//              mbarrier tracked; independent, so a K tile is requested two tiles before its S MMA
+//   warp 9     MMA issuer (one thread): S(j) = Q K_j^T into one of two TMEM S buffers, then
 //              O += P_j V_j and O_lr += P_j V_lr_j; issue order S0 S1 PV0 S2 PV1 S3 ... so the tensor
 //              pipe computes S(j+1) while the softmax warps work on S(j)
-// TMEM (512 columns): S0 [0,128) | S1 [128,256) | O [256,256+D) | O_lr [384,384+RP)
-// P goes through shared memory as a K-major SWIZZLE_128B A operand; masked entries are written as
-// exact zeros and never exponentiated (attention.hpp:171).  Rescaling of O / O_lr is lazy: only when a
-// row's running max grows by more than 8 (log2 units), which leaves the result unchanged.
+// TMEM (512 columns): S0 [0,128) | S1 [128,256) | O [256,256+D) | O_lr [384,384+RP) | Q [448,448+D/2)
+// Q and P never touch shared memory: both are written to TMEM as packed bf16 pairs (tcgen05.st) and fed
+// to tcgen05.mma as the A operand from TMEM; P(j) overwrites the first 64 columns of the S buffer it was
+// computed from.  Shared memory then carries only the K / V / V_lr tiles -- with A in shared memory a
+// 128x128x16 MMA needs 8 KB per 64 cycles, the whole 128 B/clk of the SM, and the kernel was bound by
+// shared-memory bandwidth (ncu, profiles/r1_ncu_prefill_umma_v1.txt).  Masked entries are exact zeros
+// and never exponentiated (attention.hpp:171).  Rescaling of O / O_lr is lazy: only when a row's running
+// max grows by more than 8 (log2 units), which leaves the result unchanged.
 #include <cuda_bf16.h>
 
 #include <limits>
@@ -38,7 +44,8 @@ namespace {
 
 constexpr int kBM = 128;            // MMA rows per CTA
 constexpr int kBN = 128;            // keys per tile
-constexpr int kThreads = 192;
+constexpr int kThreads = 352;        // 8 softmax warps + K producer + MMA issuer + V producer
+constexpr int kMaxStages = 3;
 constexpr float kRescaleThreshold = 8.0f;
 
 struct PrefillParams {
@@ -74,29 +81,30 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 
 struct Barriers {
   uint64_t q_full, p_full, pv_done;
-  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2];
+  uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[2];
 };
 
 template <int D, int RP>
 __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const PrefillParams p) {
   constexpr int kQBlocks = D / 64;                           // 64-column K-blocks of Q / K; 64-column N-blocks of V
   constexpr uint32_t kBlkBytes = kBN * 128;                  // one [128 rows][64] bf16 block = 16 KB
-  constexpr uint32_t kQBytes = kQBlocks * kBlkBytes;
   constexpr uint32_t kKBytes = kQBlocks * kBlkBytes;         // K tile == V tile bytes
   constexpr uint32_t kLrRow = 2 * RP;                        // bytes of one V_lr row
   constexpr uint32_t kLrBytes = kBN * kLrRow;
-  constexpr uint32_t kPBytes = 2 * kBlkBytes;                // [2 key blocks][128 rows][64 keys]
-  constexpr uint32_t kTmemS = 0, kTmemO = 256, kTmemLr = 384;
+  constexpr uint32_t kTmemS = 0, kTmemO = 256, kTmemLr = 384, kTmemQ = 448;
+  // K / V ring depth: three stages hide the L2 latency of a tile behind two tiles of work; the widest
+  // configuration (d 128, rank 64) only has room for two
+  constexpr int kStages = (2 * 3 * kKBytes + 3 * kLrBytes + 1024 <= 227 * 1024 - 4096) ? 3 : 2;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ Barriers bars;
   __shared__ uint32_t tmem_base_s;
+  __shared__ float mx_s[2][2][kBM];     // [tile parity][column half][row]: partial row maxima
+  __shared__ float l_s[2][kBM];         // [column half][row]: partial row sums for the epilogue
   unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* sQ = smem;
-  unsigned char* sK = sQ + kQBytes;                  // 2 stages
-  unsigned char* sV = sK + 2 * kKBytes;              // 2 stages
-  unsigned char* sP = sV + 2 * kKBytes;
-  unsigned char* sLR = sP + kPBytes;                 // 2 stages
+  unsigned char* sK = smem;                          // kStages stages each
+  unsigned char* sV = sK + kStages * kKBytes;
+  unsigned char* sLR = sV + kStages * kKBytes;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int PB = kBM / p.group;                                  // query positions per CTA
@@ -108,14 +116,14 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   const int n_tiles = (int)(last_visible_cta / kBN) + 1;
 
   if (tid == 0) {
-    ptx::mbar_init(&bars.q_full, 128);
-    ptx::mbar_init(&bars.p_full, 128);
+    ptx::mbar_init(&bars.q_full, 256);
+    ptx::mbar_init(&bars.p_full, 256);
     ptx::mbar_init(&bars.pv_done, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&bars.k_full[s], 1); ptx::mbar_init(&bars.k_empty[s], 1);
       ptx::mbar_init(&bars.v_full[s], 1); ptx::mbar_init(&bars.v_empty[s], 1);
-      ptx::mbar_init(&bars.s_full[s], 1);
     }
+    ptx::mbar_init(&bars.s_full[0], 1); ptx::mbar_init(&bars.s_full[1], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc(&tmem_base_s, 512);
@@ -124,16 +132,20 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_s;
 
-  if (warp == 4) {
-    // ===================== TMA producer =====================
+  if (warp == 8 || warp == 10) {
+    // ===================== TMA producers: warp 8 streams K, warp 10 streams V_base + V_lr =====================
     if (lane == 0) {
+      const bool is_k = warp == 8;
       const int tpc = p.P < kBN ? p.P : kBN;           // tokens per bulk copy
       const int n_copies = kBN / tpc;
+      uint64_t* full = is_k ? bars.k_full : bars.v_full;
+      uint64_t* empty = is_k ? bars.k_empty : bars.v_empty;
+      unsigned char* ring = is_k ? sK : sV;
+      const __nv_bfloat16* pages = is_k ? p.k_pages : p.v_pages;
       for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
-        const uint32_t par = (uint32_t)(((j >> 1) & 1) ^ 1);     // parity of the phase that freed the stage
-        if (j >= 2) ptx::mbar_wait(&bars.k_empty[s], par);
-        ptx::mbar_arrive_expect_tx(&bars.k_full[s], kKBytes);
+        const int s = j % kStages;
+        if (j >= kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));   // the phase that freed the stage
+        ptx::mbar_arrive_expect_tx(&full[s], is_k ? kKBytes : kKBytes + kLrBytes);
         for (int i = 0; i < n_copies; ++i) {
           const int64_t key0 = (int64_t)j * kBN + (int64_t)i * tpc;
           int page = (int)(key0 / p.P);
@@ -143,50 +155,35 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
                                (int64_t)tok0 * 64;
 #pragma unroll
           for (int b = 0; b < kQBlocks; ++b)
-            bulk_g2s(ptx::smem_u32(sK + s * kKBytes + b * kBlkBytes + i * tpc * 128), p.k_pages + base + (int64_t)b * p.P * 64,
-                     (uint32_t)tpc * 128u, &bars.k_full[s]);
-        }
-        if (j >= 2) ptx::mbar_wait(&bars.v_empty[s], par);
-        ptx::mbar_arrive_expect_tx(&bars.v_full[s], kKBytes + kLrBytes);
-        for (int i = 0; i < n_copies; ++i) {
-          const int64_t key0 = (int64_t)j * kBN + (int64_t)i * tpc;
-          int page = (int)(key0 / p.P);
-          const int tok0 = (int)(key0 % p.P);
-          if (page >= p.n_pages) page = p.n_pages - 1;
-          const int64_t base = p.kv_layer_off + (int64_t)kvh * p.kv_head_stride + (int64_t)p.kv_table[page] * p.kv_page_stride +
-                               (int64_t)tok0 * 64;
-#pragma unroll
-          for (int b = 0; b < kQBlocks; ++b)
-            bulk_g2s(ptx::smem_u32(sV + s * kKBytes + b * kBlkBytes + i * tpc * 128), p.v_pages + base + (int64_t)b * p.P * 64,
-                     (uint32_t)tpc * 128u, &bars.v_full[s]);
-          if (RP > 0) {
+            bulk_g2s(ptx::smem_u32(ring + s * kKBytes + b * kBlkBytes + i * tpc * 128), pages + base + (int64_t)b * p.P * 64,
+                     (uint32_t)tpc * 128u, &full[s]);
+          if (RP > 0 && !is_k) {
             const int64_t lr_base = p.lr_layer_off + (int64_t)p.lr_table[page] * p.lr_page_stride + (int64_t)tok0 * RP;
-            bulk_g2s(ptx::smem_u32(sLR + s * kLrBytes + i * tpc * kLrRow), p.lr_pages + lr_base, (uint32_t)tpc * kLrRow,
-                     &bars.v_full[s]);
+            bulk_g2s(ptx::smem_u32(sLR + s * kLrBytes + i * tpc * kLrRow), p.lr_pages + lr_base, (uint32_t)tpc * kLrRow, &full[s]);
           }
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
       const uint32_t idesc_s = ptx::instr_desc_bf16(kBM, kBN, ptx::kMajorK, ptx::kMajorK);
       const uint32_t idesc_o = ptx::instr_desc_bf16(kBM, D, ptx::kMajorK, ptx::kMajorMN);
       const uint32_t idesc_lr = ptx::instr_desc_bf16(kBM, RP > 0 ? RP : 16, ptx::kMajorK, ptx::kMajorMN);
       const uint32_t lr_mode = RP == 64 ? ptx::kSw128 : RP == 32 ? ptx::kSw64 : ptx::kSw32;
-      const uint32_t q_addr = ptx::smem_u32(sQ), p_addr = ptx::smem_u32(sP);
       auto issue_s = [&](int j) {
-        const int s = j & 1;
-        ptx::mbar_wait(&bars.k_full[s], (uint32_t)((j >> 1) & 1));
+        const int s = j & 1;                       // S buffer in TMEM
+        const int ks_stage = j % kStages;          // K stage in shared memory
+        ptx::mbar_wait(&bars.k_full[ks_stage], (uint32_t)((j / kStages) & 1));
         ptx::tc_fence_after();
-        const uint32_t k_addr = ptx::smem_u32(sK + s * kKBytes);
+        const uint32_t k_addr = ptx::smem_u32(sK + ks_stage * kKBytes);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
           const uint32_t off = (uint32_t)(ks / 4) * kBlkBytes + (uint32_t)(ks % 4) * 32u;
-          ptx::umma_bf16_ss(tmem + kTmemS + (uint32_t)s * kBN, ptx::smem_desc(q_addr + off, 16u, 1024u, ptx::kSw128),
+          ptx::umma_bf16_ts(tmem + kTmemS + (uint32_t)s * kBN, tmem + kTmemQ + 8u * ks,
                             ptx::smem_desc(k_addr + off, 16u, 1024u, ptx::kSw128), idesc_s, ks > 0 ? 1u : 0u);
         }
-        ptx::umma_commit(&bars.k_empty[s]);
+        ptx::umma_commit(&bars.k_empty[ks_stage]);
         ptx::umma_commit(&bars.s_full[s]);
       };
       ptx::mbar_wait(&bars.q_full, 0);
@@ -194,133 +191,146 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       issue_s(0);
       if (n_tiles > 1) issue_s(1);
       for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
+        const int s = j & 1, vs = j % kStages;
         ptx::mbar_wait(&bars.p_full, (uint32_t)(j & 1));
-        ptx::mbar_wait(&bars.v_full[s], (uint32_t)((j >> 1) & 1));
+        ptx::mbar_wait(&bars.v_full[vs], (uint32_t)((j / kStages) & 1));
         ptx::tc_fence_after();
-        const uint32_t v_addr = ptx::smem_u32(sV + s * kKBytes), lr_addr = ptx::smem_u32(sLR + s * kLrBytes);
+        const uint32_t v_addr = ptx::smem_u32(sV + vs * kKBytes), lr_addr = ptx::smem_u32(sLR + vs * kLrBytes);
 #pragma unroll
         for (int ks = 0; ks < kBN / 16; ++ks) {
-          const uint64_t pd = ptx::smem_desc(p_addr + (uint32_t)(ks / 4) * kBlkBytes + (uint32_t)(ks % 4) * 32u, 16u, 1024u, ptx::kSw128);
-          ptx::umma_bf16_ss(tmem + kTmemO, pd, ptx::smem_desc(v_addr + (uint32_t)ks * 2048u, kBlkBytes, 1024u, ptx::kSw128), idesc_o,
+          const uint32_t p_tmem = tmem + kTmemS + (uint32_t)s * kBN + 8u * ks;    // P(j) sits in the S(j) buffer
+          ptx::umma_bf16_ts(tmem + kTmemO, p_tmem, ptx::smem_desc(v_addr + (uint32_t)ks * 2048u, kBlkBytes, 1024u, ptx::kSw128), idesc_o,
                             (j > 0 || ks > 0) ? 1u : 0u);
           if (RP > 0)
-            ptx::umma_bf16_ss(tmem + kTmemLr, pd, ptx::smem_desc(lr_addr + (uint32_t)ks * 16u * kLrRow, kBN * kLrRow, 8u * kLrRow, lr_mode),
+            ptx::umma_bf16_ts(tmem + kTmemLr, p_tmem, ptx::smem_desc(lr_addr + (uint32_t)ks * 16u * kLrRow, kBN * kLrRow, 8u * kLrRow, lr_mode),
                               idesc_lr, (j > 0 || ks > 0) ? 1u : 0u);
         }
-        ptx::umma_commit(&bars.v_empty[s]);
+        ptx::umma_commit(&bars.v_empty[vs]);
         ptx::umma_commit(&bars.pv_done);
         if (j + 2 < n_tiles) issue_s(j + 2);
       }
     }
   } else {
-    // ===================== softmax / correction / epilogue: thread t == row t =====================
-    const int row = tid;
-    const int hg = row / PB;                                // q head within the group
+    // ===================== softmax / correction / epilogue =====================
+    // warp w and warp w + 4 share MMA rows 32 (w % 4) .. +31 (the TMEM lanes both may touch) and split
+    // the 128 key columns of a tile in halves; thread (w, lane) owns row 32 (w % 4) + lane, half w / 4
+    const int row = (warp & 3) * 32 + lane;
+    const int half = warp >> 2;
+    const int pair_bar = 1 + (warp & 3);                     // named barrier of the two warps sharing rows
+    const int hg = row / PB;                                 // q head within the group
     int64_t pos_local = row % PB;
     if (pos_local >= rows_here) pos_local = rows_here - 1;   // padding rows shadow the last real one
     const bool real_row = (row % PB) < rows_here;
     const int64_t pos = q0 + pos_local;
     const int64_t last_visible = p.query_offset + pos;
     const float ninf = -std::numeric_limits<float>::infinity();
+    constexpr int kHalf = kBN / 2;                           // key columns per thread
 
-    // ---- Q tile: coalesced fp32 rows -> bf16, K-major SWIZZLE_128B blocks ----
-    for (int rr = warp * 32; rr < warp * 32 + 32; ++rr) {
-      int64_t pl = rr % PB;
-      if (pl >= rows_here) pl = rows_here - 1;
-      const float* src = p.q + (q0 + pl) * (p.n_q_local * D) + ((int64_t)kvh * p.group + rr / PB) * D;
-      if (4 * lane < D) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(src) + lane);
-        const int col = 4 * lane;
-        const uint32_t off = (uint32_t)(col / 64) * kBlkBytes + ptx::sw128_offset((uint32_t)rr, (uint32_t)(col % 64));
-        *reinterpret_cast<uint2*>(sQ + off) = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    // ---- Q tile -> TMEM: this thread's half of its row, fp32 -> packed bf16 pairs ----
+    {
+      const float* src = p.q + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D + half * (D / 2);
+#pragma unroll
+      for (int c0 = 0; c0 < D / 4; c0 += 16) {          // D/4 packed columns per thread, 16 per store
+        uint32_t r16[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(src + 2 * (c0 + i)));
+          r16[i] = pack_bf16(v.x, v.y);
+          r16[i + 1] = pack_bf16(v.z, v.w);
+        }
+        ptx::tmem_st16(tmem + lane_base + kTmemQ + (uint32_t)half * (D / 4) + c0, r16);
       }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&bars.q_full);
     }
-    ptx::fence_proxy_async_smem();
-    ptx::mbar_arrive(&bars.q_full);
 
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    float m_used = ninf, l_run = 0.f;
+    float m_used = ninf;          // identical in both threads of a row (in raw-score units times scale_log2)
+    float l_run = 0.f;            // this thread's half of the row sum
     for (int j = 0; j < n_tiles; ++j) {
       const int sb = j & 1;
       ptx::mbar_wait(&bars.s_full[sb], (uint32_t)((j >> 1) & 1));
       ptx::tc_fence_after();
-      float sc[kBN];
+      float sc[kHalf];
       {
-        uint32_t raw[kBN];
-        ptx::tmem_ld128_wait(tmem + lane_base + kTmemS + (uint32_t)sb * kBN, raw);
+        uint32_t raw[kHalf];
+        ptx::tmem_ld64_wait(tmem + lane_base + kTmemS + (uint32_t)sb * kBN + (uint32_t)half * kHalf, raw);
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) sc[c] = __uint_as_float(raw[c]);
+        for (int c = 0; c < kHalf; ++c) sc[c] = __uint_as_float(raw[c]);
       }
 
-      const int64_t key0 = (int64_t)j * kBN;
-      const bool tile_needs_mask = key0 + kBN - 1 > p.query_offset + q0;   // CTA-uniform
-      float mx = ninf;
+      const int64_t key0 = (int64_t)j * kBN + half * kHalf;
+      const bool tile_needs_mask = (int64_t)j * kBN + kBN - 1 > p.query_offset + q0;   // CTA-uniform
       if (tile_needs_mask) {
 #pragma unroll
-        for (int c = 0; c < kBN; ++c) {
-          sc[c] = (key0 + c <= last_visible) ? sc[c] * p.scale_log2 : ninf;
-          mx = fmaxf(mx, sc[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < kBN; ++c) {
-          sc[c] *= p.scale_log2;
-          mx = fmaxf(mx, sc[c]);
-        }
+        for (int c = 0; c < kHalf; ++c)
+          if (key0 + c > last_visible) sc[c] = ninf;
       }
+      // row max of the raw scores: 8 independent chains, then the partner's half through shared memory
+      float mx8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mx8[u] = sc[u];
+#pragma unroll
+      for (int c = 8; c < kHalf; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sc[c]);
+      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])), fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      mx_s[j & 1][half][row] = mx;
+      named_bar_sync(pair_bar, 64);
+      mx = fmaxf(mx, mx_s[j & 1][half ^ 1][row]) * p.scale_log2;     // scale > 0 commutes with max; -inf stays -inf
+
       const float m_cand = fmaxf(m_used, mx);
       const bool grow = m_cand > m_used + kRescaleThreshold;
       if (j == 0) {
         m_used = m_cand;          // key 0 is visible to every row, so this is finite
       } else if (__any_sync(0xffffffffu, grow)) {
-        // correction: O and O_lr of this row are final for tile j-1 once pv_done(j-1) has fired
+        // correction: O and O_lr of this row are final for tile j-1 once pv_done(j-1) has fired;
+        // the two warps of a pair take the decision on identical values and split the columns
         ptx::mbar_wait(&bars.pv_done, (uint32_t)((j - 1) & 1));
         ptx::tc_fence_after();
         const float alpha = grow ? ex2(m_used - m_cand) : 1.f;
         if (grow) { m_used = m_cand; l_run *= alpha; }
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 16) {
+        for (int c0 = 0; c0 < D / 2; c0 += 16) {
           uint32_t r16[16];
-          ptx::tmem_ld16(tmem + lane_base + kTmemO + c0, r16);
+          const uint32_t addr = tmem + lane_base + kTmemO + (uint32_t)half * (D / 2) + c0;
+          ptx::tmem_ld16(addr, r16);
           ptx::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 16; ++i) r16[i] = __float_as_uint(__uint_as_float(r16[i]) * alpha);
-          ptx::tmem_st16(tmem + lane_base + kTmemO + c0, r16);
+          ptx::tmem_st16(addr, r16);
         }
+        if (half == 0) {
 #pragma unroll
-        for (int c0 = 0; c0 < RP; c0 += 16) {
-          uint32_t r16[16];
-          ptx::tmem_ld16(tmem + lane_base + kTmemLr + c0, r16);
-          ptx::tmem_wait_ld();
+          for (int c0 = 0; c0 < RP; c0 += 16) {
+            uint32_t r16[16];
+            ptx::tmem_ld16(tmem + lane_base + kTmemLr + c0, r16);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) r16[i] = __float_as_uint(__uint_as_float(r16[i]) * alpha);
-          ptx::tmem_st16(tmem + lane_base + kTmemLr + c0, r16);
+            for (int i = 0; i < 16; ++i) r16[i] = __float_as_uint(__uint_as_float(r16[i]) * alpha);
+            ptx::tmem_st16(tmem + lane_base + kTmemLr + c0, r16);
+          }
         }
         ptx::tmem_wait_st();
       }
-      // P = exp2(s - m); masked entries are exact zeros
-      float lsum = 0.f;
+      // P = exp2(s * scale - m) in one FFMA + MUFU; masked entries (-inf) come out as exact zeros
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < kBN; ++c) {
-        const float e = ex2(sc[c] - m_used);     // ex2(-inf) == 0 for masked entries
+      for (int c = 0; c < kHalf; ++c) {
+        const float e = ex2(fmaf(sc[c], p.scale_log2, -m_used));
         sc[c] = e;
-        lsum += e;
+        ls4[c & 3] += e;
       }
-      l_run += lsum;
-      // the P buffer (and O) is free once PV(j-1) has completed
-      if (j > 0) ptx::mbar_wait(&bars.pv_done, (uint32_t)((j - 1) & 1));
+      l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      // P(j) -> TMEM, over the first 64 columns of the S(j) buffer: both threads of the row have read
+      // their scores (the pair barrier above), and S(j+2) is issued behind PV(j) on the in-order pipe
 #pragma unroll
-      for (int ch = 0; ch < kBN / 8; ++ch) {
-        uint4 v;
-        v.x = pack_bf16(sc[8 * ch + 0], sc[8 * ch + 1]);
-        v.y = pack_bf16(sc[8 * ch + 2], sc[8 * ch + 3]);
-        v.z = pack_bf16(sc[8 * ch + 4], sc[8 * ch + 5]);
-        v.w = pack_bf16(sc[8 * ch + 6], sc[8 * ch + 7]);
-        const uint32_t off = (uint32_t)(ch / 8) * kBlkBytes + (uint32_t)row * 128u + (uint32_t)(((ch % 8) ^ (row & 7)) << 4);
-        *reinterpret_cast<uint4*>(sP + off) = v;
+      for (int c0 = 0; c0 < kHalf / 2; c0 += 16) {
+        uint32_t r16[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) r16[i] = pack_bf16(sc[2 * (c0 + i)], sc[2 * (c0 + i) + 1]);
+        ptx::tmem_st16(tmem + lane_base + kTmemS + (uint32_t)sb * kBN + (uint32_t)half * (kHalf / 2) + c0, r16);
       }
-      ptx::fence_proxy_async_smem();
+      ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bars.p_full);
     }
@@ -329,9 +339,11 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     ptx::mbar_wait(&bars.pv_done, (uint32_t)((n_tiles - 1) & 1));
     ptx::tc_fence_after();
     float* b_s = reinterpret_cast<float*>(sK);            // K stages are idle now: stage B[r][D] of this kv head
-    for (int idx = tid; idx < p.r * D; idx += 128)
+    for (int idx = tid; idx < p.r * D; idx += 256)
       b_s[idx] = p.b[(int64_t)(idx / D) * ((int64_t)p.n_kv_local * D) + (int64_t)kvh * D + idx % D];
-    named_bar_sync(1, 128);
+    l_s[half][row] = l_run;
+    named_bar_sync(9, 256);
+    const float inv_l = 1.0f / (l_s[0][row] + l_s[1][row]);
     float w[RP > 0 ? RP : 1];
 #pragma unroll
     for (int c0 = 0; c0 < RP; c0 += 16) {
@@ -341,10 +353,10 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
 #pragma unroll
       for (int i = 0; i < 16; ++i) w[c0 + i] = p.lr_scale * __uint_as_float(r16[i]);
     }
-    const float inv_l = 1.0f / l_run;
     float* dst = p.out + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D;
 #pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 16) {
+    for (int cc = 0; cc < D / 2; cc += 16) {
+      const int c0 = half * (D / 2) + cc;
       uint32_t r16[16];
       ptx::tmem_ld16(tmem + lane_base + kTmemO + c0, r16);
       ptx::tmem_wait_ld();
@@ -374,7 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
 template <int D, int RP>
 int launch_t(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid) {
   const size_t blk = (size_t)kBN * 128;
-  const size_t smem = (D / 64) * blk * 5 + 2 * blk + 2 * (size_t)kBN * 2 * RP + 1024;
+  const size_t kv = (D / 64) * blk, lr = (size_t)kBN * 2 * RP;
+  const int stages = (2 * 3 * kv + 3 * lr + 1024 <= (size_t)227 * 1024 - 4096) ? 3 : 2;   // mirrors kStages in the kernel
+  const size_t smem = stages * (2 * kv + lr) + 1024;
   auto kern = fla_prefill_umma_kernel<D, RP>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);

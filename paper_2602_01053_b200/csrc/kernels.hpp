@@ -67,6 +67,6 @@ int launch_prefill_umma(const PagedAttnCall& call);
 
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
-                  float* d);
+                  int a_in_tmem, float* d);
 
 }  // namespace lk

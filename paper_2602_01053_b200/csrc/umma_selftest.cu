@@ -21,7 +21,7 @@ namespace {
 
 __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                                int N, int K, int b_mn_major, float alpha, int rescale,
-                                                               float* __restrict__ D) {
+                                                               int a_in_tmem, float* __restrict__ D) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base_s;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
   }
   ptx::fence_proxy_async_smem();
   uint32_t cols = 32;
-  while ((int)cols < N) cols *= 2;
+  while ((int)cols < N + (a_in_tmem ? K / 2 : 0)) cols *= 2;   // A (packed bf16 pairs) sits behind the accumulator
   if (warp == 0) ptx::tmem_alloc(&tmem_base_s, cols);
   if (tid == 0) { ptx::mbar_init(&bar, 1); ptx::fence_barrier_init(); }
   ptx::tc_fence_before();
@@ -57,6 +57,24 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_s;
 
+  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+  if (a_in_tmem) {
+    // thread = row: column c of the A region holds (A[row][2c], A[row][2c+1]) as packed bf16
+    const int row = warp * 32 + lane;
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t r[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const __nv_bfloat162 v = __floats2bfloat162_rn(A[row * K + 2 * (c0 + i)], A[row * K + 2 * (c0 + i) + 1]);
+        r[i] = *reinterpret_cast<const uint32_t*>(&v);
+      }
+      ptx::tmem_st16(lane_addr + (uint32_t)N + c0, r);
+    }
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
   const uint32_t idesc = ptx::instr_desc_bf16(128, (uint32_t)N, ptx::kMajorK, b_mn_major ? ptx::kMajorMN : ptx::kMajorK);
   const uint32_t a_base = ptx::smem_u32(sA), b_base = ptx::smem_u32(sB);
   auto issue_all = [&](bool accumulate_first) {
@@ -70,7 +88,8 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
         const uint32_t mode = lay.bw == 64 ? ptx::kSw128 : lay.bw == 32 ? ptx::kSw64 : ptx::kSw32;
         db = ptx::smem_desc(b_base + (uint32_t)ks * 16u * W, (uint32_t)K * W, 8u * W, mode);
       }
-      ptx::umma_bf16_ss(tmem, da, db, idesc, (accumulate_first || ks > 0) ? 1u : 0u);
+      if (a_in_tmem) ptx::umma_bf16_ts(tmem, tmem + (uint32_t)N + 8u * ks, db, idesc, (accumulate_first || ks > 0) ? 1u : 0u);
+      else ptx::umma_bf16_ss(tmem, da, db, idesc, (accumulate_first || ks > 0) ? 1u : 0u);
     }
   };
   if (tid == 0) {
@@ -79,7 +98,6 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
   }
   ptx::mbar_wait(&bar, 0);
   ptx::tc_fence_after();
-  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
   if (rescale) {
     for (int c0 = 0; c0 < N; c0 += 16) {
       uint32_t r[16];
@@ -115,7 +133,7 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
 }  // namespace
 
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
-                  float* d) {
+                  int a_in_tmem, float* d) {
   if (!ctx || !a || !b || !d) return fail("selftest_umma: null argument");
   if (K != 64 && K != 128) return fail("selftest_umma: K must be 64 or 128");
   if (N < 16 || N > 256 || N % 16 != 0) return fail("selftest_umma: N must be a multiple of 16 in [16, 256]");
@@ -131,7 +149,7 @@ int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K,
   LK_CUDA(cudaMemcpyAsync(db, b, nb, cudaMemcpyHostToDevice, ctx->stream));
   const size_t smem = (size_t)128 * K * 2 + (size_t)N * K * 2 + 1024;
   LK_CUDA(cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  umma_selftest_kernel<<<1, 128, smem, ctx->stream>>>(da, db, N, K, b_mn_major, alpha, rescale, dd);
+  umma_selftest_kernel<<<1, 128, smem, ctx->stream>>>(da, db, N, K, b_mn_major, alpha, rescale, a_in_tmem, dd);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   LK_CUDA(cudaMemcpyAsync(d, dd, nd, cudaMemcpyDeviceToHost, ctx->stream));

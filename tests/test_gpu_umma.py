@@ -25,14 +25,15 @@ def bf16(x):
                                           (128, 128, True), (64, 128, True), (32, 128, True), (16, 128, True),
                                           (192, 64, True), (16, 64, True)])
 @pytest.mark.parametrize("rescale", [False, True])
-def test_umma_tile_matches_host_matmul(ctx, N, K, mn_major, rescale):
+@pytest.mark.parametrize("a_in_tmem", [False, True])
+def test_umma_tile_matches_host_matmul(ctx, N, K, mn_major, rescale, a_in_tmem):
     rng = np.random.default_rng(N * 1000 + K + int(mn_major))
     a = bf16(rng.standard_normal((128, K)))
     b = bf16(rng.standard_normal((K, N) if mn_major else (N, K)))
     want = a.astype(np.float64) @ (b if mn_major else b.T).astype(np.float64)
     alpha = 0.375
-    got = ctx.selftest_umma(a, b, mn_major, alpha=alpha, rescale=rescale)
+    got = ctx.selftest_umma(a, b, mn_major, alpha=alpha, rescale=rescale, a_in_tmem=a_in_tmem)
     if rescale:
         want = want * (alpha + 1.0)
     err = np.abs(got - want).max() / np.abs(want).max()
-    assert err <= 1e-5, (N, K, mn_major, rescale, err)
+    assert err <= 1e-5, (N, K, mn_major, rescale, a_in_tmem, err)

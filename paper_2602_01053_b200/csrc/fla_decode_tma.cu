@@ -24,6 +24,7 @@
 // exponentiated (p = 0 exactly), matching attention.hpp:154-171.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <limits>
 
 #include "kernels.hpp"
@@ -52,14 +53,22 @@ struct DecodeParams {
   int64_t G;             // tiles per worker
   int max_seg, n_stages;
   float scale_log2;      // (1/sqrt(d)) * log2(e)
+  uint64_t l2_policy;    // cache-hint operand of the bulk copies (0 = none)
   const float* q;        // [layers][n_batch][n_q_local * d]
   float* part;           // [workers * max_seg][16 * MW][4 + D + RP]
 };
 
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(dst), "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
-               : "memory");
+// The cache is streamed exactly once per step, so the copies carry an L2 evict-first policy: the lines
+// should not displace the small reused operands (page tables, partials, B).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  if (policy != 0)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar)), "l"(policy)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+                 : "memory");
 }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -134,44 +143,56 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
   // page-table window held across the lanes of the producer warp: lane i caches logical page base + i
   int win_base = -(1 << 30), win_kv = 0, win_lr = 0;
 
-  auto issue = [&](int i) {       // whole producer warp; lane 0 talks to the TMA engine
-    const int64_t gt = g0 + i;
-    const int64_t u = gt / p.T;
-    const int tl = (int)(gt - u * p.T);
-    const int layer_rel = (int)(u / units_per_layer);
-    const int kvh = (int)((u / p.row_blocks) % p.n_kv_local);
-    const int key0 = tl * kTK;
-    const int page = key0 / p.P, tok0 = key0 % p.P;
-    if (page < win_base || page >= win_base + 32) {
-      win_base = page;
-      const int pg = page + lane;
+  // Producer cursor.  Everything the per-tile path needs is carried incrementally (unit, tile, page,
+  // token, stage, wrap count): the only divisions happen here and at unit changes, never per tile.
+  const int T32 = (int)p.T;
+  int64_t p_unit = g0 / p.T;
+  int p_tl = (int)(g0 - p_unit * p.T);
+  int p_page = (p_tl * kTK) / p.P, p_tok = (p_tl * kTK) % p.P;
+  int p_layer = (int)(p_unit / units_per_layer), p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
+  int p_stage = 0, p_wrap = 0, p_issued = 0;
+
+  auto issue_next = [&]() {       // whole producer warp; lane 0 talks to the TMA engine
+    if (p_page < win_base || p_page >= win_base + 32) {
+      win_base = p_page;
+      const int pg = p_page + lane;
       win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
       if (RP > 0) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
     }
-    const int phys_kv = __shfl_sync(0xffffffffu, win_kv, page - win_base);
-    const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, page - win_base) : 0;
+    const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
+    const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
     if (lane == 0) {
-      const int s = i % NS;
-      const uint32_t dst = ring + (uint32_t)s * kStageBytes;
-      const int64_t layer = p.layer_begin + layer_rel;
-      const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)kvh * p.kv_head_stride +
-                             (int64_t)phys_kv * p.kv_page_stride + (int64_t)tok0 * 64;
-      ptx::mbar_arrive_expect_tx(&full[s], kStageBytes);
+      const uint32_t dst = ring + (uint32_t)p_stage * kStageBytes;
+      const int64_t layer = p.layer_begin + p_layer;
+      const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride +
+                             (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * 64;
+      ptx::mbar_arrive_expect_tx(&full[p_stage], kStageBytes);
 #pragma unroll
       for (int b = 0; b < kBlocks; ++b) {
-        bulk_g2s(dst + b * kBlockBytes, p.k_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[s]);
-        bulk_g2s(dst + kKvBytes + b * kBlockBytes, p.v_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[s]);
+        bulk_g2s(dst + b * kBlockBytes, p.k_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[p_stage], p.l2_policy);
+        bulk_g2s(dst + kKvBytes + b * kBlockBytes, p.v_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[p_stage], p.l2_policy);
       }
       if (RP > 0) {
-        const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)tok0 * RP;
-        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[s]);
+        const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
+        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.l2_policy);
       }
+    }
+    // advance the cursor
+    ++p_issued;
+    if (++p_stage == NS) { p_stage = 0; ++p_wrap; }
+    p_tok += kTK;
+    if (p_tok == p.P) { p_tok = 0; ++p_page; }
+    if (++p_tl == T32) {
+      p_tl = 0; p_page = 0; p_tok = 0;
+      ++p_unit;
+      p_layer = (int)(p_unit / units_per_layer);
+      p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
     }
   };
 
   if (producer) {
     const int pre = n < NS ? n : NS;
-    for (int i = 0; i < pre; ++i) issue(i);
+    for (int i = 0; i < pre; ++i) issue_next();
   }
 
   const float ninf = -std::numeric_limits<float>::infinity();
@@ -204,10 +225,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
   // ldmatrix lane roles
   const int mi = lane >> 3, rr = lane & 7;
 
+  // consumer cursor, carried incrementally like the producer's
+  int64_t u = g0 / p.T;
+  int tl = (int)(g0 - u * p.T);
+  int c_stage = 0, c_wrap = 0;
   for (int i = 0; i < n; ++i) {
-    const int64_t gt = g0 + i;
-    const int64_t u = gt / p.T;
-    const int tl = (int)(gt - u * p.T);
     if (u != cur_unit) {
       if (cur_unit >= 0) flush();
       cur_unit = u;
@@ -238,13 +260,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
       for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
     }
 
-    // refill the stage released one iteration ago
-    if (producer && i >= 1 && i - 1 + NS < n) {
-      ptx::mbar_wait(&empty[(i - 1) % NS], (uint32_t)(((i - 1) / NS) & 1));
-      issue(i - 1 + NS);
+    // refill the stage released one iteration ago (tile p_issued goes where tile p_issued - NS was)
+    if (producer && i >= 1 && p_issued < n) {
+      ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
+      issue_next();
     }
-    const int s = i % NS;
-    ptx::mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+    const int s = c_stage;
+    ptx::mbar_wait(&full[s], (uint32_t)(c_wrap & 1));
 
     const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
 
@@ -356,6 +378,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
     // this warp is done with the stage
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (++c_stage == NS) { c_stage = 0; ++c_wrap; }
+    if (++tl == T32) { tl = 0; ++u; }
   }
   flush();
 }
@@ -526,6 +550,11 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.L = c.L; dp.layer_begin = c.layer_begin; dp.n_q_local = c.n_q_local;
   dp.T = T; dp.total_tiles = total; dp.G = G; dp.max_seg = max_seg; dp.n_stages = n_stages;
   dp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
+  {
+    const char* env = getenv("LORAKV_DECODE_L2_HINT");   // experiment knob: 0 = no hint, 1 = evict_first (default), 2 = evict_last
+    const int mode = env ? atoi(env) : 1;
+    dp.l2_policy = mode == 1 ? ptx::kEvictFirst : mode == 2 ? ptx::kEvictLast : 0;
+  }
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, rp));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, rp));

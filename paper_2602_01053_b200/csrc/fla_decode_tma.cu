@@ -37,7 +37,7 @@ namespace lk {
 namespace {
 
 constexpr int kWarps = 8;           // warps per CTA
-constexpr int kTK = 16;             // keys per tile
+constexpr int kKeyStep = 16;        // keys per MMA k-step; a tile is KT of them
 constexpr int kMaxStages = 24;      // ring depth limit per worker
 constexpr int kRingBudget = 216 * 1024;   // of the 227 KB a CTA may own
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p stays <= 2^8 between rescales
@@ -97,9 +97,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-// D = d_head (64 / 128), RP = padded rank (0 / 8 / 16 / 32 / 64), MW = warps per worker
-template <int D, int RP, int MW>
+// D = d_head (64 / 128), RP = padded rank (0 / 8 / 16 / 32 / 64), MW = warps per worker, KT = 16-key
+// steps per tile (1 for single-warp workers whose eight rings must share the SM's shared memory; 2 for
+// the multi-warp workers, which halves their per-tile synchronisation and doubles the MMA ILP)
+template <int D, int RP, int MW, int KT>
 __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
+  constexpr int kTK = kKeyStep * KT;                    // keys per tile
   constexpr int kWorkers = kWarps / MW;
   constexpr int kBlocks = D / 64;                       // 64-column blocks of a K / V page
   constexpr uint32_t kBlockBytes = kTK * 128;           // one block of one tile
@@ -270,29 +273,33 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
 
     const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
 
-    // ---- S = Q K^T : 16 rows x 16 keys ------------------------------------------------------
-    float sc[2][4];
+    // ---- S = Q K^T : 16 rows x 16 KT keys ---------------------------------------------------
+    constexpr int NT = 2 * KT;      // n8 tiles of S
+    float sc[NT][4];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+    for (int nt = 0; nt < NT; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
     {
       const int key = (mi >> 1) * 8 + rr;
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
         const int chunk = 2 * kk + (mi & 1);
-        const uint32_t addr = sK + (uint32_t)(chunk >> 3) * kBlockBytes + (uint32_t)key * 128u +
-                              (uint32_t)(((chunk & 7) ^ rr) << 4);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(addr, b0, b1, b2, b3);
-        mma_bf16(sc[0], qa[kk], b0, b1);
-        mma_bf16(sc[1], qa[kk], b2, b3);
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const uint32_t addr = sK + (uint32_t)(chunk >> 3) * kBlockBytes + (uint32_t)(key + 16 * kt) * 128u +
+                                (uint32_t)(((chunk & 7) ^ rr) << 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(addr, b0, b1, b2, b3);
+          mma_bf16(sc[2 * kt], qa[kk], b0, b1);
+          mma_bf16(sc[2 * kt + 1], qa[kk], b2, b3);
+        }
       }
     }
 
     // ---- online softmax (exp2 domain), rows g and g + 8 ------------------------------------------
     const int64_t key_base = (int64_t)tl * kTK + 2 * t;
-    bool valid[2][2];
+    bool valid[NT][2];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) valid[nt][e] = key_base + 8 * nt + e < p.L;
     float tmax[2];
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
     for (int h = 0; h < 2; ++h) {
       float mx = ninf;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const float v = valid[nt][e] ? sc[nt][2 * h + e] * p.scale_log2 : ninf;
@@ -325,23 +332,26 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
         for (int nt = 0; nt < kNL; ++nt) { olr[nt][2 * h] *= alpha; olr[nt][2 * h + 1] *= alpha; }
       }
     }
-    uint32_t pa[4];
+    uint32_t pa[KT][4];
     {
-      float pv[2][4];
+      float pv[NT][4];
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const float x = valid[nt][e] ? ex2(sc[nt][2 * h + e] - m_used[h]) : 0.f;
             pv[nt][2 * h + e] = x;
             l_run[h] += x;
           }
-      pa[0] = pack_bf16(pv[0][0], pv[0][1]);
-      pa[1] = pack_bf16(pv[0][2], pv[0][3]);
-      pa[2] = pack_bf16(pv[1][0], pv[1][1]);
-      pa[3] = pack_bf16(pv[1][2], pv[1][3]);
+#pragma unroll
+      for (int kt = 0; kt < KT; ++kt) {
+        pa[kt][0] = pack_bf16(pv[2 * kt][0], pv[2 * kt][1]);
+        pa[kt][1] = pack_bf16(pv[2 * kt][2], pv[2 * kt][3]);
+        pa[kt][2] = pack_bf16(pv[2 * kt + 1][0], pv[2 * kt + 1][1]);
+        pa[kt][3] = pack_bf16(pv[2 * kt + 1][2], pv[2 * kt + 1][3]);
+      }
     }
 
     // ---- O += P V_base, O_lr += P V_lr ---------------------------------------------------------------
@@ -350,28 +360,37 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
 #pragma unroll
       for (int np = 0; np < D / 16; ++np) {
         const int chunk = 2 * np + (mi >> 1);
-        const uint32_t addr = sV + (uint32_t)(chunk >> 3) * kBlockBytes + (uint32_t)key * 128u +
-                              (uint32_t)(((chunk & 7) ^ rr) << 4);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(addr, b0, b1, b2, b3);
-        mma_bf16(o[2 * np], pa, b0, b1);
-        mma_bf16(o[2 * np + 1], pa, b2, b3);
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          const uint32_t addr = sV + (uint32_t)(chunk >> 3) * kBlockBytes + (uint32_t)(key + 16 * kt) * 128u +
+                                (uint32_t)(((chunk & 7) ^ rr) << 4);
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(addr, b0, b1, b2, b3);
+          mma_bf16(o[2 * np], pa[kt], b0, b1);
+          mma_bf16(o[2 * np + 1], pa[kt], b2, b3);
+        }
       }
       if (RP >= 16) {
 #pragma unroll
         for (int np = 0; np < RP / 16; ++np) {
           const int chunk = 2 * np + (mi >> 1);
-          uint32_t off = (uint32_t)key * (2u * RP) + (uint32_t)chunk * 16u;
-          off ^= ((off >> 7) & (uint32_t)(RP / 8 - 1)) << 4;
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(sLR + off, b0, b1, b2, b3);
-          mma_bf16(olr[2 * np], pa, b0, b1);
-          mma_bf16(olr[2 * np + 1], pa, b2, b3);
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            uint32_t off = (uint32_t)(key + 16 * kt) * (2u * RP) + (uint32_t)chunk * 16u;
+            off ^= ((off >> 7) & (uint32_t)(RP / 8 - 1)) << 4;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(sLR + off, b0, b1, b2, b3);
+            mma_bf16(olr[2 * np], pa[kt], b0, b1);
+            mma_bf16(olr[2 * np + 1], pa[kt], b2, b3);
+          }
         }
       } else if (RP == 8) {
-        uint32_t b0, b1;
-        ldsm_x2_t(sLR + (uint32_t)key * 16u, b0, b1);     // lanes 16..31 pass valid, unused addresses
-        mma_bf16(olr[0], pa, b0, b1);
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+          uint32_t b0, b1;
+          ldsm_x2_t(sLR + (uint32_t)(key + 16 * kt) * 16u, b0, b1);     // lanes 16..31 pass valid, unused addresses
+          mma_bf16(olr[0], pa[kt], b0, b1);
+        }
       }
     }
 
@@ -456,9 +475,9 @@ __global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMerge
   }
 }
 
-template <int D, int RP, int MW>
+template <int D, int RP, int MW, int KT>
 int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
-  auto kern = fla_decode_tma_kernel<D, RP, MW>;
+  auto kern = fla_decode_tma_kernel<D, RP, MW, KT>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);
   kern<<<grid, kWarps * 32, smem, ctx->stream>>>(dp);
@@ -469,23 +488,29 @@ int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem
 }
 
 template <int D, int RP>
-int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw) {
+int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt) {
+  if (mw == 1) return launch_t<D, RP, 1, 1>(ctx, dp, grid, smem);
+  if (kt == 2) {
+    switch (mw) {
+      case 2: return launch_t<D, RP, 2, 2>(ctx, dp, grid, smem);
+      case 4: return launch_t<D, RP, 4, 2>(ctx, dp, grid, smem);
+      default: return launch_t<D, RP, 8, 2>(ctx, dp, grid, smem);
+    }
+  }
   switch (mw) {
-    case 1: return launch_t<D, RP, 1>(ctx, dp, grid, smem);
-    case 2: return launch_t<D, RP, 2>(ctx, dp, grid, smem);
-    case 4: return launch_t<D, RP, 4>(ctx, dp, grid, smem);
-    default: return launch_t<D, RP, 8>(ctx, dp, grid, smem);
+    case 2: return launch_t<D, RP, 2, 1>(ctx, dp, grid, smem);
+    case 4: return launch_t<D, RP, 4, 1>(ctx, dp, grid, smem);
+    default: return launch_t<D, RP, 8, 1>(ctx, dp, grid, smem);
   }
 }
 
 template <int D>
-int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int rp) {
+int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt, int rp) {
   switch (rp) {
-    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw);
-    case 8: return launch_mw<D, 8>(ctx, dp, grid, smem, mw);
-    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw);
-    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw);
-    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw);
+    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw, kt);
+    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw, kt);
+    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw, kt);
+    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw, kt);
   }
 }
 
@@ -497,8 +522,8 @@ bool decode_tma_supported(const PagedAttnCall& c) {
   if (pool->dims.dtype != LORAKV_BF16) return false;       // fp32 pages keep the 1e-4 contract on FFMA
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1) return false;   // decode only
   if (d != 64 && d != 128) return false;
-  if (!(rp == 0 || rp == 8 || rp == 16 || rp == 32 || rp == 64)) return false;
-  if (pool->P % kTK != 0) return false;
+  if (!(rp == 0 || rp == 16 || rp == 32 || rp == 64)) return false;
+  if (pool->P % kKeyStep != 0) return false;             // a tile (16 or 32 keys) never straddles a page
   if (c.L < 1 || c.n_batch < 1) return false;
   return true;
 }
@@ -517,12 +542,14 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const int rows_blk = 16 * mw;
   const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
   const int workers_per_cta = kWarps / mw;
-  const uint32_t stage_bytes = kTK * (4 * d + 2 * rp);
+  const int kt = (mw > 1 && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;   // 32-key tiles for multi-warp workers
+  const int tk = kKeyStep * kt;
+  const uint32_t stage_bytes = tk * (4 * d + 2 * rp);
   int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
   if (n_stages > kMaxStages) n_stages = kMaxStages;
   const size_t smem = (size_t)workers_per_cta * n_stages * stage_bytes;
 
-  const int64_t T = (c.L + kTK - 1) / kTK;
+  const int64_t T = (c.L + tk - 1) / tk;
   const int64_t units = n_layers * pool->n_kv_local * row_blocks;
   const int64_t total = units * T;
   const int64_t max_workers = (int64_t)ctx->sm_count * workers_per_cta;
@@ -556,8 +583,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
     dp.l2_policy = mode == 1 ? ptx::kEvictFirst : mode == 2 ? ptx::kEvictLast : 0;
   }
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
-  if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, rp));
-  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, rp));
+  if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
+  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));
 
   DecodeMergeParams mp;
   mp.part = dp.part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;

@@ -24,7 +24,8 @@ namespace lorakv {
 class AdapterTable {
  public:
   AdapterTable(const KvStore<float>& store, idx n_q_heads)
-      : n_q_heads_(n_q_heads), n_kv_heads_(store.device_options().n_kv_heads) {
+      : n_q_heads_(n_q_heads), n_kv_heads_(store.device_options().n_kv_heads),
+        per_agent_a_(store.scheme().kind == SchemeKind::BaseShared) {
     const StoreDims& d = store.dims();
     const DeviceOptions& o = store.device_options();
     b200::check(lorakv_adapters_create(b200::Runtime::ctx(), d.n_layers, d.n_agents, d.d_model, d.rank, o.n_kv_heads,
@@ -36,8 +37,10 @@ class AdapterTable {
   AdapterTable& operator=(const AdapterTable&) = delete;
 
   // one adapter of one layer; under shared-A every agent's `a` is the same matrix and is uploaded once
+  // (BaseShared keeps one LR cache per agent because the down-projections differ: there every agent's A is kept)
   void set(idx layer, idx agent, const LoraAdapter<float>& adapter, bool upload_a = true) {
-    if (upload_a) b200::check(lorakv_adapters_set_a(h_, layer, adapter.a.data.data()));
+    if (per_agent_a_) b200::check(lorakv_adapters_set_a_agent(h_, layer, agent, adapter.a.data.data()));
+    else if (upload_a) b200::check(lorakv_adapters_set_a(h_, layer, adapter.a.data.data()));
     b200::check(lorakv_adapters_set_b(h_, layer, agent, adapter.b.data.data(), adapter.alpha));
   }
   void set_layer(idx layer, const MultiLoraSet<float>& set) {
@@ -49,6 +52,7 @@ class AdapterTable {
  private:
   lorakv_adapters* h_ = nullptr;
   idx n_q_heads_, n_kv_heads_;
+  bool per_agent_a_;
 };
 
 // q: [(layer_end - layer_begin) * agents.size()] rows x (n_q_local * d_head); same-shaped result

@@ -209,6 +209,10 @@ void lorakv_adapters_destroy(lorakv_adapters* ad);
 /* shared down-projection A (d_model x rank, HOST float32, dense) of one layer: shared-A multi-LoRA,
  * lora.hpp:69-73 -- one A for every agent, so X*A is computed once */
 int lorakv_adapters_set_a(lorakv_adapters* ad, int64_t layer, const float* a);
+/* per-agent down-projection (d_model x rank, HOST float32, dense): the BaseShared scheme, whose adapters do NOT
+ * share A and which therefore keeps one LR cache per agent (kvcache.hpp:127-130, 238-243).  When set, the X*A
+ * append of that agent uses it instead of the shared A. */
+int lorakv_adapters_set_a_agent(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* a);
 /* per-agent up-projection B (rank x n_kv_heads*d_head, HOST float32, dense, FULL width) and alpha;
  * the effective scale alpha/rank travels with B (lora.hpp:9-11,34) */
 int lorakv_adapters_set_b(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* b,

@@ -111,6 +111,7 @@ SIGNATURES = {
     "lorakv_adapters_create": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "lorakv_adapters_destroy": (None, [_vp]),
     "lorakv_adapters_set_a": (C.c_int, [_vp, _i64, _pf]),
+    "lorakv_adapters_set_a_agent": (C.c_int, [_vp, _i64, _i64, _pf]),
     "lorakv_adapters_set_b": (C.c_int, [_vp, _i64, _i64, _pf, C.c_double]),
     "lorakv_fla_decode_batched": (C.c_int, [_vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, _vp, C.c_int]),
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
@@ -392,6 +393,10 @@ class Adapters:
     def set_a(self, layer, a):
         a = np.ascontiguousarray(a, dtype=np.float32)
         _check(self.ctx.lib.lorakv_adapters_set_a(self.h, layer, a.ctypes.data_as(_pf)))
+
+    def set_a_agent(self, layer, agent, a):
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        _check(self.ctx.lib.lorakv_adapters_set_a_agent(self.h, layer, agent, a.ctypes.data_as(_pf)))
 
     def set_b(self, layer, agent, b, alpha):
         b = np.ascontiguousarray(b, dtype=np.float32)

@@ -520,7 +520,8 @@ int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, 
   if (ad->rank != pool->dims.rank || ad->d_model != pool->dims.d_model || layer >= ad->n_layers)
     return fail("lr_append_project: adapter table does not match the pool (rank %lld vs %lld)",
                 (long long)ad->rank, (long long)pool->dims.rank);
-  if (pool->dims.rank > 0 && !ad->a_set[(size_t)layer]) return fail("lr_append_project: A of layer %lld was never uploaded", (long long)layer);
+  const bool own_a = ad->a_agent && agent >= 0 && agent < ad->n_agents && ad->a_agent_set[(size_t)(layer * ad->n_agents + agent)];
+  if (pool->dims.rank > 0 && !own_a && !ad->a_set[(size_t)layer]) return fail("lr_append_project: A of layer %lld was never uploaded", (long long)layer);
   int64_t& have = pool->lr_rows[(size_t)set][(size_t)layer];
   int64_t skip, add;
   LK_TRY(fww("lr", have, row_begin, n_rows, &skip, &add));
@@ -531,7 +532,9 @@ int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, 
     LK_TRY(ensure_pages(pool, pool->lr_space, set, have + add));
     const float* dev; int64_t dev_ld;
     LK_TRY(stage_rows(ctx, x + skip * ld, add, pool->dims.d_model, ld, mem_kind, &dev, &dev_ld));
-    LK_TRY(launch_lr_project(pool, ad, layer, set, have, dev, add, dev_ld));
+    const float* a_dev = own_a ? ad->a_agent + (size_t)(layer * ad->n_agents + agent) * (size_t)(ad->d_model * ad->rank)
+                               : ad->a + layer * ad->d_model * ad->rank;
+    LK_TRY(launch_lr_project(pool, a_dev, ad->d_model, ad->rank, layer, set, have, dev, add, dev_ld));
     if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   have += add;
@@ -648,6 +651,7 @@ void lorakv_adapters_destroy(lorakv_adapters* ad) {
   cudaSetDevice(ad->ctx->device);
   cudaStreamSynchronize(ad->ctx->stream);
   if (ad->a) cudaFree(ad->a);
+  if (ad->a_agent) cudaFree(ad->a_agent);
   if (ad->b) cudaFree(ad->b);
   if (ad->scale) cudaFree(ad->scale);
   delete ad;
@@ -661,6 +665,24 @@ int lorakv_adapters_set_a(lorakv_adapters* ad, int64_t layer, const float* a) {
                           cudaMemcpyHostToDevice, ad->ctx->stream));
   LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
   ad->a_set[(size_t)layer] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_adapters_set_a_agent(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* a) {
+  if (!ad || !a) return fail("null argument");
+  if (layer < 0 || layer >= ad->n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (agent < 0 || agent >= ad->n_agents)
+    return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)ad->n_agents);
+  LK_CUDA(cudaSetDevice(ad->ctx->device));
+  const size_t one = (size_t)(ad->d_model * ad->rank);
+  if (!ad->a_agent) {
+    LK_CUDA(cudaMalloc(&ad->a_agent, (size_t)(ad->n_layers * ad->n_agents) * one * sizeof(float)));
+    ad->a_agent_set.assign((size_t)(ad->n_layers * ad->n_agents), 0);
+  }
+  LK_CUDA(cudaMemcpyAsync(ad->a_agent + (size_t)(layer * ad->n_agents + agent) * one, a, one * sizeof(float),
+                          cudaMemcpyHostToDevice, ad->ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
+  ad->a_agent_set[(size_t)(layer * ad->n_agents + agent)] = 1;
   return LORAKV_OK;
 }
 

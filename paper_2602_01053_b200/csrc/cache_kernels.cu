@@ -281,14 +281,14 @@ int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_
   return LORAKV_OK;
 }
 
-int launch_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer, int64_t set,
+int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set,
                       int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld) {
   if (n_rows == 0) return LORAKV_OK;
   lorakv_ctx* ctx = pool->ctx;
   const PageAddr a = make_addr(pool, LORAKV_LR, layer, set);
   if (a.width == 0) return LORAKV_OK;
   if (a.width > 128) return fail("lr_append_project: rank %lld > 128 is not supported", (long long)pool->dims.rank);
-  const float* A = ad->a + layer * ad->d_model * ad->rank;
+  const float* A = a_dev;
   const bool bf16 = pool->dims.dtype == LORAKV_BF16;
   const bool vec_ok = (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x_dev) & 15) == 0);
   auto launch = [&](auto kern, int rp) {
@@ -296,7 +296,7 @@ int launch_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t laye
     const unsigned blocks = (unsigned)((n_rows + rows_per_cta - 1) / rows_per_cta);
     const size_t smem = (size_t)2 * rp * 512;       // two [4][rp/4][32] float4 buffers
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<blocks, kProjWarps * 32, smem, ctx->stream>>>(a, row0, x_dev, n_rows, ld, A, (int)ad->d_model, (int)ad->rank, bf16, vec_ok);
+    kern<<<blocks, kProjWarps * 32, smem, ctx->stream>>>(a, row0, x_dev, n_rows, ld, A, (int)d_model, (int)rank, bf16, vec_ok);
   };
   switch (a.width) {
     case 16: bf16 ? launch(lr_append_project_kernel<__nv_bfloat16, 16>, 16) : launch(lr_append_project_kernel<float, 16>, 16); break;

@@ -128,8 +128,9 @@ struct lorakv_adapters {
   int64_t kv_head_begin = 0, n_kv_local = 0;
   int dtype = LORAKV_F32;
   float* a = nullptr;      // [n_layers][d_model][rank] float32 (values already representable in dtype)
+  float* a_agent = nullptr; // [n_layers][n_agents][d_model][rank], allocated on the first per-agent upload (BaseShared)
   float* b = nullptr;      // [n_layers][n_agents][rank][n_kv_local*d_head] float32
   float* scale = nullptr;  // [n_layers][n_agents] device copy of alpha/rank
   std::vector<float> scale_host;
-  std::vector<uint8_t> a_set, b_set;
+  std::vector<uint8_t> a_set, b_set, a_agent_set;
 };

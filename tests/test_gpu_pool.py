@@ -270,3 +270,64 @@ def test_rank_zero_and_per_agent_schemes(ctx, orc):
     assert orc.max_rel_error(o1[0], want) <= 1e-4
     with pytest.raises(LorakvError, match="per-agent"):
         ns.decode(None, 0, 1, [0, 1], n_q, np.stack([q[0][0], q[1][0]])[None])
+
+
+def test_baseshared_agent_switch_lr_prefill(ctx, orc):
+    """BaseShared (kvcache.hpp:127-130, engine.hpp:411-419): the base K/V cache is shared but every agent keeps
+    its own LR cache because the down-projections differ.  When another agent takes over it projects the whole
+    UNSEEN context through its own A (the "LR prefill"); K/V only get the fresh rows.  Planner
+    intervals, row counts and byte accounting are bit-exact vs the oracle; attention within 2e-2 (bf16 pages)."""
+    from paper_2602_01053_b200 import Adapters, Pool, abi
+    n_q, n_kv, d, r, N, d_model = 8, 2, 128, 16, 2, 192
+    first, extra = 100, 20
+    rnd = orc.round_bf16
+    g = lambda rows, cols, seed, sc: rnd(orc.gaussian(rows, cols, seed, sc, np.float32))
+    k = g(first + extra, n_kv * d, 1, 1.0 / np.sqrt(d)); v = g(first + extra, n_kv * d, 2, 1.0)
+    x = g(first + extra, d_model, 3, 1.0)
+    A = [g(d_model, r, 10 + a, 1.0 / np.sqrt(d_model)) for a in range(N)]          # per-agent A: NOT shared
+    B = [g(r, n_kv * d, 20 + a, 0.02 / np.sqrt(r)) for a in range(N)]
+    pool = Pool(ctx, "BaseShared", 1, n_kv, d, d_model, r, N, max_tokens=256, dtype=abi.BF16)
+    st = orc.store("BaseShared", 1, n_kv * d, d_model, r, N, np.float32)
+    ad = Adapters(ctx, 1, N, d_model, r, n_kv, d, dtype=abi.BF16)
+    for a in range(N):
+        ad.set_a_agent(0, a, A[a]); ad.set_b(0, a, B[a], 16.0)
+
+    # agent 0 prefills the first 100 tokens
+    plan = pool.plan_step(0, first)
+    assert plan == orc.plan_core("BaseShared", 0, 0, first)
+    assert plan["kv_project"] == (0, first) and plan["lr_project"] == (0, first)
+    pool.append_tokens(first); st.append_tokens(first)
+    pool.append_key(0, 0, 0, k[:first]); pool.append_value(0, 0, 0, v[:first])
+    st.append_key(0, 0, 0, k[:first]); st.append_value(0, 0, 0, v[:first])
+    assert pool.append_lr_project(ad, 0, 0, 0, x[:first]) == first
+    st.append_lr(0, 0, 0, orc.matmul(x[:first], A[0]))
+    pool.mark_seen(0); st.mark_seen(0)
+
+    # agent 1 takes over with 20 new tokens: K/V fresh only, LR over everything it has not seen
+    plan = pool.plan_step(1, extra)
+    assert plan == orc.plan_core("BaseShared", first, 0, extra)
+    assert plan["kv_project"] == (first, first + extra) and plan["lr_project"] == (0, first + extra)
+    pool.append_tokens(extra); st.append_tokens(extra)
+    lo, hi = plan["kv_project"]
+    pool.append_key(0, 1, lo, k[lo:hi]); pool.append_value(0, 1, lo, v[lo:hi])
+    st.append_key(0, 1, lo, k[lo:hi]); st.append_value(0, 1, lo, v[lo:hi])
+    lo, hi = plan["lr_project"]
+    assert pool.append_lr_project(ad, 0, 1, lo, x[lo:hi]) == hi - lo
+    v_lr1 = orc.matmul(x[lo:hi], A[1])
+    st.append_lr(0, 1, lo, v_lr1)
+    pool.mark_seen(1); st.mark_seen(1)
+
+    assert pool.bytes()["lr"] * 2 == st.bytes()["lr"]            # bf16 pages vs the oracle's fp32 store
+    assert pool.bytes()["key"] * 2 == st.bytes()["key"]
+    assert pool.rows(abi.LR, 0, 0) == first and pool.rows(abi.LR, 0, 1) == first + extra
+    assert pool.seen(0) == first and pool.seen(1) == first + extra
+    assert orc.max_rel_error(pool.lr_view(0, 1), v_lr1) <= 1e-2
+    # agent 1 decodes over the shared K/V and ITS low-rank cache
+    L = first + extra
+    q = g(1, n_q * d, 77, 1.0 / np.sqrt(d))
+    out = pool.decode(ad, 0, 1, [1], n_q, q[None])
+    want = orc.gqa_attention(q, k, v, v_lr1, B[1], 1.0, L - 1, n_q, n_kv)
+    assert orc.max_rel_error(out[0], want) <= 2e-2
+    with pytest.raises(Exception, match="per-agent"):
+        pool.decode(ad, 0, 1, [0, 1], n_q, np.concatenate([q, q])[None])
+    pool.close(); ad.close()

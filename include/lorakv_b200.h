@@ -254,7 +254,8 @@ int lorakv_selftest_umma(lorakv_ctx* ctx, const float* a, const float* b, int N,
                          float alpha, int rescale, int a_in_tmem, float* d);
 
 /* selects the kernel family for the fast paths: 0 = auto (tcgen05/TMA where the shape allows),
- * 1 = force the CUDA-core kernels.  Returns the previous value. */
+ * 1 = force the CUDA-core kernels, 2 = auto but keep decode on the mma.sync streaming kernel even for
+ * many query rows (A/B comparisons).  Returns the previous value. */
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy);
 /* name of the kernel family the last fast-path call on this ctx dispatched to */
 const char* lorakv_last_kernel(lorakv_ctx* ctx);

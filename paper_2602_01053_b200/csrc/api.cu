@@ -785,8 +785,9 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   call.rows_per_entry = rows_per_entry; call.query_offset = query_offset; call.n_q_local = n_q_local;
   call.L = L; call.q_dev = q_dev; call.out_dev = out_dev;
   call.agent_host = ids_host[0];
-  if (ctx->policy == 0 && decode_tma_supported(call)) LK_TRY(launch_decode_tma(call));
-  else if (ctx->policy == 0 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
+  if (ctx->policy == 0 && decode_umma_supported(call)) LK_TRY(launch_decode_umma(call));
+  else if (ctx->policy != 1 && decode_tma_supported(call)) LK_TRY(launch_decode_tma(call));
+  else if (ctx->policy != 1 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
   else LK_TRY(launch_paged_simt(call));
 
   if (host) {

@@ -455,7 +455,8 @@ __global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMerge
   __syncthreads();
   for (int c = threadIdx.x; c < p.r; c += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < ns; ++s) acc = fmaf(w_s[s], row_of(s)[4 + p.D + c], acc);
+    for (int s = 0; s < ns; ++s)
+      if (w_s[s] != 0.f) acc = fmaf(w_s[s], row_of(s)[4 + p.D + c], acc);   // an empty split carries no accumulators
     olr_s[c] = acc;
   }
   __syncthreads();
@@ -469,7 +470,8 @@ __global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMerge
   const float inv_l = 1.0f / l_total;
   for (int c = threadIdx.x; c < p.D; c += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < ns; ++s) acc = fmaf(w_s[s], row_of(s)[4 + c], acc);
+    for (int s = 0; s < ns; ++s)
+      if (w_s[s] != 0.f) acc = fmaf(w_s[s], row_of(s)[4 + c], acc);
     for (int k = 0; k < p.r; ++k) acc = fmaf(scale * olr_s[k], b[k * dkv + c], acc);
     dst[c] = acc * inv_l;
   }
@@ -515,6 +517,25 @@ int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t sme
 }
 
 }  // namespace
+
+int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
+                        int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
+                        const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers) {
+  DecodeMergeParams mp;
+  mp.part = part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;
+  mp.n_kv_local = n_kv_local; mp.n_batch = n_batch; mp.rows_total = rows_total;
+  mp.row_blocks = row_blocks; mp.T = T; mp.G = G; mp.layer_begin = layer_begin; mp.n_q_local = n_q_local;
+  mp.max_seg = max_seg; mp.agent_ids = agent_ids_dev;
+  mp.b = adapters ? adapters->b : nullptr; mp.scale = adapters ? adapters->scale : nullptr;
+  mp.n_agents = adapters ? adapters->n_agents : 1;
+  mp.out = out_dev;
+  const int ns_max = (int)((T - 1) / G + 2);
+  dim3 mgrid((unsigned)rows_total, (unsigned)(n_layers * n_kv_local));
+  fla_decode_merge_kernel<<<mgrid, 128, (size_t)(ns_max + r + 1) * sizeof(float), ctx->stream>>>(mp);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
 
 bool decode_tma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
@@ -586,19 +607,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
   if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));
 
-  DecodeMergeParams mp;
-  mp.part = dp.part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;
-  mp.n_kv_local = (int)pool->n_kv_local; mp.n_batch = (int)c.n_batch; mp.rows_total = (int)rows_total;
-  mp.row_blocks = row_blocks; mp.T = T; mp.G = G; mp.layer_begin = c.layer_begin; mp.n_q_local = c.n_q_local;
-  mp.max_seg = max_seg; mp.agent_ids = c.agent_ids_dev;
-  mp.b = c.adapters ? c.adapters->b : nullptr; mp.scale = c.adapters ? c.adapters->scale : nullptr;
-  mp.n_agents = c.adapters ? c.adapters->n_agents : 1;
-  mp.out = c.out_dev;
-  const int ns_max = (int)((T - 1) / G + 2);
-  dim3 mgrid((unsigned)rows_total, (unsigned)(n_layers * pool->n_kv_local));
-  fla_decode_merge_kernel<<<mgrid, 128, (size_t)(ns_max + r + 1) * sizeof(float), ctx->stream>>>(mp);
-  ctx->launches++;
-  LK_CUDA(cudaGetLastError());
+  LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,
+                             T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers));
   ctx->last_kernel = "fla_decode_tma";
   return LORAKV_OK;
 }

@@ -55,6 +55,10 @@ struct PrefillParams {
   int P, group, n_kv_local, n_pages, r;
   int64_t L, L_c, query_offset, n_q_local;
   int n_qblocks;
+  // decode mode (kDecode): one CTA = (layer, kv head, key split); rows = (batch entry, head in group)
+  int n_batch, rows_total, splits, tiles_per_split;
+  int64_t kv_layer_stride, lr_layer_stride, layer_begin_rel;
+  float* part;          // [units * splits][128][4 + D + RP] partial (m, l, O, O_lr), merged by fla_decode_merge
   float scale_log2, lr_scale;
   const float* q;       // [L_c][n_q_local * D]
   const float* b;       // [r][n_kv_local * D] of this (layer, agent)
@@ -84,7 +88,10 @@ struct Barriers {
   uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[2];
 };
 
-template <int D, int RP>
+// kDecode = false: prefill block (rows = head x position, causal mask, final output)
+// kDecode = true : batched decode for many rows per kv head (rows = batch entry x head, all at position L-1);
+//                  a CTA streams one split of one (layer, kv head) and writes an un-normalised partial
+template <int D, int RP, bool kDecode>
 __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const PrefillParams p) {
   constexpr int kQBlocks = D / 64;                           // 64-column K-blocks of Q / K; 64-column N-blocks of V
   constexpr uint32_t kBlkBytes = kBN * 128;                  // one [128 rows][64] bf16 block = 16 KB
@@ -107,13 +114,33 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   unsigned char* sLR = sV + kStages * kKBytes;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int PB = kBM / p.group;                                  // query positions per CTA
-  const int qb = p.n_qblocks - 1 - (int)(blockIdx.x / p.n_kv_local);   // heavy (late) blocks first
-  const int kvh = (int)(blockIdx.x % p.n_kv_local);
-  const int64_t q0 = (int64_t)qb * PB;
-  const int64_t rows_here = min((int64_t)PB, p.L_c - q0);       // real positions in this block
-  const int64_t last_visible_cta = p.query_offset + q0 + rows_here - 1;
-  const int n_tiles = (int)(last_visible_cta / kBN) + 1;
+  // ---- what this CTA owns ----
+  int PB, kvh, n_tiles, tile_begin;
+  int64_t q0, rows_here, kv_layer_off, lr_layer_off, mask_from;   // mask_from: first key that some row cannot see
+  int unit = 0, split = 0, layer_rel = 0;
+  if constexpr (!kDecode) {
+    PB = kBM / p.group;                                           // query positions per CTA
+    const int qb = p.n_qblocks - 1 - (int)(blockIdx.x / p.n_kv_local);   // heavy (late) blocks first
+    kvh = (int)(blockIdx.x % p.n_kv_local);
+    q0 = (int64_t)qb * PB;
+    rows_here = min((int64_t)PB, p.L_c - q0);                     // real positions in this block
+    const int64_t last_visible_cta = p.query_offset + q0 + rows_here - 1;
+    n_tiles = (int)(last_visible_cta / kBN) + 1;
+    tile_begin = 0;
+    kv_layer_off = p.kv_layer_off; lr_layer_off = p.lr_layer_off;
+    mask_from = p.query_offset + q0 + 1;
+  } else {
+    PB = 1; q0 = 0; rows_here = p.rows_total;
+    unit = (int)(blockIdx.x / p.splits); split = (int)(blockIdx.x % p.splits);
+    layer_rel = unit / p.n_kv_local; kvh = unit % p.n_kv_local;
+    const int total_tiles = (int)((p.L + kBN - 1) / kBN);
+    tile_begin = split * p.tiles_per_split;
+    n_tiles = min(p.tiles_per_split, total_tiles - tile_begin);
+    if (n_tiles < 0) n_tiles = 0;
+    kv_layer_off = p.kv_layer_off + (int64_t)layer_rel * p.kv_layer_stride;
+    lr_layer_off = p.lr_layer_off + (int64_t)layer_rel * p.lr_layer_stride;
+    mask_from = p.L;
+  }
 
   if (tid == 0) {
     ptx::mbar_init(&bars.q_full, 256);
@@ -147,18 +174,18 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         if (j >= kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));   // the phase that freed the stage
         ptx::mbar_arrive_expect_tx(&full[s], is_k ? kKBytes : kKBytes + kLrBytes);
         for (int i = 0; i < n_copies; ++i) {
-          const int64_t key0 = (int64_t)j * kBN + (int64_t)i * tpc;
+          const int64_t key0 = (int64_t)(tile_begin + j) * kBN + (int64_t)i * tpc;
           int page = (int)(key0 / p.P);
           const int tok0 = (int)(key0 % p.P);
           if (page >= p.n_pages) page = p.n_pages - 1;  // wholly masked keys: any finite rows will do
-          const int64_t base = p.kv_layer_off + (int64_t)kvh * p.kv_head_stride + (int64_t)p.kv_table[page] * p.kv_page_stride +
+          const int64_t base = kv_layer_off + (int64_t)kvh * p.kv_head_stride + (int64_t)p.kv_table[page] * p.kv_page_stride +
                                (int64_t)tok0 * 64;
 #pragma unroll
           for (int b = 0; b < kQBlocks; ++b)
             bulk_g2s(ptx::smem_u32(ring + s * kKBytes + b * kBlkBytes + i * tpc * 128), pages + base + (int64_t)b * p.P * 64,
                      (uint32_t)tpc * 128u, &full[s]);
           if (RP > 0 && !is_k) {
-            const int64_t lr_base = p.lr_layer_off + (int64_t)p.lr_table[page] * p.lr_page_stride + (int64_t)tok0 * RP;
+            const int64_t lr_base = lr_layer_off + (int64_t)p.lr_table[page] * p.lr_page_stride + (int64_t)tok0 * RP;
             bulk_g2s(ptx::smem_u32(sLR + s * kLrBytes + i * tpc * kLrRow), p.lr_pages + lr_base, (uint32_t)tpc * kLrRow, &full[s]);
           }
         }
@@ -186,9 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         ptx::umma_commit(&bars.k_empty[ks_stage]);
         ptx::umma_commit(&bars.s_full[s]);
       };
-      ptx::mbar_wait(&bars.q_full, 0);
-      ptx::tc_fence_after();
-      issue_s(0);
+      if (n_tiles > 0) {
+        ptx::mbar_wait(&bars.q_full, 0);
+        ptx::tc_fence_after();
+        issue_s(0);
+      }
       if (n_tiles > 1) issue_s(1);
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j & 1, vs = j % kStages;
@@ -217,19 +246,35 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     const int row = (warp & 3) * 32 + lane;
     const int half = warp >> 2;
     const int pair_bar = 1 + (warp & 3);                     // named barrier of the two warps sharing rows
-    const int hg = row / PB;                                 // q head within the group
-    int64_t pos_local = row % PB;
-    if (pos_local >= rows_here) pos_local = rows_here - 1;   // padding rows shadow the last real one
-    const bool real_row = (row % PB) < rows_here;
-    const int64_t pos = q0 + pos_local;
-    const int64_t last_visible = p.query_offset + pos;
+    // row -> (query row of the call, q head): prefill rows are (head in group, position); decode rows are
+    // (batch entry, head in group), every one at position L - 1
+    bool real_row;
+    int64_t last_visible;
+    const float* q_src;
+    float* dst = nullptr;
+    if constexpr (!kDecode) {
+      const int hg = row / PB;                                 // q head within the group
+      int64_t pos_local = row % PB;
+      if (pos_local >= rows_here) pos_local = rows_here - 1;   // padding rows shadow the last real one
+      real_row = (row % PB) < rows_here;
+      const int64_t pos = q0 + pos_local;
+      last_visible = p.query_offset + pos;
+      q_src = p.q + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D;
+      dst = p.out + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D;
+    } else {
+      real_row = row < p.rows_total;
+      const int rho = real_row ? row : p.rows_total - 1;
+      const int entry = rho / p.group, gi = rho % p.group;
+      last_visible = p.L - 1;
+      q_src = p.q + (((int64_t)(p.layer_begin_rel + layer_rel) * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
+    }
     const float ninf = -std::numeric_limits<float>::infinity();
     constexpr int kHalf = kBN / 2;                           // key columns per thread
 
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     // ---- Q tile -> TMEM: this thread's half of its row, fp32 -> packed bf16 pairs ----
     {
-      const float* src = p.q + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D + half * (D / 2);
+      const float* src = q_src + half * (D / 2);
 #pragma unroll
       for (int c0 = 0; c0 < D / 4; c0 += 16) {          // D/4 packed columns per thread, 16 per store
         uint32_t r16[16];
@@ -260,8 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         for (int c = 0; c < kHalf; ++c) sc[c] = __uint_as_float(raw[c]);
       }
 
-      const int64_t key0 = (int64_t)j * kBN + half * kHalf;
-      const bool tile_needs_mask = (int64_t)j * kBN + kBN - 1 > p.query_offset + q0;   // CTA-uniform
+      const int64_t key0 = (int64_t)(tile_begin + j) * kBN + half * kHalf;
+      const bool tile_needs_mask = (int64_t)(tile_begin + j) * kBN + kBN - 1 >= mask_from;   // CTA-uniform
       if (tile_needs_mask) {
 #pragma unroll
         for (int c = 0; c < kHalf; ++c)
@@ -335,6 +380,43 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       ptx::mbar_arrive(&bars.p_full);
     }
 
+    if constexpr (kDecode) {
+      // ---- partial of this split: (m, l, O, O_lr) un-normalised, merged (+ B epilogue) by fla_decode_merge ----
+      constexpr int PS = 4 + D + RP;
+      float* prow = p.part + ((int64_t)blockIdx.x * kBM + row) * PS;
+      if (n_tiles > 0) {
+        ptx::mbar_wait(&bars.pv_done, (uint32_t)((n_tiles - 1) & 1));
+        ptx::tc_fence_after();
+      }
+      l_s[half][row] = l_run;
+      named_bar_sync(pair_bar, 64);
+      if (half == 0) { prow[0] = n_tiles > 0 ? m_used : ninf; prow[1] = l_s[0][row] + l_s[1][row]; }
+      if (n_tiles > 0) {
+#pragma unroll
+        for (int cc = 0; cc < D / 2; cc += 16) {
+          const int c0 = half * (D / 2) + cc;
+          uint32_t r16[16];
+          ptx::tmem_ld16(tmem + lane_base + kTmemO + c0, r16);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(prow + 4 + c0 + i) = make_float4(__uint_as_float(r16[i]), __uint_as_float(r16[i + 1]),
+                                                                        __uint_as_float(r16[i + 2]), __uint_as_float(r16[i + 3]));
+        }
+        if (half == 0) {
+#pragma unroll
+          for (int c0 = 0; c0 < RP; c0 += 16) {
+            uint32_t r16[16];
+            ptx::tmem_ld16(tmem + lane_base + kTmemLr + c0, r16);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              *reinterpret_cast<float4*>(prow + 4 + D + c0 + i) = make_float4(__uint_as_float(r16[i]), __uint_as_float(r16[i + 1]),
+                                                                              __uint_as_float(r16[i + 2]), __uint_as_float(r16[i + 3]));
+          }
+        }
+      }
+    } else {
     // ---- epilogue: o += (lr_scale * o_lr[p]) * B[p,:], out = o / l ----
     ptx::mbar_wait(&bars.pv_done, (uint32_t)((n_tiles - 1) & 1));
     ptx::tc_fence_after();
@@ -353,7 +435,6 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
 #pragma unroll
       for (int i = 0; i < 16; ++i) w[c0 + i] = p.lr_scale * __uint_as_float(r16[i]);
     }
-    float* dst = p.out + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D;
 #pragma unroll
     for (int cc = 0; cc < D / 2; cc += 16) {
       const int c0 = half * (D / 2) + cc;
@@ -376,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
           *reinterpret_cast<float4*>(dst + c0 + i) = make_float4(acc[i] * inv_l, acc[i + 1] * inv_l, acc[i + 2] * inv_l, acc[i + 3] * inv_l);
       }
     }
+    }
   }
 
   ptx::tc_fence_before();
@@ -383,13 +465,13 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   if (warp == 0) ptx::tmem_dealloc(tmem, 512);
 }
 
-template <int D, int RP>
+template <int D, int RP, bool kDecode>
 int launch_t(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid) {
   const size_t blk = (size_t)kBN * 128;
   const size_t kv = (D / 64) * blk, lr = (size_t)kBN * 2 * RP;
   const int stages = (2 * 3 * kv + 3 * lr + 1024 <= (size_t)227 * 1024 - 4096) ? 3 : 2;   // mirrors kStages in the kernel
   const size_t smem = stages * (2 * kv + lr) + 1024;
-  auto kern = fla_prefill_umma_kernel<D, RP>;
+  auto kern = fla_prefill_umma_kernel<D, RP, kDecode>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);
   kern<<<grid, kThreads, smem, ctx->stream>>>(pp);
@@ -399,28 +481,54 @@ int launch_t(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid) {
   return LORAKV_OK;
 }
 
-template <int D>
+template <int D, bool kDecode>
 int launch_rp(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid, int rp) {
   switch (rp) {
-    case 0: return launch_t<D, 0>(ctx, pp, grid);
-    case 16: return launch_t<D, 16>(ctx, pp, grid);
-    case 32: return launch_t<D, 32>(ctx, pp, grid);
-    default: return launch_t<D, 64>(ctx, pp, grid);
+    case 0: return launch_t<D, 0, kDecode>(ctx, pp, grid);
+    case 16: return launch_t<D, 16, kDecode>(ctx, pp, grid);
+    case 32: return launch_t<D, 32, kDecode>(ctx, pp, grid);
+    default: return launch_t<D, 64, kDecode>(ctx, pp, grid);
   }
+}
+
+void fill_common(PrefillParams& pp, const PagedAttnCall& c) {
+  lorakv_pool* pool = c.pool;
+  const int d = (int)pool->dims.d_head, rp = (int)pool->r_pad;
+  pp.k_pages = static_cast<const __nv_bfloat16*>(pool->k_pages);
+  pp.v_pages = static_cast<const __nv_bfloat16*>(pool->v_pages);
+  pp.lr_pages = static_cast<const __nv_bfloat16*>(pool->lr_pages);
+  pp.kv_table = pool->kv_space.dev_table + c.kv_set * pool->kv_space.max_pages;
+  pp.lr_table = rp > 0 ? pool->lr_space.dev_table + c.lr_set * pool->lr_space.max_pages : nullptr;
+  pp.kv_layer_off = c.layer_begin * pool->kv_layer_stride(); pp.kv_head_stride = pool->kv_head_stride();
+  pp.kv_page_stride = pool->kv_page_stride();
+  pp.lr_layer_off = c.layer_begin * pool->lr_layer_stride(); pp.lr_page_stride = pool->lr_page_stride();
+  pp.kv_layer_stride = pool->kv_layer_stride(); pp.lr_layer_stride = pool->lr_layer_stride();
+  pp.P = (int)pool->P; pp.group = (int)(c.n_q_local / pool->n_kv_local); pp.n_kv_local = (int)pool->n_kv_local;
+  pp.n_pages = (int)((c.L + pool->P - 1) / pool->P); pp.r = (int)pool->dims.rank;
+  pp.L = c.L; pp.L_c = c.rows_per_entry; pp.query_offset = c.query_offset; pp.n_q_local = c.n_q_local;
+  pp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
+  pp.q = c.q_dev; pp.out = c.out_dev;
+  pp.n_qblocks = 0; pp.n_batch = (int)c.n_batch; pp.rows_total = 0; pp.splits = 1; pp.tiles_per_split = 0;
+  pp.layer_begin_rel = 0; pp.part = nullptr; pp.lr_scale = 0.f; pp.b = nullptr;
+}
+
+bool umma_shape_ok(const lorakv_pool* pool) {
+  const int64_t d = pool->dims.d_head, rp = pool->r_pad, P = pool->P;
+  if (pool->dims.dtype != LORAKV_BF16) return false;
+  if (d != 64 && d != 128) return false;
+  if (!(rp == 0 || rp == 16 || rp == 32 || rp == 64)) return false;
+  if (P < 16 || (P & (P - 1)) != 0) return false;           // power-of-two pages: tiles are made of whole runs
+  return true;
 }
 
 }  // namespace
 
 bool prefill_umma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
-  const int64_t d = pool->dims.d_head, rp = pool->r_pad, P = pool->P;
-  if (pool->dims.dtype != LORAKV_BF16) return false;
+  if (!umma_shape_ok(pool)) return false;
   if (c.n_batch != 1 || c.rows_per_entry < 2 || c.layer_end - c.layer_begin != 1) return false;
-  if (d != 64 && d != 128) return false;
-  if (!(rp == 0 || rp == 16 || rp == 32 || rp == 64)) return false;
   const int64_t group = c.n_q_local / pool->n_kv_local;
   if (group < 1 || group > kBM || kBM % group != 0) return false;
-  if (P < 16 || (P & (P - 1)) != 0) return false;           // power-of-two pages: tiles are made of whole runs
   if (c.L < 1) return false;
   return true;
 }
@@ -430,32 +538,63 @@ int launch_prefill_umma(const PagedAttnCall& c) {
   lorakv_ctx* ctx = pool->ctx;
   const int d = (int)pool->dims.d_head, r = (int)pool->dims.rank, rp = (int)pool->r_pad;
   if (r > 0 && !c.adapters) return fail("paged attention: rank %lld cache needs adapter tables", (long long)r);
-  const int group = (int)(c.n_q_local / pool->n_kv_local);
-  const int PB = kBM / group;
-  const int64_t layer = c.layer_begin;
-  // the single batch entry's agent id is on the host side of the call (api.cu stages it); B / scale are per agent
   PrefillParams pp;
-  pp.k_pages = static_cast<const __nv_bfloat16*>(pool->k_pages);
-  pp.v_pages = static_cast<const __nv_bfloat16*>(pool->v_pages);
-  pp.lr_pages = static_cast<const __nv_bfloat16*>(pool->lr_pages);
-  pp.kv_table = pool->kv_space.dev_table + c.kv_set * pool->kv_space.max_pages;
-  pp.lr_table = rp > 0 ? pool->lr_space.dev_table + c.lr_set * pool->lr_space.max_pages : nullptr;
-  pp.kv_layer_off = layer * pool->kv_layer_stride(); pp.kv_head_stride = pool->kv_head_stride();
-  pp.kv_page_stride = pool->kv_page_stride();
-  pp.lr_layer_off = layer * pool->lr_layer_stride(); pp.lr_page_stride = pool->lr_page_stride();
-  pp.P = (int)pool->P; pp.group = group; pp.n_kv_local = (int)pool->n_kv_local;
-  pp.n_pages = (int)((c.L + pool->P - 1) / pool->P); pp.r = r;
-  pp.L = c.L; pp.L_c = c.rows_per_entry; pp.query_offset = c.query_offset; pp.n_q_local = c.n_q_local;
+  fill_common(pp, c);
+  const int PB = kBM / pp.group;
+  const int64_t layer = c.layer_begin, agent = c.agent_host;
   pp.n_qblocks = (int)((c.rows_per_entry + PB - 1) / PB);
-  pp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
-  const int64_t agent = c.agent_host;
   pp.lr_scale = (r > 0) ? c.adapters->scale_host[(size_t)(layer * c.adapters->n_agents + agent)] : 0.f;
   pp.b = (r > 0) ? c.adapters->b + ((layer * c.adapters->n_agents + agent) * r) * (pool->n_kv_local * (int64_t)d) : nullptr;
-  pp.q = c.q_dev; pp.out = c.out_dev;
   const unsigned grid = (unsigned)((int64_t)pp.n_qblocks * pool->n_kv_local);
-  if (d == 128) LK_TRY(launch_rp<128>(ctx, pp, grid, rp));
-  else LK_TRY(launch_rp<64>(ctx, pp, grid, rp));
+  if (d == 128) LK_TRY((launch_rp<128, false>(ctx, pp, grid, rp)));
+  else LK_TRY((launch_rp<64, false>(ctx, pp, grid, rp)));
   ctx->last_kernel = "fla_prefill_umma";
+  return LORAKV_OK;
+}
+
+// Batched decode with many query rows per kv head (more than 32 = agents x group): the tcgen05 kernel in
+// decode mode.  One CTA streams one split of one (layer, kv head); rows (batch entry, head) fill the 128 MMA
+// rows (blocks of 128 when there are more).  Partials go through the same merge + epilogue kernel as
+// fla_decode_tma.
+bool decode_umma_supported(const PagedAttnCall& c) {
+  const lorakv_pool* pool = c.pool;
+  if (!umma_shape_ok(pool)) return false;
+  if (c.rows_per_entry != 1 || c.query_offset != c.L - 1 || c.L < 1 || c.n_batch < 1) return false;
+  const int64_t rows_total = c.n_batch * (c.n_q_local / pool->n_kv_local);
+  return rows_total > 32 && rows_total <= kBM;
+}
+
+int launch_decode_umma(const PagedAttnCall& c) {
+  lorakv_pool* pool = c.pool;
+  lorakv_ctx* ctx = pool->ctx;
+  const int d = (int)pool->dims.d_head, r = (int)pool->dims.rank, rp = (int)pool->r_pad;
+  if (r > 0 && !c.adapters) return fail("paged attention: rank %lld cache needs adapter tables", (long long)r);
+  PrefillParams pp;
+  fill_common(pp, c);
+  const int64_t n_layers = c.layer_end - c.layer_begin;
+  const int64_t units = n_layers * pool->n_kv_local;
+  const int64_t total_tiles = (c.L + kBN - 1) / kBN;
+  // splits: enough CTAs for ~4 waves of the machine, at least 4 tiles each
+  int64_t splits = (4 * (int64_t)ctx->sm_count + units - 1) / units;
+  if (splits > total_tiles / 4) splits = total_tiles / 4;
+  if (splits < 1) splits = 1;
+  const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
+  splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
+  pp.rows_total = (int)(c.n_batch * pp.group);
+  pp.splits = (int)splits; pp.tiles_per_split = (int)tiles_per_split;
+  const int PS = 4 + d + rp;
+  const size_t part_bytes = (size_t)(units * splits) * kBM * PS * sizeof(float);
+  LK_TRY(scratch_reserve(ctx, ctx->work, part_bytes));
+  pp.part = static_cast<float*>(ctx->work.ptr);
+  const unsigned grid = (unsigned)(units * splits);
+  if (d == 128) LK_TRY((launch_rp<128, true>(ctx, pp, grid, rp)));
+  else LK_TRY((launch_rp<64, true>(ctx, pp, grid, rp)));
+  // merge + B epilogue: the partial slots are [unit][split], i.e. fla_decode_merge's closed form with
+  // T = splits * G tiles per unit and G tiles per worker, one segment per worker
+  LK_TRY(launch_decode_merge(ctx, pp.part, d, rp, r, /*MW=*/8, pp.group, (int)pool->n_kv_local, (int)c.n_batch, pp.rows_total,
+                             /*row_blocks=*/1, /*T=*/splits * tiles_per_split, /*G=*/tiles_per_split, c.layer_begin, c.n_q_local,
+                             /*max_seg=*/1, c.agent_ids_dev, c.adapters, c.out_dev, n_layers));
+  ctx->last_kernel = "fla_decode_umma";
   return LORAKV_OK;
 }
 

@@ -60,10 +60,16 @@ int launch_paged_simt(const PagedAttnCall& call);
 // fla_decode_tma.cu (TMA bulk-copy rings + tensor-core MMA; bf16 pages, decode) -------------------
 bool decode_tma_supported(const PagedAttnCall& call);
 int launch_decode_tma(const PagedAttnCall& call);
+// split merge + up-projection epilogue over the partial layout both decode kernels write
+int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
+                        int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
+                        const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers);
 
 // fla_prefill_umma.cu (tcgen05 / TMEM / TMA; bf16 pages, prefill blocks) ---------------------------------
 bool prefill_umma_supported(const PagedAttnCall& call);
 int launch_prefill_umma(const PagedAttnCall& call);
+bool decode_umma_supported(const PagedAttnCall& call);     // decode with 33..128 query rows per kv head
+int launch_decode_umma(const PagedAttnCall& call);
 
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,

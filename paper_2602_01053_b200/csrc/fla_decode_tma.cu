@@ -78,9 +78,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
 }
-__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
-}
 __device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -97,7 +94,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&v);
 }
 
-// D = d_head (64 / 128), RP = padded rank (0 / 8 / 16 / 32 / 64), MW = warps per worker, KT = 16-key
+// D = d_head (64 / 128), RP = padded rank (0 / 16 / 32 / 64), MW = warps per worker, KT = 16-key
 // steps per tile (1 for single-warp workers whose eight rings must share the SM's shared memory; 2 for
 // the multi-warp workers, which halves their per-tile synchronisation and doubles the MMA ILP)
 template <int D, int RP, int MW, int KT>
@@ -383,13 +380,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
             mma_bf16(olr[2 * np], pa[kt], b0, b1);
             mma_bf16(olr[2 * np + 1], pa[kt], b2, b3);
           }
-        }
-      } else if (RP == 8) {
-#pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-          uint32_t b0, b1;
-          ldsm_x2_t(sLR + (uint32_t)(key + 16 * kt) * 16u, b0, b1);     // lanes 16..31 pass valid, unused addresses
-          mma_bf16(olr[0], pa[kt], b0, b1);
         }
       }
     }

@@ -54,7 +54,6 @@ struct lorakv_ctx {
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
   void* pinned = nullptr;             // small pinned staging buffer
   size_t pinned_bytes = 0;
-  void* tma_encode = nullptr;         // cuTensorMapEncodeTiled, resolved through the runtime
   bool profiling = false;             // bracket the dominant kernel of fast-path calls with events
   cudaEvent_t prof_ev[2] = {nullptr, nullptr};
   bool prof_valid = false;
@@ -101,12 +100,6 @@ struct lorakv_pool {
   void* v_pages = nullptr;
   void* lr_pages = nullptr;  // [n_layers][lr_total_pages][P][r_pad]
   uint64_t reserved_bytes = 0;
-  // cached TMA descriptors (built lazily by the tcgen05 paths); opaque 128-byte blobs
-  alignas(64) unsigned char tmap_k[128];
-  alignas(64) unsigned char tmap_v[128];
-  alignas(64) unsigned char tmap_lr[128];
-  bool tmaps_ready = false;
-
   int64_t kv_sets() const { return dims.scheme == LORAKV_NONSHARED ? dims.n_agents : 1; }
   int64_t lr_sets() const {
     if (dims.scheme == LORAKV_BASESHARED) return dims.n_agents;

@@ -406,9 +406,17 @@ struct DecodeMergeParams {
   float* out;            // [layers][n_batch][n_q_local * d]
 };
 
-__global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMergeParams p) {
-  extern __shared__ float sm[];          // [ns] weights, then [r] merged O_lr
-  __shared__ float l_total;
+constexpr int kMergeWarps = 8;
+
+// One CTA per (query row, layer x kv head).  The splits of the row are spread over the warps (warp w takes
+// splits w, w + 8, ...), the 4 + D + RP columns of a partial over the lanes, so every global read is a
+// coalesced 128-byte line and a row with ~150 partials (one layer per launch) costs ~20 dependent steps,
+// not 150.
+__global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(const DecodeMergeParams p) {
+  extern __shared__ float sm[];          // [ns] weights | [kMergeWarps][D + RP] per-warp sums
+  __shared__ float red_s[kMergeWarps];
+  __shared__ float stat_s[2];            // row max, row denominator
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rho = blockIdx.x;
   const int kvh = blockIdx.y % p.n_kv_local;
   const int64_t layer_rel = blockIdx.y / p.n_kv_local;
@@ -417,39 +425,69 @@ __global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMerge
   const int64_t u = (layer_rel * p.n_kv_local + kvh) * p.row_blocks + rb;
   const int64_t w_lo = (u * p.T) / p.G, w_hi = ((u + 1) * p.T - 1) / p.G;
   const int ns = (int)(w_hi - w_lo + 1);
-  const int PS = 4 + p.D + p.RP;
+  const int PS = 4 + p.D + p.RP, C = p.D + p.RP;
   float* w_s = sm;
-  float* olr_s = sm + ns;
+  float* acc_s = sm + ns;
   const float ninf = -std::numeric_limits<float>::infinity();
   auto row_of = [&](int s) -> const float* {
     const int64_t w = w_lo + s;
     const int64_t slot = w * p.max_seg + (u - (w * p.G) / p.T);
     return p.part + (slot * rows_blk + r_in) * PS;
   };
-  if (threadIdx.x < 32) {
-    float mx = ninf;
-    for (int s = threadIdx.x; s < ns; s += 32) mx = fmaxf(mx, row_of(s)[0]);
+  // ---- row max over the splits ----
+  float mx = ninf;
+  for (int s = tid; s < ns; s += kMergeWarps * 32) mx = fmaxf(mx, row_of(s)[0]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float l = 0.f;
-    for (int s = threadIdx.x; s < ns; s += 32) {
-      const float* row = row_of(s);
-      const float wgt = (row[0] == ninf) ? 0.f : exp2f(row[0] - mx);
-      w_s[s] = wgt;
-      l += wgt * row[1];
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red_s[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    float m = red_s[0];
+    for (int i = 1; i < kMergeWarps; ++i) m = fmaxf(m, red_s[i]);
+    stat_s[0] = m;
+  }
+  __syncthreads();
+  mx = stat_s[0];
+  // ---- weights and the denominator ----
+  float l = 0.f;
+  for (int s = tid; s < ns; s += kMergeWarps * 32) {
+    const float* row = row_of(s);
+    const float wgt = (row[0] == ninf) ? 0.f : exp2f(row[0] - mx);
+    w_s[s] = wgt;
+    l += wgt * row[1];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  __syncthreads();                       // red_s reused; w_s complete
+  if (lane == 0) red_s[warp] = l;
+  __syncthreads();
+  if (tid == 0) {
+    float t = 0.f;
+    for (int i = 0; i < kMergeWarps; ++i) t += red_s[i];
+    stat_s[1] = t;
+  }
+  // ---- weighted sums of O and O_lr: warps over splits, lanes over columns ----
+  constexpr int kMaxCols = 6;            // (D + RP) <= 192 columns / 32 lanes
+  float acc[kMaxCols];
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) acc[i] = 0.f;
+  for (int s = warp; s < ns; s += kMergeWarps) {
+    const float wgt = w_s[s];
+    if (wgt == 0.f) continue;            // an empty split carries no accumulators
+    const float* row = row_of(s) + 4;
+#pragma unroll
+    for (int i = 0; i < kMaxCols; ++i) {
+      const int c = lane + 32 * i;
+      if (c < C) acc[i] = fmaf(wgt, row[c], acc[i]);
     }
+  }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (threadIdx.x == 0) l_total = l;
+  for (int i = 0; i < kMaxCols; ++i) {
+    const int c = lane + 32 * i;
+    if (c < C) acc_s[warp * C + c] = acc[i];
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < p.r; c += blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < ns; ++s)
-      if (w_s[s] != 0.f) acc = fmaf(w_s[s], row_of(s)[4 + p.D + c], acc);   // an empty split carries no accumulators
-    olr_s[c] = acc;
-  }
-  __syncthreads();
+  // ---- epilogue: o += (lr_scale * o_lr[k]) * B[agent][k,:], out = o / l (attention.hpp:244-259) ----
   const int gi = rho % p.group, entry = rho / p.group;
   const int64_t layer = p.layer_begin + layer_rel;
   const int64_t dkv = (int64_t)p.n_kv_local * p.D;
@@ -457,13 +495,16 @@ __global__ void __launch_bounds__(128) fla_decode_merge_kernel(const DecodeMerge
   const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
   float* dst = p.out + ((layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * p.D;
-  const float inv_l = 1.0f / l_total;
-  for (int c = threadIdx.x; c < p.D; c += blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < ns; ++s)
-      if (w_s[s] != 0.f) acc = fmaf(w_s[s], row_of(s)[4 + c], acc);
-    for (int k = 0; k < p.r; ++k) acc = fmaf(scale * olr_s[k], b[k * dkv + c], acc);
-    dst[c] = acc * inv_l;
+  const float inv_l = 1.0f / stat_s[1];
+  auto total = [&](int c) {
+    float t = 0.f;
+    for (int wq = 0; wq < kMergeWarps; ++wq) t += acc_s[wq * C + c];
+    return t;
+  };
+  for (int c = tid; c < p.D; c += kMergeWarps * 32) {
+    float o = total(c);
+    for (int k = 0; k < p.r; ++k) o = fmaf(scale * total(p.D + k), b[k * dkv + c], o);
+    dst[c] = o * inv_l;
   }
 }
 
@@ -521,7 +562,8 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
   mp.out = out_dev;
   const int ns_max = (int)((T - 1) / G + 2);
   dim3 mgrid((unsigned)rows_total, (unsigned)(n_layers * n_kv_local));
-  fla_decode_merge_kernel<<<mgrid, 128, (size_t)(ns_max + r + 1) * sizeof(float), ctx->stream>>>(mp);
+  if (d + rp > 192) return fail("decode merge: d_head + padded rank %d exceeds 192 columns", d + rp);
+  fla_decode_merge_kernel<<<mgrid, kMergeWarps * 32, (size_t)(ns_max + kMergeWarps * (d + rp)) * sizeof(float), ctx->stream>>>(mp);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
     }
     const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
     const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
-    if (lane == 0) {
+    if (ptx::elect_one()) {     // not `lane == 0`: no ELECT / BRA.U.ANY waterfall loop around each UBLKCP
       const uint32_t dst = ring + (uint32_t)p_stage * kStageBytes;
       const int64_t layer = p.layer_begin + p_layer;
       const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride +

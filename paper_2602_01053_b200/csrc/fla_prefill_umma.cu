@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
 
   if (warp == 8 || warp == 10) {
     // ===================== TMA producers: warp 8 streams K, warp 10 streams V_base + V_lr =====================
-    if (lane == 0) {
+    if (ptx::elect_one()) {
       const bool is_k = warp == 8;
       const int tpc = p.P < kBN ? p.P : kBN;           // tokens per bulk copy
       const int n_copies = kBN / tpc;
@@ -193,7 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     }
   } else if (warp == 9) {
     // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // elect.sync (not `lane == 0`): the compiler then knows one thread of a converged warp runs this
+    // block and emits straight-line UTCHMMA / UTCBAR; under `lane == 0` every tcgen05 instruction was
+    // wrapped in an ELECT / BRA.U.ANY waterfall loop (~80 cycles per MMA, the issue thread became the
+    // bottleneck of the whole CTA: ncu source view, profiles/r1_ncu_prefill_umma_v4_issue.txt)
+    if (ptx::elect_one()) {
       const uint32_t idesc_s = ptx::instr_desc_bf16(kBM, kBN, ptx::kMajorK, ptx::kMajorK);
       const uint32_t idesc_o = ptx::instr_desc_bf16(kBM, D, ptx::kMajorK, ptx::kMajorMN);
       const uint32_t idesc_lr = ptx::instr_desc_bf16(kBM, RP > 0 ? RP : 16, ptx::kMajorK, ptx::kMajorMN);

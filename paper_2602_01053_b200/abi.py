@@ -9,7 +9,7 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _CSRC = os.path.join(_PKG, "csrc")
-_LIB = os.path.join(_PKG, "lib", "liblorakv_b200.so")
+_LIB = os.environ.get("LORAKV_B200_LIB") or os.path.join(_PKG, "lib", "liblorakv_b200.so")   # the override is for A/B kernel builds (tools/)
 
 F32, BF16 = 0, 1
 HOST, DEVICE = 0, 1

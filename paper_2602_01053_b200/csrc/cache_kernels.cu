@@ -215,6 +215,129 @@ __global__ void __launch_bounds__(kProjWarps * 32) lr_append_project_kernel(
   for (int u = 0; u < 4; ++u) dst[u] = to_store<S>(c0 + u < rank ? acc[u] : 0.f);
 }
 
+// ---- tensor-core X * A for bf16 pools -------------------------------------------------------------
+// The CUDA-core kernel above issues 2 * r FFMA per element of X and tops out near 560 GB/s of X; the
+// product is HBM-bound (one pass over X, d_model * 4 bytes per row) once the MACs run on the tensor
+// pipe.  bf16 pools round X to bf16 anyway (the cache stores bf16), so X tiles are converted in
+// registers and fed to mma.sync.m16n8k16 (bf16 x bf16 -> fp32); A is split into bf16 hi + lo parts
+// (two MMAs), which keeps its fp32 value to 2^-17 whatever the caller uploaded.
+//
+// Layout of the work: a warp owns 16 * MT rows and one quarter of the reduction dimension (split-K
+// across the 4 warps of a CTA, combined through shared memory), so 4x as many warps stream X
+// concurrently.  A lane reads X as float4 (a quad covers 64 contiguous bytes of a row); the k order
+// inside a 16-wide step is permuted accordingly (slots 2t, 2t+1, 2t+8, 2t+9 <-> k0 + 4t .. 4t+3) and
+// the B fragments are pre-packed in that order by lr_project_pack_a, one 16-byte load per lane.
+constexpr int kMmaProjWarps = 4;
+
+__global__ void lr_project_pack_a_kernel(const float* __restrict__ A, int d_model, int rank, int n_tiles, uint4* __restrict__ frag) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;          // (k16 block, n8 tile, lane)
+  const int total = (d_model / 16) * n_tiles * 32;
+  if (idx >= total) return;
+  const int lane = idx % 32, nt = (idx / 32) % n_tiles, kb = idx / (32 * n_tiles);
+  const int g = lane >> 2, t = lane & 3, n = nt * 8 + g;
+  float v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = n < rank ? A[(int64_t)(kb * 16 + 4 * t + u) * rank + n] : 0.f;
+  __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) { hi[u] = __float2bfloat16_rn(v[u]); lo[u] = __float2bfloat16_rn(v[u] - __bfloat162float(hi[u])); }
+  auto pack = [](__nv_bfloat16 a, __nv_bfloat16 b) { return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16); };
+  frag[idx] = make_uint4(pack(hi[0], hi[1]), pack(hi[2], hi[3]), pack(lo[0], lo[1]), pack(lo[2], lo[3]));
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int RP, int MT>
+__global__ void __launch_bounds__(kMmaProjWarps * 32) lr_append_project_mma_kernel(
+    PageAddr a, int64_t row0, const float* __restrict__ x, int64_t n_rows, int64_t ld, const uint4* __restrict__ frag,
+    int d_model, int rank) {
+  constexpr int NT = RP / 8, ROWS = 16 * MT;
+  __shared__ float red[kMmaProjWarps][ROWS][RP + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int64_t r_first = (int64_t)blockIdx.x * ROWS;
+  const int kb_total = d_model / 16;
+  const int kb0 = (int)((int64_t)kb_total * warp / kMmaProjWarps), kb1 = (int)((int64_t)kb_total * (warp + 1) / kMmaProjWarps);
+
+  float acc[MT][NT][4];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[m][n][u] = 0.f;
+
+  const float* xr[MT][2];
+  bool ok[MT][2];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = r_first + 16 * m + g + 8 * h;
+      ok[m][h] = row < n_rows;
+      xr[m][h] = x + (ok[m][h] ? row : 0) * ld + 4 * t;
+    }
+  auto pack2 = [](float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+  };
+#pragma unroll 2
+  for (int kb = kb0; kb < kb1; ++kb) {
+    float4 xv[MT][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        xv[m][h] = ok[m][h] ? __ldcs(reinterpret_cast<const float4*>(xr[m][h] + kb * 16)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint4 bf[NT];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) bf[n] = __ldg(frag + ((int64_t)kb * NT + n) * 32 + lane);
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      uint32_t af[4];
+      af[0] = pack2(xv[m][0].x, xv[m][0].y); af[1] = pack2(xv[m][1].x, xv[m][1].y);
+      af[2] = pack2(xv[m][0].z, xv[m][0].w); af[3] = pack2(xv[m][1].z, xv[m][1].w);
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        mma_bf16_16816(acc[m][n], af, bf[n].x, bf[n].y);
+        mma_bf16_16816(acc[m][n], af, bf[n].z, bf[n].w);
+      }
+    }
+  }
+  // split-K partials -> shared memory, then 8 consecutive columns of a row (one 16-byte chunk of the
+  // swizzled page) per thread
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      red[warp][16 * m + g][8 * n + 2 * t] = acc[m][n][0]; red[warp][16 * m + g][8 * n + 2 * t + 1] = acc[m][n][1];
+      red[warp][16 * m + g + 8][8 * n + 2 * t] = acc[m][n][2]; red[warp][16 * m + g + 8][8 * n + 2 * t + 1] = acc[m][n][3];
+    }
+  __syncthreads();
+  for (int item = tid; item < ROWS * NT; item += kMmaProjWarps * 32) {
+    const int rr = item / NT, c0 = (item % NT) * 8;
+    const int64_t i_row = r_first + rr;
+    if (i_row >= n_rows) continue;
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      float sum = 0.f;
+#pragma unroll
+      for (int w = 0; w < kMmaProjWarps; ++w) sum += red[w][rr][c0 + u];
+      v[u] = c0 + u < rank ? sum : 0.f;
+    }
+    const int64_t row = row0 + i_row;
+    const int64_t phys = a.table[row / a.P];
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(a.base) + phys * a.page_stride + page_offset(a.lay, (int)(row % a.P), c0);
+    uint4 pk;
+    pk.x = pack2(v[0], v[1]); pk.y = pack2(v[2], v[3]); pk.z = pack2(v[4], v[5]); pk.w = pack2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(dst) = pk;
+  }
+}
+
 PageAddr make_addr(const lorakv_pool* pool, int which, int64_t layer, int64_t set) {
   PageAddr a;
   const int64_t elem = pool->elem;
@@ -291,6 +414,27 @@ int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, in
   const float* A = a_dev;
   const bool bf16 = pool->dims.dtype == LORAKV_BF16;
   const bool vec_ok = (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x_dev) & 15) == 0);
+  // bf16 pools: tensor-core kernel (policy 1 keeps the CUDA-core kernel for cross-checks)
+  if (bf16 && ctx->policy != 1 && vec_ok && d_model % 16 == 0 && d_model >= 64 && a.width <= 64 && a.lay.bw == a.width && a.width % 8 == 0) {
+    const int nt = a.width / 8;
+    const size_t frag_bytes = (size_t)(d_model / 16) * nt * 32 * sizeof(uint4);
+    LK_TRY(scratch_reserve(ctx, ctx->work, frag_bytes));
+    uint4* frag = static_cast<uint4*>(ctx->work.ptr);
+    const int total = (int)(d_model / 16) * nt * 32;
+    lr_project_pack_a_kernel<<<(total + 255) / 256, 256, 0, ctx->stream>>>(A, (int)d_model, (int)rank, nt, frag);
+    auto go = [&](auto kern, int rows) {
+      kern<<<(unsigned)((n_rows + rows - 1) / rows), kMmaProjWarps * 32, 0, ctx->stream>>>(a, row0, x_dev, n_rows, ld, frag, (int)d_model, (int)rank);
+    };
+    switch (a.width) {
+      case 8: go(lr_append_project_mma_kernel<8, 2>, 32); break;
+      case 16: go(lr_append_project_mma_kernel<16, 2>, 32); break;
+      case 32: go(lr_append_project_mma_kernel<32, 2>, 32); break;
+      default: go(lr_append_project_mma_kernel<64, 1>, 16); break;
+    }
+    ctx->launches += 2;
+    LK_CUDA(cudaGetLastError());
+    return LORAKV_OK;
+  }
   auto launch = [&](auto kern, int rp) {
     const int rows_per_cta = kProjWarps * (128 / rp);
     const unsigned blocks = (unsigned)((n_rows + rows_per_cta - 1) / rows_per_cta);

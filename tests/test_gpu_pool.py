@@ -230,6 +230,39 @@ def test_lr_append_project_matches_matmul(ctx, orc):
     pool.close()
 
 
+@pytest.mark.parametrize("r,L,d_model,P", [(16, 300, 192, 64), (8, 77, 64, 16), (2, 45, 128, 32), (32, 1000, 4096, 64),
+                                            (64, 130, 256, 128), (24, 95, 320, 64)])
+def test_lr_append_project_bf16_tensor_core_kernel(ctx, orc, r, L, d_model, P):
+    """bf16 pools compute V_lr = X * A (engine.hpp:414-418) with mma.sync (X rounded to bf16 as the cache dtype
+    implies, A kept to fp32 accuracy by a hi + lo split) and store bf16 into the swizzled LR pages.  Checked
+    against matmul (matrix.hpp:101-111) of the rounded X and the caller's un-rounded A, for every rank padding,
+    ragged row counts, an append that starts mid-page and against the CUDA-core kernel (policy 1)."""
+    from paper_2602_01053_b200 import Adapters, Pool, abi
+    x = orc.round_bf16(orc.gaussian(L, d_model, orc.child(900 + r, 1), 1.0, np.float32))
+    A = orc.gaussian(d_model, r, orc.child(900 + r, 2), 1.0 / np.sqrt(d_model), np.float32)     # NOT bf16-representable
+    want = orc.matmul(x, A)
+    got = {}
+    for policy in (0, 1):
+        ctx.set_kernel_policy(policy)
+        pool = Pool(ctx, "BaseLRShared", 1, 2, 32, d_model, r, 2, max_tokens=L + 8, dtype=abi.BF16, page_tokens=P)
+        ad = Adapters(ctx, 1, 2, d_model, r, 2, 32, dtype=abi.BF16)
+        ad.set_a(0, A)
+        pool.append_tokens(L)
+        first = min(L, 37)
+        assert pool.append_lr_project(ad, 0, 0, 0, x[:first]) == first
+        assert pool.append_lr_project(ad, 0, 0, first, x[first:]) == L - first      # starts mid-page
+        assert pool.append_lr_project(ad, 0, 0, 0, x) == 0                          # first writer wins
+        got[policy] = pool.lr_view(0, 0)
+        assert got[policy].shape == want.shape
+        # bf16 storage: half an ulp of bf16 (2^-9) on each element, relative to the largest one
+        assert orc.max_rel_error(got[policy], want) <= 4e-3, policy
+        pool.close(); ad.close()
+    ctx.set_kernel_policy(0)
+    # same products, fp32 accumulation in a different order: the two kernels may differ by one bf16 rounding flip
+    assert orc.max_rel_error(got[0], got[1]) <= 4e-3
+    assert np.mean(got[0] == got[1]) > 0.98
+
+
 @pytest.mark.parametrize("dtype_name,tol", [("F32", 1e-4), ("BF16", 2e-2)])
 def test_prefill_block_matches_reference_path(ctx, orc, dtype_name, tol):
     """Append-step attention: L_c new rows at query_offset = L_p on a cache that already holds them

@@ -10,25 +10,32 @@
 //
 // Mapping.  One CTA owns the g q heads of one kv head for PB = 128 / g consecutive query positions:
 // the 128 MMA rows are (head-in-group, position), so a K/V tile is fetched once for the whole group
-// (the reference re-reads it per q head, :347-361).  Key tiles of 128 are visited up to the causal
-// boundary of the CTA's last row; only the boundary tiles pay for the mask.
+// (the reference re-reads it per q head, :347-361).  Keys are visited up to the causal boundary of the
+// CTA's last row; only the boundary tiles pay for the mask.
 //
 // Roles (352 threads):
-//   warps 0-7  softmax + correction + epilogue; warps w and w+4 share MMA rows 32(w%4)..+31 (= TMEM
-//              lanes) and split the 128 key columns of a tile in halves (row max exchanged through smem)
-//   warp 8/10  TMA producers: bulk copies of K (warp 8) and of V_base + V_lr (warp 10) into 3-stage rings,
-//              mbarrier tracked; independent, so a K tile is requested two tiles before its S MMA
-//   warp 9     MMA issuer (one thread): S(j) = Q K_j^T into one of two TMEM S buffers, then
-//              O += P_j V_j and O_lr += P_j V_lr_j; issue order S0 S1 PV0 S2 PV1 S3 ... so the tensor
-//              pipe computes S(j+1) while the softmax warps work on S(j)
-// TMEM (512 columns): S0 [0,128) | S1 [128,256) | O [256,256+D) | O_lr [384,384+RP) | Q [448,448+D/2)
+//   warps 0-7  softmax + correction + epilogue.  A softmax tile is 128 rows x 64 keys; thread (w, lane)
+//              owns the whole row 32 (w % 4) + lane of it (64 scores in registers, no cross-thread
+//              reduction).  Warps 0-3 take the even tiles, warps 4-7 the odd ones: the two warps that
+//              share a scheduler (w and w + 4: same TMEM lanes) are always half a tile apart, so one
+//              warp's TMEM load / row max / bookkeeping runs under the other's exp phase and the MUFU
+//              (16 ex2 / clk / SM -- the longest per-tile resource next to the tensor pipe) never idles.
+//              The running row maximum is handed from tile j to tile j + 1 through one 8-byte shared-memory
+//              word per row (sequence number | value), so only the two threads of a row ever wait for each other.
+//   warp 8/10  TMA producers: bulk copies of K (warp 8) and of V_base + V_lr (warp 10) into 3-stage rings
+//              of 128-key stages, mbarrier tracked, independent of each other
+//   warp 9     MMA issuer (one elected thread): S(j) = Q K_j^T (N = 64) into one of FOUR TMEM S buffers,
+//              O += P_j V_j and O_lr += P_j V_lr_j; issue order S0 S1 S2 | PV0 S3 | PV1 S4 | ... so three
+//              score tiles are always in flight ahead of the softmax warps
+// TMEM (512 columns): S0..S3 [0,256) 64 each | O [256,256+D) | O_lr [384,384+RP) | Q [448,448+D/2)
 // Q and P never touch shared memory: both are written to TMEM as packed bf16 pairs (tcgen05.st) and fed
-// to tcgen05.mma as the A operand from TMEM; P(j) overwrites the first 64 columns of the S buffer it was
+// to tcgen05.mma as the A operand from TMEM; P(j) overwrites the first 32 columns of the S buffer it was
 // computed from.  Shared memory then carries only the K / V / V_lr tiles -- with A in shared memory a
 // 128x128x16 MMA needs 8 KB per 64 cycles, the whole 128 B/clk of the SM, and the kernel was bound by
 // shared-memory bandwidth (ncu, profiles/r1_ncu_prefill_umma_v1.txt).  Masked entries are exact zeros
 // and never exponentiated (attention.hpp:171).  Rescaling of O / O_lr is lazy: only when a row's running
-// max grows by more than 8 (log2 units), which leaves the result unchanged.
+// max grows by more than 8 (log2 units), which leaves the result unchanged; the thread that sees the
+// growth waits for PV(j-1), rescales its row and only then hands the new maximum on.
 #include <cuda_bf16.h>
 
 #include <limits>
@@ -43,7 +50,8 @@ namespace lk {
 namespace {
 
 constexpr int kBM = 128;            // MMA rows per CTA
-constexpr int kBN = 128;            // keys per tile
+constexpr int kBN = 128;            // keys per K / V stage in shared memory
+constexpr int kSN = 64;             // keys per softmax tile (one S buffer in TMEM)
 constexpr int kThreads = 352;        // 8 softmax warps + K producer + MMA issuer + V producer
 constexpr int kMaxStages = 3;
 constexpr float kRescaleThreshold = 8.0f;
@@ -84,8 +92,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 }
 
 struct Barriers {
-  uint64_t q_full, p_full, pv_done;
-  uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[2];
+  uint64_t q_full, p_full[4], pv_done[4], all_done;
+  uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[4];
 };
 
 // kDecode = false: prefill block (rows = head x position, causal mask, final output)
@@ -95,26 +103,27 @@ template <int D, int RP, bool kDecode>
 __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const PrefillParams p) {
   constexpr int kQBlocks = D / 64;                           // 64-column K-blocks of Q / K; 64-column N-blocks of V
   constexpr uint32_t kBlkBytes = kBN * 128;                  // one [128 rows][64] bf16 block = 16 KB
-  constexpr uint32_t kKBytes = kQBlocks * kBlkBytes;         // K tile == V tile bytes
+  constexpr uint32_t kKBytes = kQBlocks * kBlkBytes;         // K stage == V stage bytes
   constexpr uint32_t kLrRow = 2 * RP;                        // bytes of one V_lr row
   constexpr uint32_t kLrBytes = kBN * kLrRow;
   constexpr uint32_t kTmemS = 0, kTmemO = 256, kTmemLr = 384, kTmemQ = 448;
-  // K / V ring depth: three stages hide the L2 latency of a tile behind two tiles of work; the widest
+  // K / V ring depth: three stages hide the L2 latency of a stage behind two stages of work; the widest
   // configuration (d 128, rank 64) only has room for two
   constexpr int kStages = (2 * 3 * kKBytes + 3 * kLrBytes + 1024 <= 227 * 1024 - 4096) ? 3 : 2;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ Barriers bars;
   __shared__ uint32_t tmem_base_s;
-  __shared__ float mx_s[2][2][kBM];     // [tile parity][column half][row]: partial row maxima
-  __shared__ float l_s[2][kBM];         // [column half][row]: partial row sums for the epilogue
+  __shared__ unsigned long long hand_s[kBM];   // (tile count << 32 | running row maximum): owner of tile j -> owner of j + 1
+  __shared__ float l_s[2][kBM];         // [softmax warpgroup][row]: partial row sums for the epilogue ...
+  __shared__ float mref_s[2][kBM];      // ... and the maximum each of them is relative to
   unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* sK = smem;                          // kStages stages each
   unsigned char* sV = sK + kStages * kKBytes;
   unsigned char* sLR = sV + kStages * kKBytes;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // ---- what this CTA owns ----
+  // ---- what this CTA owns: n_tiles softmax tiles of kSN keys starting at key tile_begin * kSN ----
   int PB, kvh, n_tiles, tile_begin;
   int64_t q0, rows_here, kv_layer_off, lr_layer_off, mask_from;   // mask_from: first key that some row cannot see
   int unit = 0, split = 0, layer_rel = 0;
@@ -125,7 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     q0 = (int64_t)qb * PB;
     rows_here = min((int64_t)PB, p.L_c - q0);                     // real positions in this block
     const int64_t last_visible_cta = p.query_offset + q0 + rows_here - 1;
-    n_tiles = (int)(last_visible_cta / kBN) + 1;
+    n_tiles = (int)(last_visible_cta / kSN) + 1;
     tile_begin = 0;
     kv_layer_off = p.kv_layer_off; lr_layer_off = p.lr_layer_off;
     mask_from = p.query_offset + q0 + 1;
@@ -133,24 +142,27 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     PB = 1; q0 = 0; rows_here = p.rows_total;
     unit = (int)(blockIdx.x / p.splits); split = (int)(blockIdx.x % p.splits);
     layer_rel = unit / p.n_kv_local; kvh = unit % p.n_kv_local;
-    const int total_tiles = (int)((p.L + kBN - 1) / kBN);
-    tile_begin = split * p.tiles_per_split;
-    n_tiles = min(p.tiles_per_split, total_tiles - tile_begin);
+    const int total_tiles = (int)((p.L + kSN - 1) / kSN);
+    tile_begin = split * p.tiles_per_split * (kBN / kSN);         // the host splits in stages of kBN keys
+    n_tiles = min(p.tiles_per_split * (kBN / kSN), total_tiles - tile_begin);
     if (n_tiles < 0) n_tiles = 0;
     kv_layer_off = p.kv_layer_off + (int64_t)layer_rel * p.kv_layer_stride;
     lr_layer_off = p.lr_layer_off + (int64_t)layer_rel * p.lr_layer_stride;
     mask_from = p.L;
   }
+  const int n_stages_needed = (n_tiles + 1) / 2;                  // kBN-key stages the producers stream
 
+  if (tid < kBM) hand_s[tid] = 0ull;
   if (tid == 0) {
     ptx::mbar_init(&bars.q_full, 256);
-    ptx::mbar_init(&bars.p_full, 256);
-    ptx::mbar_init(&bars.pv_done, 1);
+    for (int s = 0; s < 4; ++s) ptx::mbar_init(&bars.p_full[s], 128);
+    for (int s = 0; s < 4; ++s) ptx::mbar_init(&bars.pv_done[s], 1);
+    ptx::mbar_init(&bars.all_done, 1);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&bars.k_full[s], 1); ptx::mbar_init(&bars.k_empty[s], 1);
       ptx::mbar_init(&bars.v_full[s], 1); ptx::mbar_init(&bars.v_empty[s], 1);
     }
-    ptx::mbar_init(&bars.s_full[0], 1); ptx::mbar_init(&bars.s_full[1], 1);
+    for (int s = 0; s < 4; ++s) ptx::mbar_init(&bars.s_full[s], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc(&tmem_base_s, 512);
@@ -169,12 +181,13 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       uint64_t* empty = is_k ? bars.k_empty : bars.v_empty;
       unsigned char* ring = is_k ? sK : sV;
       const __nv_bfloat16* pages = is_k ? p.k_pages : p.v_pages;
-      for (int j = 0; j < n_tiles; ++j) {
+      const int64_t stage_key0 = (int64_t)tile_begin * kSN;
+      for (int j = 0; j < n_stages_needed; ++j) {
         const int s = j % kStages;
         if (j >= kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));   // the phase that freed the stage
         ptx::mbar_arrive_expect_tx(&full[s], is_k ? kKBytes : kKBytes + kLrBytes);
         for (int i = 0; i < n_copies; ++i) {
-          const int64_t key0 = (int64_t)(tile_begin + j) * kBN + (int64_t)i * tpc;
+          const int64_t key0 = stage_key0 + (int64_t)j * kBN + (int64_t)i * tpc;
           int page = (int)(key0 / p.P);
           const int tok0 = (int)(key0 % p.P);
           if (page >= p.n_pages) page = p.n_pages - 1;  // wholly masked keys: any finite rows will do
@@ -196,60 +209,74 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     // elect.sync (not `lane == 0`): the compiler then knows one thread of a converged warp runs this
     // block and emits straight-line UTCHMMA / UTCBAR; under `lane == 0` every tcgen05 instruction was
     // wrapped in an ELECT / BRA.U.ANY waterfall loop (~80 cycles per MMA, the issue thread became the
-    // bottleneck of the whole CTA: ncu source view, profiles/r1_ncu_prefill_umma_v4_issue.txt)
+    // bottleneck of the whole CTA: ncu source view, profiles/r1_ncu_prefill_umma_v5_elect.txt)
     if (ptx::elect_one()) {
-      const uint32_t idesc_s = ptx::instr_desc_bf16(kBM, kBN, ptx::kMajorK, ptx::kMajorK);
+      // The issue thread is the scarcest resource of the CTA (one instruction every few cycles): everything
+      // that does not change per tile is folded into descriptor words computed once, a tile only adds its
+      // stage offset to the low word (the 14-bit start-address field, units of 16 bytes).
+      const uint32_t idesc_s = ptx::instr_desc_bf16(kBM, kBN, ptx::kMajorK, ptx::kMajorK);     // S of TWO tiles at once
       const uint32_t idesc_o = ptx::instr_desc_bf16(kBM, D, ptx::kMajorK, ptx::kMajorMN);
       const uint32_t idesc_lr = ptx::instr_desc_bf16(kBM, RP > 0 ? RP : 16, ptx::kMajorK, ptx::kMajorMN);
       const uint32_t lr_mode = RP == 64 ? ptx::kSw128 : RP == 32 ? ptx::kSw64 : ptx::kSw32;
-      auto issue_s = [&](int j) {
-        const int s = j & 1;                       // S buffer in TMEM
-        const int ks_stage = j % kStages;          // K stage in shared memory
-        ptx::mbar_wait(&bars.k_full[ks_stage], (uint32_t)((j / kStages) & 1));
+      const uint64_t kd = ptx::smem_desc(ptx::smem_u32(sK), 16u, 1024u, ptx::kSw128);
+      const uint64_t vd = ptx::smem_desc(ptx::smem_u32(sV), kBlkBytes, 1024u, ptx::kSw128);
+      const uint64_t ld = ptx::smem_desc(ptx::smem_u32(sLR), kBN * kLrRow, 8u * kLrRow, lr_mode);
+      const uint32_t kd_hi = (uint32_t)(kd >> 32), vd_hi = (uint32_t)(vd >> 32), ld_hi = (uint32_t)(ld >> 32);
+      auto desc = [](uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; };
+      // S of tiles (j, j + 1), j even: one N = 128 MMA chain over the whole K stage (j / 2) % kStages into the
+      // adjacent S buffers j % 4 and j % 4 + 1
+      auto issue_s2 = [&](int j) {
+        const int st = j >> 1, ks_stage = st % kStages;
+        ptx::mbar_wait(&bars.k_full[ks_stage], (uint32_t)((st / kStages) & 1));
         ptx::tc_fence_after();
-        const uint32_t k_addr = ptx::smem_u32(sK + ks_stage * kKBytes);
+        const uint32_t k_lo = (uint32_t)kd + (uint32_t)ks_stage * (kKBytes >> 4);
+        const uint32_t s_tmem = tmem + kTmemS + (uint32_t)(j & 3) * kSN;
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t off = (uint32_t)(ks / 4) * kBlkBytes + (uint32_t)(ks % 4) * 32u;
-          ptx::umma_bf16_ts(tmem + kTmemS + (uint32_t)s * kBN, tmem + kTmemQ + 8u * ks,
-                            ptx::smem_desc(k_addr + off, 16u, 1024u, ptx::kSw128), idesc_s, ks > 0 ? 1u : 0u);
-        }
+        for (int ks = 0; ks < D / 16; ++ks)
+          ptx::umma_bf16_ts(s_tmem, tmem + kTmemQ + 8u * ks, desc(kd_hi, k_lo + (uint32_t)(((ks / 4) * kBlkBytes + (ks % 4) * 32u) >> 4)),
+                            idesc_s, ks > 0 ? 1u : 0u);
         ptx::umma_commit(&bars.k_empty[ks_stage]);
-        ptx::umma_commit(&bars.s_full[s]);
+        ptx::umma_commit(&bars.s_full[j & 3]);
+        ptx::umma_commit(&bars.s_full[(j & 3) + 1]);
       };
       if (n_tiles > 0) {
         ptx::mbar_wait(&bars.q_full, 0);
         ptx::tc_fence_after();
-        issue_s(0);
+        issue_s2(0);
       }
-      if (n_tiles > 1) issue_s(1);
+      if (n_tiles > 2) issue_s2(2);
       for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1, vs = j % kStages;
-        ptx::mbar_wait(&bars.p_full, (uint32_t)(j & 1));
-        ptx::mbar_wait(&bars.v_full[vs], (uint32_t)((j / kStages) & 1));
+        const int st = j >> 1, vs = st % kStages, h = j & 1;
+        // one P barrier per S buffer (not per warpgroup): a warpgroup can finish tile j + 2 before this thread
+        // has looked at tile j (S(j+2) is issued ahead of PV(j)), and a parity wait two phases late never returns;
+        // P(j+4) needs S(j+4), which is only issued behind PV(j+1)
+        ptx::mbar_wait(&bars.p_full[j & 3], (uint32_t)((j >> 2) & 1));
+        if (h == 0) ptx::mbar_wait(&bars.v_full[vs], (uint32_t)((st / kStages) & 1));
         ptx::tc_fence_after();
-        const uint32_t v_addr = ptx::smem_u32(sV + vs * kKBytes), lr_addr = ptx::smem_u32(sLR + vs * kLrBytes);
+        const uint32_t v_lo = (uint32_t)vd + (uint32_t)vs * (kKBytes >> 4) + (uint32_t)h * ((kSN / 16) * 2048u >> 4);
+        const uint32_t l_lo = (uint32_t)ld + (uint32_t)vs * (kLrBytes >> 4) + (uint32_t)h * ((kSN / 16) * 16u * kLrRow >> 4);
+        const uint32_t p_tmem = tmem + kTmemS + (uint32_t)(j & 3) * kSN;                 // P(j) sits in the S(j) buffer
 #pragma unroll
-        for (int ks = 0; ks < kBN / 16; ++ks) {
-          const uint32_t p_tmem = tmem + kTmemS + (uint32_t)s * kBN + 8u * ks;    // P(j) sits in the S(j) buffer
-          ptx::umma_bf16_ts(tmem + kTmemO, p_tmem, ptx::smem_desc(v_addr + (uint32_t)ks * 2048u, kBlkBytes, 1024u, ptx::kSw128), idesc_o,
+        for (int ks = 0; ks < kSN / 16; ++ks) {
+          ptx::umma_bf16_ts(tmem + kTmemO, p_tmem + 8u * ks, desc(vd_hi, v_lo + (uint32_t)ks * (2048u >> 4)), idesc_o,
                             (j > 0 || ks > 0) ? 1u : 0u);
           if (RP > 0)
-            ptx::umma_bf16_ts(tmem + kTmemLr, p_tmem, ptx::smem_desc(lr_addr + (uint32_t)ks * 16u * kLrRow, kBN * kLrRow, 8u * kLrRow, lr_mode),
-                              idesc_lr, (j > 0 || ks > 0) ? 1u : 0u);
+            ptx::umma_bf16_ts(tmem + kTmemLr, p_tmem + 8u * ks, desc(ld_hi, l_lo + (uint32_t)ks * (16u * kLrRow >> 4)), idesc_lr,
+                              (j > 0 || ks > 0) ? 1u : 0u);
         }
-        ptx::umma_commit(&bars.v_empty[vs]);
-        ptx::umma_commit(&bars.pv_done);
-        if (j + 2 < n_tiles) issue_s(j + 2);
+        if (h == 1 || j == n_tiles - 1) ptx::umma_commit(&bars.v_empty[vs]);
+        ptx::umma_commit(&bars.pv_done[j & 3]);
+        if (j == n_tiles - 1) ptx::umma_commit(&bars.all_done);
+        // S of tiles (j + 3, j + 4) into the buffers of tiles (j - 1, j), both of whose PV are issued by now
+        if (h == 1 && j + 3 < n_tiles) issue_s2(j + 3);
       }
     }
   } else {
     // ===================== softmax / correction / epilogue =====================
-    // warp w and warp w + 4 share MMA rows 32 (w % 4) .. +31 (the TMEM lanes both may touch) and split
-    // the 128 key columns of a tile in halves; thread (w, lane) owns row 32 (w % 4) + lane, half w / 4
+    // thread (w, lane) owns MMA row 32 (w % 4) + lane (= its TMEM lane); warpgroup wg = w / 4 takes the
+    // tiles j with j % 2 == wg
     const int row = (warp & 3) * 32 + lane;
-    const int half = warp >> 2;
-    const int pair_bar = 1 + (warp & 3);                     // named barrier of the two warps sharing rows
+    const int wg = warp >> 2;
     // row -> (query row of the call, q head): prefill rows are (head in group, position); decode rows are
     // (batch entry, head in group), every one at position L - 1
     bool real_row;
@@ -273,12 +300,11 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       q_src = p.q + (((int64_t)(p.layer_begin_rel + layer_rel) * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
     }
     const float ninf = -std::numeric_limits<float>::infinity();
-    constexpr int kHalf = kBN / 2;                           // key columns per thread
 
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     // ---- Q tile -> TMEM: this thread's half of its row, fp32 -> packed bf16 pairs ----
     {
-      const float* src = q_src + half * (D / 2);
+      const float* src = q_src + wg * (D / 2);
 #pragma unroll
       for (int c0 = 0; c0 < D / 4; c0 += 16) {          // D/4 packed columns per thread, 16 per store
         uint32_t r16[16];
@@ -288,67 +314,79 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
           r16[i] = pack_bf16(v.x, v.y);
           r16[i + 1] = pack_bf16(v.z, v.w);
         }
-        ptx::tmem_st16(tmem + lane_base + kTmemQ + (uint32_t)half * (D / 4) + c0, r16);
+        ptx::tmem_st16(tmem + lane_base + kTmemQ + (uint32_t)wg * (D / 4) + c0, r16);
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bars.q_full);
     }
 
-    float m_used = ninf;          // identical in both threads of a row (in raw-score units times scale_log2)
-    float l_run = 0.f;            // this thread's half of the row sum
-    for (int j = 0; j < n_tiles; ++j) {
-      const int sb = j & 1;
-      ptx::mbar_wait(&bars.s_full[sb], (uint32_t)((j >> 1) & 1));
+    float m_mine = ninf;          // the maximum this thread's row sum is relative to (scaled, log2 units)
+    float l_run = 0.f;            // row sum over this warpgroup's tiles
+    for (int j = wg; j < n_tiles; j += 2) {
+      const int sb = j & 3;
+      ptx::mbar_wait(&bars.s_full[sb], (uint32_t)((j >> 2) & 1));
       ptx::tc_fence_after();
-      float sc[kHalf];
+      float sc[kSN];
       {
-        uint32_t raw[kHalf];
-        ptx::tmem_ld64_wait(tmem + lane_base + kTmemS + (uint32_t)sb * kBN + (uint32_t)half * kHalf, raw);
+        uint32_t raw[kSN];
+        ptx::tmem_ld64_wait(tmem + lane_base + kTmemS + (uint32_t)sb * kSN, raw);
 #pragma unroll
-        for (int c = 0; c < kHalf; ++c) sc[c] = __uint_as_float(raw[c]);
+        for (int c = 0; c < kSN; ++c) sc[c] = __uint_as_float(raw[c]);
       }
 
-      const int64_t key0 = (int64_t)(tile_begin + j) * kBN + half * kHalf;
-      const bool tile_needs_mask = (int64_t)(tile_begin + j) * kBN + kBN - 1 >= mask_from;   // CTA-uniform
+      const int64_t key0 = (int64_t)(tile_begin + j) * kSN;
+      const bool tile_needs_mask = key0 + kSN - 1 >= mask_from;   // CTA-uniform
       if (tile_needs_mask) {
 #pragma unroll
-        for (int c = 0; c < kHalf; ++c)
+        for (int c = 0; c < kSN; ++c)
           if (key0 + c > last_visible) sc[c] = ninf;
       }
-      // row max of the raw scores: 8 independent chains, then the partner's half through shared memory
+      // row max of the raw scores: 8 independent chains
       float mx8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) mx8[u] = sc[u];
 #pragma unroll
-      for (int c = 8; c < kHalf; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sc[c]);
-      float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])), fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      mx_s[j & 1][half][row] = mx;
-      named_bar_sync(pair_bar, 64);
-      mx = fmaxf(mx, mx_s[j & 1][half ^ 1][row]) * p.scale_log2;     // scale > 0 commutes with max; -inf stays -inf
+      for (int c = 8; c < kSN; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], sc[c]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])), fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) *
+                       p.scale_log2;                       // scale > 0 commutes with max; -inf stays -inf
 
-      const float m_cand = fmaxf(m_used, mx);
-      const bool grow = m_cand > m_used + kRescaleThreshold;
+      // the running maximum after tile j - 1, published by the partner warp
+      float m_prev = ninf;
+      if (j > 0) {                  // one 8-byte word per row: the sequence number says the value is the one after tile j - 1
+        unsigned long long hv;
+        do { hv = *reinterpret_cast<volatile unsigned long long*>(&hand_s[row]); } while ((uint32_t)(hv >> 32) != (uint32_t)j);
+        m_prev = __uint_as_float((uint32_t)hv);
+      }
+      float m_used = m_prev;
+      const float m_cand = fmaxf(m_prev, mx);
       if (j == 0) {
         m_used = m_cand;          // key 0 is visible to every row, so this is finite
-      } else if (__any_sync(0xffffffffu, grow)) {
-        // correction: O and O_lr of this row are final for tile j-1 once pv_done(j-1) has fired;
-        // the two warps of a pair take the decision on identical values and split the columns
-        ptx::mbar_wait(&bars.pv_done, (uint32_t)((j - 1) & 1));
-        ptx::tc_fence_after();
-        const float alpha = grow ? ex2(m_used - m_cand) : 1.f;
-        if (grow) { m_used = m_cand; l_run *= alpha; }
+      } else {
+        const bool grow = m_cand > m_prev + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, grow)) {
+          // correction: O and O_lr of this row are final for tile j-1 once PV(j-1) has completed, and PV(j)
+          // cannot start before this thread delivers P(j).  A parity wait is only meaningful while the barrier
+          // is at most one phase away from the one asked for, so PV completion is tracked by FOUR barriers
+          // (tile % 4), each advancing once per four tiles: S(j) having arrived guarantees PV(j-4) (S of an
+          // odd tile is issued with its even neighbour, behind PV(j-4)), hence PV(j-5), and PV(j+3) cannot
+          // have been issued.
+          ptx::mbar_wait(&bars.pv_done[(j - 1) & 3], (uint32_t)(((j - 1) >> 2) & 1));
+          ptx::tc_fence_after();
+          // tcgen05.ld / st are warp-collective (.sync.aligned): every lane takes part, lanes whose row did not
+          // grow scale by 1
+          const float alpha = grow ? ex2(m_prev - m_cand) : 1.f;
+          if (grow) m_used = m_cand;
 #pragma unroll
-        for (int c0 = 0; c0 < D / 2; c0 += 16) {
-          uint32_t r16[16];
-          const uint32_t addr = tmem + lane_base + kTmemO + (uint32_t)half * (D / 2) + c0;
-          ptx::tmem_ld16(addr, r16);
-          ptx::tmem_wait_ld();
+          for (int c0 = 0; c0 < D; c0 += 16) {
+            uint32_t r16[16];
+            const uint32_t addr = tmem + lane_base + kTmemO + c0;
+            ptx::tmem_ld16(addr, r16);
+            ptx::tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) r16[i] = __float_as_uint(__uint_as_float(r16[i]) * alpha);
-          ptx::tmem_st16(addr, r16);
-        }
-        if (half == 0) {
+            for (int i = 0; i < 16; ++i) r16[i] = __float_as_uint(__uint_as_float(r16[i]) * alpha);
+            ptx::tmem_st16(addr, r16);
+          }
 #pragma unroll
           for (int c0 = 0; c0 < RP; c0 += 16) {
             uint32_t r16[16];
@@ -358,47 +396,65 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
             for (int i = 0; i < 16; ++i) r16[i] = __float_as_uint(__uint_as_float(r16[i]) * alpha);
             ptx::tmem_st16(tmem + lane_base + kTmemLr + c0, r16);
           }
+          ptx::tmem_wait_st();
         }
-        ptx::tmem_wait_st();
+      }
+      // hand the maximum to the owner of tile j + 1
+      if (j + 1 < n_tiles)
+        *reinterpret_cast<volatile unsigned long long*>(&hand_s[row]) = ((unsigned long long)(uint32_t)(j + 1) << 32) | __float_as_uint(m_used);
+      // bring this warpgroup's row sum to the new reference (its last tile was j - 2)
+      if (m_used != m_mine) {
+        l_run *= (m_mine == ninf) ? 0.f : ex2(m_mine - m_used);
+        m_mine = m_used;
       }
       // P = exp2(s * scale - m) in one FFMA + MUFU; masked entries (-inf) come out as exact zeros
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < kHalf; ++c) {
+      for (int c = 0; c < kSN; ++c) {
         const float e = ex2(fmaf(sc[c], p.scale_log2, -m_used));
         sc[c] = e;
         ls4[c & 3] += e;
       }
       l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
-      // P(j) -> TMEM, over the first 64 columns of the S(j) buffer: both threads of the row have read
-      // their scores (the pair barrier above), and S(j+2) is issued behind PV(j) on the in-order pipe
+      // P(j) -> TMEM, over the first 32 columns of the S(j) buffer (this thread has its scores in registers;
+      // S(j+4) is issued behind PV(j) on the in-order pipe)
 #pragma unroll
-      for (int c0 = 0; c0 < kHalf / 2; c0 += 16) {
+      for (int c0 = 0; c0 < kSN / 2; c0 += 16) {
         uint32_t r16[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) r16[i] = pack_bf16(sc[2 * (c0 + i)], sc[2 * (c0 + i) + 1]);
-        ptx::tmem_st16(tmem + lane_base + kTmemS + (uint32_t)sb * kBN + (uint32_t)half * (kHalf / 2) + c0, r16);
+        ptx::tmem_st16(tmem + lane_base + kTmemS + (uint32_t)sb * kSN + c0, r16);
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&bars.p_full);
+      ptx::mbar_arrive(&bars.p_full[sb]);
+    }
+
+    // ---- both warpgroups: wait for the last PV, bring the two partial row sums to the final maximum ----
+    if (n_tiles > 0) {
+      ptx::mbar_wait(&bars.all_done, 0);
+      ptx::tc_fence_after();
+    }
+    l_s[wg][row] = l_run;
+    mref_s[wg][row] = m_mine;
+    named_bar_sync(9, 256);
+    const float m_fin = fmaxf(mref_s[0][row], mref_s[1][row]);     // the maximum never decreases: the later tile holds it
+    float l_tot = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < 2; ++w2) {
+      const float mr = mref_s[w2][row];
+      if (mr != ninf) l_tot += l_s[w2][row] * ex2(mr - m_fin);
     }
 
     if constexpr (kDecode) {
       // ---- partial of this split: (m, l, O, O_lr) un-normalised, merged (+ B epilogue) by fla_decode_merge ----
       constexpr int PS = 4 + D + RP;
       float* prow = p.part + ((int64_t)blockIdx.x * kBM + row) * PS;
-      if (n_tiles > 0) {
-        ptx::mbar_wait(&bars.pv_done, (uint32_t)((n_tiles - 1) & 1));
-        ptx::tc_fence_after();
-      }
-      l_s[half][row] = l_run;
-      named_bar_sync(pair_bar, 64);
-      if (half == 0) { prow[0] = n_tiles > 0 ? m_used : ninf; prow[1] = l_s[0][row] + l_s[1][row]; }
+      if (wg == 0) { prow[0] = m_fin; prow[1] = l_tot; }
       if (n_tiles > 0) {
 #pragma unroll
         for (int cc = 0; cc < D / 2; cc += 16) {
-          const int c0 = half * (D / 2) + cc;
+          const int c0 = wg * (D / 2) + cc;
           uint32_t r16[16];
           ptx::tmem_ld16(tmem + lane_base + kTmemO + c0, r16);
           ptx::tmem_wait_ld();
@@ -407,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
             *reinterpret_cast<float4*>(prow + 4 + c0 + i) = make_float4(__uint_as_float(r16[i]), __uint_as_float(r16[i + 1]),
                                                                         __uint_as_float(r16[i + 2]), __uint_as_float(r16[i + 3]));
         }
-        if (half == 0) {
+        if (wg == 0) {
 #pragma unroll
           for (int c0 = 0; c0 < RP; c0 += 16) {
             uint32_t r16[16];
@@ -421,46 +477,43 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         }
       }
     } else {
-    // ---- epilogue: o += (lr_scale * o_lr[p]) * B[p,:], out = o / l ----
-    ptx::mbar_wait(&bars.pv_done, (uint32_t)((n_tiles - 1) & 1));
-    ptx::tc_fence_after();
-    float* b_s = reinterpret_cast<float*>(sK);            // K stages are idle now: stage B[r][D] of this kv head
-    for (int idx = tid; idx < p.r * D; idx += 256)
-      b_s[idx] = p.b[(int64_t)(idx / D) * ((int64_t)p.n_kv_local * D) + (int64_t)kvh * D + idx % D];
-    l_s[half][row] = l_run;
-    named_bar_sync(9, 256);
-    const float inv_l = 1.0f / (l_s[0][row] + l_s[1][row]);
-    float w[RP > 0 ? RP : 1];
+      // ---- epilogue: o += (lr_scale * o_lr[p]) * B[p,:], out = o / l ----
+      float* b_s = reinterpret_cast<float*>(sK);            // K stages are idle now: stage B[r][D] of this kv head
+      for (int idx = tid; idx < p.r * D; idx += 256)
+        b_s[idx] = p.b[(int64_t)(idx / D) * ((int64_t)p.n_kv_local * D) + (int64_t)kvh * D + idx % D];
+      named_bar_sync(9, 256);
+      const float inv_l = 1.0f / l_tot;
+      float w[RP > 0 ? RP : 1];
 #pragma unroll
-    for (int c0 = 0; c0 < RP; c0 += 16) {
-      uint32_t r16[16];
-      ptx::tmem_ld16(tmem + lane_base + kTmemLr + c0, r16);
-      ptx::tmem_wait_ld();
+      for (int c0 = 0; c0 < RP; c0 += 16) {
+        uint32_t r16[16];
+        ptx::tmem_ld16(tmem + lane_base + kTmemLr + c0, r16);
+        ptx::tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) w[c0 + i] = p.lr_scale * __uint_as_float(r16[i]);
-    }
+        for (int i = 0; i < 16; ++i) w[c0 + i] = p.lr_scale * __uint_as_float(r16[i]);
+      }
 #pragma unroll
-    for (int cc = 0; cc < D / 2; cc += 16) {
-      const int c0 = half * (D / 2) + cc;
-      uint32_t r16[16];
-      ptx::tmem_ld16(tmem + lane_base + kTmemO + c0, r16);
-      ptx::tmem_wait_ld();
-      float acc[16];
+      for (int cc = 0; cc < D / 2; cc += 16) {
+        const int c0 = wg * (D / 2) + cc;
+        uint32_t r16[16];
+        ptx::tmem_ld16(tmem + lane_base + kTmemO + c0, r16);
+        ptx::tmem_wait_ld();
+        float acc[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] = __uint_as_float(r16[i]);
+        for (int i = 0; i < 16; ++i) acc[i] = __uint_as_float(r16[i]);
 #pragma unroll
-      for (int k = 0; k < RP; ++k) {
-        if (k < p.r) {
+        for (int k = 0; k < RP; ++k) {
+          if (k < p.r) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[i] = fmaf(w[k], b_s[k * D + c0 + i], acc[i]);
+            for (int i = 0; i < 16; ++i) acc[i] = fmaf(w[k], b_s[k * D + c0 + i], acc[i]);
+          }
+        }
+        if (real_row) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + c0 + i) = make_float4(acc[i] * inv_l, acc[i + 1] * inv_l, acc[i + 2] * inv_l, acc[i + 3] * inv_l);
         }
       }
-      if (real_row) {
-#pragma unroll
-        for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<float4*>(dst + c0 + i) = make_float4(acc[i] * inv_l, acc[i + 1] * inv_l, acc[i + 2] * inv_l, acc[i + 3] * inv_l);
-      }
-    }
     }
   }
 

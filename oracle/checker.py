@@ -91,6 +91,7 @@ class Checker:
             f(f"max_rel_error_{suf}", C.c_double, P, P, C.c_int64)
             f(f"max_abs_diff_{suf}", C.c_double, P, P, C.c_int64)
             f(f"expand_lr_{suf}", C.c_int, S, S, C.c_int64, C.c_double, P)
+            f(f"apply_rope_{suf}", C.c_int, P, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64)
         f("gqa_attention_f32_mt", C.c_int, SpanF32, SpanF32, SpanF32, SpanF32, SpanF32, C.c_float,
           C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_float), C.c_int)
         f("plan_core", C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
@@ -240,6 +241,15 @@ class Checker:
         out = np.zeros((y_lr.shape[0], b.shape[1]), dtype=y_lr.dtype)
         self._check(getattr(self, f"_expand_lr_{suf}")(*sp, rank, alpha,
                                                       out.ctypes.data_as(C.POINTER(T))))
+        return out
+
+    def apply_rope(self, m, n_heads, d_head, pos_begin):
+        """detail::apply_rope (engine.hpp:225-243): returns the rotated copy; row i is position pos_begin + i."""
+        out = np.array(m, copy=True, order="C")
+        suf, _, T = self._dt(out)
+        assert out.ndim == 2 and out.shape[1] == n_heads * d_head
+        self._check(getattr(self, f"_apply_rope_{suf}")(out.ctypes.data_as(C.POINTER(T)), out.shape[0], out.shape[1],
+                                                       n_heads, d_head, pos_begin))
         return out
 
     def max_rel_error(self, a, b):

@@ -407,3 +407,31 @@ float orc_round_bf16(float x) {
 void orc_round_bf16_array(const float* in, float* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = orc_round_bf16(in[i]);
 }
+
+/* ---- engine.hpp:225-243  apply_rope: half-dim rotation per head; row i carries position pos_begin + i.
+ * freq = 10000^(-2c/d_head) in double, cos / sin in double, cast to T, then x0*c - x1*s and x0*s + x1*c in T
+ * (no FMA: the reference build pins -ffp-contract=off). ------------------------------------------------ */
+#define ORC_ROPE(SUF, T)                                                                                   \
+  int orc_apply_rope_##SUF(T* m, int64_t rows, int64_t stride, int64_t n_heads, int64_t d_head,            \
+                           int64_t pos_begin) {                                                            \
+    if (!m || rows < 0 || n_heads < 0 || d_head < 0 || stride < n_heads * d_head)                          \
+      return orc_fail("apply_rope: bad arguments");                                                        \
+    const int64_t half = d_head / 2;                                                                       \
+    for (int64_t i = 0; i < rows; ++i) {                                                                   \
+      const double pos = (double)(pos_begin + i);                                                          \
+      for (int64_t h = 0; h < n_heads; ++h) {                                                              \
+        T* base = m + i * stride + h * d_head;                                                             \
+        for (int64_t c = 0; c < half; ++c) {                                                               \
+          const double freq = pow(10000.0, -2.0 * (double)c / (double)d_head);                             \
+          const T cos_t = (T)cos(pos * freq);                                                              \
+          const T sin_t = (T)sin(pos * freq);                                                              \
+          const T x0 = base[c], x1 = base[c + half];                                                       \
+          base[c] = x0 * cos_t - x1 * sin_t;                                                               \
+          base[c + half] = x0 * sin_t + x1 * cos_t;                                                        \
+        }                                                                                                  \
+      }                                                                                                    \
+    }                                                                                                      \
+    return ORC_OK;                                                                                         \
+  }
+ORC_ROPE(f32, float)
+ORC_ROPE(f64, double)

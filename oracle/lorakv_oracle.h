@@ -151,6 +151,10 @@ void orc_page_of(int64_t row, int64_t page_tokens, int64_t* logical_page, int64_
 float orc_round_bf16(float x);
 void  orc_round_bf16_array(const float* in, float* out, int64_t n);
 
+/* engine.hpp:225-243 (detail::apply_rope), in place on a row-major matrix with the given row stride */
+int orc_apply_rope_f32(float* m, int64_t rows, int64_t stride, int64_t n_heads, int64_t d_head, int64_t pos_begin);
+int orc_apply_rope_f64(double* m, int64_t rows, int64_t stride, int64_t n_heads, int64_t d_head, int64_t pos_begin);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "lorakv/attention.hpp"
+#include "lorakv/engine.hpp"
 #include "lorakv/fuzz.hpp"
 #include "lorakv/kvcache.hpp"
 #include "lorakv/lora.hpp"
@@ -287,5 +288,22 @@ void ref_store_bytes(const ref_store* s, uint64_t out[4]) {
 uint64_t ref_store_allocated_elements(const ref_store* s) {
   return ON_STORE(s->f->allocated_elements(), s->d->allocated_elements());
 }
+
+
+// detail::apply_rope (engine.hpp:225-243) on a strided row-major matrix, in place
+#define REF_ROPE(SUF, T)                                                                                  \
+  int ref_apply_rope_##SUF(T* m, int64_t rows, int64_t stride, int64_t n_heads, int64_t d_head,           \
+                           int64_t pos_begin) {                                                           \
+    return guarded([&] {                                                                                  \
+      Matrix<T> tmp(rows, n_heads * d_head);                                                              \
+      for (int64_t i = 0; i < rows; ++i)                                                                  \
+        for (int64_t j = 0; j < n_heads * d_head; ++j) tmp(i, j) = m[i * stride + j];                     \
+      detail::apply_rope(tmp, n_heads, d_head, pos_begin);                                                \
+      for (int64_t i = 0; i < rows; ++i)                                                                  \
+        for (int64_t j = 0; j < n_heads * d_head; ++j) m[i * stride + j] = tmp(i, j);                     \
+    });                                                                                                   \
+  }
+REF_ROPE(f32, float)
+REF_ROPE(f64, double)
 
 }  // extern "C"

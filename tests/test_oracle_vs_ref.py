@@ -70,3 +70,14 @@ def test_oracle_store_equals_reference(orc, ref):
                     assert np.array_equal(so.value_view(layer, a), sr.value_view(layer, a))
                     assert np.array_equal(so.lr_view(layer, a), sr.lr_view(layer, a))
                     assert so.seen(a) == sr.seen(a)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_oracle_rope_equals_reference(orc, ref, dtype):
+    """detail::apply_rope (engine.hpp:225-243): the restatement is bit-identical to the reference's own code,
+    including positions far into a 128K trajectory."""
+    for n_heads, d_head, rows, pos in [(2, 64, 5, 0), (8, 128, 3, 131000), (1, 8, 7, 12345), (3, 6, 4, 1)]:
+        m = orc.gaussian(rows, n_heads * d_head, 77 + rows, 1.0, dtype)
+        a, b = orc.apply_rope(m, n_heads, d_head, pos), ref.apply_rope(m, n_heads, d_head, pos)
+        assert np.array_equal(a, b)
+        assert not np.array_equal(a, m) or pos == 0 and rows == 1

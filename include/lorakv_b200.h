@@ -184,6 +184,25 @@ int lorakv_pool_append(lorakv_pool* pool, int which, int64_t layer, int64_t agen
 int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* adapters, int64_t layer,
                                   int64_t agent, int64_t row_begin, const float* x, int64_t n_rows,
                                   int64_t ld, int mem_kind, int64_t* appended);
+/* ---- the projection that feeds the cache ------------------------------------
+ * Replaces, for the rows of the plan's kv range (proj/include/lorakv/engine.hpp:376-403):
+ *     k_rows = x_norm * Wk;  if (rope) apply_rope(k_rows, n_kv_heads, d_head, row_begin);   (:380-383, :225-243)
+ *     v_rows = x_norm * Wv;                                                                  (:384)
+ *     store.append_key(layer, agent, row_begin, k_rows); store.append_value(..., v_rows);    (:402-403)
+ * lorakv_proj holds Wk, Wv (d_model x n_kv_heads*d_head, row-major float32, HOST) per layer; the shard
+ * arguments and dtype must equal the pool's.  bf16 pools with d_head 128 run ONE tcgen05 kernel that
+ * projects, rotates and writes bf16 pages; other pools use the reference's summation order in fp32. */
+typedef struct lorakv_proj lorakv_proj;
+int lorakv_proj_create(lorakv_ctx* ctx, int64_t n_layers, int64_t d_model, int64_t n_kv_heads,
+                       int64_t d_head, int64_t kv_head_begin, int64_t n_kv_local, int dtype,
+                       lorakv_proj** out);
+void lorakv_proj_destroy(lorakv_proj* proj);
+int lorakv_proj_set_kv(lorakv_proj* proj, int64_t layer, const float* wk, const float* wv);
+/* x: n_rows x d_model float32 (x_norm rows of logical rows [row_begin, row_begin+n_rows)), HOST or
+ * DEVICE.  First-writer-wins as in lorakv_pool_append; *appended = rows newly written. */
+int lorakv_pool_append_kv_project(lorakv_pool* pool, const lorakv_proj* proj, int64_t layer,
+                                  int64_t agent, int64_t row_begin, const float* x, int64_t n_rows,
+                                  int64_t ld, int mem_kind, int rope, int64_t* appended);
 /* rows currently materialised in the buffer (layer, agent) resolves to (GrowMat::rows) */
 int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows);
 /* key_view / value_view / lr_view, :307-324: de-paginate rows [row_begin, row_begin+n_rows) into a

@@ -102,6 +102,10 @@ SIGNATURES = {
     "lorakv_pool_plan_step": (C.c_int, [_vp, _i64, _i64, C.POINTER(_i64)]),
     "lorakv_pool_append": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.POINTER(_i64)]),
     "lorakv_pool_append_lr_project": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.POINTER(_i64)]),
+    "lorakv_proj_create": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
+    "lorakv_proj_destroy": (None, [_vp]),
+    "lorakv_proj_set_kv": (C.c_int, [_vp, _i64, _pf, _pf]),
+    "lorakv_pool_append_kv_project": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.c_int, C.POINTER(_i64)]),
     "lorakv_pool_rows": (C.c_int, [_vp, C.c_int, _i64, _i64, C.POINTER(_i64)]),
     "lorakv_pool_read": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _i64, _pf]),
     "lorakv_pool_bytes": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
@@ -403,6 +407,33 @@ class Adapters:
         _check(self.ctx.lib.lorakv_adapters_set_b(self.h, layer, agent, b.ctypes.data_as(_pf), alpha))
 
 
+class Projection:
+    """lorakv_proj: Wk / Wv per layer for the fused projection + RoPE + append (engine.hpp:376-403)."""
+
+    def __init__(self, ctx: Context, n_layers, d_model, n_kv_heads, d_head, kv_head_begin=0, n_kv_local=0, dtype=F32):
+        self.ctx = ctx
+        h = _vp()
+        _check(ctx.lib.lorakv_proj_create(ctx.h, n_layers, d_model, n_kv_heads, d_head, kv_head_begin, n_kv_local,
+                                          dtype, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.lorakv_proj_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_kv(self, layer, wk, wv):
+        wk = np.ascontiguousarray(wk, dtype=np.float32)
+        wv = np.ascontiguousarray(wv, dtype=np.float32)
+        _check(self.ctx.lib.lorakv_proj_set_kv(self.h, layer, wk.ctypes.data_as(_pf), wv.ctypes.data_as(_pf)))
+
+
 class Pool:
     """lorakv_pool: the paged HBM cache of one trajectory with KvStore's interface (kvcache.hpp:213)."""
 
@@ -488,6 +519,20 @@ class Pool:
         else:
             _check(self.ctx.lib.lorakv_pool_append_lr_project(self.h, adapters.h, layer, agent, row_begin,
                                                               _vp(dev_ptr), n_rows, ld, DEVICE, C.byref(added)))
+        return added.value
+
+    def append_kv_project(self, proj: "Projection", layer, agent, row_begin, x=None, rope=True, dev_ptr=None,
+                          n_rows=None, ld=None):
+        added = _i64()
+        if dev_ptr is None:
+            x = np.asarray(x, dtype=np.float32)
+            ptr, ld_ = _span(x, _f)
+            _check(self.ctx.lib.lorakv_pool_append_kv_project(self.h, proj.h, layer, agent, row_begin,
+                                                              C.cast(ptr, _vp), x.shape[0], ld_, HOST, int(rope),
+                                                              C.byref(added)))
+        else:
+            _check(self.ctx.lib.lorakv_pool_append_kv_project(self.h, proj.h, layer, agent, row_begin, _vp(dev_ptr),
+                                                              n_rows, ld, DEVICE, int(rope), C.byref(added)))
         return added.value
 
     def rows(self, which, layer, agent):

@@ -542,6 +542,111 @@ int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, 
   return LORAKV_OK;
 }
 
+// ---- K / V_base projection + RoPE + append (engine.hpp:376-403) --------------------------------------
+int lorakv_proj_create(lorakv_ctx* ctx, int64_t n_layers, int64_t d_model, int64_t n_kv_heads, int64_t d_head,
+                       int64_t kv_head_begin, int64_t n_kv_local, int dtype, lorakv_proj** out) {
+  if (!ctx || !out) return fail("proj_create: null argument");
+  *out = nullptr;
+  if (n_layers < 1 || d_model < 1 || n_kv_heads < 1 || d_head < 1) return fail("proj_create: invalid shape");
+  if (d_head % 2 != 0) return fail("proj_create: d_head %lld must be even (half-dim rotation)", (long long)d_head);
+  if (n_kv_local <= 0) { kv_head_begin = 0; n_kv_local = n_kv_heads; }
+  if (kv_head_begin < 0 || kv_head_begin + n_kv_local > n_kv_heads) return fail("proj_create: kv head shard out of range");
+  if (dtype != LORAKV_F32 && dtype != LORAKV_BF16) return fail("proj_create: bad dtype %d", dtype);
+  LK_CUDA(cudaSetDevice(ctx->device));
+  lorakv_proj* pr = new (std::nothrow) lorakv_proj();
+  if (!pr) return fail("proj_create: out of host memory");
+  pr->ctx = ctx; pr->n_layers = n_layers; pr->d_model = d_model; pr->n_kv_heads = n_kv_heads; pr->d_head = d_head;
+  pr->kv_head_begin = kv_head_begin; pr->n_kv_local = n_kv_local; pr->dtype = dtype;
+  pr->fused = kv_project_fused_shape(dtype, d_head, d_model);
+  pr->set.assign((size_t)n_layers, 0);
+  cudaError_t e;
+  if (pr->fused) {
+    e = cudaMalloc(&pr->packed, (size_t)(n_layers * kv_project_packed_elems(d_model, n_kv_local, d_head)) * 2);
+  } else {
+    const size_t bytes = (size_t)(n_layers * d_model * n_kv_heads * d_head) * sizeof(float);
+    e = cudaMalloc(&pr->wk, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&pr->wv, bytes);
+  }
+  if (e != cudaSuccess) { lorakv_proj_destroy(pr); return fail("proj_create: %s", cudaGetErrorString(e)); }
+  *out = pr;
+  return LORAKV_OK;
+}
+
+void lorakv_proj_destroy(lorakv_proj* pr) {
+  if (!pr) return;
+  cudaSetDevice(pr->ctx->device);
+  cudaStreamSynchronize(pr->ctx->stream);
+  if (pr->packed) cudaFree(pr->packed);
+  if (pr->wk) cudaFree(pr->wk);
+  if (pr->wv) cudaFree(pr->wv);
+  delete pr;
+}
+
+int lorakv_proj_set_kv(lorakv_proj* pr, int64_t layer, const float* wk, const float* wv) {
+  if (!pr || !wk || !wv) return fail("null argument");
+  if (layer < 0 || layer >= pr->n_layers) return fail("layer %lld out of range", (long long)layer);
+  lorakv_ctx* ctx = pr->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  const int64_t dkv_full = pr->n_kv_heads * pr->d_head, dkv = pr->n_kv_local * pr->d_head;
+  const size_t one = (size_t)(pr->d_model * dkv_full) * sizeof(float);
+  if (pr->fused) {
+    LK_TRY(scratch_reserve(ctx, ctx->in, 2 * one));
+    float* sk = static_cast<float*>(ctx->in.ptr);
+    float* sv = reinterpret_cast<float*>(static_cast<char*>(ctx->in.ptr) + one);
+    LK_CUDA(cudaMemcpyAsync(sk, wk, one, cudaMemcpyHostToDevice, ctx->stream));
+    LK_CUDA(cudaMemcpyAsync(sv, wv, one, cudaMemcpyHostToDevice, ctx->stream));
+    char* dst = static_cast<char*>(pr->packed) + (size_t)(layer * kv_project_packed_elems(pr->d_model, pr->n_kv_local, pr->d_head)) * 2;
+    LK_TRY(launch_pack_w(ctx, sk, dkv_full, pr->kv_head_begin * pr->d_head, dkv, pr->d_model, 0, dst));
+    LK_TRY(launch_pack_w(ctx, sv, dkv_full, pr->kv_head_begin * pr->d_head, dkv, pr->d_model, dkv / 64, dst));
+  } else {
+    LK_CUDA(cudaMemcpyAsync(pr->wk + (size_t)layer * (one / sizeof(float)), wk, one, cudaMemcpyHostToDevice, ctx->stream));
+    LK_CUDA(cudaMemcpyAsync(pr->wv + (size_t)layer * (one / sizeof(float)), wv, one, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  pr->set[(size_t)layer] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_pool_append_kv_project(lorakv_pool* pool, const lorakv_proj* pr, int64_t layer, int64_t agent, int64_t row_begin,
+                                  const float* x, int64_t n_rows, int64_t ld, int mem_kind, int rope, int64_t* appended) {
+  if (!pool || !pr) return fail("null argument");
+  if (appended) *appended = 0;
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, LORAKV_KEY, layer, agent, &set, &none));
+  if (pr->d_model != pool->dims.d_model || pr->n_kv_heads != pool->dims.n_kv_heads || pr->d_head != pool->dims.d_head ||
+      pr->kv_head_begin != pool->dims.kv_head_begin || pr->n_kv_local != pool->n_kv_local || pr->dtype != pool->dims.dtype ||
+      layer >= pr->n_layers)
+    return fail("append_kv_project: projection weights do not match the pool (d_model %lld vs %lld, d_kv %lld vs %lld)",
+                (long long)pr->d_model, (long long)pool->dims.d_model, (long long)(pr->n_kv_heads * pr->d_head),
+                (long long)(pool->dims.n_kv_heads * pool->dims.d_head));
+  if (!pr->set[(size_t)layer]) return fail("append_kv_project: Wk / Wv of layer %lld were never uploaded", (long long)layer);
+  if (n_rows < 0) return fail("append: negative row count");
+  int64_t& have_k = pool->key_rows[(size_t)set][(size_t)layer];
+  int64_t& have_v = pool->value_rows[(size_t)set][(size_t)layer];
+  int64_t skip_k, add_k, skip_v, add_v;
+  LK_TRY(fww("key", have_k, row_begin, n_rows, &skip_k, &add_k));
+  LK_TRY(fww("value", have_v, row_begin, n_rows, &skip_v, &add_v));
+  const int64_t add = std::max(add_k, add_v);
+  if (add == 0) return LORAKV_OK;
+  if (!x) return fail("append: null rows");
+  const int64_t skip = n_rows - add;
+  lorakv_ctx* ctx = pool->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  LK_TRY(ensure_pages(pool, pool->kv_space, set, row_begin + n_rows));
+  const float* dev; int64_t dev_ld;
+  LK_TRY(stage_rows(ctx, x + skip * ld, add, pool->dims.d_model, ld, mem_kind, &dev, &dev_ld));
+  const size_t w_off = (size_t)(layer * pr->d_model * pr->n_kv_heads * pr->d_head);
+  const void* packed = pr->fused ? static_cast<const char*>(pr->packed) +
+                                       (size_t)(layer * kv_project_packed_elems(pr->d_model, pr->n_kv_local, pr->d_head)) * 2
+                                 : nullptr;
+  LK_TRY(launch_kv_project(pool, packed, pr->fused ? nullptr : pr->wk + w_off, pr->fused ? nullptr : pr->wv + w_off, layer, set,
+                           row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld, rope != 0));
+  if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  have_k += add_k; have_v += add_v;
+  if (appended) *appended = add;
+  return LORAKV_OK;
+}
+
 int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows) {
   if (!pool || !rows) return fail("null argument");
   int64_t set; bool none;

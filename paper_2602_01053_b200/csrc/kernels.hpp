@@ -71,6 +71,13 @@ int launch_prefill_umma(const PagedAttnCall& call);
 bool decode_umma_supported(const PagedAttnCall& call);     // decode with 33..128 query rows per kv head
 int launch_decode_umma(const PagedAttnCall& call);
 
+// kv_project_umma.cu (K / V_base projection + RoPE + append in one pass; tcgen05 for bf16 pools) -----------
+bool kv_project_fused_shape(int dtype, int64_t d_head, int64_t d_model);
+int64_t kv_project_packed_elems(int64_t d_model, int64_t n_kv_local, int64_t d_head);
+int launch_pack_w(lorakv_ctx* ctx, const float* w_dev, int64_t ldw, int64_t col0, int64_t n_cols, int64_t d_model, int64_t nb0, void* packed);
+int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
+                      int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope);
+
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
                   int a_in_tmem, float* d);

@@ -1,0 +1,361 @@
+// kv_project_umma.cu -- the step that feeds the cache: K / V_base projection of new context rows, RoPE on the
+// keys and the append into the paged cache, in one pass.
+//
+// Reference (proj/include/lorakv/engine.hpp:376-403): for the rows of the plan's kv range
+//     k_rows = x_norm * Wk ; apply_rope(k_rows, n_kv_heads, d_head, kv_range.begin)   (:380-383, :225-243)
+//     v_rows = x_norm * Wv                                                             (:384)
+//     store.append_key / append_value(layer, agent, kv_range.begin, ...)               (:402-403)
+// i.e. two triple-loop matmuls (matrix.hpp:101-111), a rotation pass and two row-by-row copies.
+//
+// Here, for bf16 pools with d_head 128:
+//   pack_x        X (fp32, caller's layout) -> bf16 A-operand tiles [row tile 128][k block 64][128][64], SWIZZLE_128B,
+//                 so that one plain cp.async.bulk of 16 KB lands as a canonical K-major tcgen05 operand
+//   pack_w        (once per upload) [Wk | Wv] of the pool's kv heads -> bf16 [n block 64][d_model][64], SWIZZLE_128B:
+//                 a 64-row slice of a block is a canonical MN-major B operand (the layout V pages use)
+//   rope_table    cos / sin of pos * 10000^(-2c/d) in double, stored as float2 (the reference casts the double
+//                 cos / sin to T, engine.hpp:235-236)
+//   kv_project    one CTA per 128 rows x 256 output columns (two heads): warp 0 streams operand stages with the TMA
+//                 engine, warp 1 issues tcgen05.mma (M 128, N 256, accumulators in TMEM), warps 2-5 read the
+//                 accumulators, rotate key heads (pairs c, c + 64 sit in the same thread), round to bf16 and store
+//                 16-byte chunks straight into the swizzled pages of the right head -- no K / V round trip through HBM.
+// fp32 pools (tolerance 1e-4 rules out bf16 operands) and other head sizes take proj_matmul (the reference's
+// summation order, bit for bit) + rope + the scatter kernel of cache_kernels.cu.
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include "kernels.hpp"
+#include "page_layout.cuh"
+#include "state.hpp"
+#include "umma.cuh"
+
+namespace lk {
+
+namespace {
+
+constexpr int kBM = 128, kBN = 256, kBK = 64;
+constexpr int kStages = 4;
+constexpr uint32_t kABytes = kBM * kBK * 2;            // 16 KB
+constexpr uint32_t kBBlk = kBK * 128;                  // one 64-column n block of a k block: 8 KB
+constexpr uint32_t kBBytes = (kBN / 64) * kBBlk;       // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// X[n_rows][d_model] fp32 (row stride ld) -> packed bf16 A tiles; one thread per 16-byte chunk (8 columns)
+__global__ void pack_x_kernel(const float* __restrict__ x, int64_t n_rows, int64_t ld, int d_model, __nv_bfloat16* __restrict__ out) {
+  const int kb_n = d_model / kBK;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = ((n_rows + kBM - 1) / kBM) * kBM * (int64_t)(d_model / 8);
+  if (idx >= total) return;
+  const int chunk = (int)(idx % (d_model / 8));
+  const int64_t row = idx / (d_model / 8);
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (row < n_rows) {
+    const float* src = x + row * ld + (int64_t)chunk * 8;
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(src)), b = __ldcs(reinterpret_cast<const float4*>(src + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[u];
+    }
+  }
+  const int64_t tile = row / kBM;
+  const int r = (int)(row % kBM), kb = chunk / 8, c = (chunk % 8) * 8;
+  unsigned char* dst = reinterpret_cast<unsigned char*>(out) + ((tile * kb_n + kb) * (int64_t)kABytes) + ptx::sw128_offset((uint32_t)r, (uint32_t)c);
+  uint4 pk;
+  pk.x = pack_bf16(v[0], v[1]); pk.y = pack_bf16(v[2], v[3]); pk.z = pack_bf16(v[4], v[5]); pk.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(dst) = pk;
+}
+
+// W[d_model][n_src] fp32 row-major (device), columns [col0, col0 + n_cols) -> packed bf16 n blocks starting at block nb0
+__global__ void pack_w_kernel(const float* __restrict__ w, int64_t ldw, int64_t col0, int n_cols, int d_model, int nb0,
+                              __nv_bfloat16* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;       // (k row, 8-column chunk)
+  const int chunks = n_cols / 8;
+  if (idx >= (int64_t)d_model * chunks) return;
+  const int k = (int)(idx / chunks), ch = (int)(idx % chunks);
+  const float* src = w + (int64_t)k * ldw + col0 + (int64_t)ch * 8;
+  float v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = src[u];
+  const int nb = nb0 + ch / 8, c = (ch % 8) * 8;
+  unsigned char* dst = reinterpret_cast<unsigned char*>(out) + (int64_t)nb * d_model * 128 + ptx::sw128_offset((uint32_t)k, (uint32_t)c);
+  uint4 pk;
+  pk.x = pack_bf16(v[0], v[1]); pk.y = pack_bf16(v[2], v[3]); pk.z = pack_bf16(v[4], v[5]); pk.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(dst) = pk;
+}
+
+// cos / sin table of engine.hpp:233-236 for positions [pos0, pos0 + n): tab[(i * half + c)] = (cos, sin)
+__global__ void rope_table_kernel(int64_t pos0, int64_t n, int d_head, float2* __restrict__ tab) {
+  const int half = d_head / 2;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * half) return;
+  const int c = (int)(idx % half);
+  const double pos = (double)(pos0 + idx / half);
+  const double freq = pow(10000.0, -2.0 * (double)c / (double)d_head);
+  double s, co;
+  sincos(pos * freq, &s, &co);
+  tab[idx] = make_float2((float)co, (float)s);
+}
+
+struct ProjParams {
+  const __nv_bfloat16* xa;     // packed X tiles
+  const __nv_bfloat16* wb;     // packed [Wk | Wv] of this layer
+  const float2* rope;          // [n_rows][64] or null
+  __nv_bfloat16 *k_pages, *v_pages;   // page arrays of this layer
+  const int32_t* table;        // logical -> physical page of the kv set
+  int64_t head_stride, page_stride;
+  int P, d_model, n_kv_local;
+  int64_t row0, n_rows;        // first logical row of the call's rows; rows computed
+  int64_t k_from, v_from;      // logical rows below these already exist in the K / V cache (first writer wins)
+};
+
+struct ProjBarriers {
+  uint64_t full[kStages], empty[kStages], acc_full;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const ProjParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ ProjBarriers bars;
+  __shared__ uint32_t tmem_base_s;
+  unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.x, nblk = blockIdx.y;            // 128-row tile, 256-column block (two heads)
+  const int kb_n = p.d_model / kBK;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&bars.full[s], 1); ptx::mbar_init(&bars.empty[s], 1); }
+    ptx::mbar_init(&bars.acc_full, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(&tmem_base_s, kBN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (ptx::elect_one()) {
+      const unsigned char* a_src = reinterpret_cast<const unsigned char*>(p.xa) + (int64_t)tile * kb_n * kABytes;
+      const unsigned char* b_src = reinterpret_cast<const unsigned char*>(p.wb) + (int64_t)nblk * (kBN / 64) * p.d_model * 128;
+      for (int kb = 0; kb < kb_n; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) ptx::mbar_wait(&bars.empty[s], (uint32_t)(((kb / kStages) & 1) ^ 1));
+        ptx::mbar_arrive_expect_tx(&bars.full[s], kStageBytes);
+        const uint32_t dst = ptx::smem_u32(smem + s * kStageBytes);
+        bulk_g2s(dst, a_src + (int64_t)kb * kABytes, kABytes, &bars.full[s]);
+#pragma unroll
+        for (int nb = 0; nb < kBN / 64; ++nb)
+          bulk_g2s(dst + kABytes + nb * kBBlk, b_src + (int64_t)nb * p.d_model * 128 + (int64_t)kb * kBBlk, kBBlk, &bars.full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (ptx::elect_one()) {
+      const uint32_t idesc = ptx::instr_desc_bf16(kBM, kBN, ptx::kMajorK, ptx::kMajorMN);
+      const uint64_t ad = ptx::smem_desc(ptx::smem_u32(smem), 16u, 1024u, ptx::kSw128);
+      const uint64_t bd = ptx::smem_desc(ptx::smem_u32(smem) + kABytes, kBBlk, 1024u, ptx::kSw128);
+      const uint32_t ad_hi = (uint32_t)(ad >> 32), bd_hi = (uint32_t)(bd >> 32);
+      for (int kb = 0; kb < kb_n; ++kb) {
+        const int s = kb % kStages;
+        ptx::mbar_wait(&bars.full[s], (uint32_t)((kb / kStages) & 1));
+        ptx::tc_fence_after();
+        const uint32_t a_lo = (uint32_t)ad + (uint32_t)s * (kStageBytes >> 4), b_lo = (uint32_t)bd + (uint32_t)s * (kStageBytes >> 4);
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks)
+          ptx::umma_bf16_ss(tmem, ((uint64_t)ad_hi << 32) | (a_lo + (uint32_t)ks * 2u), ((uint64_t)bd_hi << 32) | (b_lo + (uint32_t)ks * (2048u >> 4)),
+                            idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+        ptx::umma_commit(&bars.empty[s]);
+      }
+      ptx::umma_commit(&bars.acc_full);
+    }
+  } else {
+    // ===================== epilogue: TMEM -> (RoPE) -> bf16 -> swizzled pages =====================
+    const int q4 = warp & 3;                                    // TMEM lane quarter this warp may read
+    const int r = q4 * 32 + lane;
+    const int64_t i_row = (int64_t)tile * kBM + r;              // row of the call
+    const int64_t row = p.row0 + i_row;                         // logical row of the trajectory = position
+    const bool live = i_row < p.n_rows;
+    ptx::mbar_wait(&bars.acc_full, 0);
+    ptx::tc_fence_after();
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const int64_t phys = live ? p.table[row / p.P] : 0;
+    const int t = (int)(row % p.P);
+#pragma unroll 1
+    for (int hb = 0; hb < kBN / 128; ++hb) {
+      const int gb = nblk * (kBN / 128) + hb;                   // head block among [K heads | V heads]
+      const bool is_k = gb < p.n_kv_local;
+      const int head = is_k ? gb : gb - p.n_kv_local;
+      const bool write = live && row >= (is_k ? p.k_from : p.v_from);
+      __nv_bfloat16* page = (is_k ? p.k_pages : p.v_pages) + (int64_t)head * p.head_stride + phys * p.page_stride;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t lo_u[32], hi_u[32];
+        ptx::tmem_ld32(tmem + lane_base + (uint32_t)(hb * 128 + c0), lo_u);
+        ptx::tmem_ld32(tmem + lane_base + (uint32_t)(hb * 128 + 64 + c0), hi_u);
+        ptx::tmem_wait_ld();
+        float lo[32], hi[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) { lo[i] = __uint_as_float(lo_u[i]); hi[i] = __uint_as_float(hi_u[i]); }
+        if (is_k && p.rope != nullptr && live) {
+          const float2* tab = p.rope + i_row * 64 + c0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 cs = __ldg(tab + i);
+            const float x0 = lo[i], x1 = hi[i];
+            lo[i] = x0 * cs.x - x1 * cs.y;                      // engine.hpp:239-240
+            hi[i] = x0 * cs.y + x1 * cs.x;
+          }
+        }
+        if (write) {
+          // page = [2 column blocks][P tokens][64] with the 16-byte chunks of a token's 128-byte row XOR-swizzled by t % 8
+          unsigned char* b0 = reinterpret_cast<unsigned char*>(page) + (int64_t)t * 128;
+          unsigned char* b1 = b0 + (int64_t)p.P * 128;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const int chunk = ((c0 / 8 + ch) ^ (t & 7)) * 16;
+            uint4 a, b;
+            a.x = pack_bf16(lo[8 * ch + 0], lo[8 * ch + 1]); a.y = pack_bf16(lo[8 * ch + 2], lo[8 * ch + 3]);
+            a.z = pack_bf16(lo[8 * ch + 4], lo[8 * ch + 5]); a.w = pack_bf16(lo[8 * ch + 6], lo[8 * ch + 7]);
+            b.x = pack_bf16(hi[8 * ch + 0], hi[8 * ch + 1]); b.y = pack_bf16(hi[8 * ch + 2], hi[8 * ch + 3]);
+            b.z = pack_bf16(hi[8 * ch + 4], hi[8 * ch + 5]); b.w = pack_bf16(hi[8 * ch + 6], hi[8 * ch + 7]);
+            *reinterpret_cast<uint4*>(b0 + chunk) = a;
+            *reinterpret_cast<uint4*>(b1 + chunk) = b;
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc(tmem, kBN);
+}
+
+// ---- exact fp32 path: the reference's matmul order (matrix.hpp:101-111) and rotation ------------------------
+__global__ void proj_matmul_kernel(const float* __restrict__ x, int64_t ld, const float* __restrict__ w, int64_t ldw, int64_t col0,
+                                   int64_t M, int K, int N, float* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * N) return;
+  const int64_t i = idx / N, j = idx % N;
+  float acc = 0.f;
+  for (int k = 0; k < K; ++k) acc = __fadd_rn(acc, __fmul_rn(x[i * ld + k], w[(int64_t)k * ldw + col0 + j]));
+  out[idx] = acc;
+}
+__global__ void rope_rows_kernel(float* __restrict__ m, int64_t n_rows, int n_heads, int d_head, const float2* __restrict__ tab) {
+  const int half = d_head / 2;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_rows * n_heads * half) return;
+  const int c = (int)(idx % half), h = (int)((idx / half) % n_heads);
+  const int64_t i = idx / ((int64_t)half * n_heads);
+  float* base = m + i * ((int64_t)n_heads * d_head) + (int64_t)h * d_head;
+  const float2 cs = tab[i * half + c];
+  const float x0 = base[c], x1 = base[c + half];
+  base[c] = __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+  base[c + half] = __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x));
+}
+
+}  // namespace
+
+bool kv_project_fused_shape(int dtype, int64_t d_head, int64_t d_model) {
+  return dtype == LORAKV_BF16 && d_head == 128 && d_model % kBK == 0 && d_model >= kBK;
+}
+
+int64_t kv_project_packed_elems(int64_t d_model, int64_t n_kv_local, int64_t d_head) { return 2 * n_kv_local * d_head * d_model; }
+
+int launch_pack_w(lorakv_ctx* ctx, const float* w_dev, int64_t ldw, int64_t col0, int64_t n_cols, int64_t d_model, int64_t nb0, void* packed) {
+  const int64_t n = d_model * (n_cols / 8);
+  pack_w_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(w_dev, ldw, col0, (int)n_cols, (int)d_model, (int)nb0,
+                                                                        static_cast<__nv_bfloat16*>(packed));
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+// rows [row0, row0 + n_rows) of the trajectory from x_dev (row i of x_dev is logical row row0 + i); K rows below k_from and V
+// rows below v_from are already cached and are not written
+int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
+                      int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope) {
+  if (n_rows == 0) return LORAKV_OK;
+  lorakv_ctx* ctx = pool->ctx;
+  const int64_t d = pool->dims.d_head, d_model = pool->dims.d_model, n_kv = pool->n_kv_local;
+  const int64_t half = d / 2;
+  auto up = [](size_t x) { return (x + 1023) / 1024 * 1024; };
+  const size_t tab_bytes = rope ? up((size_t)(n_rows * half) * sizeof(float2)) : 0;
+  if (w_packed) {
+    const int64_t tiles = (n_rows + kBM - 1) / kBM;
+    const size_t xa_bytes = (size_t)tiles * kBM * d_model * 2;
+    LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + xa_bytes));
+    float2* tab = rope ? static_cast<float2*>(ctx->work.ptr) : nullptr;
+    __nv_bfloat16* xa = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ctx->work.ptr) + tab_bytes);
+    if (rope) {
+      const int64_t n = n_rows * half;
+      rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(row0, n_rows, (int)d, tab);
+      ctx->launches++;
+    }
+    const int64_t nx = tiles * kBM * (d_model / 8);
+    pack_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, ctx->stream>>>(x_dev, n_rows, ld, (int)d_model, xa);
+    ctx->launches++;
+    ProjParams pp;
+    pp.xa = xa; pp.wb = static_cast<const __nv_bfloat16*>(w_packed); pp.rope = tab;
+    pp.k_pages = static_cast<__nv_bfloat16*>(pool->k_pages) + layer * pool->kv_layer_stride();
+    pp.v_pages = static_cast<__nv_bfloat16*>(pool->v_pages) + layer * pool->kv_layer_stride();
+    pp.table = pool->kv_space.dev_table + set * pool->kv_space.max_pages;
+    pp.head_stride = pool->kv_head_stride(); pp.page_stride = pool->kv_page_stride();
+    pp.P = (int)pool->P; pp.d_model = (int)d_model; pp.n_kv_local = (int)n_kv;
+    pp.row0 = row0; pp.n_rows = n_rows; pp.k_from = k_from; pp.v_from = v_from;
+    const size_t smem = (size_t)kStages * kStageBytes + 1024;
+    LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 grid((unsigned)tiles, (unsigned)(2 * n_kv * d / kBN));
+    prof_mark(ctx, 0);
+    kv_project_umma_kernel<<<grid, kThreads, smem, ctx->stream>>>(pp);
+    prof_mark(ctx, 1);
+    ctx->launches++;
+    LK_CUDA(cudaGetLastError());
+    ctx->last_kernel = "kv_project_umma";
+    return LORAKV_OK;
+  }
+  // exact fp32 path
+  const int64_t dkv = n_kv * d;
+  const size_t mat_bytes = up((size_t)(n_rows * dkv) * sizeof(float));
+  LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + 2 * mat_bytes));
+  char* base = static_cast<char*>(ctx->work.ptr);
+  float2* tab = rope ? reinterpret_cast<float2*>(base) : nullptr;
+  float* kbuf = reinterpret_cast<float*>(base + tab_bytes);
+  float* vbuf = reinterpret_cast<float*>(base + tab_bytes + mat_bytes);
+  const int64_t col0 = pool->dims.kv_head_begin * d, ldw = pool->dims.n_kv_heads * d;
+  const int64_t n = n_rows * dkv;
+  proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, wk_dev, ldw, col0, n_rows, (int)d_model, (int)dkv, kbuf);
+  proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, wv_dev, ldw, col0, n_rows, (int)d_model, (int)dkv, vbuf);
+  ctx->launches += 2;
+  if (rope) {
+    const int64_t nt = n_rows * half, nr = n_rows * n_kv * half;
+    rope_table_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, ctx->stream>>>(row0, n_rows, (int)d, tab);
+    rope_rows_kernel<<<(unsigned)((nr + 255) / 256), 256, 0, ctx->stream>>>(kbuf, n_rows, (int)n_kv, (int)d, tab);
+    ctx->launches += 2;
+  }
+  LK_CUDA(cudaGetLastError());
+  if (k_from < row0 + n_rows) {
+    const int64_t skip = k_from > row0 ? k_from - row0 : 0;
+    LK_TRY(launch_append_scatter(pool, LORAKV_KEY, layer, set, row0 + skip, kbuf + skip * dkv, n_rows - skip, dkv));
+  }
+  if (v_from < row0 + n_rows) {
+    const int64_t skip = v_from > row0 ? v_from - row0 : 0;
+    LK_TRY(launch_append_scatter(pool, LORAKV_VALUE, layer, set, row0 + skip, vbuf + skip * dkv, n_rows - skip, dkv));
+  }
+  ctx->last_kernel = "kv_project_f32";
+  return LORAKV_OK;
+}
+
+}  // namespace lk

@@ -127,3 +127,17 @@ struct lorakv_adapters {
   std::vector<float> scale_host;
   std::vector<uint8_t> a_set, b_set, a_agent_set;
 };
+
+// Projection weights of the step that feeds the cache (engine.hpp:376-403): Wk, Wv per layer, restricted to
+// the kv heads this shard holds.  bf16 pools with d_head 128 keep them packed for the tcgen05 kernel
+// (kv_project_umma.cu), every other case keeps the caller's float32 matrices.
+struct lorakv_proj {
+  lorakv_ctx* ctx = nullptr;
+  int64_t n_layers = 0, d_model = 0, n_kv_heads = 0, d_head = 0, kv_head_begin = 0, n_kv_local = 0;
+  int dtype = LORAKV_F32;
+  bool fused = false;
+  void* packed = nullptr;    // [n_layers][2 * n_kv_local * d_head / 64 blocks][d_model][64] bf16, SWIZZLE_128B
+  float* wk = nullptr;       // [n_layers][d_model][n_kv_heads * d_head] float32 (exact path only)
+  float* wv = nullptr;
+  std::vector<uint8_t> set;
+};

@@ -1,0 +1,134 @@
+"""The projection that feeds the cache: K / V_base projection of new context rows, RoPE on the
+keys and the append into the paged cache in one call, against the reference path restated by the oracle:
+    k = matmul(x, Wk); apply_rope(k, n_kv, d, row_begin); v = matmul(x, Wv); append_key / append_value
+(engine.hpp:376-403, :225-243; matmul matrix.hpp:101-111).  bf16 pools with d_head 128 run the tcgen05 kernel
+(kv_project_umma), fp32 pools the reference's own summation order.  Needs a B200."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2602_01053_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def reference_kv(orc, x, wk, wv, n_kv, d, row_begin, rope):
+    k = orc.matmul(x, wk)
+    if rope:
+        k = orc.apply_rope(k, n_kv, d, row_begin)
+    return k, orc.matmul(x, wv)
+
+
+def make_inputs(orc, seed, L, d_model, n_kv, d, bf16):
+    x = orc.gaussian(L, d_model, orc.child(seed, 1), 1.0, np.float32)
+    wk = orc.gaussian(d_model, n_kv * d, orc.child(seed, 2), 1.0 / np.sqrt(d_model), np.float32)   # engine.hpp:152-153
+    wv = orc.gaussian(d_model, n_kv * d, orc.child(seed, 3), 1.0 / np.sqrt(d_model), np.float32)
+    if bf16:
+        x, wk, wv = orc.round_bf16(x), orc.round_bf16(wk), orc.round_bf16(wv)
+    return x, wk, wv
+
+
+# L, d_model, n_kv, P, row chunks (appended one after the other, so later chunks start mid-page / mid-tile), rope
+BF16_CASES = [
+    (300, 256, 2, 64, (300,), True),
+    (200, 192, 1, 32, (37, 100, 63), True),          # one kv head: a tile holds a K head and a V head
+    (1000, 512, 4, 64, (128, 872), True),            # several 256-column blocks, a full first tile
+    (130, 64, 2, 16, (130,), False),                 # single k block, no rotation
+    (90, 4096, 2, 128, (90,), True),                 # the Llama reduction depth
+]
+
+
+@pytest.mark.parametrize("L,d_model,n_kv,P,chunks,rope", BF16_CASES)
+def test_fused_projection_rope_append_bf16(ctx, orc, L, d_model, n_kv, P, chunks, rope):
+    from paper_2602_01053_b200 import Pool, Projection, abi
+    d = 128
+    x, wk, wv = make_inputs(orc, 700 + L, L, d_model, n_kv, d, True)
+    pool = Pool(ctx, "FullShared", 2, n_kv, d, d_model, 0, 1, max_tokens=L + 8, dtype=abi.BF16, page_tokens=P)
+    proj = Projection(ctx, 2, d_model, n_kv, d, dtype=abi.BF16)
+    proj.set_kv(1, wk, wv)
+    pool.append_tokens(L)
+    r0 = 0
+    for n in chunks:
+        assert pool.append_kv_project(proj, 1, 0, r0, x[r0:r0 + n], rope=rope) == n
+        assert ctx.last_kernel() == "kv_project_umma"
+        r0 += n
+    assert pool.append_kv_project(proj, 1, 0, 0, x, rope=rope) == 0            # first writer wins: nothing to add
+    want_k, want_v = reference_kv(orc, x, wk, wv, n_kv, d, 0, rope)
+    got_k, got_v = pool.key_view(1, 0), pool.value_view(1, 0)
+    assert got_k.shape == want_k.shape and got_v.shape == want_v.shape
+    # bf16 storage of fp32-accumulated exact products: half a bf16 ulp (2^-9) of the largest element
+    assert orc.max_rel_error(got_k, want_k) <= 4e-3
+    assert orc.max_rel_error(got_v, want_v) <= 4e-3
+    assert np.mean(got_v == orc.round_bf16(want_v)) > 0.97                       # the rest are 1-ulp rounding flips
+    assert pool.rows(abi.KEY, 0, 0) == 0                                         # the other layer is untouched
+    pool.close(); proj.close()
+
+
+def test_fused_projection_then_attention_matches_reference_step(ctx, orc):
+    """The hot path end to end on one layer: project + rotate + append K / V, project V_lr = X * A, then decode over
+    the cache -- against gqa_attention on the reference's k / v / v_lr (engine.hpp:376-443)."""
+    from paper_2602_01053_b200 import Adapters, Pool, Projection, abi
+    L, d_model, n_q, n_kv, d, r, A = 333, 256, 8, 2, 128, 16, 2
+    x, wk, wv = make_inputs(orc, 4242, L, d_model, n_kv, d, True)
+    a = orc.round_bf16(orc.gaussian(d_model, r, orc.child(4242, 4), 1.0 / np.sqrt(d_model), np.float32))
+    b = [orc.round_bf16(orc.gaussian(r, n_kv * d, orc.child(4242, 10 + i), 0.02 / np.sqrt(r), np.float32)) for i in range(A)]
+    q = [orc.round_bf16(orc.gaussian(1, n_q * d, orc.child(4242, 20 + i), 1.0 / np.sqrt(d), np.float32)) for i in range(A)]
+    pool = Pool(ctx, "BaseLRShared", 1, n_kv, d, d_model, r, A, max_tokens=L, dtype=abi.BF16)
+    proj = Projection(ctx, 1, d_model, n_kv, d, dtype=abi.BF16)
+    ad = Adapters(ctx, 1, A, d_model, r, n_kv, d, dtype=abi.BF16)
+    proj.set_kv(0, wk, wv); ad.set_a(0, a)
+    for i in range(A):
+        ad.set_b(0, i, b[i], 16.0)
+    pool.append_tokens(L)
+    assert pool.append_kv_project(proj, 0, 0, 0, x) == L
+    assert pool.append_lr_project(ad, 0, 0, 0, x) == L
+    out = pool.decode(ad, 0, 1, list(range(A)), n_q, np.stack([q[i][0] for i in range(A)])[None])
+    k, v = reference_kv(orc, x, wk, wv, n_kv, d, 0, True)
+    v_lr = orc.matmul(x, a)
+    for i in range(A):
+        want = orc.gqa_attention(q[i], k, v, v_lr, b[i], 16.0 / r, L - 1, n_q, n_kv)
+        assert orc.max_rel_error(out[0, i][None, :], want) <= 2e-2
+    pool.close(); proj.close(); ad.close()
+
+
+@pytest.mark.parametrize("d,n_kv,rope", [(32, 2, True), (128, 1, True), (64, 3, False)])
+def test_projection_rope_append_fp32_is_the_reference_order(ctx, orc, d, n_kv, rope):
+    """fp32 pools: matmul in the reference's order (bit-identical) and the rotation with double-precision angles."""
+    from paper_2602_01053_b200 import Pool, Projection, abi
+    L, d_model = 150, 96
+    x, wk, wv = make_inputs(orc, 31 + d, L, d_model, n_kv, d, False)
+    pool = Pool(ctx, "FullShared", 1, n_kv, d, d_model, 0, 1, max_tokens=L, dtype=abi.F32, page_tokens=32)
+    proj = Projection(ctx, 1, d_model, n_kv, d, dtype=abi.F32)
+    proj.set_kv(0, wk, wv)
+    pool.append_tokens(L)
+    assert pool.append_kv_project(proj, 0, 0, 0, x[:70], rope=rope) == 70
+    assert pool.append_kv_project(proj, 0, 0, 40, x[40:], rope=rope) == L - 70       # overlaps 30 cached rows
+    assert ctx.last_kernel() == "kv_project_f32"
+    want_k, want_v = reference_kv(orc, x, wk, wv, n_kv, d, 0, rope)
+    assert np.array_equal(pool.value_view(0, 0), want_v)
+    assert orc.max_rel_error(pool.key_view(0, 0), want_k) <= 1e-6
+    if not rope:
+        assert np.array_equal(pool.key_view(0, 0), want_k)
+    pool.close(); proj.close()
+
+
+def test_projection_errors(ctx, orc):
+    from paper_2602_01053_b200 import LorakvError, Pool, Projection, abi
+    pool = Pool(ctx, "FullShared", 1, 2, 128, 64, 0, 1, max_tokens=64, dtype=abi.BF16)
+    proj = Projection(ctx, 1, 64, 2, 128, dtype=abi.BF16)
+    x = np.zeros((4, 64), np.float32)
+    pool.append_tokens(8)
+    with pytest.raises(LorakvError, match="never uploaded"):
+        pool.append_kv_project(proj, 0, 0, 0, x)
+    proj.set_kv(0, np.zeros((64, 256), np.float32), np.zeros((64, 256), np.float32))
+    with pytest.raises(LorakvError, match="gap"):
+        pool.append_kv_project(proj, 0, 0, 3, x)                                       # kvcache.hpp:401-403
+    other = Projection(ctx, 1, 128, 2, 128, dtype=abi.BF16)
+    with pytest.raises(LorakvError, match="do not match"):
+        pool.append_kv_project(other, 0, 0, 0, x)
+    pool.close(); proj.close(); other.close()

@@ -284,7 +284,22 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
         p1.record()
         res["xa_project_ms"] = p0.elapsed_ms(p1) / 3
         res["xa_project_gbs"] = L_c * d_model * 4 / (res["xa_project_ms"] * 1e-3) / 1e9
-        res["ttft_ms_per_layer"] = attn_ms + res["xa_project_ms"]
+        # K / V_base projection + RoPE + append of the same rows (engine.hpp:376-403) in one tcgen05 kernel
+        pj = pkg.Projection(ctx, 1, d_model, n_kv, d, dtype=pool.dims.dtype)
+        wrng = np.random.default_rng(9)
+        pj.set_kv(0, (wrng.standard_normal((d_model, n_kv * d)) / np.sqrt(d_model)).astype(np.float32),
+                  (wrng.standard_normal((d_model, n_kv * d)) / np.sqrt(d_model)).astype(np.float32))
+        sp.append_kv_project(pj, 0, 0, 0, dev_ptr=x.data_ptr(), n_rows=L_c, ld=d_model)             # warm-up
+        k0e, k1e = ctx.event(), ctx.event()
+        k0e.record()
+        for i in range(1, 4):
+            sp.append_kv_project(pj, 0, 0, i * L_c, dev_ptr=x.data_ptr(), n_rows=L_c, ld=d_model)
+        k1e.record()
+        res["kv_project_ms"] = k0e.elapsed_ms(k1e) / 3
+        res["kv_project_tflops"] = 2 * L_c * d_model * 2 * n_kv * d / (res["kv_project_ms"] * 1e-3) / 1e12
+        res["kv_project_kernel"] = ctx.last_kernel()
+        res["ttft_ms_per_layer"] = attn_ms + res["xa_project_ms"] + res["kv_project_ms"]
+        pj.close()
         sp.close(); sa.close()
     except Exception as e:
         res["xa_project_error"] = str(e)[:200]

@@ -9,6 +9,10 @@
 //       == gqa_attention(q, key_view, value_view, lr_view, B[agent], alpha/rank, query_offset, ...)
 //   append_lr_project(store, tables, layer, agent, row_begin, x)
 //       == store.append_lr(layer, agent, row_begin, matmul(x, A))           (engine.hpp:414-418)
+//   append_kv_project(store, weights, layer, agent, row_begin, x, rope)
+//       == k = matmul(x, Wk); if (rope) apply_rope(k, n_kv_heads, d_head, row_begin); v = matmul(x, Wv);
+//          store.append_key(layer, agent, row_begin, k); store.append_value(layer, agent, row_begin, v)
+//                                                                           (engine.hpp:376-403, :225-243)
 //
 // AdapterTable keeps the shared down-projection A per layer and B / alpha per (layer, agent) in HBM
 // (lora.hpp:13-87; shared-A multi-LoRA, lora.hpp:69-73).
@@ -83,6 +87,40 @@ inline idx append_lr_project(KvStore<float>& store, const AdapterTable& tables, 
   std::int64_t added = 0;
   b200::check(lorakv_pool_append_lr_project(store.handle(), tables.handle(), layer, agent, row_begin, x.data, x.rows,
                                             x.stride, LORAKV_HOST, &added));
+  return added;
+}
+
+// Wk / Wv of every layer (engine.hpp LayerWeights::wk, wv), restricted to the store's kv-head shard
+class ProjectionTable {
+ public:
+  explicit ProjectionTable(const KvStore<float>& store) {
+    const StoreDims& d = store.dims();
+    const DeviceOptions& o = store.device_options();
+    b200::check(lorakv_proj_create(b200::Runtime::ctx(), d.n_layers, d.d_model, o.n_kv_heads, d.d_kv / o.n_kv_heads,
+                                   o.kv_head_begin, o.n_kv_local, o.bf16 ? LORAKV_BF16 : LORAKV_F32, &h_));
+  }
+  ~ProjectionTable() { lorakv_proj_destroy(h_); }
+  ProjectionTable(const ProjectionTable&) = delete;
+  ProjectionTable& operator=(const ProjectionTable&) = delete;
+  // wk, wv: d_model x d_kv, row-major (Matrix<float> storage)
+  void set_layer(idx layer, const Matrix<float>& wk, const Matrix<float>& wv) {
+    if (wk.rows != wv.rows || wk.cols != wv.cols)
+      fail("ProjectionTable: wk is " + shape_str(wk.rows, wk.cols) + " but wv is " + shape_str(wv.rows, wv.cols));
+    b200::check(lorakv_proj_set_kv(h_, layer, wk.data.data(), wv.data.data()));
+  }
+  lorakv_proj* handle() const { return h_; }
+
+ private:
+  lorakv_proj* h_ = nullptr;
+};
+
+// K / V_base projection of new context rows, rotation of the keys and the append, in one device pass;
+// returns the rows actually appended (first writer wins)
+inline idx append_kv_project(KvStore<float>& store, const ProjectionTable& weights, idx layer, idx agent, idx row_begin,
+                             Span2D<const float> x, bool rope = true) {
+  std::int64_t added = 0;
+  b200::check(lorakv_pool_append_kv_project(store.handle(), weights.handle(), layer, agent, row_begin, x.data, x.rows,
+                                            x.stride, LORAKV_HOST, rope ? 1 : 0, &added));
   return added;
 }
 

@@ -20,8 +20,8 @@
 //              share a scheduler (w and w + 4: same TMEM lanes) are always half a tile apart, so one
 //              warp's TMEM load / row max / bookkeeping runs under the other's exp phase and the MUFU
 //              (16 ex2 / clk / SM -- the longest per-tile resource next to the tensor pipe) never idles.
-//              The running row maximum is handed from tile j to tile j + 1 through one 8-byte shared-memory
-//              word per row (sequence number | value), so only the two threads of a row ever wait for each other.
+//              The running row maximum is handed from tile j to tile j + 1 through shared memory, ordered by an
+//              mbarrier per (warp pair, direction): 32 arrivals by the owner of j, a parity wait by the owner of j + 1.
 //   warp 8/10  TMA producers: bulk copies of K (warp 8) and of V_base + V_lr (warp 10) into 3-stage rings
 //              of 128-key stages, mbarrier tracked, independent of each other
 //   warp 9     MMA issuer (one elected thread): S(j) = Q K_j^T (N = 64) into one of FOUR TMEM S buffers,
@@ -93,7 +93,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 
 struct Barriers {
   uint64_t q_full, p_full[4], pv_done[4], all_done;
-  uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[4];
+  uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[4], hand[8];
 };
 
 // kDecode = false: prefill block (rows = head x position, causal mask, final output)
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ Barriers bars;
   __shared__ uint32_t tmem_base_s;
-  __shared__ unsigned long long hand_s[kBM];   // (tile count << 32 | running row maximum): owner of tile j -> owner of j + 1
+  __shared__ float m_s[kBM];            // running row maximum: owner of tile j -> owner of tile j + 1 (bars.hand orders it)
   __shared__ float l_s[2][kBM];         // [softmax warpgroup][row]: partial row sums for the epilogue ...
   __shared__ float mref_s[2][kBM];      // ... and the maximum each of them is relative to
   unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -152,7 +152,6 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   }
   const int n_stages_needed = (n_tiles + 1) / 2;                  // kBN-key stages the producers stream
 
-  if (tid < kBM) hand_s[tid] = 0ull;
   if (tid == 0) {
     ptx::mbar_init(&bars.q_full, 256);
     for (int s = 0; s < 4; ++s) ptx::mbar_init(&bars.p_full[s], 128);
@@ -163,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       ptx::mbar_init(&bars.v_full[s], 1); ptx::mbar_init(&bars.v_empty[s], 1);
     }
     for (int s = 0; s < 4; ++s) ptx::mbar_init(&bars.s_full[s], 1);
+    for (int s = 0; s < 8; ++s) ptx::mbar_init(&bars.hand[s], 32);
     ptx::fence_barrier_init();
   }
   if (warp == 0) ptx::tmem_alloc(&tmem_base_s, 512);
@@ -353,10 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
 
       // the running maximum after tile j - 1, published by the partner warp
       float m_prev = ninf;
-      if (j > 0) {                  // one 8-byte word per row: the sequence number says the value is the one after tile j - 1
-        unsigned long long hv;
-        do { hv = *reinterpret_cast<volatile unsigned long long*>(&hand_s[row]); } while ((uint32_t)(hv >> 32) != (uint32_t)j);
-        m_prev = __uint_as_float((uint32_t)hv);
+      if (j > 0) {                  // the partner warp (same rows, other warpgroup) published after tile j - 1
+        ptx::mbar_wait(&bars.hand[(warp & 3) * 2 + (wg ^ 1)], (uint32_t)(((j - 1) >> 1) & 1));
+        m_prev = *reinterpret_cast<volatile float*>(&m_s[row]);
       }
       float m_used = m_prev;
       const float m_cand = fmaxf(m_prev, mx);
@@ -400,8 +399,10 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         }
       }
       // hand the maximum to the owner of tile j + 1
-      if (j + 1 < n_tiles)
-        *reinterpret_cast<volatile unsigned long long*>(&hand_s[row]) = ((unsigned long long)(uint32_t)(j + 1) << 32) | __float_as_uint(m_used);
+      if (j + 1 < n_tiles) {        // mbarrier.arrive releases the store; one barrier per (warp pair, direction), 32 arrivals
+        m_s[row] = m_used;
+        ptx::mbar_arrive(&bars.hand[(warp & 3) * 2 + wg]);
+      }
       // bring this warpgroup's row sum to the new reference (its last tile was j - 2)
       if (m_used != m_mine) {
         l_run *= (m_mine == ninf) ? 0.f : ex2(m_mine - m_used);

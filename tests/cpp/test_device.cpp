@@ -92,3 +92,36 @@ TEST_CASE("tiny config on bf16 pages") { run_config(true, 2e-2, 512, 4, 2, 64, 8
 TEST_CASE("Llama-shaped heads (32q/8kv, d=128, r=16, 3 agents), two layers, bf16 pages, ragged length") {
   run_config(true, 2e-2, 1000, 32, 8, 128, 16, 3, 2, 512);
 }
+
+// engine.hpp:376-403 through the drop-in header: project, rotate, append in one device pass, read back through the
+// store's views and compare with matmul + apply_rope of the checker
+TEST_CASE("append_kv_project == append_key(rope(x Wk)), append_value(x Wv) on bf16 and fp32 pages") {
+  for (int bf16 = 0; bf16 < 2; ++bf16) {
+    const idx L = 150, d_model = 128, n_kv = 2, d = 128;
+    auto rnd = [&](Matrix<float> m) { return bf16 ? oracle::round_bf16(m) : m; };
+    KvStore<float> store(CacheScheme{SchemeKind::FullShared, {}}, StoreDims{1, n_kv * d, d_model, 0, 1}, DeviceOptions{n_kv, L, bf16 != 0});
+    ProjectionTable weights(store);
+    const Matrix<float> x = rnd(Matrix<float>::gaussian(L, d_model, Rng(5), 1.0));
+    const Matrix<float> wk = rnd(Matrix<float>::gaussian(d_model, n_kv * d, Rng(6), 1.0 / std::sqrt(double(d_model))));
+    const Matrix<float> wv = rnd(Matrix<float>::gaussian(d_model, n_kv * d, Rng(7), 1.0 / std::sqrt(double(d_model))));
+    weights.set_layer(0, wk, wv);
+    store.append_tokens(std::vector<std::int32_t>(static_cast<std::size_t>(L), 1));
+    CHECK(append_kv_project(store, weights, 0, 0, 0, x.view().row_range(0, 60)) == 60);
+    CHECK(append_kv_project(store, weights, 0, 0, 60, x.view().row_range(60, L)) == L - 60);
+    CHECK(append_kv_project(store, weights, 0, 0, 0, x.view()) == 0);
+    Matrix<float> k_want = oracle::matmul(x, wk);
+    oracle::ok(orc_apply_rope_f32(k_want.data.data(), L, n_kv * d, n_kv, d, 0));
+    const Matrix<float> v_want = oracle::matmul(x, wv);
+    const Span2D<const float> kv = store.key_view(0, 0), vv = store.value_view(0, 0);
+    REQUIRE(kv.rows == L); REQUIRE(vv.rows == L);
+    Matrix<float> k_got(L, n_kv * d), v_got(L, n_kv * d);
+    for (idx i = 0; i < L; ++i) for (idx c = 0; c < n_kv * d; ++c) { k_got(i, c) = kv(i, c); v_got(i, c) = vv(i, c); }
+    CHECK_LE(max_rel_error(k_got, k_want), bf16 ? 4e-3 : 1e-6);
+    CHECK_LE(max_rel_error(v_got, v_want), bf16 ? 4e-3 : 0.0);
+    bool threw = false;
+    try { append_kv_project(store, weights, 0, 0, L + 5, x.view()); } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()).find("gap") != std::string::npos;     // kvcache.hpp:401-403
+    }
+    CHECK(threw);
+  }
+}

@@ -131,7 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
   __shared__ uint32_t tmem_base_s;
   unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int tile = blockIdx.x, nblk = blockIdx.y;            // 128-row tile, 256-column block (two heads)
+  // column block fastest: the CTAs that share an X tile run in the same wave, so X is read from HBM once
+  // (with the row tile fastest it was re-read per column block: 982 MB of DRAM reads for 151 MB of operands)
+  const int nblk = blockIdx.x, tile = blockIdx.y;            // 256-column block (two heads), 128-row tile
   const int kb_n = p.d_model / kBK;
 
   if (tid == 0) {
@@ -317,7 +319,7 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     pp.row0 = row0; pp.n_rows = n_rows; pp.k_from = k_from; pp.v_from = v_from;
     const size_t smem = (size_t)kStages * kStageBytes + 1024;
     LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const dim3 grid((unsigned)tiles, (unsigned)(2 * n_kv * d / kBN));
+    const dim3 grid((unsigned)(2 * n_kv * d / kBN), (unsigned)tiles);
     prof_mark(ctx, 0);
     kv_project_umma_kernel<<<grid, kThreads, smem, ctx->stream>>>(pp);
     prof_mark(ctx, 1);

@@ -549,6 +549,80 @@ int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t sme
 
 }  // namespace
 
+// The same merge when a row has at most 32 partials (a whole decode step in one launch: ~5 per row): one WARP per
+// (query row, layer x kv head) and no block-level barrier -- lanes over the splits for the maximum and the
+// denominator, then lanes over the columns for the weighted sums.  A CTA per row spent its time in four
+// __syncthreads with 250 of its 256 threads idle (31 us per cfg-2 step for 13 MB of partials).
+__global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel(const DecodeMergeParams p, int64_t n_rows_units) {
+  __shared__ float olr_s[kMergeWarps][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * kMergeWarps + warp;
+  if (gw >= n_rows_units) return;
+  const int rho = (int)(gw % p.rows_total);
+  const int64_t y = gw / p.rows_total;
+  const int kvh = (int)(y % p.n_kv_local);
+  const int64_t layer_rel = y / p.n_kv_local;
+  const int rows_blk = 16 * p.MW;
+  const int rb = rho / rows_blk, r_in = rho % rows_blk;
+  const int64_t u = (layer_rel * p.n_kv_local + kvh) * p.row_blocks + rb;
+  const int64_t w_lo = (u * p.T) / p.G, w_hi = ((u + 1) * p.T - 1) / p.G;
+  const int ns = (int)(w_hi - w_lo + 1);                     // <= 32, checked by the launcher
+  const int PS = 4 + p.D + p.RP, C = p.D + p.RP;
+  const float ninf = -std::numeric_limits<float>::infinity();
+  auto row_of = [&](int s) -> const float* {
+    const int64_t w = w_lo + s;
+    const int64_t slot = w * p.max_seg + (u - (w * p.G) / p.T);
+    return p.part + (slot * rows_blk + r_in) * PS;
+  };
+  float m = ninf, l = 0.f;
+  if (lane < ns) { const float2 ml = *reinterpret_cast<const float2*>(row_of(lane)); m = ml.x; l = ml.y; }
+  float mx = m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const float wgt = (m == ninf) ? 0.f : exp2f(m - mx);
+  float lsum = wgt * l;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  constexpr int kMaxCols = 6;            // (D + RP) <= 192 columns / 32 lanes
+  float acc[kMaxCols];
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) acc[i] = 0.f;
+  for (int s = 0; s < ns; ++s) {
+    const float ws = __shfl_sync(0xffffffffu, wgt, s);
+    if (ws == 0.f) continue;             // an empty split carries no accumulators (warp-uniform)
+    const float* row = row_of(s) + 4;
+#pragma unroll
+    for (int i = 0; i < kMaxCols; ++i) {
+      const int c = lane + 32 * i;
+      if (c < C) acc[i] = fmaf(ws, row[c], acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= p.D && c < C) olr_s[warp][c - p.D] = acc[i];
+  }
+  __syncwarp();
+  // ---- epilogue: o += (lr_scale * o_lr[k]) * B[agent][k,:], out = o / l (attention.hpp:244-259) ----
+  const int gi = rho % p.group, entry = rho / p.group;
+  const int64_t layer = p.layer_begin + layer_rel;
+  const int64_t dkv = (int64_t)p.n_kv_local * p.D;
+  const int agent = p.agent_ids ? p.agent_ids[entry] : 0;
+  const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
+  const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
+  float* dst = p.out + ((layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * p.D;
+  const float inv_l = 1.0f / lsum;
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) {
+    const int c = lane + 32 * i;
+    if (c < p.D) {
+      float o = acc[i];
+      for (int k = 0; k < p.r; ++k) o = fmaf(scale * olr_s[warp][k], b[k * dkv + c], o);
+      dst[c] = o * inv_l;
+    }
+  }
+}
+
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
                         const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers) {
@@ -563,7 +637,12 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
   const int ns_max = (int)((T - 1) / G + 2);
   dim3 mgrid((unsigned)rows_total, (unsigned)(n_layers * n_kv_local));
   if (d + rp > 192) return fail("decode merge: d_head + padded rank %d exceeds 192 columns", d + rp);
-  fla_decode_merge_kernel<<<mgrid, kMergeWarps * 32, (size_t)(ns_max + kMergeWarps * (d + rp)) * sizeof(float), ctx->stream>>>(mp);
+  if (ns_max <= 32 && rp <= 64) {
+    const int64_t n = (int64_t)rows_total * n_layers * n_kv_local;
+    fla_decode_merge_warp_kernel<<<(unsigned)((n + kMergeWarps - 1) / kMergeWarps), kMergeWarps * 32, 0, ctx->stream>>>(mp, n);
+  } else {
+    fla_decode_merge_kernel<<<mgrid, kMergeWarps * 32, (size_t)(ns_max + kMergeWarps * (d + rp)) * sizeof(float), ctx->stream>>>(mp);
+  }
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;

@@ -198,6 +198,16 @@ int lorakv_proj_create(lorakv_ctx* ctx, int64_t n_layers, int64_t d_model, int64
                        lorakv_proj** out);
 void lorakv_proj_destroy(lorakv_proj* proj);
 int lorakv_proj_set_kv(lorakv_proj* proj, int64_t layer, const float* wk, const float* wv);
+/* The query side of the same step (engine.hpp:362-373, :422):
+ *     q = x_norm * Wq;  q += (alpha/rank) * ((x_norm * A_q) * B_q[agent]);  if (rope) apply_rope(q, n_q_heads, d_head, pos_begin)
+ * wq: d_model x n_q_heads*d_head, a_q: d_model x rank (shared by all agents, lora.hpp:69-73), b_q: rank x
+ * n_q_heads*d_head, all row-major float32 HOST.  lorakv_proj_query writes n_rows x (n_q_local*d_head) float32 rows
+ * (the shard's q heads) into q_out, HOST or DEVICE like x; agent < 0 skips the adapter. */
+int lorakv_proj_set_q(lorakv_proj* proj, int64_t layer, int64_t n_q_heads, const float* wq);
+int lorakv_proj_set_q_lora(lorakv_proj* proj, int64_t layer, int64_t agent, int64_t n_agents, int64_t rank,
+                           const float* a_q, const float* b_q, double alpha);
+int lorakv_proj_query(lorakv_proj* proj, int64_t layer, int64_t agent, int64_t pos_begin, const float* x,
+                      int64_t n_rows, int64_t ld, int rope, float* q_out, int mem_kind);
 /* x: n_rows x d_model float32 (x_norm rows of logical rows [row_begin, row_begin+n_rows)), HOST or
  * DEVICE.  First-writer-wins as in lorakv_pool_append; *appended = rows newly written. */
 int lorakv_pool_append_kv_project(lorakv_pool* pool, const lorakv_proj* proj, int64_t layer,

@@ -105,6 +105,9 @@ SIGNATURES = {
     "lorakv_proj_create": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "lorakv_proj_destroy": (None, [_vp]),
     "lorakv_proj_set_kv": (C.c_int, [_vp, _i64, _pf, _pf]),
+    "lorakv_proj_set_q": (C.c_int, [_vp, _i64, _i64, _pf]),
+    "lorakv_proj_set_q_lora": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _pf, _pf, C.c_double]),
+    "lorakv_proj_query": (C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, _vp, C.c_int]),
     "lorakv_pool_append_kv_project": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.c_int, C.POINTER(_i64)]),
     "lorakv_pool_rows": (C.c_int, [_vp, C.c_int, _i64, _i64, C.POINTER(_i64)]),
     "lorakv_pool_read": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _i64, _pf]),
@@ -432,6 +435,29 @@ class Projection:
         wk = np.ascontiguousarray(wk, dtype=np.float32)
         wv = np.ascontiguousarray(wv, dtype=np.float32)
         _check(self.ctx.lib.lorakv_proj_set_kv(self.h, layer, wk.ctypes.data_as(_pf), wv.ctypes.data_as(_pf)))
+
+    def set_q(self, layer, n_q_heads, wq):
+        wq = np.ascontiguousarray(wq, dtype=np.float32)
+        self._dq_full = wq.shape[1]
+        _check(self.ctx.lib.lorakv_proj_set_q(self.h, layer, n_q_heads, wq.ctypes.data_as(_pf)))
+
+    def set_q_lora(self, layer, agent, n_agents, a_q, b_q, alpha):
+        a_q = np.ascontiguousarray(a_q, dtype=np.float32)
+        b_q = np.ascontiguousarray(b_q, dtype=np.float32)
+        _check(self.ctx.lib.lorakv_proj_set_q_lora(self.h, layer, agent, n_agents, a_q.shape[1], a_q.ctypes.data_as(_pf),
+                                                   b_q.ctypes.data_as(_pf), alpha))
+
+    def query(self, layer, agent, pos_begin, x, n_q_local_cols, rope=True):
+        """q rows of the shard's heads for x (host arrays); agent < 0 skips the adapter."""
+        x = np.asarray(x, dtype=np.float32)
+        ptr, ld_ = _span(x, _f)
+        out = np.empty((x.shape[0], n_q_local_cols), dtype=np.float32)
+        _check(self.ctx.lib.lorakv_proj_query(self.h, layer, agent, pos_begin, C.cast(ptr, _vp), x.shape[0], ld_, int(rope),
+                                              out.ctypes.data_as(_vp), HOST))
+        return out
+
+    def query_device(self, layer, agent, pos_begin, x_ptr, n_rows, ld, q_ptr, rope=True):
+        _check(self.ctx.lib.lorakv_proj_query(self.h, layer, agent, pos_begin, _vp(x_ptr), n_rows, ld, int(rope), _vp(q_ptr), DEVICE))
 
 
 class Pool:

@@ -153,7 +153,7 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush})
+  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj})
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (cudaEvent_t e : ctx->prof_ev) if (e) cudaEventDestroy(e);
@@ -579,6 +579,7 @@ void lorakv_proj_destroy(lorakv_proj* pr) {
   if (pr->packed) cudaFree(pr->packed);
   if (pr->wk) cudaFree(pr->wk);
   if (pr->wv) cudaFree(pr->wv);
+  for (void* q : {pr->wq_packed, (void*)pr->wq, (void*)pr->aq, (void*)pr->bq}) if (q) cudaFree(q);
   delete pr;
 }
 
@@ -604,6 +605,120 @@ int lorakv_proj_set_kv(lorakv_proj* pr, int64_t layer, const float* wk, const fl
   }
   LK_CUDA(cudaStreamSynchronize(ctx->stream));
   pr->set[(size_t)layer] = 1;
+  return LORAKV_OK;
+}
+
+// ---- query projection (engine.hpp:362-373, :422) ----------------------------------------------------
+int lorakv_proj_set_q(lorakv_proj* pr, int64_t layer, int64_t n_q_heads, const float* wq) {
+  if (!pr || !wq) return fail("null argument");
+  if (layer < 0 || layer >= pr->n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (n_q_heads < 1 || n_q_heads % pr->n_kv_heads != 0)
+    return fail("gqa_attention: n_q_heads %lld not divisible by n_kv_heads %lld", (long long)n_q_heads, (long long)pr->n_kv_heads);
+  if (pr->n_q_heads != 0 && pr->n_q_heads != n_q_heads) return fail("proj_set_q: n_q_heads changed from %lld to %lld", (long long)pr->n_q_heads, (long long)n_q_heads);
+  lorakv_ctx* ctx = pr->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  const int64_t group = n_q_heads / pr->n_kv_heads, n_q_local = group * pr->n_kv_local;
+  const int64_t dq_full = n_q_heads * pr->d_head, dq = n_q_local * pr->d_head;
+  const size_t one = (size_t)(pr->d_model * dq_full) * sizeof(float);
+  if (pr->n_q_heads == 0) {
+    pr->q_fused = pr->fused && dq % 256 == 0;
+    if (pr->q_fused) LK_CUDA(cudaMalloc(&pr->wq_packed, (size_t)(pr->n_layers * pr->d_model * dq) * 2));
+    else LK_CUDA(cudaMalloc(&pr->wq, (size_t)pr->n_layers * one));
+    pr->n_q_heads = n_q_heads;
+    pr->q_set.assign((size_t)pr->n_layers, 0);
+  }
+  if (pr->q_fused) {
+    LK_TRY(scratch_reserve(ctx, ctx->in, one));
+    float* sq = static_cast<float*>(ctx->in.ptr);
+    LK_CUDA(cudaMemcpyAsync(sq, wq, one, cudaMemcpyHostToDevice, ctx->stream));
+    LK_TRY(launch_pack_w(ctx, sq, dq_full, pr->kv_head_begin * group * pr->d_head, dq, pr->d_model, 0,
+                         static_cast<char*>(pr->wq_packed) + (size_t)(layer * pr->d_model * dq) * 2));
+  } else {
+    LK_CUDA(cudaMemcpyAsync(pr->wq + (size_t)layer * (one / sizeof(float)), wq, one, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  pr->q_set[(size_t)layer] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_proj_set_q_lora(lorakv_proj* pr, int64_t layer, int64_t agent, int64_t n_agents, int64_t rank, const float* a_q,
+                           const float* b_q, double alpha) {
+  if (!pr || !a_q || !b_q) return fail("null argument");
+  if (pr->n_q_heads == 0) return fail("proj_set_q_lora: upload Wq first (lorakv_proj_set_q)");
+  if (layer < 0 || layer >= pr->n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (rank < 1) return fail("LoraAdapter: rank must be >= 1, got %lld", (long long)rank);
+  if (rank > 64) return fail("proj_set_q_lora: rank %lld > 64 is not supported", (long long)rank);
+  if (agent < 0 || agent >= n_agents) return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)n_agents);
+  const double sc = alpha / (double)rank;
+  if (!(std::isfinite(sc) && sc > 0.0)) return fail("LoraAdapter: effective scale alpha/rank must be finite and positive");
+  lorakv_ctx* ctx = pr->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  const int64_t dq_full = pr->n_q_heads * pr->d_head;
+  if (!pr->aq) {
+    LK_CUDA(cudaMalloc(&pr->aq, (size_t)(pr->n_layers * pr->d_model * rank) * sizeof(float)));
+    LK_CUDA(cudaMalloc(&pr->bq, (size_t)(pr->n_layers * n_agents * rank * dq_full) * sizeof(float)));
+    pr->q_rank = rank; pr->q_agents = n_agents;
+    pr->q_scale.assign((size_t)(pr->n_layers * n_agents), 0.f);
+    pr->q_lora_set.assign((size_t)(pr->n_layers * n_agents), 0);
+  }
+  if (rank != pr->q_rank || n_agents != pr->q_agents) return fail("proj_set_q_lora: rank / agent count changed");
+  // shared-A multi-LoRA (lora.hpp:69-73): every agent's down-projection is the same matrix, the last upload stays
+  LK_CUDA(cudaMemcpyAsync(pr->aq + (size_t)(layer * pr->d_model * rank), a_q, (size_t)(pr->d_model * rank) * sizeof(float),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  LK_CUDA(cudaMemcpyAsync(pr->bq + (size_t)((layer * n_agents + agent) * rank * dq_full), b_q, (size_t)(rank * dq_full) * sizeof(float),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  pr->q_scale[(size_t)(layer * n_agents + agent)] = (float)sc;
+  pr->q_lora_set[(size_t)(layer * n_agents + agent)] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_proj_query(lorakv_proj* pr, int64_t layer, int64_t agent, int64_t pos_begin, const float* x, int64_t n_rows,
+                      int64_t ld, int rope, float* q_out, int mem_kind) {
+  if (!pr || !q_out) return fail("null argument");
+  if (layer < 0 || layer >= pr->n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (pr->n_q_heads == 0 || !pr->q_set[(size_t)layer]) return fail("proj_query: Wq of layer %lld was never uploaded", (long long)layer);
+  if (n_rows < 0 || pos_begin < 0) return fail("proj_query: negative row count or position");
+  if (n_rows == 0) return LORAKV_OK;
+  if (!x) return fail("proj_query: null rows");
+  const bool lora = agent >= 0;
+  if (lora) {
+    if (!pr->aq || agent >= pr->q_agents) return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)pr->q_agents);
+    if (!pr->q_lora_set[(size_t)(layer * pr->q_agents + agent)]) return fail("proj_query: q adapter of layer %lld agent %lld was never uploaded", (long long)layer, (long long)agent);
+  }
+  const bool host = mem_kind == LORAKV_HOST;
+  if (!host && mem_kind != LORAKV_DEVICE) return fail("bad mem_kind %d", mem_kind);
+  lorakv_ctx* ctx = pr->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  const int64_t group = pr->n_q_heads / pr->n_kv_heads, n_q_local = group * pr->n_kv_local;
+  const int64_t dq_full = pr->n_q_heads * pr->d_head, dq = n_q_local * pr->d_head;
+  const int64_t col0 = pr->kv_head_begin * group * pr->d_head;
+  const float* dev; int64_t dev_ld;
+  LK_TRY(stage_rows(ctx, x, n_rows, pr->d_model, ld, mem_kind, &dev, &dev_ld));
+  float* q_dev = q_out;
+  const size_t q_bytes = (size_t)(n_rows * dq) * sizeof(float);
+  if (host) { LK_TRY(scratch_reserve(ctx, ctx->out, q_bytes)); q_dev = static_cast<float*>(ctx->out.ptr); }
+  const int64_t rank = lora ? pr->q_rank : 0;
+  const float* aq = lora ? pr->aq + (size_t)(layer * pr->d_model * rank) : nullptr;
+  const float* bq = lora ? pr->bq + (size_t)((layer * pr->q_agents + agent) * rank * dq_full) : nullptr;
+  const float sc = lora ? pr->q_scale[(size_t)(layer * pr->q_agents + agent)] : 0.f;
+  const bool fused = pr->q_fused && (dev_ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(dev) & 15) == 0);
+  if (!fused && pr->q_fused) return fail("proj_query: rows must be 16-byte aligned with a stride that is a multiple of 4");
+  float* down = nullptr;
+  if (fused && lora) {
+    LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(n_rows * rank) * sizeof(float)));
+    down = static_cast<float*>(ctx->proj.ptr);
+    LK_TRY(launch_xa_dense(ctx, aq, pr->d_model, rank, dev, n_rows, dev_ld, down));
+  }
+  const void* packed = fused ? static_cast<const char*>(pr->wq_packed) + (size_t)(layer * pr->d_model * dq) * 2 : nullptr;
+  const float* wq = fused ? nullptr : pr->wq + (size_t)(layer * pr->d_model * dq_full);
+  // the packed matrix already holds only this shard's columns: its column origin is 0, B_q keeps the full width
+  LK_TRY(launch_q_project(ctx, fused, packed, wq, dq_full, col0, pr->d_model, dq, pr->d_head, down, aq, bq, dq_full, rank, sc,
+                          pos_begin, dev, n_rows, dev_ld, rope != 0, q_dev));
+  if (host) {
+    LK_CUDA(cudaMemcpyAsync(q_out, q_dev, q_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   return LORAKV_OK;
 }
 

@@ -254,7 +254,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
 template <int RP, int MT>
 __global__ void __launch_bounds__(kMmaProjWarps * 32) lr_append_project_mma_kernel(
     PageAddr a, int64_t row0, const float* __restrict__ x, int64_t n_rows, int64_t ld, const uint4* __restrict__ frag,
-    int d_model, int rank) {
+    int d_model, int rank, float* __restrict__ dense) {
   constexpr int NT = RP / 8, ROWS = 16 * MT;
   __shared__ float red[kMmaProjWarps][ROWS][RP + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -328,6 +328,12 @@ __global__ void __launch_bounds__(kMmaProjWarps * 32) lr_append_project_mma_kern
 #pragma unroll
       for (int w = 0; w < kMmaProjWarps; ++w) sum += red[w][rr][c0 + u];
       v[u] = c0 + u < rank ? sum : 0.f;
+    }
+    if (dense != nullptr) {               // float32 rows [n_rows][rank] instead of pages (the q-LoRA down-projection)
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c0 + u < rank) dense[i_row * rank + c0 + u] = v[u];
+      continue;
     }
     const int64_t row = row0 + i_row;
     const int64_t phys = a.table[row / a.P];
@@ -423,7 +429,7 @@ int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, in
     const int total = (int)(d_model / 16) * nt * 32;
     lr_project_pack_a_kernel<<<(total + 255) / 256, 256, 0, ctx->stream>>>(A, (int)d_model, (int)rank, nt, frag);
     auto go = [&](auto kern, int rows) {
-      kern<<<(unsigned)((n_rows + rows - 1) / rows), kMmaProjWarps * 32, 0, ctx->stream>>>(a, row0, x_dev, n_rows, ld, frag, (int)d_model, (int)rank);
+      kern<<<(unsigned)((n_rows + rows - 1) / rows), kMmaProjWarps * 32, 0, ctx->stream>>>(a, row0, x_dev, n_rows, ld, frag, (int)d_model, (int)rank, nullptr);
     };
     switch (a.width) {
       case 8: go(lr_append_project_mma_kernel<8, 2>, 32); break;
@@ -450,6 +456,35 @@ int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, in
     default: return fail("lr_append_project: padded rank %d is not one of 16/32/64/128", a.width);
   }
   ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+// x * A as dense float32 rows [n_rows][rank] (tensor-core kernel above; bf16 X, A kept to fp32 accuracy): the q-LoRA
+// down-projection of engine.hpp:366-367
+int launch_xa_dense(lorakv_ctx* ctx, const float* a_dev, int64_t d_model, int64_t rank, const float* x_dev, int64_t n_rows, int64_t ld,
+                    float* out_dev) {
+  if (n_rows == 0 || rank == 0) return LORAKV_OK;
+  if (rank > 64 || d_model % 16 != 0 || ld % 4 != 0 || (reinterpret_cast<uintptr_t>(x_dev) & 15) != 0)
+    return fail("xa_dense: unsupported shape (rank %lld, d_model %lld)", (long long)rank, (long long)d_model);
+  const int rp = rank <= 8 ? 8 : rank <= 16 ? 16 : rank <= 32 ? 32 : 64;
+  const int nt = rp / 8;
+  const size_t frag_bytes = (size_t)(d_model / 16) * nt * 32 * sizeof(uint4);
+  LK_TRY(scratch_reserve(ctx, ctx->work, frag_bytes));
+  uint4* frag = static_cast<uint4*>(ctx->work.ptr);
+  const int total = (int)(d_model / 16) * nt * 32;
+  lr_project_pack_a_kernel<<<(total + 255) / 256, 256, 0, ctx->stream>>>(a_dev, (int)d_model, (int)rank, nt, frag);
+  PageAddr none{};
+  auto go = [&](auto kern, int rows) {
+    kern<<<(unsigned)((n_rows + rows - 1) / rows), kMmaProjWarps * 32, 0, ctx->stream>>>(none, 0, x_dev, n_rows, ld, frag, (int)d_model, (int)rank, out_dev);
+  };
+  switch (rp) {
+    case 8: go(lr_append_project_mma_kernel<8, 2>, 32); break;
+    case 16: go(lr_append_project_mma_kernel<16, 2>, 32); break;
+    case 32: go(lr_append_project_mma_kernel<32, 2>, 32); break;
+    default: go(lr_append_project_mma_kernel<64, 1>, 16); break;
+  }
+  ctx->launches += 2;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;
 }

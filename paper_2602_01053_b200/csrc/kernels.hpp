@@ -78,6 +78,14 @@ int launch_pack_w(lorakv_ctx* ctx, const float* w_dev, int64_t ldw, int64_t col0
 int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
                       int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope);
 
+int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const float* wq_dev, int64_t ldw, int64_t col0,
+                     int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev, const float* aq_dev, const float* bq_dev,
+                     int64_t ldb, int64_t rank, float q_scale, int64_t pos0, const float* x_dev, int64_t n_rows, int64_t ld, bool rope,
+                     float* q_dev);
+// cache_kernels.cu: x * A as dense float32 rows (tensor cores)
+int launch_xa_dense(lorakv_ctx* ctx, const float* a_dev, int64_t d_model, int64_t rank, const float* x_dev, int64_t n_rows, int64_t ld,
+                    float* out_dev);
+
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
                   int a_in_tmem, float* d);

@@ -119,12 +119,21 @@ struct ProjParams {
   int P, d_model, n_kv_local;
   int64_t row0, n_rows;        // first logical row of the call's rows; rows computed
   int64_t k_from, v_from;      // logical rows below these already exist in the K / V cache (first writer wins)
+  // query mode (kQuery): q = rope(x * Wq + q_scale * (x * A_q) * B_q[agent]) as float32 rows (engine.hpp:362-373, :422)
+  float* q_out;                // [n_rows][ldq]
+  int64_t ldq;
+  const float* down;           // x * A_q, [n_rows][r] float32, or null without adapters
+  const float* bq;             // B_q[agent] restricted to this shard's heads: [r][ldb]
+  int64_t ldb;
+  int r;
+  float q_scale;
 };
 
 struct ProjBarriers {
   uint64_t full[kStages], empty[kStages], acc_full;
 };
 
+template <bool kQuery>
 __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const ProjParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ ProjBarriers bars;
@@ -193,6 +202,50 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
     ptx::mbar_wait(&bars.acc_full, 0);
     ptx::tc_fence_after();
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    if constexpr (kQuery) {
+      // every 128-column block is one q head: add the LoRA up-projection, rotate, store float32 rows
+      const float* dn = (p.down != nullptr) ? p.down + (live ? i_row : 0) * p.r : nullptr;    // this row's x * A_q
+#pragma unroll 1
+      for (int hb = 0; hb < kBN / 128; ++hb) {
+        const int64_t col0 = (int64_t)(nblk * (kBN / 128) + hb) * 128;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t lo_u[32], hi_u[32];
+          ptx::tmem_ld32(tmem + lane_base + (uint32_t)(hb * 128 + c0), lo_u);
+          ptx::tmem_ld32(tmem + lane_base + (uint32_t)(hb * 128 + 64 + c0), hi_u);
+          ptx::tmem_wait_ld();
+          float lo[32], hi[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) { lo[i] = __uint_as_float(lo_u[i]); hi[i] = __uint_as_float(hi_u[i]); }
+          if (p.down != nullptr) {
+            for (int k = 0; k < p.r; ++k) {
+              const float* brow = p.bq + (int64_t)k * p.ldb + col0 + c0;     // the same address for the whole warp: broadcast
+              const float dk = p.q_scale * __ldg(dn + k);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) { lo[i] = fmaf(dk, __ldg(brow + i), lo[i]); hi[i] = fmaf(dk, __ldg(brow + 64 + i), hi[i]); }
+            }
+          }
+          if (p.rope != nullptr && live) {
+            const float2* tab = p.rope + i_row * 64 + c0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float2 cs = __ldg(tab + i);
+              const float x0 = lo[i], x1 = hi[i];
+              lo[i] = x0 * cs.x - x1 * cs.y;
+              hi[i] = x0 * cs.y + x1 * cs.x;
+            }
+          }
+          if (live) {
+            float* dst = p.q_out + i_row * p.ldq + col0 + c0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              *reinterpret_cast<float4*>(dst + i) = make_float4(lo[i], lo[i + 1], lo[i + 2], lo[i + 3]);
+              *reinterpret_cast<float4*>(dst + 64 + i) = make_float4(hi[i], hi[i + 1], hi[i + 2], hi[i + 3]);
+            }
+          }
+        }
+      }
+    } else {
     const int64_t phys = live ? p.table[row / p.P] : 0;
     const int t = (int)(row % p.P);
 #pragma unroll 1
@@ -238,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
           }
         }
       }
+    }
     }
   }
   ptx::tc_fence_before();
@@ -317,11 +371,12 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     pp.head_stride = pool->kv_head_stride(); pp.page_stride = pool->kv_page_stride();
     pp.P = (int)pool->P; pp.d_model = (int)d_model; pp.n_kv_local = (int)n_kv;
     pp.row0 = row0; pp.n_rows = n_rows; pp.k_from = k_from; pp.v_from = v_from;
+    pp.q_out = nullptr; pp.ldq = 0; pp.down = nullptr; pp.bq = nullptr; pp.ldb = 0; pp.r = 0; pp.q_scale = 0.f;
     const size_t smem = (size_t)kStages * kStageBytes + 1024;
-    LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const dim3 grid((unsigned)(2 * n_kv * d / kBN), (unsigned)tiles);
     prof_mark(ctx, 0);
-    kv_project_umma_kernel<<<grid, kThreads, smem, ctx->stream>>>(pp);
+    kv_project_umma_kernel<false><<<grid, kThreads, smem, ctx->stream>>>(pp);
     prof_mark(ctx, 1);
     ctx->launches++;
     LK_CUDA(cudaGetLastError());
@@ -357,6 +412,78 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     LK_TRY(launch_append_scatter(pool, LORAKV_VALUE, layer, set, row0 + skip, vbuf + skip * dkv, n_rows - skip, dkv));
   }
   ctx->last_kernel = "kv_project_f32";
+  return LORAKV_OK;
+}
+
+// ---- query projection: q = rope(x * Wq + scale * (x * A_q) * B_q[agent]) (engine.hpp:362-373, :422) -------------------
+__global__ void axpy_rn_kernel(float* __restrict__ y, const float* __restrict__ x, float a, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __fadd_rn(y[i], __fmul_rn(a, x[i]));       // q.data[i] += q_scale * q_up.data[i], engine.hpp:372
+}
+
+int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const float* wq_dev, int64_t ldw, int64_t col0,
+                     int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev, const float* aq_dev, const float* bq_dev,
+                     int64_t ldb, int64_t rank, float q_scale, int64_t pos0, const float* x_dev, int64_t n_rows, int64_t ld, bool rope,
+                     float* q_dev) {
+  if (n_rows == 0 || n_cols == 0) return LORAKV_OK;
+  const int64_t half = d_head / 2;
+  auto up = [](size_t x) { return (x + 1023) / 1024 * 1024; };
+  const size_t tab_bytes = rope ? up((size_t)(n_rows * half) * sizeof(float2)) : 0;
+  if (fused) {
+    const int64_t tiles = (n_rows + kBM - 1) / kBM;
+    const size_t xa_bytes = (size_t)tiles * kBM * d_model * 2;
+    LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + xa_bytes));
+    float2* tab = rope ? static_cast<float2*>(ctx->work.ptr) : nullptr;
+    __nv_bfloat16* xa = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ctx->work.ptr) + tab_bytes);
+    if (rope) {
+      const int64_t n = n_rows * half;
+      rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(pos0, n_rows, (int)d_head, tab);
+      ctx->launches++;
+    }
+    const int64_t nx = tiles * kBM * (d_model / 8);
+    pack_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, ctx->stream>>>(x_dev, n_rows, ld, (int)d_model, xa);
+    ctx->launches++;
+    ProjParams pp{};
+    pp.xa = xa; pp.wb = static_cast<const __nv_bfloat16*>(wq_packed); pp.rope = tab;
+    pp.d_model = (int)d_model; pp.row0 = pos0; pp.n_rows = n_rows; pp.P = 1; pp.n_kv_local = 0;
+    pp.q_out = q_dev; pp.ldq = n_cols; pp.down = rank > 0 ? down_dev : nullptr; pp.bq = bq_dev ? bq_dev + col0 : nullptr; pp.ldb = ldb;
+    pp.r = (int)rank; pp.q_scale = q_scale;
+    const size_t smem = (size_t)kStages * kStageBytes + 1024;
+    LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const dim3 grid((unsigned)(n_cols / kBN), (unsigned)tiles);
+    prof_mark(ctx, 0);
+    kv_project_umma_kernel<true><<<grid, kThreads, smem, ctx->stream>>>(pp);
+    prof_mark(ctx, 1);
+    ctx->launches++;
+    LK_CUDA(cudaGetLastError());
+    ctx->last_kernel = "q_project_umma";
+    return LORAKV_OK;
+  }
+  // exact fp32 path in the reference's order: q = x Wq; q_down = x A; q_up = q_down B; q += s * q_up; rope
+  const int64_t n = n_rows * n_cols;
+  const size_t up_bytes = rank > 0 ? up((size_t)n * sizeof(float)) + up((size_t)(n_rows * rank) * sizeof(float)) : 0;
+  LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + up_bytes));
+  char* base = static_cast<char*>(ctx->work.ptr);
+  float2* tab = rope ? reinterpret_cast<float2*>(base) : nullptr;
+  proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, wq_dev, ldw, col0, n_rows, (int)d_model, (int)n_cols, q_dev);
+  ctx->launches++;
+  if (rank > 0) {
+    float* qup = reinterpret_cast<float*>(base + tab_bytes);
+    float* qdown = reinterpret_cast<float*>(base + tab_bytes + up((size_t)n * sizeof(float)));
+    const int64_t nd = n_rows * rank;
+    proj_matmul_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, aq_dev, rank, 0, n_rows, (int)d_model, (int)rank, qdown);
+    proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(qdown, rank, bq_dev, ldb, col0, n_rows, (int)rank, (int)n_cols, qup);
+    axpy_rn_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(q_dev, qup, q_scale, n);
+    ctx->launches += 3;
+  }
+  if (rope) {
+    const int64_t nt = n_rows * half, nr = n_rows * (n_cols / d_head) * half;
+    rope_table_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, ctx->stream>>>(pos0, n_rows, (int)d_head, tab);
+    rope_rows_kernel<<<(unsigned)((nr + 255) / 256), 256, 0, ctx->stream>>>(q_dev, n_rows, (int)(n_cols / d_head), (int)d_head, tab);
+    ctx->launches += 2;
+  }
+  LK_CUDA(cudaGetLastError());
+  ctx->last_kernel = "q_project_f32";
   return LORAKV_OK;
 }
 

@@ -52,6 +52,7 @@ struct lorakv_ctx {
   int policy = 0;
   const char* last_kernel = "none";
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
+  lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection
   void* pinned = nullptr;             // small pinned staging buffer
   size_t pinned_bytes = 0;
   bool profiling = false;             // bracket the dominant kernel of fast-path calls with events
@@ -140,4 +141,13 @@ struct lorakv_proj {
   float* wk = nullptr;       // [n_layers][d_model][n_kv_heads * d_head] float32 (exact path only)
   float* wv = nullptr;
   std::vector<uint8_t> set;
+  // query projection (engine.hpp:362-373): Wq, the shared q-LoRA down-projection and per-agent up-projections
+  int64_t n_q_heads = 0, q_rank = 0, q_agents = 0;
+  bool q_fused = false;
+  void* wq_packed = nullptr; // [n_layers][n_q_local * d_head / 64 blocks][d_model][64] bf16
+  float* wq = nullptr;       // [n_layers][d_model][n_q_heads * d_head] float32 (exact path only)
+  float* aq = nullptr;       // [n_layers][d_model][q_rank]
+  float* bq = nullptr;       // [n_layers][q_agents][q_rank][n_q_heads * d_head]
+  std::vector<float> q_scale;          // [n_layers][q_agents] alpha / rank
+  std::vector<uint8_t> q_set, q_lora_set;
 };

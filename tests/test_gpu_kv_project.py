@@ -132,3 +132,58 @@ def test_projection_errors(ctx, orc):
     with pytest.raises(LorakvError, match="do not match"):
         pool.append_kv_project(other, 0, 0, 0, x)
     pool.close(); proj.close(); other.close()
+
+
+def reference_q(orc, x, wq, a, b, alpha, n_q, d, pos, rope):
+    """engine.hpp:362-373, :422"""
+    q = orc.matmul(x, wq)
+    if a is not None:
+        q = q + np.float32(alpha / a.shape[1]) * orc.matmul(orc.matmul(x, a), b)
+    return orc.apply_rope(q, n_q, d, pos) if rope else q
+
+
+@pytest.mark.parametrize("L,d_model,n_q,n_kv,r,pos,rope,shard", [
+    (200, 256, 8, 2, 16, 37, True, None),
+    (130, 192, 4, 2, 8, 0, True, None),
+    (300, 512, 16, 4, 64, 1000, True, (2, 2)),      # this shard holds kv heads 2..3 -> q heads 8..15
+    (77, 128, 4, 1, 2, 5, False, None),
+])
+def test_query_projection_with_q_lora_and_rope_bf16(ctx, orc, L, d_model, n_q, n_kv, r, pos, rope, shard):
+    """q = rope(x Wq + (alpha/r) (x A_q) B_q[agent]) on the tcgen05 kernel (bf16 operands, fp32 accumulation and output)."""
+    from paper_2602_01053_b200 import Projection, abi
+    d, A = 128, 2
+    x = orc.round_bf16(orc.gaussian(L, d_model, orc.child(L, 1), 1.0, np.float32))
+    wq = orc.round_bf16(orc.gaussian(d_model, n_q * d, orc.child(L, 2), 1.0 / np.sqrt(d_model), np.float32))
+    a = orc.round_bf16(orc.gaussian(d_model, r, orc.child(L, 3), 1.0 / np.sqrt(d_model), np.float32))
+    b = [orc.round_bf16(orc.gaussian(r, n_q * d, orc.child(L, 10 + i), 0.02 / np.sqrt(r), np.float32)) for i in range(A)]
+    kb, kn = shard if shard else (0, n_kv)
+    proj = Projection(ctx, 1, d_model, n_kv, d, kv_head_begin=kb, n_kv_local=kn, dtype=abi.BF16)
+    proj.set_q(0, n_q, wq)
+    for i in range(A):
+        proj.set_q_lora(0, i, A, a, b[i], 16.0)
+    g = n_q // n_kv
+    cols = slice(kb * g * d, (kb + kn) * g * d)
+    for agent in (1, -1):
+        got = proj.query(0, agent, pos, x, kn * g * d, rope=rope)
+        assert ctx.last_kernel() == "q_project_umma"
+        want = reference_q(orc, x, wq, a if agent >= 0 else None, b[agent] if agent >= 0 else None, 16.0, n_q, d, pos, rope)[:, cols]
+        assert orc.max_rel_error(got, want) <= 1e-4, agent
+    proj.close()
+
+
+def test_query_projection_fp32_is_the_reference_order(ctx, orc):
+    from paper_2602_01053_b200 import Projection, abi
+    L, d_model, n_q, n_kv, d, r = 90, 96, 4, 2, 32, 4
+    x = orc.gaussian(L, d_model, 1, 1.0, np.float32)
+    wq = orc.gaussian(d_model, n_q * d, 2, 1.0 / np.sqrt(d_model), np.float32)
+    a = orc.gaussian(d_model, r, 3, 1.0 / np.sqrt(d_model), np.float32)
+    b = orc.gaussian(r, n_q * d, 4, 0.02 / np.sqrt(r), np.float32)
+    proj = Projection(ctx, 1, d_model, n_kv, d, dtype=abi.F32)
+    proj.set_q(0, n_q, wq)
+    proj.set_q_lora(0, 0, 1, a, b, 16.0)
+    got = proj.query(0, 0, 11, x, n_q * d, rope=False)
+    assert ctx.last_kernel() == "q_project_f32"
+    assert np.array_equal(got, reference_q(orc, x, wq, a, b, 16.0, n_q, d, 11, False))        # bit for bit
+    got = proj.query(0, 0, 11, x, n_q * d, rope=True)
+    assert orc.max_rel_error(got, reference_q(orc, x, wq, a, b, 16.0, n_q, d, 11, True)) <= 1e-6
+    proj.close()

@@ -298,7 +298,20 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
         res["kv_project_ms"] = k0e.elapsed_ms(k1e) / 3
         res["kv_project_tflops"] = 2 * L_c * d_model * 2 * n_kv * d / (res["kv_project_ms"] * 1e-3) / 1e12
         res["kv_project_kernel"] = ctx.last_kernel()
-        res["ttft_ms_per_layer"] = attn_ms + res["xa_project_ms"] + res["kv_project_ms"]
+        # query projection with q-LoRA and RoPE of the same rows (engine.hpp:362-373, :422)
+        pj.set_q(0, n_q, (wrng.standard_normal((d_model, n_q * d)) / np.sqrt(d_model)).astype(np.float32))
+        if r > 0:
+            pj.set_q_lora(0, 0, 1, (wrng.standard_normal((d_model, r)) / np.sqrt(d_model)).astype(np.float32),
+                          (wrng.standard_normal((r, n_q * d)) * (0.02 / np.sqrt(r))).astype(np.float32), 16.0)
+        pj.query_device(0, 0 if r > 0 else -1, L - L_c, x.data_ptr(), L_c, d_model, q.data_ptr())      # warm-up
+        q0e, q1e = ctx.event(), ctx.event()
+        q0e.record()
+        for i in range(3):
+            pj.query_device(0, 0 if r > 0 else -1, L - L_c, x.data_ptr(), L_c, d_model, q.data_ptr())
+        q1e.record()
+        res["q_project_ms"] = q0e.elapsed_ms(q1e) / 3
+        res["q_project_tflops"] = 2 * L_c * d_model * n_q * d / (res["q_project_ms"] * 1e-3) / 1e12
+        res["ttft_ms_per_layer"] = attn_ms + res["xa_project_ms"] + res["kv_project_ms"] + res["q_project_ms"]
         pj.close()
         sp.close(); sa.close()
     except Exception as e:

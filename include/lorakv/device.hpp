@@ -108,11 +108,33 @@ class ProjectionTable {
       fail("ProjectionTable: wk is " + shape_str(wk.rows, wk.cols) + " but wv is " + shape_str(wv.rows, wv.cols));
     b200::check(lorakv_proj_set_kv(h_, layer, wk.data.data(), wv.data.data()));
   }
+  // query side (engine.hpp LayerWeights::wq, q_lora): wq d_model x d_model; shared-A adapters of every agent
+  void set_query_layer(idx layer, idx n_q_heads, const Matrix<float>& wq, const MultiLoraSet<float>* q_lora = nullptr) {
+    b200::check(lorakv_proj_set_q(h_, layer, n_q_heads, wq.data.data()));
+    n_q_cols_ = wq.cols;
+    if (q_lora)
+      for (idx a = 0; a < q_lora->num_agents(); ++a) {
+        const LoraAdapter<float>& ad = q_lora->adapter(a);
+        b200::check(lorakv_proj_set_q_lora(h_, layer, a, q_lora->num_agents(), ad.rank, ad.a.data.data(), ad.b.data.data(), ad.alpha));
+      }
+  }
   lorakv_proj* handle() const { return h_; }
+  idx n_q_cols() const { return n_q_cols_; }
 
  private:
   lorakv_proj* h_ = nullptr;
+  idx n_q_cols_ = 0;
 };
+
+// q = rope(x Wq + (alpha/rank) (x A_q) B_q[agent]) for rows at positions [pos_begin, pos_begin + x.rows)
+// (engine.hpp:362-373, :422); agent < 0 skips the adapter.  n_q_local_cols = columns of the store's q-head shard.
+inline Matrix<float> project_query(const ProjectionTable& weights, idx layer, idx agent, idx pos_begin, Span2D<const float> x,
+                                   idx n_q_local_cols, bool rope = true) {
+  Matrix<float> q(x.rows, n_q_local_cols);
+  b200::check(lorakv_proj_query(weights.handle(), layer, agent, pos_begin, x.data, x.rows, x.stride, rope ? 1 : 0, q.data.data(),
+                                LORAKV_HOST));
+  return q;
+}
 
 // K / V_base projection of new context rows, rotation of the keys and the append, in one device pass;
 // returns the rows actually appended (first writer wins)

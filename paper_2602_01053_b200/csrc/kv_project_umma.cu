@@ -205,6 +205,17 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
     if constexpr (kQuery) {
       // every 128-column block is one q head: add the LoRA up-projection, rotate, store float32 rows
       const float* dn = (p.down != nullptr) ? p.down + (live ? i_row : 0) * p.r : nullptr;    // this row's x * A_q
+      // B_q[agent][:, the 256 columns of this CTA] -> shared memory (the operand stages are idle once acc_full has
+      // fired): the up-projection then reads broadcast float4s instead of 2 * r global loads per element
+      float* bq_s = reinterpret_cast<float*>(smem);
+      if (p.down != nullptr) {
+        const int et = tid - 64;                                   // 0..127 over the four epilogue warps
+        for (int idx = et; idx < p.r * (kBN / 4); idx += 128) {
+          const int k = idx / (kBN / 4), c4 = idx % (kBN / 4);
+          reinterpret_cast<float4*>(bq_s)[idx] = __ldg(reinterpret_cast<const float4*>(p.bq + (int64_t)k * p.ldb + (int64_t)nblk * kBN) + c4);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
 #pragma unroll 1
       for (int hb = 0; hb < kBN / 128; ++hb) {
         const int64_t col0 = (int64_t)(nblk * (kBN / 128) + hb) * 128;
@@ -219,10 +230,16 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
           for (int i = 0; i < 32; ++i) { lo[i] = __uint_as_float(lo_u[i]); hi[i] = __uint_as_float(hi_u[i]); }
           if (p.down != nullptr) {
             for (int k = 0; k < p.r; ++k) {
-              const float* brow = p.bq + (int64_t)k * p.ldb + col0 + c0;     // the same address for the whole warp: broadcast
+              const float4* brow = reinterpret_cast<const float4*>(bq_s + k * kBN + hb * 128 + c0);   // same address in every lane: broadcast
               const float dk = p.q_scale * __ldg(dn + k);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) { lo[i] = fmaf(dk, __ldg(brow + i), lo[i]); hi[i] = fmaf(dk, __ldg(brow + 64 + i), hi[i]); }
+              for (int i = 0; i < 8; ++i) {
+                const float4 bl = brow[i], bh = brow[16 + i];
+                lo[4 * i] = fmaf(dk, bl.x, lo[4 * i]); lo[4 * i + 1] = fmaf(dk, bl.y, lo[4 * i + 1]);
+                lo[4 * i + 2] = fmaf(dk, bl.z, lo[4 * i + 2]); lo[4 * i + 3] = fmaf(dk, bl.w, lo[4 * i + 3]);
+                hi[4 * i] = fmaf(dk, bh.x, hi[4 * i]); hi[4 * i + 1] = fmaf(dk, bh.y, hi[4 * i + 1]);
+                hi[4 * i + 2] = fmaf(dk, bh.z, hi[4 * i + 2]); hi[4 * i + 3] = fmaf(dk, bh.w, hi[4 * i + 3]);
+              }
             }
           }
           if (p.rope != nullptr && live) {

@@ -125,3 +125,24 @@ TEST_CASE("append_kv_project == append_key(rope(x Wk)), append_value(x Wv) on bf
     CHECK(threw);
   }
 }
+
+TEST_CASE("project_query == rope(x Wq + s (x A_q) B_q[agent]) through the drop-in header") {
+  const idx L = 70, d_model = 128, n_q = 4, n_kv = 2, d = 128, r = 8, agents = 2;
+  KvStore<float> store(CacheScheme{SchemeKind::FullShared, {}}, StoreDims{1, n_kv * d, d_model, 0, agents}, DeviceOptions{n_kv, L, true});
+  ProjectionTable weights(store);
+  auto rnd = [](Matrix<float> m) { return oracle::round_bf16(m); };
+  const Matrix<float> x = rnd(Matrix<float>::gaussian(L, d_model, Rng(15), 1.0));
+  const Matrix<float> wq = rnd(Matrix<float>::gaussian(d_model, n_q * d, Rng(16), 1.0 / std::sqrt(double(d_model))));
+  const Matrix<float> a = rnd(Matrix<float>::gaussian(d_model, r, Rng(17), 1.0 / std::sqrt(double(d_model))));
+  std::vector<LoraAdapter<float>> ads;
+  for (idx i = 0; i < agents; ++i)
+    ads.emplace_back(a, rnd(Matrix<float>::gaussian(r, n_q * d, Rng(18 + std::uint64_t(i)), 0.02 / std::sqrt(double(r)))), r, 16.0);
+  const MultiLoraSet<float> set(wq, ads, /*shared_a=*/true);
+  weights.set_query_layer(0, n_q, wq, &set);
+  const Matrix<float> got = project_query(weights, 0, 1, 9, x.view(), n_q * d);
+  Matrix<float> want = oracle::matmul(x, wq);
+  const Matrix<float> upm = oracle::matmul(oracle::matmul(x, a), ads[1].b);
+  for (std::size_t i = 0; i < want.data.size(); ++i) want.data[i] += float(16.0 / double(r)) * upm.data[i];
+  oracle::ok(orc_apply_rope_f32(want.data.data(), L, n_q * d, n_q, d, 9));
+  CHECK_LE(max_rel_error(got, want), 1e-4);
+}

@@ -196,6 +196,24 @@ class KvStore {
   // HBM actually reserved for pages (capacity, not occupancy)
   std::uint64_t reserved_bytes() const { return lorakv_pool_reserved_bytes(pool_); }
 
+  // The reference's snapshot container (kvcache.hpp:438-546 of the reference), written from / read into HBM pages.
+  // load_snapshot needs the device options a snapshot does not carry (head split, capacity, storage dtype).
+  void save_snapshot(const std::string& path) const {
+    b200::check(lorakv_pool_save_snapshot(pool_, path.c_str(), tokens_.data(), static_cast<idx>(tokens_.size())));
+  }
+  static KvStore load_snapshot(const std::string& path, DeviceOptions opt = DeviceOptions{}) {
+    lorakv_pool* pool = nullptr;
+    std::int64_t n_tokens = 0;
+    std::vector<std::int32_t> tokens(static_cast<std::size_t>(1) << 20);
+    b200::check(lorakv_pool_load_snapshot(b200::Runtime::ctx(), path.c_str(), opt.bf16 ? LORAKV_BF16 : LORAKV_F32, opt.n_kv_heads,
+                                          opt.page_tokens, opt.max_tokens, &pool, tokens.data(), static_cast<idx>(tokens.size()),
+                                          &n_tokens));
+    tokens.resize(static_cast<std::size_t>(std::min<std::int64_t>(n_tokens, static_cast<std::int64_t>(tokens.size()))));
+    lorakv_pool_dims pd{};
+    b200::check(lorakv_pool_dims_get(pool, &pd));
+    return KvStore(pool, pd, opt, std::move(tokens));
+  }
+
   // logical page -> physical page of the page set (which, agent) resolves to
   std::vector<std::int32_t> page_table(int which, idx agent) const {
     std::int64_t n = 0;
@@ -206,6 +224,12 @@ class KvStore {
   }
 
  private:
+  KvStore(lorakv_pool* pool, const lorakv_pool_dims& pd, DeviceOptions opt, std::vector<std::int32_t> tokens)
+      : scheme_{static_cast<SchemeKind>(pd.scheme), {}}, dims_{pd.n_layers, pd.n_kv_heads * pd.d_head, pd.d_model, pd.rank, pd.n_agents},
+        opt_(opt), pool_(pool), tokens_(std::move(tokens)) {
+    opt_.page_tokens = pd.page_tokens; opt_.max_tokens = pd.max_tokens;
+  }
+
   void append(int which, idx layer, idx agent, idx row_begin, Span2D<const T> rows) {
     const idx want = which == LORAKV_LR ? dims_.rank : dims_.d_kv;
     const bool has_buffer = which != LORAKV_LR || scheme_.kind == SchemeKind::BaseShared || scheme_.kind == SchemeKind::BaseLRShared;

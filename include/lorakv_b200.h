@@ -213,6 +213,17 @@ int lorakv_proj_query(lorakv_proj* proj, int64_t layer, int64_t agent, int64_t p
 int lorakv_pool_append_kv_project(lorakv_pool* pool, const lorakv_proj* proj, int64_t layer,
                                   int64_t agent, int64_t row_begin, const float* x, int64_t n_rows,
                                   int64_t ld, int mem_kind, int rope, int64_t* appended);
+/* ---- snapshot / resume --------------------------------------------------------
+ * KvStore::save_snapshot / load_snapshot (kvcache.hpp:438-546): the reference's "lorakv-cache-snapshot" v1
+ * container, written from / read into the paged pool; dtype "f32" (bf16 pools de-paginate exactly).  A pool
+ * holding the same state as a reference KvStore<float> writes the reference's file byte for byte.  The token
+ * ids of the trajectory are the caller's (the pool keeps only their count); load returns them in tokens_out
+ * (up to tokens_cap) and their number in *n_tokens (both may be NULL).  n_kv_heads / page_tokens / max_tokens /
+ * dtype are the device options a snapshot does not carry. */
+int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const int32_t* tokens, int64_t n_tokens);
+int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int64_t n_kv_heads,
+                              int64_t page_tokens, int64_t max_tokens, lorakv_pool** out,
+                              int32_t* tokens_out, int64_t tokens_cap, int64_t* n_tokens);
 /* rows currently materialised in the buffer (layer, agent) resolves to (GrowMat::rows) */
 int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows);
 /* key_view / value_view / lr_view, :307-324: de-paginate rows [row_begin, row_begin+n_rows) into a

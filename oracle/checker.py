@@ -109,6 +109,9 @@ class Checker:
           C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64))
         f("store_bytes", None, C.c_void_p, C.POINTER(C.c_uint64))
         f("store_allocated_elements", C.c_uint64, C.c_void_p)
+        if prefix == "ref_":
+            f("store_save_snapshot", C.c_int, C.c_void_p, C.c_char_p)
+            f("store_load_snapshot", C.c_void_p, C.c_char_p, C.c_int)
         if prefix == "orc_":
             f("append_fww", C.c_int, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int64),
               C.POINTER(C.c_int64))

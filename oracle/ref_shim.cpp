@@ -290,6 +290,21 @@ uint64_t ref_store_allocated_elements(const ref_store* s) {
 }
 
 
+// KvStore::save_snapshot / load_snapshot (kvcache.hpp:438-546): the reference's own writer and reader
+int ref_store_save_snapshot(const ref_store* s, const char* path) {
+  return guarded([&] { if (s->elem == 4) s->f->save_snapshot(path); else s->d->save_snapshot(path); });
+}
+ref_store* ref_store_load_snapshot(const char* path, int elem_size) {
+  ref_store* s = nullptr;
+  const int rc = guarded([&] {
+    s = new ref_store{elem_size, nullptr, nullptr};
+    if (elem_size == 4) s->f = new KvStore<float>(KvStore<float>::load_snapshot(path));
+    else s->d = new KvStore<double>(KvStore<double>::load_snapshot(path));
+  });
+  if (rc != ORC_OK) { delete s; return nullptr; }
+  return s;
+}
+
 // detail::apply_rope (engine.hpp:225-243) on a strided row-major matrix, in place
 #define REF_ROPE(SUF, T)                                                                                  \
   int ref_apply_rope_##SUF(T* m, int64_t rows, int64_t stride, int64_t n_heads, int64_t d_head,           \

@@ -102,6 +102,9 @@ SIGNATURES = {
     "lorakv_pool_plan_step": (C.c_int, [_vp, _i64, _i64, C.POINTER(_i64)]),
     "lorakv_pool_append": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.POINTER(_i64)]),
     "lorakv_pool_append_lr_project": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.POINTER(_i64)]),
+    "lorakv_pool_save_snapshot": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_int32), _i64]),
+    "lorakv_pool_load_snapshot": (C.c_int, [_vp, C.c_char_p, C.c_int, _i64, _i64, _i64, C.POINTER(_vp), C.POINTER(C.c_int32), _i64,
+                                            C.POINTER(_i64)]),
     "lorakv_proj_create": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "lorakv_proj_destroy": (None, [_vp]),
     "lorakv_proj_set_kv": (C.c_int, [_vp, _i64, _pf, _pf]),
@@ -475,6 +478,27 @@ class Pool:
         got = PoolDims()
         _check(ctx.lib.lorakv_pool_dims_get(h, C.byref(got)))
         self.dims = got
+
+    @classmethod
+    def load_snapshot(cls, ctx: Context, path, n_kv_heads, dtype=F32, page_tokens=0, max_tokens=0):
+        """KvStore::load_snapshot (kvcache.hpp:472-521) into a new pool; returns (pool, token ids)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        h, n = _vp(), _i64()
+        cap = 1 << 20
+        toks = (C.c_int32 * cap)()
+        _check(ctx.lib.lorakv_pool_load_snapshot(ctx.h, str(path).encode(), dtype, n_kv_heads, page_tokens, max_tokens,
+                                                 C.byref(h), toks, cap, C.byref(n)))
+        self.h = h
+        got = PoolDims()
+        _check(ctx.lib.lorakv_pool_dims_get(h, C.byref(got)))
+        self.dims = got
+        return self, list(toks[:min(n.value, cap)])
+
+    def save_snapshot(self, path, tokens):
+        """KvStore::save_snapshot (kvcache.hpp:438-470); tokens = the trajectory's token ids."""
+        arr = (C.c_int32 * len(tokens))(*tokens)
+        _check(self.ctx.lib.lorakv_pool_save_snapshot(self.h, str(path).encode(), arr, len(tokens)))
 
     def close(self):
         if getattr(self, "h", None):

@@ -43,3 +43,35 @@ def synthetic_layer(chk, seed, L, L_c, n_q, n_kv, d, r, n_agents, dtype=np.float
          for a in range(n_agents)]
     lr_scale = 16.0 / r if r > 0 else 1.0
     return q, k, v, v_lr, b, lr_scale
+
+
+# ---- snapshot fixtures (kvcache.hpp:438-546): one small caught-up store per scheme, values are small integers so
+# that fp32 and bf16 pools hold them exactly (the pattern of tests/test_kvcache.cpp fill_rows / fill_caught_up) ----
+SNAPSHOT_DIMS = dict(n_layers=2, d_kv=16, d_model=16, rank=2, n_agents=3, n_kv_heads=2, L=9)
+SNAPSHOT_SCHEMES = ["NonShared", "FullShared", "BaseShared", "BaseLRShared"]
+
+
+def snapshot_rows(kind, layer, agent, L, cols):
+    """kind 0 key, 1 value, 2 lr"""
+    i = np.arange(L)[:, None]; j = np.arange(cols)[None, :]
+    v = (i * 17 + j * 3 + 1000 * layer + 7 * agent + 50 * kind) % 251 - 100
+    return v.astype(np.float32)
+
+
+def snapshot_fill(store_like, scheme):
+    """Drive any object with append_tokens / append_key / append_value / append_lr / mark_seen the same way."""
+    d = SNAPSHOT_DIMS
+    L = d["L"]
+    store_like.append_tokens(L)
+    kv_agents = range(d["n_agents"]) if scheme == "NonShared" else [0]
+    for layer in range(d["n_layers"]):
+        for a in kv_agents:
+            store_like.append_key(layer, a, 0, snapshot_rows(0, layer, a, L, d["d_kv"]))
+            store_like.append_value(layer, a, 0, snapshot_rows(1, layer, a, L, d["d_kv"]))
+        if scheme == "BaseShared":
+            for a in range(d["n_agents"]):
+                store_like.append_lr(layer, a, 0, snapshot_rows(2, layer, a, L - a, d["rank"]))     # ragged LR prefills
+        elif scheme == "BaseLRShared":
+            store_like.append_lr(layer, 0, 0, snapshot_rows(2, layer, 0, L, d["rank"]))
+    store_like.mark_seen(0)
+    store_like.mark_seen(2)

@@ -5,6 +5,11 @@
 #include <cstdint>
 #include <vector>
 
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <iterator>
+
 #include "check.hpp"
 #include "lorakv/kvcache.hpp"
 #include "oracle_glue.hpp"
@@ -162,4 +167,48 @@ TEST_CASE("pages are handed out in first-touch order (logical row -> row / P, ro
   CHECK(st.page_table(LORAKV_KEY, 1) == (std::vector<std::int32_t>{0, 1, 5}));
   CHECK(st.page_table(LORAKV_KEY, 0) == (std::vector<std::int32_t>{2, 3, 4}));
   CHECK(same(st.key_view(0, 0), b));
+}
+
+// test_kvcache.cpp:279-305 of the reference: a snapshot round-trips bit-exactly and re-dumps identically
+TEST_CASE("snapshot round-trips bit-exactly and re-dumps identically (paged store)") {
+  for (SchemeKind kind : {SchemeKind::NonShared, SchemeKind::FullShared, SchemeKind::BaseShared, SchemeKind::BaseLRShared}) {
+    for (int bf16 = 0; bf16 < 2; ++bf16) {
+      const idx L = 9, n_layers = 2, d_kv = 16, rank = 2, n_agents = 3;
+      KvStore<float> store(CacheScheme{kind, {}}, StoreDims{n_layers, d_kv, 16, rank, n_agents}, DeviceOptions{2, 32, bf16 != 0, 8});
+      store.append_tokens(std::vector<std::int32_t>(static_cast<std::size_t>(L), 7));
+      auto rows = [](idx n, idx cols, double base) {
+        Matrix<float> m(n, cols);
+        for (idx i = 0; i < n; ++i) for (idx j = 0; j < cols; ++j) m(i, j) = float(std::fmod(base + double(i * cols + j), 200.0) - 100.0);
+        return m;
+      };
+      for (idx l = 0; l < n_layers; ++l) {
+        for (idx a = 0; a < (kind == SchemeKind::NonShared ? n_agents : 1); ++a) {
+          store.append_key(l, a, 0, rows(L, d_kv, 10.0 * double(l) + double(a)).view());
+          store.append_value(l, a, 0, rows(L, d_kv, 50.0 + 10.0 * double(l) + double(a)).view());
+        }
+        if (kind == SchemeKind::BaseShared) for (idx a = 0; a < n_agents; ++a) store.append_lr(l, a, 0, rows(L - a, rank, 3.0 * double(a)).view());
+        if (kind == SchemeKind::BaseLRShared) store.append_lr(l, 0, 0, rows(L, rank, 5.0).view());
+      }
+      store.mark_seen(1);
+      const std::string path = "/tmp/lorakv_b200_snapshot_test.bin", path2 = path + ".again";
+      store.save_snapshot(path);
+      KvStore<float> loaded = KvStore<float>::load_snapshot(path, DeviceOptions{2, 64, bf16 != 0, 16});
+      CHECK(loaded.length() == store.length());
+      CHECK(loaded.tokens() == store.tokens());
+      CHECK(loaded.seen(1) == L); CHECK(loaded.seen(0) == 0);
+      CHECK(loaded.bytes().total() == store.bytes().total());
+      for (idx l = 0; l < n_layers; ++l) {
+        const Span2D<const float> a = store.key_view(l, 0), b = loaded.key_view(l, 0);
+        REQUIRE(a.rows == b.rows); REQUIRE(a.cols == b.cols);
+        for (idx i = 0; i < a.rows; ++i) for (idx j = 0; j < a.cols; ++j) REQUIRE(a(i, j) == b(i, j));
+      }
+      loaded.save_snapshot(path2);
+      std::ifstream f1(path, std::ios::binary), f2(path2, std::ios::binary);
+      const std::string b1((std::istreambuf_iterator<char>(f1)), std::istreambuf_iterator<char>());
+      const std::string b2((std::istreambuf_iterator<char>(f2)), std::istreambuf_iterator<char>());
+      CHECK(b1 == b2);
+      CHECK(b1.size() > 8);
+      std::remove(path.c_str()); std::remove(path2.c_str());
+    }
+  }
 }

@@ -248,10 +248,16 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
     pairs = L_c * off + L_c * (L_c + 1) // 2
     flops = 2 * n_q * pairs * (2 * d + r) + 2 * n_q * L_c * r * d
     peak, peak_src = load_tensor_peak()
+    traffic = None
+    try:   # DRAM bytes of one launch from the committed `ncu --set full` capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"cfg3_{args.dtype}_{kernel}")
+    except Exception:
+        pass
     res = {"workload": "cfg3", "L_c": L_c, "query_offset": off, "attention_ms_per_layer": attn_ms,
            "attention_tflops": flops / (attn_ms * 1e-3) / 1e12, "algorithmic_flops": flops, "kernel": kernel,
            "roofline": {"bound": "tensor", "achieved": flops / (attn_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
-                        "frac": flops / (attn_ms * 1e-3) / 1e12 / peak, "peak_source": peak_src}}
+                        "frac": flops / (attn_ms * 1e-3) / 1e12 / peak, "traffic": traffic, "peak_source": peak_src}}
     # parity: a seeded sample of query rows against the reference CPU path (rows via L_c = 1)
     if not args.no_cpu_baseline:
         from oracle import checker

@@ -709,11 +709,7 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.L = c.L; dp.layer_begin = c.layer_begin; dp.n_q_local = c.n_q_local;
   dp.T = T; dp.total_tiles = total; dp.G = G; dp.max_seg = max_seg; dp.n_stages = n_stages;
   dp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
-  {
-    const char* env = getenv("LORAKV_DECODE_L2_HINT");   // experiment knob: 0 = no hint, 1 = evict_first (default), 2 = evict_last
-    const int mode = env ? atoi(env) : 1;
-    dp.l2_policy = mode == 1 ? ptx::kEvictFirst : mode == 2 ? ptx::kEvictLast : 0;
-  }
+  dp.l2_policy = ptx::kEvictFirst;      // the cache is streamed once per step: do not let it push the partials and q out of L2
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));

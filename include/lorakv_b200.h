@@ -224,6 +224,12 @@ int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const i
 int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int64_t n_kv_heads,
                               int64_t page_tokens, int64_t max_tokens, lorakv_pool** out,
                               int32_t* tokens_out, int64_t tokens_cap, int64_t* n_tokens);
+/* The "full values" variant of engine.hpp:385-393 (NonShared, FullShared): the stored value rows are
+ * v_base + (alpha/rank) * ((x * A_v) * B_v[agent]) with A_v, B_v, alpha from the adapter table. */
+int lorakv_pool_append_kv_project_full(lorakv_pool* pool, const lorakv_proj* proj,
+                                       const lorakv_adapters* adapters, int64_t layer, int64_t agent,
+                                       int64_t row_begin, const float* x, int64_t n_rows, int64_t ld,
+                                       int mem_kind, int rope, int64_t* appended);
 /* rows currently materialised in the buffer (layer, agent) resolves to (GrowMat::rows) */
 int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows);
 /* key_view / value_view / lr_view, :307-324: de-paginate rows [row_begin, row_begin+n_rows) into a

@@ -105,6 +105,7 @@ SIGNATURES = {
     "lorakv_pool_save_snapshot": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_int32), _i64]),
     "lorakv_pool_load_snapshot": (C.c_int, [_vp, C.c_char_p, C.c_int, _i64, _i64, _i64, C.POINTER(_vp), C.POINTER(C.c_int32), _i64,
                                             C.POINTER(_i64)]),
+    "lorakv_pool_append_kv_project_full": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, C.c_int, C.POINTER(_i64)]),
     "lorakv_proj_create": (C.c_int, [_vp, _i64, _i64, _i64, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "lorakv_proj_destroy": (None, [_vp]),
     "lorakv_proj_set_kv": (C.c_int, [_vp, _i64, _pf, _pf]),
@@ -572,8 +573,15 @@ class Pool:
         return added.value
 
     def append_kv_project(self, proj: "Projection", layer, agent, row_begin, x=None, rope=True, dev_ptr=None,
-                          n_rows=None, ld=None):
+                          n_rows=None, ld=None, merge: "Adapters" = None):
         added = _i64()
+        if merge is not None:        # "full values": V rows carry the agent's LoRA contribution (engine.hpp:385-393)
+            x = np.asarray(x, dtype=np.float32)
+            ptr, ld_ = _span(x, _f)
+            _check(self.ctx.lib.lorakv_pool_append_kv_project_full(self.h, proj.h, merge.h, layer, agent, row_begin,
+                                                                   C.cast(ptr, _vp), x.shape[0], ld_, HOST, int(rope),
+                                                                   C.byref(added)))
+            return added.value
         if dev_ptr is None:
             x = np.asarray(x, dtype=np.float32)
             ptr, ld_ = _span(x, _f)

@@ -722,8 +722,25 @@ int lorakv_proj_query(lorakv_proj* pr, int64_t layer, int64_t agent, int64_t pos
   return LORAKV_OK;
 }
 
+static int append_kv_project_impl(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_adapters* merge, int64_t layer, int64_t agent,
+                                  int64_t row_begin, const float* x, int64_t n_rows, int64_t ld, int mem_kind, int rope,
+                                  int64_t* appended);
+
 int lorakv_pool_append_kv_project(lorakv_pool* pool, const lorakv_proj* pr, int64_t layer, int64_t agent, int64_t row_begin,
                                   const float* x, int64_t n_rows, int64_t ld, int mem_kind, int rope, int64_t* appended) {
+  return append_kv_project_impl(pool, pr, nullptr, layer, agent, row_begin, x, n_rows, ld, mem_kind, rope, appended);
+}
+
+int lorakv_pool_append_kv_project_full(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_adapters* ad, int64_t layer,
+                                       int64_t agent, int64_t row_begin, const float* x, int64_t n_rows, int64_t ld,
+                                       int mem_kind, int rope, int64_t* appended) {
+  if (!ad) return fail("append_kv_project_full: null adapter table");
+  return append_kv_project_impl(pool, pr, ad, layer, agent, row_begin, x, n_rows, ld, mem_kind, rope, appended);
+}
+
+static int append_kv_project_impl(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_adapters* merge, int64_t layer, int64_t agent,
+                                  int64_t row_begin, const float* x, int64_t n_rows, int64_t ld, int mem_kind, int rope,
+                                  int64_t* appended) {
   if (!pool || !pr) return fail("null argument");
   if (appended) *appended = 0;
   int64_t set; bool none;
@@ -754,8 +771,31 @@ int lorakv_pool_append_kv_project(lorakv_pool* pool, const lorakv_proj* pr, int6
   const void* packed = pr->fused ? static_cast<const char*>(pr->packed) +
                                        (size_t)(layer * kv_project_packed_elems(pr->d_model, pr->n_kv_local, pr->d_head)) * 2
                                  : nullptr;
+  // "full values" (engine.hpp:385-393): the value rows carry the agent's LoRA contribution
+  const float *av = nullptr, *bv = nullptr, *down = nullptr;
+  int64_t rank = 0; float v_scale = 0.f;
+  if (merge) {
+    if (merge->rank < 1 || merge->d_model != pr->d_model || merge->n_kv_local != pr->n_kv_local || merge->d_head != pr->d_head ||
+        layer >= merge->n_layers)
+      return fail("append_kv_project_full: adapter table does not match the projection (rank %lld)", (long long)merge->rank);
+    if (agent < 0 || agent >= merge->n_agents) return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)merge->n_agents);
+    if (!merge->a_set[(size_t)layer] || !merge->b_set[(size_t)(layer * merge->n_agents + agent)])
+      return fail("append_kv_project_full: A / B of layer %lld agent %lld were never uploaded", (long long)layer, (long long)agent);
+    rank = merge->rank;
+    if (rank > 64) return fail("append_kv_project_full: rank %lld > 64 is not supported", (long long)rank);
+    av = merge->a + layer * merge->d_model * rank;
+    bv = merge->b + ((layer * merge->n_agents + agent) * rank) * (merge->n_kv_local * merge->d_head);
+    v_scale = merge->scale_host[(size_t)(layer * merge->n_agents + agent)];
+    if (pr->fused) {
+      LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(add * rank) * sizeof(float)));
+      float* dn = static_cast<float*>(ctx->proj.ptr);
+      LK_TRY(launch_xa_dense(ctx, av, pr->d_model, rank, dev, add, dev_ld, dn));
+      down = dn;
+    }
+  }
   LK_TRY(launch_kv_project(pool, packed, pr->fused ? nullptr : pr->wk + w_off, pr->fused ? nullptr : pr->wv + w_off, layer, set,
-                           row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld, rope != 0));
+                           row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld, rope != 0, down, av, bv, rank,
+                           v_scale));
   if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
   have_k += add_k; have_v += add_v;
   if (appended) *appended = add;

@@ -76,7 +76,8 @@ bool kv_project_fused_shape(int dtype, int64_t d_head, int64_t d_model);
 int64_t kv_project_packed_elems(int64_t d_model, int64_t n_kv_local, int64_t d_head);
 int launch_pack_w(lorakv_ctx* ctx, const float* w_dev, int64_t ldw, int64_t col0, int64_t n_cols, int64_t d_model, int64_t nb0, void* packed);
 int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
-                      int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope);
+                      int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope,
+                      const float* down_dev, const float* av_dev, const float* bv_dev, int64_t rank, float v_scale);
 
 int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const float* wq_dev, int64_t ldw, int64_t col0,
                      int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev, const float* aq_dev, const float* bq_dev,

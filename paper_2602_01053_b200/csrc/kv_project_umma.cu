@@ -265,6 +265,22 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
     } else {
     const int64_t phys = live ? p.table[row / p.P] : 0;
     const int t = (int)(row % p.P);
+    // "full values" schemes (NonShared, FullShared) store v_base + (alpha/r) (x A_v) B_v[agent] (engine.hpp:385-393):
+    // the B_v columns of this CTA's value heads go to the idle operand stages, as in query mode
+    const float* dn = (p.down != nullptr) ? p.down + (live ? i_row : 0) * p.r : nullptr;
+    float* bq_s = reinterpret_cast<float*>(smem);
+    if (p.down != nullptr) {
+      const int et = tid - 64;
+      for (int idx = et; idx < p.r * (kBN / 4); idx += 128) {
+        const int k = idx / (kBN / 4), c4 = idx % (kBN / 4);
+        const int gbv = nblk * (kBN / 128) + c4 / 32;            // head block of this float4
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gbv >= p.n_kv_local)
+          v = __ldg(reinterpret_cast<const float4*>(p.bq + (int64_t)k * p.ldb + (int64_t)(gbv - p.n_kv_local) * 128) + c4 % 32);
+        reinterpret_cast<float4*>(bq_s)[idx] = v;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
 #pragma unroll 1
     for (int hb = 0; hb < kBN / 128; ++hb) {
       const int gb = nblk * (kBN / 128) + hb;                   // head block among [K heads | V heads]
@@ -289,6 +305,20 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
             const float x0 = lo[i], x1 = hi[i];
             lo[i] = x0 * cs.x - x1 * cs.y;                      // engine.hpp:239-240
             hi[i] = x0 * cs.y + x1 * cs.x;
+          }
+        }
+        if (!is_k && p.down != nullptr) {
+          for (int k = 0; k < p.r; ++k) {
+            const float4* brow = reinterpret_cast<const float4*>(bq_s + k * kBN + hb * 128 + c0);
+            const float dk = p.q_scale * __ldg(dn + k);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 bl = brow[i], bh = brow[16 + i];
+              lo[4 * i] = fmaf(dk, bl.x, lo[4 * i]); lo[4 * i + 1] = fmaf(dk, bl.y, lo[4 * i + 1]);
+              lo[4 * i + 2] = fmaf(dk, bl.z, lo[4 * i + 2]); lo[4 * i + 3] = fmaf(dk, bl.w, lo[4 * i + 3]);
+              hi[4 * i] = fmaf(dk, bh.x, hi[4 * i]); hi[4 * i + 1] = fmaf(dk, bh.y, hi[4 * i + 1]);
+              hi[4 * i + 2] = fmaf(dk, bh.z, hi[4 * i + 2]); hi[4 * i + 3] = fmaf(dk, bh.w, hi[4 * i + 3]);
+            }
           }
         }
         if (write) {
@@ -326,6 +356,10 @@ __global__ void proj_matmul_kernel(const float* __restrict__ x, int64_t ld, cons
   for (int k = 0; k < K; ++k) acc = __fadd_rn(acc, __fmul_rn(x[i * ld + k], w[(int64_t)k * ldw + col0 + j]));
   out[idx] = acc;
 }
+__global__ void axpy_rn_kernel(float* __restrict__ y, const float* __restrict__ x, float a, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = __fadd_rn(y[i], __fmul_rn(a, x[i]));       // q.data[i] += q_scale * q_up.data[i], engine.hpp:372
+}
 __global__ void rope_rows_kernel(float* __restrict__ m, int64_t n_rows, int n_heads, int d_head, const float2* __restrict__ tab) {
   const int half = d_head / 2;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -359,7 +393,8 @@ int launch_pack_w(lorakv_ctx* ctx, const float* w_dev, int64_t ldw, int64_t col0
 // rows [row0, row0 + n_rows) of the trajectory from x_dev (row i of x_dev is logical row row0 + i); K rows below k_from and V
 // rows below v_from are already cached and are not written
 int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
-                      int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope) {
+                      int64_t row0, int64_t k_from, int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope,
+                      const float* down_dev, const float* av_dev, const float* bv_dev, int64_t rank, float v_scale) {
   if (n_rows == 0) return LORAKV_OK;
   lorakv_ctx* ctx = pool->ctx;
   const int64_t d = pool->dims.d_head, d_model = pool->dims.d_model, n_kv = pool->n_kv_local;
@@ -388,7 +423,7 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     pp.head_stride = pool->kv_head_stride(); pp.page_stride = pool->kv_page_stride();
     pp.P = (int)pool->P; pp.d_model = (int)d_model; pp.n_kv_local = (int)n_kv;
     pp.row0 = row0; pp.n_rows = n_rows; pp.k_from = k_from; pp.v_from = v_from;
-    pp.q_out = nullptr; pp.ldq = 0; pp.down = nullptr; pp.bq = nullptr; pp.ldb = 0; pp.r = 0; pp.q_scale = 0.f;
+    pp.q_out = nullptr; pp.ldq = 0; pp.down = down_dev; pp.bq = bv_dev; pp.ldb = n_kv * d; pp.r = (int)rank; pp.q_scale = v_scale;
     const size_t smem = (size_t)kStages * kStageBytes + 1024;
     LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const dim3 grid((unsigned)(2 * n_kv * d / kBN), (unsigned)tiles);
@@ -419,6 +454,16 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     rope_rows_kernel<<<(unsigned)((nr + 255) / 256), 256, 0, ctx->stream>>>(kbuf, n_rows, (int)n_kv, (int)d, tab);
     ctx->launches += 2;
   }
+  if (av_dev != nullptr && rank > 0) {        // v_store = v_base + v_scale * ((x A_v) B_v), engine.hpp:385-393, in the reference's order
+    LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(n_rows * rank + n) * sizeof(float)));
+    float* vdown = static_cast<float*>(ctx->proj.ptr);
+    float* vup = vdown + n_rows * rank;
+    const int64_t nd = n_rows * rank;
+    proj_matmul_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, av_dev, rank, 0, n_rows, (int)d_model, (int)rank, vdown);
+    proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(vdown, rank, bv_dev, dkv, 0, n_rows, (int)rank, (int)dkv, vup);
+    axpy_rn_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(vbuf, vup, v_scale, n);
+    ctx->launches += 3;
+  }
   LK_CUDA(cudaGetLastError());
   if (k_from < row0 + n_rows) {
     const int64_t skip = k_from > row0 ? k_from - row0 : 0;
@@ -433,10 +478,6 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
 }
 
 // ---- query projection: q = rope(x * Wq + scale * (x * A_q) * B_q[agent]) (engine.hpp:362-373, :422) -------------------
-__global__ void axpy_rn_kernel(float* __restrict__ y, const float* __restrict__ x, float a, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) y[i] = __fadd_rn(y[i], __fmul_rn(a, x[i]));       // q.data[i] += q_scale * q_up.data[i], engine.hpp:372
-}
 
 int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const float* wq_dev, int64_t ldw, int64_t col0,
                      int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev, const float* aq_dev, const float* bq_dev,

@@ -187,3 +187,38 @@ def test_query_projection_fp32_is_the_reference_order(ctx, orc):
     got = proj.query(0, 0, 11, x, n_q * d, rope=True)
     assert orc.max_rel_error(got, reference_q(orc, x, wq, a, b, 16.0, n_q, d, 11, True)) <= 1e-6
     proj.close()
+
+
+@pytest.mark.parametrize("dtype_name,d,scheme", [("BF16", 128, "NonShared"), ("BF16", 128, "FullShared"), ("F32", 32, "NonShared")])
+def test_full_values_projection_merges_the_value_lora(ctx, orc, dtype_name, d, scheme):
+    """NonShared / FullShared store v_base + (alpha/r) (x A_v) B_v[agent] (engine.hpp:385-393) and attend with r = 0."""
+    from paper_2602_01053_b200 import Adapters, Pool, Projection, abi
+    dtype = getattr(abi, dtype_name)
+    bf16 = dtype == abi.BF16
+    L, d_model, n_kv, r, A = 140, 128, 2, 8, 2
+    x, wk, wv = make_inputs(orc, 9000 + d, L, d_model, n_kv, d, bf16)
+    rnd = orc.round_bf16 if bf16 else (lambda m: m)
+    a = rnd(orc.gaussian(d_model, r, orc.child(9000, 4), 1.0 / np.sqrt(d_model), np.float32))
+    b = [rnd(orc.gaussian(r, n_kv * d, orc.child(9000, 10 + i), 0.02 / np.sqrt(r), np.float32)) for i in range(A)]
+    pool = Pool(ctx, scheme, 1, n_kv, d, d_model, 0, A, max_tokens=L, dtype=dtype, page_tokens=32)
+    proj = Projection(ctx, 1, d_model, n_kv, d, dtype=dtype)
+    ad = Adapters(ctx, 1, A, d_model, r, n_kv, d, dtype=dtype)
+    proj.set_kv(0, wk, wv); ad.set_a(0, a)
+    for i in range(A):
+        ad.set_b(0, i, b[i], 16.0)
+    pool.append_tokens(L)
+    agents = range(A) if scheme == "NonShared" else [1]
+    for i in agents:
+        assert pool.append_kv_project(proj, 0, i, 0, x, merge=ad) == L
+        want_k = orc.apply_rope(orc.matmul(x, wk), n_kv, d, 0)
+        want_v = orc.matmul(x, wv) + np.float32(16.0 / r) * orc.matmul(orc.matmul(x, a), b[i])
+        got_k, got_v = pool.key_view(0, i), pool.value_view(0, i)
+        if bf16:
+            assert ctx.last_kernel() == "kv_project_umma"
+            assert orc.max_rel_error(got_k, want_k) <= 4e-3 and orc.max_rel_error(got_v, want_v) <= 4e-3
+        else:
+            assert np.array_equal(got_v, want_v)                     # the reference's order, bit for bit
+            assert orc.max_rel_error(got_k, want_k) <= 1e-6
+    if scheme == "FullShared":                                       # the next agent finds the rows there (first writer wins)
+        assert pool.append_kv_project(proj, 0, 0, 0, x, merge=ad) == 0
+    pool.close(); proj.close(); ad.close()

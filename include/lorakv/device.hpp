@@ -27,10 +27,13 @@ namespace lorakv {
 
 class AdapterTable {
  public:
-  AdapterTable(const KvStore<float>& store, idx n_q_heads)
+  // rank = 0 takes the store's; the "full values" schemes keep no LR cache (store rank 0) but still merge a rank-r
+  // value adapter into the rows they store (engine.hpp:385-393), so their tables name the rank explicitly
+  AdapterTable(const KvStore<float>& store, idx n_q_heads, idx rank = 0)
       : n_q_heads_(n_q_heads), n_kv_heads_(store.device_options().n_kv_heads),
         per_agent_a_(store.scheme().kind == SchemeKind::BaseShared) {
-    const StoreDims& d = store.dims();
+    StoreDims d = store.dims();
+    if (rank > 0) d.rank = rank;
     const DeviceOptions& o = store.device_options();
     b200::check(lorakv_adapters_create(b200::Runtime::ctx(), d.n_layers, d.n_agents, d.d_model, d.rank, o.n_kv_heads,
                                        d.d_kv / o.n_kv_heads, o.kv_head_begin, o.n_kv_local,

@@ -705,12 +705,23 @@ int lorakv_proj_query(lorakv_proj* pr, int64_t layer, int64_t agent, int64_t pos
   const bool fused = pr->q_fused && (dev_ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(dev) & 15) == 0);
   if (!fused && pr->q_fused) return fail("proj_query: rows must be 16-byte aligned with a stride that is a multiple of 4");
   float* down = nullptr;
+  const bool small = fused && ctx->policy != 1 && rows_project_supported(n_rows, pr->d_model, rank);
   if (fused && lora) {
     LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(n_rows * rank) * sizeof(float)));
     down = static_cast<float*>(ctx->proj.ptr);
-    LK_TRY(launch_xa_dense(ctx, aq, pr->d_model, rank, dev, n_rows, dev_ld, down));
+    if (small) LK_TRY(launch_rows_xa(ctx, aq, pr->d_model, rank, dev, n_rows, dev_ld, down));
+    else LK_TRY(launch_xa_dense(ctx, aq, pr->d_model, rank, dev, n_rows, dev_ld, down));
   }
   const void* packed = fused ? static_cast<const char*>(pr->wq_packed) + (size_t)(layer * pr->d_model * dq) * 2 : nullptr;
+  if (small) {
+    LK_TRY(launch_rows_q_project(ctx, packed, pr->d_model, dq, pr->d_head, down, bq ? bq + col0 : nullptr, dq_full, rank, sc, pos_begin,
+                                 dev, n_rows, dev_ld, rope != 0, q_dev));
+    if (host) {
+      LK_CUDA(cudaMemcpyAsync(q_out, q_dev, q_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      LK_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    return LORAKV_OK;
+  }
   const float* wq = fused ? nullptr : pr->wq + (size_t)(layer * pr->d_model * dq_full);
   // the packed matrix already holds only this shard's columns: its column origin is 0, B_q keeps the full width
   LK_TRY(launch_q_project(ctx, fused, packed, wq, dq_full, col0, pr->d_model, dq, pr->d_head, down, aq, bq, dq_full, rank, sc,
@@ -789,9 +800,19 @@ static int append_kv_project_impl(lorakv_pool* pool, const lorakv_proj* pr, cons
     if (pr->fused) {
       LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(add * rank) * sizeof(float)));
       float* dn = static_cast<float*>(ctx->proj.ptr);
-      LK_TRY(launch_xa_dense(ctx, av, pr->d_model, rank, dev, add, dev_ld, dn));
+      if (rows_project_supported(add, pr->d_model, rank)) LK_TRY(launch_rows_xa(ctx, av, pr->d_model, rank, dev, add, dev_ld, dn));
+      else LK_TRY(launch_xa_dense(ctx, av, pr->d_model, rank, dev, add, dev_ld, dn));
       down = dn;
     }
+  }
+  if (pr->fused && ctx->policy != 1 && rows_project_supported(add, pr->d_model, rank)) {
+    // a decode step's handful of rows: weight-streaming GEMVs over all SMs instead of one 128-row tcgen05 tile
+    LK_TRY(launch_rows_kv_project(pool, packed, layer, set, row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld,
+                                  rope != 0, down, bv, rank, v_scale));
+    if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+    have_k += add_k; have_v += add_v;
+    if (appended) *appended = add;
+    return LORAKV_OK;
   }
   LK_TRY(launch_kv_project(pool, packed, pr->fused ? nullptr : pr->wk + w_off, pr->fused ? nullptr : pr->wv + w_off, layer, set,
                            row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld, rope != 0, down, av, bv, rank,

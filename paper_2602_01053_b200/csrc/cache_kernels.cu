@@ -420,6 +420,11 @@ int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, in
   const float* A = a_dev;
   const bool bf16 = pool->dims.dtype == LORAKV_BF16;
   const bool vec_ok = (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x_dev) & 15) == 0);
+  // a decode step's handful of rows: one CTA per row streams A (rows_project.cu) instead of a latency-bound MMA tile
+  if (bf16 && ctx->policy != 1 && rows_project_supported(n_rows, d_model, rank) && a.width <= 64 && a.lay.bw == a.width && a.width % 8 == 0) {
+    LK_TRY(launch_rows_lr_project(pool, A, d_model, rank, layer, set, row0, x_dev, n_rows, ld));
+    return LORAKV_OK;
+  }
   // bf16 pools: tensor-core kernel (policy 1 keeps the CUDA-core kernel for cross-checks)
   if (bf16 && ctx->policy != 1 && vec_ok && d_model % 16 == 0 && d_model >= 64 && a.width <= 64 && a.lay.bw == a.width && a.width % 8 == 0) {
     const int nt = a.width / 8;

@@ -587,15 +587,26 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   float acc[kMaxCols];
 #pragma unroll
   for (int i = 0; i < kMaxCols; ++i) acc[i] = 0.f;
-  for (int s = 0; s < ns; ++s) {
-    const float ws = __shfl_sync(0xffffffffu, wgt, s);
-    if (ws == 0.f) continue;             // an empty split carries no accumulators (warp-uniform)
-    const float* row = row_of(s) + 4;
+  // four splits per round so that their loads are in flight together (one at a time cost ~0.7 us of latency each);
+  // an empty split carries no accumulators, so its values are never read (weight 0, predicate off)
+  for (int s0 = 0; s0 < ns; s0 += 4) {
+    float ws[4], v[4][kMaxCols];
 #pragma unroll
-    for (int i = 0; i < kMaxCols; ++i) {
-      const int c = lane + 32 * i;
-      if (c < C) acc[i] = fmaf(ws, row[c], acc[i]);
+    for (int u = 0; u < 4; ++u) {
+      const int sidx = s0 + u;
+      ws[u] = __shfl_sync(0xffffffffu, wgt, sidx & 31);
+      if (sidx >= ns) ws[u] = 0.f;
+      const float* row = row_of(sidx < ns ? sidx : 0) + 4;
+#pragma unroll
+      for (int i = 0; i < kMaxCols; ++i) {
+        const int c = lane + 32 * i;
+        v[u][i] = (ws[u] != 0.f && c < C) ? row[c] : 0.f;
+      }
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int i = 0; i < kMaxCols; ++i) acc[i] = fmaf(ws[u], v[u][i], acc[i]);
   }
 #pragma unroll
   for (int i = 0; i < kMaxCols; ++i) {

@@ -87,6 +87,19 @@ int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const f
 int launch_xa_dense(lorakv_ctx* ctx, const float* a_dev, int64_t d_model, int64_t rank, const float* x_dev, int64_t n_rows, int64_t ld,
                     float* out_dev);
 
+// rows_project.cu: the same projections for <= 8 rows (a decode step) as weight-streaming GEMVs over all SMs
+bool rows_project_supported(int64_t n_rows, int64_t d_model, int64_t rank);
+int launch_rows_xa(lorakv_ctx* ctx, const float* a_dev, int64_t d_model, int64_t rank, const float* x_dev, int64_t n_rows, int64_t ld,
+                   float* down_dev);
+int launch_rows_kv_project(lorakv_pool* pool, const void* w_packed, int64_t layer, int64_t set, int64_t row0, int64_t k_from,
+                           int64_t v_from, const float* x_dev, int64_t n_rows, int64_t ld, bool rope, const float* down_dev,
+                           const float* bv_dev, int64_t rank, float v_scale);
+int launch_rows_q_project(lorakv_ctx* ctx, const void* wq_packed, int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev,
+                          const float* bq_dev, int64_t ldb, int64_t rank, float q_scale, int64_t pos0, const float* x_dev, int64_t n_rows,
+                          int64_t ld, bool rope, float* q_dev);
+int launch_rows_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set, int64_t row0,
+                           const float* x_dev, int64_t n_rows, int64_t ld);
+
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
                   int a_in_tmem, float* d);

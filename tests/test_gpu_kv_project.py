@@ -222,3 +222,45 @@ def test_full_values_projection_merges_the_value_lora(ctx, orc, dtype_name, d, s
     if scheme == "FullShared":                                       # the next agent finds the rows there (first writer wins)
         assert pool.append_kv_project(proj, 0, 0, 0, x, merge=ad) == 0
     pool.close(); proj.close(); ad.close()
+
+
+@pytest.mark.parametrize("n_rows", [1, 3, 8])
+def test_decode_step_rows_take_the_gemv_path(ctx, orc, n_rows):
+    """<= 8 new rows (a decode step) stream the packed weights as GEMVs over all SMs (rows_project.cu) instead of one
+    128-row tcgen05 tile: K / V (+ value adapter), V_lr and q must equal what the GEMM path gives for the same rows."""
+    from paper_2602_01053_b200 import Adapters, Pool, Projection, abi
+    L0, d_model, n_q, n_kv, d, r, A = 45, 256, 8, 2, 128, 16, 2
+    L = L0 + n_rows
+    x, wk, wv = make_inputs(orc, 6100 + n_rows, L, d_model, n_kv, d, True)
+    rnd = orc.round_bf16
+    wq = rnd(orc.gaussian(d_model, n_q * d, orc.child(61, 2), 1.0 / np.sqrt(d_model), np.float32))
+    a = rnd(orc.gaussian(d_model, r, orc.child(61, 3), 1.0 / np.sqrt(d_model), np.float32))
+    bq = [rnd(orc.gaussian(r, n_q * d, orc.child(61, 10 + i), 0.02 / np.sqrt(r), np.float32)) for i in range(A)]
+    bv = [rnd(orc.gaussian(r, n_kv * d, orc.child(61, 20 + i), 0.02 / np.sqrt(r), np.float32)) for i in range(A)]
+    for scheme, merge in (("BaseLRShared", False), ("FullShared", True)):
+        pool = Pool(ctx, scheme, 1, n_kv, d, d_model, 0 if merge else r, A, max_tokens=L, dtype=abi.BF16, page_tokens=16)
+        proj = Projection(ctx, 1, d_model, n_kv, d, dtype=abi.BF16)
+        ad = Adapters(ctx, 1, A, d_model, r, n_kv, d, dtype=abi.BF16)
+        proj.set_kv(0, wk, wv); proj.set_q(0, n_q, wq); ad.set_a(0, a)
+        for i in range(A):
+            proj.set_q_lora(0, i, A, a, bq[i], 16.0); ad.set_b(0, i, bv[i], 16.0)
+        pool.append_tokens(L)
+        kw = dict(merge=ad) if merge else {}
+        assert pool.append_kv_project(proj, 0, 1, 0, x[:L0], **kw) == L0          # the GEMM path
+        assert ctx.last_kernel() == "kv_project_umma"
+        assert pool.append_kv_project(proj, 0, 1, L0, x[L0:], **kw) == n_rows     # the GEMV path, mid-page
+        assert ctx.last_kernel() == "rows_kv_project"
+        want_k = orc.apply_rope(orc.matmul(x, wk), n_kv, d, 0)
+        want_v = orc.matmul(x, wv) + (np.float32(16.0 / r) * orc.matmul(orc.matmul(x, a), bv[1]) if merge else 0)
+        assert orc.max_rel_error(pool.key_view(0, 1 if scheme == "NonShared" else 0), want_k) <= 4e-3
+        assert orc.max_rel_error(pool.value_view(0, 0), want_v) <= 4e-3
+        if not merge:
+            assert pool.append_lr_project(ad, 0, 0, 0, x[:L0]) == L0
+            assert pool.append_lr_project(ad, 0, 0, L0, x[L0:]) == n_rows
+            assert orc.max_rel_error(pool.lr_view(0, 0), orc.matmul(x, a)) <= 4e-3
+        got_q = proj.query(0, 1, L0, x[L0:], n_q * d)
+        assert ctx.last_kernel() == "rows_q_project"
+        want_q = reference_q(orc, x[L0:], wq, a, bq[1], 16.0, n_q, d, L0, True)
+        assert orc.max_rel_error(got_q, want_q) <= 1e-4
+        assert orc.max_rel_error(proj.query(0, -1, L0, x[L0:], n_q * d), reference_q(orc, x[L0:], wq, None, None, 16.0, n_q, d, L0, True)) <= 1e-4
+        pool.close(); proj.close(); ad.close()

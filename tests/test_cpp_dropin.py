@@ -29,7 +29,7 @@ def test_headers_compile_and_suite_links():
     build()
     assert os.path.exists(BIN)
     probe = ('#include "lorakv/attention.hpp"\n#include "lorakv/kvcache.hpp"\n#include "lorakv/lora.hpp"\n'
-             '#include "lorakv/device.hpp"\n#include "lorakv/fuzz.hpp"\nint main() { return 0; }\n')
+             '#include "lorakv/device.hpp"\n#include "lorakv/replay.hpp"\n#include "lorakv/fuzz.hpp"\nint main() { return 0; }\n')
     for std in ("c++17", "c++20"):
         res = subprocess.run(["g++", f"-std={std}", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
                               "-I" + os.path.join(ROOT, "include"), "-x", "c++", "-"],

@@ -22,6 +22,7 @@
 // summation order, bit for bit) + rope + the scatter kernel of cache_kernels.cu.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.hpp"
@@ -119,6 +120,7 @@ struct ProjParams {
   int P, d_model, n_kv_local;
   int64_t row0, n_rows;        // first logical row of the call's rows; rows computed
   int64_t k_from, v_from;      // logical rows below these already exist in the K / V cache (first writer wins)
+  int n_col_blocks, n_row_tiles;      // the persistent CTAs walk tiles t = blockIdx.x + i * gridDim.x, column block fastest
   // query mode (kQuery): q = rope(x * Wq + q_scale * (x * A_q) * B_q[agent]) as float32 rows (engine.hpp:362-373, :422)
   float* q_out;                // [n_rows][ldq]
   int64_t ldq;
@@ -130,8 +132,10 @@ struct ProjParams {
 };
 
 struct ProjBarriers {
-  uint64_t full[kStages], empty[kStages], acc_full;
+  uint64_t full[kStages], empty[kStages], acc_full[2], acc_empty[2];
 };
+constexpr int kLoraSmemRank = 32;                                   // B slice [r][256] float32 fits beside the stages up to this rank
+constexpr uint32_t kLoraSmemBytes = kLoraSmemRank * kBN * 4;        // 32 KB
 
 template <bool kQuery>
 __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const ProjParams p) {
@@ -140,17 +144,19 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
   __shared__ uint32_t tmem_base_s;
   unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // column block fastest: the CTAs that share an X tile run in the same wave, so X is read from HBM once
-  // (with the row tile fastest it was re-read per column block: 982 MB of DRAM reads for 151 MB of operands)
-  const int nblk = blockIdx.x, tile = blockIdx.y;            // 256-column block (two heads), 128-row tile
+  // Persistent: CTA b walks tiles t = b, b + gridDim.x, ...; t -> (column block t % n_col_blocks, row tile t / n_col_blocks), column
+  // block fastest so that the CTAs sharing an X tile run together and X is read from HBM once (with the row tile fastest it
+  // was re-read per column block: 982 MB of DRAM reads for 151 MB of operands).  Two accumulators in TMEM (2 x 256 columns):
+  // the epilogue warps drain tile i while the MMA thread already accumulates tile i + 1.
   const int kb_n = p.d_model / kBK;
+  const int total_tiles = p.n_col_blocks * p.n_row_tiles;
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) { ptx::mbar_init(&bars.full[s], 1); ptx::mbar_init(&bars.empty[s], 1); }
-    ptx::mbar_init(&bars.acc_full, 1);
+    for (int a = 0; a < 2; ++a) { ptx::mbar_init(&bars.acc_full[a], 1); ptx::mbar_init(&bars.acc_empty[a], 128); }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc(&tmem_base_s, kBN);
+  if (warp == 1) ptx::tmem_alloc(&tmem_base_s, 2 * kBN);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -159,17 +165,21 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (ptx::elect_one()) {
-      const unsigned char* a_src = reinterpret_cast<const unsigned char*>(p.xa) + (int64_t)tile * kb_n * kABytes;
-      const unsigned char* b_src = reinterpret_cast<const unsigned char*>(p.wb) + (int64_t)nblk * (kBN / 64) * p.d_model * 128;
-      for (int kb = 0; kb < kb_n; ++kb) {
-        const int s = kb % kStages;
-        if (kb >= kStages) ptx::mbar_wait(&bars.empty[s], (uint32_t)(((kb / kStages) & 1) ^ 1));
-        ptx::mbar_arrive_expect_tx(&bars.full[s], kStageBytes);
-        const uint32_t dst = ptx::smem_u32(smem + s * kStageBytes);
-        bulk_g2s(dst, a_src + (int64_t)kb * kABytes, kABytes, &bars.full[s]);
+      int kbg = 0;                                   // k blocks issued so far: the ring runs on across tiles
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        const int nblk = t % p.n_col_blocks, tile = t / p.n_col_blocks;
+        const unsigned char* a_src = reinterpret_cast<const unsigned char*>(p.xa) + (int64_t)tile * kb_n * kABytes;
+        const unsigned char* b_src = reinterpret_cast<const unsigned char*>(p.wb) + (int64_t)nblk * (kBN / 64) * p.d_model * 128;
+        for (int kb = 0; kb < kb_n; ++kb, ++kbg) {
+          const int s = kbg % kStages;
+          if (kbg >= kStages) ptx::mbar_wait(&bars.empty[s], (uint32_t)(((kbg / kStages) & 1) ^ 1));
+          ptx::mbar_arrive_expect_tx(&bars.full[s], kStageBytes);
+          const uint32_t dst = ptx::smem_u32(smem + s * kStageBytes);
+          bulk_g2s(dst, a_src + (int64_t)kb * kABytes, kABytes, &bars.full[s]);
 #pragma unroll
-        for (int nb = 0; nb < kBN / 64; ++nb)
-          bulk_g2s(dst + kABytes + nb * kBBlk, b_src + (int64_t)nb * p.d_model * 128 + (int64_t)kb * kBBlk, kBBlk, &bars.full[s]);
+          for (int nb = 0; nb < kBN / 64; ++nb)
+            bulk_g2s(dst + kABytes + nb * kBBlk, b_src + (int64_t)nb * p.d_model * 128 + (int64_t)kb * kBBlk, kBBlk, &bars.full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -179,36 +189,47 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
       const uint64_t ad = ptx::smem_desc(ptx::smem_u32(smem), 16u, 1024u, ptx::kSw128);
       const uint64_t bd = ptx::smem_desc(ptx::smem_u32(smem) + kABytes, kBBlk, 1024u, ptx::kSw128);
       const uint32_t ad_hi = (uint32_t)(ad >> 32), bd_hi = (uint32_t)(bd >> 32);
-      for (int kb = 0; kb < kb_n; ++kb) {
-        const int s = kb % kStages;
-        ptx::mbar_wait(&bars.full[s], (uint32_t)((kb / kStages) & 1));
-        ptx::tc_fence_after();
-        const uint32_t a_lo = (uint32_t)ad + (uint32_t)s * (kStageBytes >> 4), b_lo = (uint32_t)bd + (uint32_t)s * (kStageBytes >> 4);
+      int kbg = 0, li = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++li) {
+        const int ab = li & 1;                       // accumulator of this tile
+        if (li >= 2) {                               // the epilogue warps have drained its previous tile
+          ptx::mbar_wait(&bars.acc_empty[ab], (uint32_t)(((li >> 1) & 1) ^ 1));
+          ptx::tc_fence_after();
+        }
+        for (int kb = 0; kb < kb_n; ++kb, ++kbg) {
+          const int s = kbg % kStages;
+          ptx::mbar_wait(&bars.full[s], (uint32_t)((kbg / kStages) & 1));
+          ptx::tc_fence_after();
+          const uint32_t a_lo = (uint32_t)ad + (uint32_t)s * (kStageBytes >> 4), b_lo = (uint32_t)bd + (uint32_t)s * (kStageBytes >> 4);
 #pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks)
-          ptx::umma_bf16_ss(tmem, ((uint64_t)ad_hi << 32) | (a_lo + (uint32_t)ks * 2u), ((uint64_t)bd_hi << 32) | (b_lo + (uint32_t)ks * (2048u >> 4)),
-                            idesc, (kb > 0 || ks > 0) ? 1u : 0u);
-        ptx::umma_commit(&bars.empty[s]);
+          for (int ks = 0; ks < kBK / 16; ++ks)
+            ptx::umma_bf16_ss(tmem + (uint32_t)ab * kBN, ((uint64_t)ad_hi << 32) | (a_lo + (uint32_t)ks * 2u),
+                              ((uint64_t)bd_hi << 32) | (b_lo + (uint32_t)ks * (2048u >> 4)), idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+          ptx::umma_commit(&bars.empty[s]);
+        }
+        ptx::umma_commit(&bars.acc_full[ab]);
       }
-      ptx::umma_commit(&bars.acc_full);
     }
   } else {
     // ===================== epilogue: TMEM -> (RoPE) -> bf16 -> swizzled pages =====================
     const int q4 = warp & 3;                                    // TMEM lane quarter this warp may read
     const int r = q4 * 32 + lane;
+    float* bq_s = reinterpret_cast<float*>(smem + kStages * kStageBytes);      // LoRA slice of the current tile
+    const bool lora_smem = p.down != nullptr && p.r <= kLoraSmemRank;
+    int li = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++li) {
+    const int nblk = t % p.n_col_blocks, tile = t / p.n_col_blocks, ab = li & 1;
     const int64_t i_row = (int64_t)tile * kBM + r;              // row of the call
     const int64_t row = p.row0 + i_row;                         // logical row of the trajectory = position
     const bool live = i_row < p.n_rows;
-    ptx::mbar_wait(&bars.acc_full, 0);
-    ptx::tc_fence_after();
-    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const uint32_t lane_base = ((uint32_t)(q4 * 32) << 16) + (uint32_t)ab * kBN;
     if constexpr (kQuery) {
       // every 128-column block is one q head: add the LoRA up-projection, rotate, store float32 rows
       const float* dn = (p.down != nullptr) ? p.down + (live ? i_row : 0) * p.r : nullptr;    // this row's x * A_q
-      // B_q[agent][:, the 256 columns of this CTA] -> shared memory (the operand stages are idle once acc_full has
-      // fired): the up-projection then reads broadcast float4s instead of 2 * r global loads per element
-      float* bq_s = reinterpret_cast<float*>(smem);
-      if (p.down != nullptr) {
+      // B_q[agent][:, the 256 columns of this tile] -> shared memory beside the stages (rank <= 32): the up-projection
+      // then reads broadcast float4s instead of 2 * r global loads per element; wider ranks read B through L1
+      if (lora_smem) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");             // the previous tile's readers are done
         const int et = tid - 64;                                   // 0..127 over the four epilogue warps
         for (int idx = et; idx < p.r * (kBN / 4); idx += 128) {
           const int k = idx / (kBN / 4), c4 = idx % (kBN / 4);
@@ -216,6 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
+      ptx::mbar_wait(&bars.acc_full[ab], (uint32_t)((li >> 1) & 1));
+      ptx::tc_fence_after();
 #pragma unroll 1
       for (int hb = 0; hb < kBN / 128; ++hb) {
         const int64_t col0 = (int64_t)(nblk * (kBN / 128) + hb) * 128;
@@ -230,7 +253,8 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
           for (int i = 0; i < 32; ++i) { lo[i] = __uint_as_float(lo_u[i]); hi[i] = __uint_as_float(hi_u[i]); }
           if (p.down != nullptr) {
             for (int k = 0; k < p.r; ++k) {
-              const float4* brow = reinterpret_cast<const float4*>(bq_s + k * kBN + hb * 128 + c0);   // same address in every lane: broadcast
+              const float4* brow = lora_smem ? reinterpret_cast<const float4*>(bq_s + k * kBN + hb * 128 + c0)   // same address in every lane
+                                             : reinterpret_cast<const float4*>(p.bq + (int64_t)k * p.ldb + col0 + c0);
               const float dk = p.q_scale * __ldg(dn + k);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -264,12 +288,12 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
       }
     } else {
     const int64_t phys = live ? p.table[row / p.P] : 0;
-    const int t = (int)(row % p.P);
+    const int tok = (int)(row % p.P);
     // "full values" schemes (NonShared, FullShared) store v_base + (alpha/r) (x A_v) B_v[agent] (engine.hpp:385-393):
-    // the B_v columns of this CTA's value heads go to the idle operand stages, as in query mode
+    // the B_v columns of this tile's value heads are staged beside the operand stages, as in query mode
     const float* dn = (p.down != nullptr) ? p.down + (live ? i_row : 0) * p.r : nullptr;
-    float* bq_s = reinterpret_cast<float*>(smem);
-    if (p.down != nullptr) {
+    if (lora_smem) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");             // the previous tile's readers are done
       const int et = tid - 64;
       for (int idx = et; idx < p.r * (kBN / 4); idx += 128) {
         const int k = idx / (kBN / 4), c4 = idx % (kBN / 4);
@@ -281,6 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
+    ptx::mbar_wait(&bars.acc_full[ab], (uint32_t)((li >> 1) & 1));
+    ptx::tc_fence_after();
 #pragma unroll 1
     for (int hb = 0; hb < kBN / 128; ++hb) {
       const int gb = nblk * (kBN / 128) + hb;                   // head block among [K heads | V heads]
@@ -309,7 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
         }
         if (!is_k && p.down != nullptr) {
           for (int k = 0; k < p.r; ++k) {
-            const float4* brow = reinterpret_cast<const float4*>(bq_s + k * kBN + hb * 128 + c0);
+            const float4* brow = lora_smem ? reinterpret_cast<const float4*>(bq_s + k * kBN + hb * 128 + c0)
+                                           : reinterpret_cast<const float4*>(p.bq + (int64_t)k * p.ldb + (int64_t)head * 128 + c0);
             const float dk = p.q_scale * __ldg(dn + k);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -322,12 +349,12 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
           }
         }
         if (write) {
-          // page = [2 column blocks][P tokens][64] with the 16-byte chunks of a token's 128-byte row XOR-swizzled by t % 8
-          unsigned char* b0 = reinterpret_cast<unsigned char*>(page) + (int64_t)t * 128;
+          // page = [2 column blocks][P tokens][64] with the 16-byte chunks of a token's 128-byte row XOR-swizzled by token % 8
+          unsigned char* b0 = reinterpret_cast<unsigned char*>(page) + (int64_t)tok * 128;
           unsigned char* b1 = b0 + (int64_t)p.P * 128;
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
-            const int chunk = ((c0 / 8 + ch) ^ (t & 7)) * 16;
+            const int chunk = ((c0 / 8 + ch) ^ (tok & 7)) * 16;
             uint4 a, b;
             a.x = pack_bf16(lo[8 * ch + 0], lo[8 * ch + 1]); a.y = pack_bf16(lo[8 * ch + 2], lo[8 * ch + 3]);
             a.z = pack_bf16(lo[8 * ch + 4], lo[8 * ch + 5]); a.w = pack_bf16(lo[8 * ch + 6], lo[8 * ch + 7]);
@@ -340,10 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
       }
     }
     }
+    // this thread's TMEM reads of the tile are complete (every tcgen05.ld above was waited for): hand the accumulator back
+    ptx::tc_fence_before();
+    ptx::mbar_arrive(&bars.acc_empty[ab]);
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc(tmem, kBN);
+  if (warp == 1) ptx::tmem_dealloc(tmem, 2 * kBN);
 }
 
 // ---- exact fp32 path: the reference's matmul order (matrix.hpp:101-111) and rotation ------------------------
@@ -424,9 +455,10 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     pp.P = (int)pool->P; pp.d_model = (int)d_model; pp.n_kv_local = (int)n_kv;
     pp.row0 = row0; pp.n_rows = n_rows; pp.k_from = k_from; pp.v_from = v_from;
     pp.q_out = nullptr; pp.ldq = 0; pp.down = down_dev; pp.bq = bv_dev; pp.ldb = n_kv * d; pp.r = (int)rank; pp.q_scale = v_scale;
-    const size_t smem = (size_t)kStages * kStageBytes + 1024;
+    pp.n_col_blocks = (int)(2 * n_kv * d / kBN); pp.n_row_tiles = (int)tiles;
+    const size_t smem = (size_t)kStages * kStageBytes + kLoraSmemBytes + 1024;
     LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const dim3 grid((unsigned)(2 * n_kv * d / kBN), (unsigned)tiles);
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)pp.n_col_blocks * pp.n_row_tiles, ctx->sm_count);
     prof_mark(ctx, 0);
     kv_project_umma_kernel<false><<<grid, kThreads, smem, ctx->stream>>>(pp);
     prof_mark(ctx, 1);
@@ -506,9 +538,10 @@ int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const f
     pp.d_model = (int)d_model; pp.row0 = pos0; pp.n_rows = n_rows; pp.P = 1; pp.n_kv_local = 0;
     pp.q_out = q_dev; pp.ldq = n_cols; pp.down = rank > 0 ? down_dev : nullptr; pp.bq = bq_dev ? bq_dev + col0 : nullptr; pp.ldb = ldb;
     pp.r = (int)rank; pp.q_scale = q_scale;
-    const size_t smem = (size_t)kStages * kStageBytes + 1024;
+    pp.n_col_blocks = (int)(n_cols / kBN); pp.n_row_tiles = (int)tiles;
+    const size_t smem = (size_t)kStages * kStageBytes + kLoraSmemBytes + 1024;
     LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const dim3 grid((unsigned)(n_cols / kBN), (unsigned)tiles);
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)pp.n_col_blocks * pp.n_row_tiles, ctx->sm_count);
     prof_mark(ctx, 0);
     kv_project_umma_kernel<true><<<grid, kThreads, smem, ctx->stream>>>(pp);
     prof_mark(ctx, 1);

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define LORAKV_ABI_VERSION 1
+#define LORAKV_ABI_VERSION 2   /* 2: projections (lorakv_proj_*), snapshot / resume */
 
 typedef struct lorakv_ctx lorakv_ctx;           /* device + stream + scratch */
 typedef struct lorakv_pool lorakv_pool;         /* paged cache of one trajectory (KvStore<T>) */

@@ -149,7 +149,7 @@ def load_library(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lorakv_abi_version() != 1:
+    if lib.lorakv_abi_version() != 2:
         raise LorakvError("liblorakv_b200.so ABI version mismatch")
     if path is None:
         _lib = lib

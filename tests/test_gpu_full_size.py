@@ -101,3 +101,46 @@ def test_full_size_prefill_block_against_decode(ctx, orc, layer):
     one = pool.decode(ad, 0, 1, [1], N_Q, q[None, L_c - 1:L_c])[0]
     assert orc.max_rel_error(blk[L_c - 1:L_c], one) <= 2e-3
     pool.close(); ad.close()
+
+
+def test_full_size_projections_sampled_rows(ctx, orc):
+    """cfg 3's append: 16 384 new rows x d_model 4096 through the persistent tcgen05 projection kernels (2 048 tiles over 148
+    CTAs, every CTA walks ~14 tiles) -- a seeded sample of rows against matmul / apply_rope / the LoRA terms of the
+    reference path (engine.hpp:362-403), K / V / V_lr read back from the pages, q from the query projection."""
+    import torch
+    from paper_2602_01053_b200 import Adapters, Pool, Projection, abi
+    n_rows, d_model, r, row0 = 16384, 4096, R, 0
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev); gen.manual_seed(5)
+    x_dev = torch.randn((n_rows, d_model), generator=gen, device=dev, dtype=torch.float32).to(torch.bfloat16).to(torch.float32)
+    rnd = orc.round_bf16
+    g = lambda rows, cols, key, scale: rnd(orc.gaussian(rows, cols, orc.child(303, key), scale, np.float32))
+    wq, wk, wv = g(d_model, N_Q * D, 1, d_model ** -0.5), g(d_model, N_KV * D, 2, d_model ** -0.5), g(d_model, N_KV * D, 3, d_model ** -0.5)
+    a_q, a_v = g(d_model, r, 4, d_model ** -0.5), g(d_model, r, 5, d_model ** -0.5)
+    b_q = g(r, N_Q * D, 6, 0.02 / np.sqrt(r))
+    pool = Pool(ctx, "BaseLRShared", 1, N_KV, D, d_model, r, 1, max_tokens=n_rows, dtype=abi.BF16)
+    proj = Projection(ctx, 1, d_model, N_KV, D, dtype=abi.BF16)
+    ad = Adapters(ctx, 1, 1, d_model, r, N_KV, D, dtype=abi.BF16)
+    proj.set_kv(0, wk, wv); proj.set_q(0, N_Q, wq); proj.set_q_lora(0, 0, 1, a_q, b_q, 16.0); ad.set_a(0, a_v)
+    pool.append_tokens(n_rows)
+    torch.cuda.synchronize()
+    assert pool.append_kv_project(proj, 0, 0, row0, dev_ptr=x_dev.data_ptr(), n_rows=n_rows, ld=d_model) == n_rows
+    assert ctx.last_kernel() == "kv_project_umma"
+    assert pool.append_lr_project(ad, 0, 0, row0, dev_ptr=x_dev.data_ptr(), n_rows=n_rows, ld=d_model) == n_rows
+    q_dev = torch.empty((n_rows, N_Q * D), device=dev, dtype=torch.float32)
+    proj.query_device(0, 0, row0, x_dev.data_ptr(), n_rows, d_model, q_dev.data_ptr())
+    assert ctx.last_kernel() == "q_project_umma"
+    ctx.synchronize()
+    rows = np.array([0, 1, 127, 128, 5000, 9999, 16255, 16383])      # first / last tiles, tile edges, the middle
+    xs = x_dev[torch.from_numpy(rows).to(dev)].cpu().numpy()
+    k_got, v_got, lr_got = pool.key_view(0, 0)[rows], pool.value_view(0, 0)[rows], pool.lr_view(0, 0)[rows]
+    q_got = q_dev[torch.from_numpy(rows).to(dev)].cpu().numpy()
+    for i, row in enumerate(rows):
+        xi = xs[i:i + 1]
+        k_want = orc.apply_rope(orc.matmul(xi, wk), N_KV, D, int(row))
+        q_want = orc.apply_rope(orc.matmul(xi, wq) + np.float32(16.0 / r) * orc.matmul(orc.matmul(xi, a_q), b_q), N_Q, D, int(row))
+        assert orc.max_rel_error(k_got[i:i + 1], k_want) <= 4e-3, row
+        assert orc.max_rel_error(v_got[i:i + 1], orc.matmul(xi, wv)) <= 4e-3, row
+        assert orc.max_rel_error(lr_got[i:i + 1], orc.matmul(xi, a_v)) <= 4e-3, row
+        assert orc.max_rel_error(q_got[i:i + 1], q_want) <= 1e-4, row
+    pool.close(); proj.close(); ad.close()

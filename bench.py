@@ -215,12 +215,15 @@ def run_reference(args, wl):
 
 
 def load_tensor_peak():
+    """(burst peak, source, sustained peak or None): the burst figure is the roofline denominator of a kernel timed
+    alone; the sustained one (cuBLAS under the 1 kW power cap) is reported beside it because the prefill kernel runs at
+    the cap as well (sw_power_cap active, SM clock ~1.6 GHz: profiles/r1_clocks_prefill.txt)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)"
+        return float(p["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst)", p.get("bf16_tflops_sustained")
     except Exception:
-        return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s)"
+        return 1590.0, "fallback (B200_PROFILING.md 1.59 PFLOP/s)", 1400.0
 
 
 def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L, d_model):
@@ -239,15 +242,19 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
     for _ in range(2):
         pool.prefill_device(ad, 0, 1, n_q, q.data_ptr(), L_c, off, out.data_ptr())
     ev0, ev1 = ctx.event(), ctx.event()
+    sampler = ClockSampler(torch.cuda.current_device())
+    torch.cuda.synchronize()
+    sampler.start()
     ev0.record()
     for i in range(steps):
         pool.prefill_device(ad, i % n_layers, 1, n_q, q.data_ptr(), L_c, off, out.data_ptr())
     ev1.record()
     attn_ms = ev0.elapsed_ms(ev1) / steps
+    prefill_clocks = sampler.stop()
     kernel = ctx.last_kernel()
     pairs = L_c * off + L_c * (L_c + 1) // 2
     flops = 2 * n_q * pairs * (2 * d + r) + 2 * n_q * L_c * r * d
-    peak, peak_src = load_tensor_peak()
+    peak, peak_src, peak_sustained = load_tensor_peak()
     traffic = None
     try:   # DRAM bytes of one launch from the committed `ncu --set full` capture (profiles/)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -257,7 +264,10 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
     res = {"workload": "cfg3", "L_c": L_c, "query_offset": off, "attention_ms_per_layer": attn_ms,
            "attention_tflops": flops / (attn_ms * 1e-3) / 1e12, "algorithmic_flops": flops, "kernel": kernel,
            "roofline": {"bound": "tensor", "achieved": flops / (attn_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
-                        "frac": flops / (attn_ms * 1e-3) / 1e12 / peak, "traffic": traffic, "peak_source": peak_src}}
+                        "frac": flops / (attn_ms * 1e-3) / 1e12 / peak, "traffic": traffic, "peak_source": peak_src,
+                        "peak_sustained": peak_sustained,
+                        "frac_of_sustained": (flops / (attn_ms * 1e-3) / 1e12 / peak_sustained) if peak_sustained else None},
+           "clocks": prefill_clocks}
     # parity: a seeded sample of query rows against the reference CPU path (rows via L_c = 1)
     if not args.no_cpu_baseline:
         from oracle import checker

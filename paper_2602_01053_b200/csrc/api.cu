@@ -579,7 +579,7 @@ void lorakv_proj_destroy(lorakv_proj* pr) {
   if (pr->packed) cudaFree(pr->packed);
   if (pr->wk) cudaFree(pr->wk);
   if (pr->wv) cudaFree(pr->wv);
-  for (void* q : {pr->wq_packed, (void*)pr->wq, (void*)pr->aq, (void*)pr->bq}) if (q) cudaFree(q);
+  for (void* q : {pr->wq_packed, (void*)pr->wq, (void*)pr->aq, (void*)pr->bq, pr->bq_extra}) if (q) cudaFree(q);
   delete pr;
 }
 
@@ -658,6 +658,10 @@ int lorakv_proj_set_q_lora(lorakv_proj* pr, int64_t layer, int64_t agent, int64_
     LK_CUDA(cudaMalloc(&pr->aq, (size_t)(pr->n_layers * pr->d_model * rank) * sizeof(float)));
     LK_CUDA(cudaMalloc(&pr->bq, (size_t)(pr->n_layers * n_agents * rank * dq_full) * sizeof(float)));
     pr->q_rank = rank; pr->q_agents = n_agents;
+    if (pr->q_fused && rank <= 32) {
+      const int64_t dq_local = (pr->n_q_heads / pr->n_kv_heads) * pr->n_kv_local * pr->d_head;
+      LK_CUDA(cudaMalloc(&pr->bq_extra, (size_t)(pr->n_layers * n_agents * dq_local * 64) * 2));
+    }
     pr->q_scale.assign((size_t)(pr->n_layers * n_agents), 0.f);
     pr->q_lora_set.assign((size_t)(pr->n_layers * n_agents), 0);
   }
@@ -667,6 +671,12 @@ int lorakv_proj_set_q_lora(lorakv_proj* pr, int64_t layer, int64_t agent, int64_
                           cudaMemcpyHostToDevice, ctx->stream));
   LK_CUDA(cudaMemcpyAsync(pr->bq + (size_t)((layer * n_agents + agent) * rank * dq_full), b_q, (size_t)(rank * dq_full) * sizeof(float),
                           cudaMemcpyHostToDevice, ctx->stream));
+  if (pr->bq_extra) {
+    const int64_t group = pr->n_q_heads / pr->n_kv_heads, dq_local = group * pr->n_kv_local * pr->d_head;
+    LK_TRY(launch_pack_lora_b(ctx, pr->bq + (size_t)((layer * n_agents + agent) * rank * dq_full), dq_full,
+                              pr->kv_head_begin * group * pr->d_head, dq_local, rank,
+                              static_cast<char*>(pr->bq_extra) + (size_t)((layer * n_agents + agent) * dq_local * 64) * 2));
+  }
   LK_CUDA(cudaStreamSynchronize(ctx->stream));
   pr->q_scale[(size_t)(layer * n_agents + agent)] = (float)sc;
   pr->q_lora_set[(size_t)(layer * n_agents + agent)] = 1;
@@ -724,8 +734,10 @@ int lorakv_proj_query(lorakv_proj* pr, int64_t layer, int64_t agent, int64_t pos
   }
   const float* wq = fused ? nullptr : pr->wq + (size_t)(layer * pr->d_model * dq_full);
   // the packed matrix already holds only this shard's columns: its column origin is 0, B_q keeps the full width
+  const void* bq_extra = (fused && lora && pr->bq_extra) ? static_cast<const char*>(pr->bq_extra) + (size_t)((layer * pr->q_agents + agent) * dq * 64) * 2
+                                                         : nullptr;
   LK_TRY(launch_q_project(ctx, fused, packed, wq, dq_full, col0, pr->d_model, dq, pr->d_head, down, aq, bq, dq_full, rank, sc,
-                          pos_begin, dev, n_rows, dev_ld, rope != 0, q_dev));
+                          pos_begin, dev, n_rows, dev_ld, rope != 0, q_dev, bq_extra));
   if (host) {
     LK_CUDA(cudaMemcpyAsync(q_out, q_dev, q_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     LK_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -82,7 +82,8 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
 int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const float* wq_dev, int64_t ldw, int64_t col0,
                      int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev, const float* aq_dev, const float* bq_dev,
                      int64_t ldb, int64_t rank, float q_scale, int64_t pos0, const float* x_dev, int64_t n_rows, int64_t ld, bool rope,
-                     float* q_dev);
+                     float* q_dev, const void* bq_extra);
+int launch_pack_lora_b(lorakv_ctx* ctx, const float* b_dev, int64_t ldb, int64_t col0, int64_t n_cols, int64_t rank, void* packed);
 // cache_kernels.cu: x * A as dense float32 rows (tensor cores)
 int launch_xa_dense(lorakv_ctx* ctx, const float* a_dev, int64_t d_model, int64_t rank, const float* x_dev, int64_t n_rows, int64_t ld,
                     float* out_dev);

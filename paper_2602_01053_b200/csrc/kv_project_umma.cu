@@ -97,6 +97,43 @@ __global__ void pack_w_kernel(const float* __restrict__ w, int64_t ldw, int64_t 
   *reinterpret_cast<uint4*>(dst) = pk;
 }
 
+// the LoRA k block, A side: [hi(s d) | lo(s d) | 0] per row, d = x A (float32 [n_rows][rank]), as one packed A tile per row tile
+__global__ void pack_down_kernel(const float* __restrict__ down, int64_t n_rows, int rank, float scale, __nv_bfloat16* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;       // (row, 8-column chunk)
+  const int64_t total = ((n_rows + kBM - 1) / kBM) * kBM * 8;
+  if (idx >= total) return;
+  const int64_t row = idx / 8;
+  const int c = (int)(idx % 8) * 8;
+  __nv_bfloat16 v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int col = c + u;
+    float x = 0.f;
+    if (row < n_rows && col < 2 * rank) {
+      const float d = scale * down[row * rank + col % rank];
+      const float hi = __bfloat162float(__float2bfloat16_rn(d));
+      x = col < rank ? hi : d - hi;
+    }
+    v[u] = __float2bfloat16_rn(x);
+  }
+  unsigned char* dst = reinterpret_cast<unsigned char*>(out) + (row / kBM) * (int64_t)kABytes + ptx::sw128_offset((uint32_t)(row % kBM), (uint32_t)c);
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+}
+
+// the LoRA k block, B side: rows [0, r) and [r, 2r) both hold B[k][col0 + n] (bf16), the rest is zero
+__global__ void pack_lora_b_kernel(const float* __restrict__ b, int64_t ldb, int64_t col0, int n_cols, int rank, __nv_bfloat16* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;       // (k row of 64, 8-column chunk)
+  const int chunks = n_cols / 8;
+  if (idx >= (int64_t)64 * chunks) return;
+  const int k = (int)(idx / chunks), ch = (int)(idx % chunks);
+  __nv_bfloat16 v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = __float2bfloat16_rn(k < 2 * rank ? b[(int64_t)(k % rank) * ldb + col0 + (int64_t)ch * 8 + u] : 0.f);
+  const int nb = ch / 8, c = (ch % 8) * 8;
+  unsigned char* dst = reinterpret_cast<unsigned char*>(out) + (int64_t)nb * kBBlk + ptx::sw128_offset((uint32_t)k, (uint32_t)c);
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+}
+
 // cos / sin table of engine.hpp:233-236 for positions [pos0, pos0 + n): tab[(i * half + c)] = (cos, sin)
 __global__ void rope_table_kernel(int64_t pos0, int64_t n, int d_head, float2* __restrict__ tab) {
   const int half = d_head / 2;
@@ -121,6 +158,11 @@ struct ProjParams {
   int64_t row0, n_rows;        // first logical row of the call's rows; rows computed
   int64_t k_from, v_from;      // logical rows below these already exist in the K / V cache (first writer wins)
   int n_col_blocks, n_row_tiles;      // the persistent CTAs walk tiles t = blockIdx.x + i * gridDim.x, column block fastest
+  // LoRA up-projection folded into the GEMM as ONE more k block (query mode, rank <= 32): A = [hi(s d) | lo(s d) | 0],
+  // B = [B_q ; B_q ; 0] with d = x A_q -- the tensor pipe adds (s d) B_q for 1.5 % more MMA work instead of 2 r FMAs per
+  // output element in the epilogue
+  const __nv_bfloat16* xa_extra;      // [row tile][128][64] or null
+  const __nv_bfloat16* wb_extra;      // [64-column block][64][64] of this (layer, agent) or null
   // query mode (kQuery): q = rope(x * Wq + q_scale * (x * A_q) * B_q[agent]) as float32 rows (engine.hpp:362-373, :422)
   float* q_out;                // [n_rows][ldq]
   int64_t ldq;
@@ -148,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
   // block fastest so that the CTAs sharing an X tile run together and X is read from HBM once (with the row tile fastest it
   // was re-read per column block: 982 MB of DRAM reads for 151 MB of operands).  Two accumulators in TMEM (2 x 256 columns):
   // the epilogue warps drain tile i while the MMA thread already accumulates tile i + 1.
-  const int kb_n = p.d_model / kBK;
+  const int kb_w = p.d_model / kBK;                               // k blocks of the weight matrix
+  const int kb_n = kb_w + (p.xa_extra != nullptr ? 1 : 0);         // + the LoRA block
   const int total_tiles = p.n_col_blocks * p.n_row_tiles;
 
   if (tid == 0) {
@@ -168,17 +211,22 @@ __global__ void __launch_bounds__(kThreads, 1) kv_project_umma_kernel(const Proj
       int kbg = 0;                                   // k blocks issued so far: the ring runs on across tiles
       for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
         const int nblk = t % p.n_col_blocks, tile = t / p.n_col_blocks;
-        const unsigned char* a_src = reinterpret_cast<const unsigned char*>(p.xa) + (int64_t)tile * kb_n * kABytes;
+        const unsigned char* a_src = reinterpret_cast<const unsigned char*>(p.xa) + (int64_t)tile * kb_w * kABytes;
         const unsigned char* b_src = reinterpret_cast<const unsigned char*>(p.wb) + (int64_t)nblk * (kBN / 64) * p.d_model * 128;
         for (int kb = 0; kb < kb_n; ++kb, ++kbg) {
           const int s = kbg % kStages;
           if (kbg >= kStages) ptx::mbar_wait(&bars.empty[s], (uint32_t)(((kbg / kStages) & 1) ^ 1));
           ptx::mbar_arrive_expect_tx(&bars.full[s], kStageBytes);
           const uint32_t dst = ptx::smem_u32(smem + s * kStageBytes);
-          bulk_g2s(dst, a_src + (int64_t)kb * kABytes, kABytes, &bars.full[s]);
+          if (kb < kb_w) {
+            bulk_g2s(dst, a_src + (int64_t)kb * kABytes, kABytes, &bars.full[s]);
 #pragma unroll
-          for (int nb = 0; nb < kBN / 64; ++nb)
-            bulk_g2s(dst + kABytes + nb * kBBlk, b_src + (int64_t)nb * p.d_model * 128 + (int64_t)kb * kBBlk, kBBlk, &bars.full[s]);
+            for (int nb = 0; nb < kBN / 64; ++nb)
+              bulk_g2s(dst + kABytes + nb * kBBlk, b_src + (int64_t)nb * p.d_model * 128 + (int64_t)kb * kBBlk, kBBlk, &bars.full[s]);
+          } else {                                   // the LoRA block
+            bulk_g2s(dst, reinterpret_cast<const unsigned char*>(p.xa_extra) + (int64_t)tile * kABytes, kABytes, &bars.full[s]);
+            bulk_g2s(dst + kABytes, reinterpret_cast<const unsigned char*>(p.wb_extra) + (int64_t)nblk * kBBytes, kBBytes, &bars.full[s]);
+          }
         }
       }
     }
@@ -421,6 +469,15 @@ int launch_pack_w(lorakv_ctx* ctx, const float* w_dev, int64_t ldw, int64_t col0
   return LORAKV_OK;
 }
 
+int launch_pack_lora_b(lorakv_ctx* ctx, const float* b_dev, int64_t ldb, int64_t col0, int64_t n_cols, int64_t rank, void* packed) {
+  const int64_t n = 64 * (n_cols / 8);
+  pack_lora_b_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(b_dev, ldb, col0, (int)n_cols, (int)rank,
+                                                                             static_cast<__nv_bfloat16*>(packed));
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
 // rows [row0, row0 + n_rows) of the trajectory from x_dev (row i of x_dev is logical row row0 + i); K rows below k_from and V
 // rows below v_from are already cached and are not written
 int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
@@ -455,6 +512,7 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     pp.P = (int)pool->P; pp.d_model = (int)d_model; pp.n_kv_local = (int)n_kv;
     pp.row0 = row0; pp.n_rows = n_rows; pp.k_from = k_from; pp.v_from = v_from;
     pp.q_out = nullptr; pp.ldq = 0; pp.down = down_dev; pp.bq = bv_dev; pp.ldb = n_kv * d; pp.r = (int)rank; pp.q_scale = v_scale;
+    pp.xa_extra = nullptr; pp.wb_extra = nullptr;
     pp.n_col_blocks = (int)(2 * n_kv * d / kBN); pp.n_row_tiles = (int)tiles;
     const size_t smem = (size_t)kStages * kStageBytes + kLoraSmemBytes + 1024;
     LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -514,7 +572,7 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
 int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const float* wq_dev, int64_t ldw, int64_t col0,
                      int64_t d_model, int64_t n_cols, int64_t d_head, const float* down_dev, const float* aq_dev, const float* bq_dev,
                      int64_t ldb, int64_t rank, float q_scale, int64_t pos0, const float* x_dev, int64_t n_rows, int64_t ld, bool rope,
-                     float* q_dev) {
+                     float* q_dev, const void* bq_extra) {
   if (n_rows == 0 || n_cols == 0) return LORAKV_OK;
   const int64_t half = d_head / 2;
   auto up = [](size_t x) { return (x + 1023) / 1024 * 1024; };
@@ -522,9 +580,11 @@ int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const f
   if (fused) {
     const int64_t tiles = (n_rows + kBM - 1) / kBM;
     const size_t xa_bytes = (size_t)tiles * kBM * d_model * 2;
-    LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + xa_bytes));
+    const bool fold = rank > 0 && bq_extra != nullptr && down_dev != nullptr;      // LoRA as one more k block
+    LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + xa_bytes + (fold ? (size_t)tiles * kABytes : 0)));
     float2* tab = rope ? static_cast<float2*>(ctx->work.ptr) : nullptr;
     __nv_bfloat16* xa = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ctx->work.ptr) + tab_bytes);
+    __nv_bfloat16* xe = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ctx->work.ptr) + tab_bytes + xa_bytes);
     if (rope) {
       const int64_t n = n_rows * half;
       rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(pos0, n_rows, (int)d_head, tab);
@@ -533,11 +593,17 @@ int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const f
     const int64_t nx = tiles * kBM * (d_model / 8);
     pack_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, ctx->stream>>>(x_dev, n_rows, ld, (int)d_model, xa);
     ctx->launches++;
+    if (fold) {
+      const int64_t nd = tiles * kBM * 8;
+      pack_down_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, ctx->stream>>>(down_dev, n_rows, (int)rank, q_scale, xe);
+      ctx->launches++;
+    }
     ProjParams pp{};
     pp.xa = xa; pp.wb = static_cast<const __nv_bfloat16*>(wq_packed); pp.rope = tab;
     pp.d_model = (int)d_model; pp.row0 = pos0; pp.n_rows = n_rows; pp.P = 1; pp.n_kv_local = 0;
-    pp.q_out = q_dev; pp.ldq = n_cols; pp.down = rank > 0 ? down_dev : nullptr; pp.bq = bq_dev ? bq_dev + col0 : nullptr; pp.ldb = ldb;
+    pp.q_out = q_dev; pp.ldq = n_cols; pp.down = (rank > 0 && !fold) ? down_dev : nullptr; pp.bq = bq_dev ? bq_dev + col0 : nullptr; pp.ldb = ldb;
     pp.r = (int)rank; pp.q_scale = q_scale;
+    pp.xa_extra = fold ? xe : nullptr; pp.wb_extra = fold ? static_cast<const __nv_bfloat16*>(bq_extra) : nullptr;
     pp.n_col_blocks = (int)(n_cols / kBN); pp.n_row_tiles = (int)tiles;
     const size_t smem = (size_t)kStages * kStageBytes + kLoraSmemBytes + 1024;
     LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -148,6 +148,7 @@ struct lorakv_proj {
   float* wq = nullptr;       // [n_layers][d_model][n_q_heads * d_head] float32 (exact path only)
   float* aq = nullptr;       // [n_layers][d_model][q_rank]
   float* bq = nullptr;       // [n_layers][q_agents][q_rank][n_q_heads * d_head]
+  void* bq_extra = nullptr;  // [n_layers][q_agents][n_q_local * d_head / 64 blocks][64][64] bf16: B_q as one more k block (rank <= 32)
   std::vector<float> q_scale;          // [n_layers][q_agents] alpha / rank
   std::vector<uint8_t> q_set, q_lora_set;
 };

@@ -342,6 +342,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: output gather through peer-memory stores from the decode epilogue (default) or NCCL all_gather")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--per-layer-launch", action="store_true", help="one launch per layer instead of one per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -361,10 +363,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test rig for a 1-GPU box: every rank on cuda:0, rendezvous over gloo (NCCL refuses two ranks on one device).  The
+    # numbers of such a run mean nothing (the ranks time-slice one GPU); it exercises the N > 1 code path end to end.
+    share_gpu = os.environ.get("LORAKV_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local_rank = 0
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
         torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -422,7 +432,32 @@ def main():
     gathered = torch.zeros((world, n_layers, A, n_q_local * d), device=dev, dtype=torch.float32) if world > 1 else None
     agent_ids = list(range(A))
 
+    # N > 1: the end-of-step output gather.  "peer": the decode epilogue stores its rows into every rank's buffer over
+    # NVLink peer memory and a handshake kernel publishes the step (csrc/peer_gather.cu); "nccl": local slab + all_gather.
+    gather = None
+    gather_mode = "none"
+    if world > 1:
+        gather_mode = args.gather
+        if gather_mode == "peer" and not args.per_layer_launch:
+            from paper_2602_01053_b200.sharding import exchange_handles
+            try:
+                gather = pkg.Gather(ctx, rank, world, n_layers * A * n_q * d)
+                gather.connect(exchange_handles(gather.export(), device=dev))
+                flag = torch.ones(1, device=dev)
+            except abi.LorakvError as e_:
+                print(f"[bench] rank {rank}: peer gather unavailable ({e_}); using the NCCL all_gather", file=sys.stderr)
+                gather = None
+                flag = torch.zeros(1, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)          # every rank or none
+            if flag.item() == 0:
+                gather, gather_mode = None, "nccl (peer mapping failed)"
+        elif gather_mode == "peer":
+            gather_mode = "nccl (per-layer launches)"
+
     def step_device():
+        if gather is not None:
+            pool.decode_gather(ad, gather, 0, n_layers, agent_ids, n_q, q_dev=q_dev.data_ptr(), want_host=False)
+            return
         if args.per_layer_launch:
             for layer in range(n_layers):
                 pool.decode_device(ad, layer, layer + 1, agent_ids, n_q,
@@ -477,12 +512,16 @@ def main():
     q_pin[...] = q_local_host
     out_pin = ctx.pinned_array(q_local_host.shape)
     gathered_pin = ctx.pinned_array((world,) + q_local_host.shape) if world > 1 else None
+    full_pin = ctx.pinned_array((n_layers, A, n_q * d)) if gather is not None else None
 
     def step_e2e():
         if world == 1:
             pool.decode(ad, 0, n_layers, agent_ids, n_q, q_pin, out=out_pin)   # HOST call: H2D + kernels + D2H + sync
             return
-        # N > 1: pinned q -> device, kernels, the output gather, gathered slab -> pinned host
+        if gather is not None:    # pinned q -> device, kernels storing into the peers, handshake, gathered rows -> pinned host
+            pool.decode_gather(ad, gather, 0, n_layers, agent_ids, n_q, q=q_pin, out=full_pin)
+            return
+        # NCCL variant: pinned q -> device, kernels, all_gather, gathered slab -> pinned host
         ctx.h2d(q_dev.data_ptr(), q_pin)
         pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
         dist.all_gather_into_tensor(gathered.view(-1), out_dev.view(-1))   # same stream as the kernels
@@ -504,6 +543,22 @@ def main():
     e2e_value = A / (e2e_ms * 1e-3)
     io_bytes = int(q_local_host.nbytes)
     d2h_bytes = io_bytes * (world if world > 1 else 1)
+    gather_check = None
+    if gather is not None:
+        # the rows the epilogue stored into this rank's buffer against slab + all_gather + re-assembly of the same step
+        from paper_2602_01053_b200.sharding import assemble
+        got, _ = pool.decode_gather(ad, gather, 0, n_layers, agent_ids, n_q, q_dev=q_dev.data_ptr())
+        pool.decode_device(ad, 0, n_layers, agent_ids, n_q, q_dev.data_ptr(), out_dev.data_ptr())
+        dist.all_gather_into_tensor(gathered.view(-1), out_dev.view(-1))
+        torch.cuda.synchronize()
+        same = torch.tensor([float(np.array_equal(got, assemble(gathered, d).cpu().numpy()))], device=dev)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        gather_check = "bit-exact vs all_gather on every rank" if same.item() == 1.0 else "MISMATCH vs all_gather"
+    if gather is not None:      # CUDA IPC tear-down order: unmap the peers, barrier, free
+        gather.check()
+        gather.disconnect()
+        barrier()
+        gather.close()
 
     if rank != 0:
         if world > 1:
@@ -529,7 +584,7 @@ def main():
                    "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "launch": "per-layer" if args.per_layer_launch else "one launch per step over all layers",
                    "l2": f"inputs ({alg / 1e9:.2f} GB per step) larger than L2; no flush needed",
-                   "kernel": ctx.last_kernel()},
+                   "kernel": ctx.last_kernel(), "output_gather": gather_mode, "output_gather_check": gather_check},
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": d2h_bytes,
                 "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define LORAKV_ABI_VERSION 2   /* 2: projections (lorakv_proj_*), snapshot / resume */
+#define LORAKV_ABI_VERSION 3   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory */
 
 typedef struct lorakv_ctx lorakv_ctx;           /* device + stream + scratch */
 typedef struct lorakv_pool lorakv_pool;         /* paged cache of one trajectory (KvStore<T>) */
@@ -276,6 +276,43 @@ int lorakv_fla_decode_batched(lorakv_pool* pool, const lorakv_adapters* adapters
                               int64_t layer_begin, int64_t layer_end, const int32_t* agent_ids,
                               int64_t n_batch, int64_t n_q_heads, const float* q, float* out,
                               int mem_kind);
+/* ---- end-of-step output gather of a kv-head-sharded decode, over peer memory --------------------
+ * gqa_attention returns L_c x (n_q*d) rows (attention.hpp:346,359-360); q head h reads only kv head h/g
+ * (:348-354), so a rank holding kv heads [kv_head_begin, +n_kv_local) (lorakv_pool_dims) owns a column slice of
+ * every row and putting the slices side by side is the only exchange of a step.  A lorakv_gather
+ * owns one device allocation per rank -- two full outputs (alternating by step) and a flag page -- mapped into
+ * every other rank through CUDA IPC.  The decode epilogue stores its finished rows into ALL ranks' buffers
+ * directly (NVLink / NVSwitch peer stores), a one-block kernel then publishes the step number to the peers
+ * and waits for theirs; no collective library call, no local slab.
+ *   create : full_elems = (layer_end-layer_begin) * n_batch * n_q_heads * d_head floats of one step's output
+ *   export : writes this rank's LORAKV_GATHER_HANDLE_BYTES-byte handle; the caller all-gathers the handles of
+ *            ranks 0..world-1 by whatever means it has (torch.distributed, MPI, a file) ...
+ *   connect: ... and passes them back in rank order (world * LORAKV_GATHER_HANDLE_BYTES bytes)
+ * world == 1 needs no export / connect.  Ranks must issue the same sequence of gather steps. */
+typedef struct lorakv_gather lorakv_gather;
+#define LORAKV_GATHER_HANDLE_BYTES 64
+int lorakv_gather_create(lorakv_ctx* ctx, int rank, int world, int64_t full_elems, lorakv_gather** out);
+/* Tear-down order across ranks: every rank disconnects (unmaps its peers), the caller runs a barrier, then every
+ * rank destroys -- an exported allocation must outlive the mappings of it (CUDA IPC rule). */
+int lorakv_gather_disconnect(lorakv_gather* g);
+void lorakv_gather_destroy(lorakv_gather* g);
+int lorakv_gather_export(lorakv_gather* g, unsigned char* handle);
+int lorakv_gather_connect(lorakv_gather* g, const unsigned char* handles);
+/* how long a rank waits for its peers before the step fails instead of hanging (default 20 s) */
+int lorakv_gather_set_timeout_ms(lorakv_gather* g, int64_t ms);
+int lorakv_gather_steps(const lorakv_gather* g, int64_t* steps);
+/* synchronises the ctx stream and fails if a handshake enqueued so far timed out */
+int lorakv_gather_check(lorakv_gather* g);
+/* lorakv_fla_decode_batched on this rank's shard, ending in the gather.
+ *   q: [layers][n_batch][n_q_local*d_head] float32 (this rank's heads), HOST or DEVICE per q_mem_kind
+ *   out_host: NULL, or [layers][n_batch][n_q_heads*d_head] float32 HOST: the gathered rows (synchronises)
+ *   out_dev : NULL, or receives the DEVICE pointer of the gathered rows of this step; valid until the step after
+ *             next is issued; reads must be ordered on the ctx stream */
+int lorakv_fla_decode_batched_gather(lorakv_pool* pool, const lorakv_adapters* adapters, lorakv_gather* g,
+                                     int64_t layer_begin, int64_t layer_end, const int32_t* agent_ids,
+                                     int64_t n_batch, int64_t n_q_heads, const float* q, int q_mem_kind,
+                                     float* out_host, float** out_dev);
+
 /* Prefill / append-step attention of one agent on one layer: q rows cover positions
  * [query_offset, query_offset+L_c) of the cached trajectory (causal rule attention.hpp:44-46).
  *   q/out: L_c x (n_q_local*d_head) float32, dense. */

@@ -5,7 +5,7 @@ The product is ``lib/liblorakv_b200.so`` (hand-written CUDA for sm_100a behind t
 package is only the thin ctypes binding that the tests and ``bench.py`` drive the C ABI through; it
 contains no compute and no fallback: every call fails loudly when the CUDA library or a B200 is missing.
 """
-from .abi import (Adapters, Context, LorakvError, Pool, Projection, build, lib_path, load_library,  # noqa: F401
+from .abi import (Adapters, Context, Gather, LorakvError, Pool, Projection, build, lib_path, load_library,  # noqa: F401
                   BF16, F32, HOST, DEVICE, SCHEMES)
 
 __all__ = ["Adapters", "Context", "LorakvError", "Pool", "Projection", "build", "lib_path", "load_library",

@@ -125,6 +125,16 @@ SIGNATURES = {
     "lorakv_adapters_set_a_agent": (C.c_int, [_vp, _i64, _i64, _pf]),
     "lorakv_adapters_set_b": (C.c_int, [_vp, _i64, _i64, _pf, C.c_double]),
     "lorakv_fla_decode_batched": (C.c_int, [_vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, _vp, C.c_int]),
+    "lorakv_gather_create": (C.c_int, [_vp, C.c_int, C.c_int, _i64, C.POINTER(_vp)]),
+    "lorakv_gather_destroy": (None, [_vp]),
+    "lorakv_gather_disconnect": (C.c_int, [_vp]),
+    "lorakv_gather_export": (C.c_int, [_vp, C.POINTER(C.c_ubyte)]),
+    "lorakv_gather_connect": (C.c_int, [_vp, C.POINTER(C.c_ubyte)]),
+    "lorakv_gather_set_timeout_ms": (C.c_int, [_vp, _i64]),
+    "lorakv_gather_steps": (C.c_int, [_vp, C.POINTER(_i64)]),
+    "lorakv_gather_check": (C.c_int, [_vp]),
+    "lorakv_fla_decode_batched_gather": (C.c_int, [_vp, _vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, C.c_int, _vp,
+                                                   C.POINTER(_vp)]),
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
     "lorakv_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "lorakv_ctx_last_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
@@ -149,7 +159,7 @@ def load_library(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lorakv_abi_version() != 2:
+    if lib.lorakv_abi_version() != 3:
         raise LorakvError("liblorakv_b200.so ABI version mismatch")
     if path is None:
         _lib = lib
@@ -414,6 +424,56 @@ class Adapters:
         _check(self.ctx.lib.lorakv_adapters_set_b(self.h, layer, agent, b.ctypes.data_as(_pf), alpha))
 
 
+class Gather:
+    """lorakv_gather: the end-of-step output gather of a kv-head-sharded decode over peer memory."""
+    HANDLE_BYTES = 64
+
+    def __init__(self, ctx: Context, rank: int, world: int, full_elems: int):
+        self.ctx, self.rank, self.world, self.full_elems = ctx, rank, world, int(full_elems)
+        h = _vp()
+        _check(ctx.lib.lorakv_gather_create(ctx.h, rank, world, self.full_elems, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.lorakv_gather_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def disconnect(self):
+        """Unmap the peers' buffers; barrier across ranks before close()."""
+        _check(self.ctx.lib.lorakv_gather_disconnect(self.h))
+
+    def export(self) -> bytes:
+        buf = (C.c_ubyte * self.HANDLE_BYTES)()
+        _check(self.ctx.lib.lorakv_gather_export(self.h, buf))
+        return bytes(buf)
+
+    def connect(self, handles):
+        """handles: the exported handles of ranks 0..world-1, in rank order (bytes each, or one joined blob)."""
+        blob = handles if isinstance(handles, (bytes, bytearray)) else b"".join(handles)
+        if len(blob) != self.world * self.HANDLE_BYTES:
+            raise LorakvError(f"gather_connect: {len(blob)} handle bytes for world size {self.world}")
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(self.ctx.lib.lorakv_gather_connect(self.h, buf))
+
+    def set_timeout_ms(self, ms: int):
+        _check(self.ctx.lib.lorakv_gather_set_timeout_ms(self.h, ms))
+
+    def steps(self) -> int:
+        n = _i64()
+        _check(self.ctx.lib.lorakv_gather_steps(self.h, C.byref(n)))
+        return n.value
+
+    def check(self):
+        _check(self.ctx.lib.lorakv_gather_check(self.h))
+
+
 class Projection:
     """lorakv_proj: Wk / Wv per layer for the fused projection + RoPE + append (engine.hpp:376-403)."""
 
@@ -656,6 +716,26 @@ class Pool:
         _check(self.ctx.lib.lorakv_fla_decode_batched(
             self.h, adapters.h if adapters else None, layer_begin, layer_end,
             ids.ctypes.data_as(C.POINTER(C.c_int32)), len(ids), n_q_heads, _vp(q_dev), _vp(out_dev), DEVICE))
+
+    def decode_gather(self, adapters, gather, layer_begin, layer_end, agent_ids, n_q_heads, q=None, q_dev=None, out=None,
+                      want_host=True):
+        """This rank's shard of a decode step ending in the peer-memory output gather.  Returns (full host array or
+        None, device pointer of the gathered rows)."""
+        ids = np.ascontiguousarray(agent_ids, dtype=np.int32)
+        n_layers = layer_end - layer_begin
+        if q is not None:
+            q = np.ascontiguousarray(q, dtype=np.float32)
+            qp, kind = q.ctypes.data_as(_vp), HOST
+        else:
+            qp, kind = _vp(q_dev), DEVICE
+        if want_host and out is None:
+            out = np.zeros((n_layers, len(ids), gather.full_elems // (n_layers * len(ids))), dtype=np.float32)
+        dev = _vp()
+        _check(self.ctx.lib.lorakv_fla_decode_batched_gather(
+            self.h, adapters.h if adapters else None, gather.h, layer_begin, layer_end,
+            ids.ctypes.data_as(C.POINTER(C.c_int32)), len(ids), n_q_heads, qp, kind,
+            out.ctypes.data_as(_vp) if want_host else None, C.byref(dev)))
+        return (out if want_host else None), dev.value
 
     def prefill(self, adapters, layer, agent, n_q_heads, q, query_offset):
         q = np.ascontiguousarray(q, dtype=np.float32)

@@ -1021,7 +1021,7 @@ static int visible_rows(const lorakv_pool* pool, int64_t layer, int64_t kv_set, 
 static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer_begin, int64_t layer_end,
                      int64_t kv_set, int64_t lr_set, const int32_t* agent_ids, int64_t n_batch,
                      int64_t rows_per_entry, int64_t query_offset, int64_t n_q_heads, const float* q,
-                     float* out, int mem_kind) {
+                     float* out, int mem_kind, const lk::PeerOut* peers = nullptr) {
   lorakv_ctx* ctx = pool->ctx;
   LK_CUDA(cudaSetDevice(ctx->device));
   if (layer_begin < 0 || layer_end > pool->dims.n_layers || layer_begin >= layer_end) return fail("attention: bad layer range");
@@ -1059,15 +1059,17 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   const size_t q_bytes = (size_t)n_elems * sizeof(float);
   const bool host = mem_kind == LORAKV_HOST;
   if (!host && mem_kind != LORAKV_DEVICE) return fail("bad mem_kind %d", mem_kind);
-  LK_TRY(scratch_reserve(ctx, ctx->out, ids_bytes + (host ? 2 * ((q_bytes + 255) / 256 * 256) : 0)));
+  // with a peer gather the rows go to the gather buffers; the local slab only serves the paths without a merge epilogue
+  const bool local_slab = host || peers;
+  LK_TRY(scratch_reserve(ctx, ctx->out, ids_bytes + (local_slab ? 2 * ((q_bytes + 255) / 256 * 256) : 0)));
   char* base = static_cast<char*>(ctx->out.ptr);
   int32_t* ids_dev = reinterpret_cast<int32_t*>(base);
   LK_CUDA(cudaMemcpyAsync(ids_dev, ids_host, (size_t)n_batch * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
   const float* q_dev = q;
   float* out_dev = out;
+  if (local_slab) out_dev = reinterpret_cast<float*>(base + ids_bytes + (q_bytes + 255) / 256 * 256);
   if (host) {
     float* qd = reinterpret_cast<float*>(base + ids_bytes);
-    out_dev = reinterpret_cast<float*>(base + ids_bytes + (q_bytes + 255) / 256 * 256);
     LK_CUDA(cudaMemcpyAsync(qd, q, q_bytes, cudaMemcpyHostToDevice, ctx->stream));
     q_dev = qd;
   }
@@ -1078,10 +1080,17 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   call.rows_per_entry = rows_per_entry; call.query_offset = query_offset; call.n_q_local = n_q_local;
   call.L = L; call.q_dev = q_dev; call.out_dev = out_dev;
   call.agent_host = ids_host[0];
-  if (ctx->policy == 0 && decode_umma_supported(call)) LK_TRY(launch_decode_umma(call));
-  else if (ctx->policy != 1 && decode_tma_supported(call)) LK_TRY(launch_decode_tma(call));
+  call.peers = peers;
+  bool rows_at_peers = false;    // the decode kernels' merge epilogue stores straight into the gather buffers
+  if (ctx->policy == 0 && decode_umma_supported(call)) { LK_TRY(launch_decode_umma(call)); rows_at_peers = true; }
+  else if (ctx->policy != 1 && decode_tma_supported(call)) { LK_TRY(launch_decode_tma(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
   else LK_TRY(launch_paged_simt(call));
+  if (peers) {
+    if (!rows_at_peers)
+      LK_TRY(launch_peer_scatter(ctx, out_dev, n_layers * n_batch * rows_per_entry, n_q_local, pool->dims.d_head, *peers));
+    return LORAKV_OK;      // the caller publishes the step and reads the gathered rows
+  }
 
   if (host) {
     LK_CUDA(cudaMemcpyAsync(out, out_dev, q_bytes, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1110,6 +1119,57 @@ int lorakv_fla_decode_batched(lorakv_pool* pool, const lorakv_adapters* ad, int6
   LK_TRY(visible_rows(pool, layer_begin, kv_set, lr_set, &L));
   if (L < 1) return fail("attention: query_offset 0 with L_c 1 exceeds L 0");
   return run_paged(pool, ad, layer_begin, layer_end, kv_set, lr_set, agent_ids, n_batch, 1, L - 1, n_q_heads, q, out, mem_kind);
+}
+
+// Sharded decode step ending in the output gather over peer memory (peer_gather.cu).
+int lorakv_fla_decode_batched_gather(lorakv_pool* pool, const lorakv_adapters* ad, lorakv_gather* g, int64_t layer_begin,
+                                     int64_t layer_end, const int32_t* agent_ids, int64_t n_batch, int64_t n_q_heads,
+                                     const float* q, int q_mem_kind, float* out_host, float** out_dev) {
+  if (!pool || !g || !q) return fail("fla_decode_batched_gather: null argument");
+  if (n_batch < 1) return fail("fla_decode_batched: empty batch");
+  if (g->ctx != pool->ctx) return fail("fla_decode_batched_gather: the gather and the pool belong to different contexts");
+  if (!g->connected) return fail("fla_decode_batched_gather: the gather is not connected to its peers (lorakv_gather_connect)");
+  if (pool->dims.scheme == LORAKV_NONSHARED || (pool->dims.scheme == LORAKV_BASESHARED && pool->r_pad > 0))
+    return fail("fla_decode_batched_gather: scheme %s keeps per-agent caches; batch one agent per call", kSchemeName[pool->dims.scheme]);
+  if (n_q_heads < 1 || n_q_heads % pool->dims.n_kv_heads != 0)
+    return fail("gqa_attention: n_q_heads %lld not divisible by n_kv_heads %lld", (long long)n_q_heads, (long long)pool->dims.n_kv_heads);
+  const int64_t n_layers = layer_end - layer_begin;
+  const int64_t full = n_layers * n_batch * n_q_heads * pool->dims.d_head;
+  if (full != g->full_elems)
+    return fail("fla_decode_batched_gather: the step produces %lld output floats, the gather was created for %lld", (long long)full,
+                (long long)g->full_elems);
+  int64_t L;
+  LK_TRY(visible_rows(pool, layer_begin, 0, 0, &L));
+  if (L < 1) return fail("attention: query_offset 0 with L_c 1 exceeds L 0");
+  const uint32_t epoch = g->epoch + 1;
+  lk::PeerOut peers;
+  peers.n = g->world;
+  for (int i = 0; i < g->world; ++i) peers.dst[i] = lk::gather_buffer(g, i, epoch);
+  peers.n_q_total = n_q_heads;
+  peers.q_head_begin = pool->dims.kv_head_begin * (n_q_heads / pool->dims.n_kv_heads);
+  LK_TRY(run_paged(pool, ad, layer_begin, layer_end, 0, 0, agent_ids, n_batch, 1, L - 1, n_q_heads, q, nullptr, q_mem_kind, &peers));
+  g->epoch = epoch;
+  LK_TRY(lk::gather_sync(g));
+  float* mine = lk::gather_buffer(g, g->rank, epoch);
+  if (out_dev) *out_dev = mine;
+  if (out_host) {
+    lorakv_ctx* ctx = pool->ctx;
+    LK_CUDA(cudaMemcpyAsync(out_host, mine, (size_t)full * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    LK_TRY(lk::gather_read_status(g));
+    LK_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (*g->status_host != 0) return fail("peer gather: rank %d waited %.1f s for a peer that never published step %u", g->rank,
+                                          g->timeout_ns * 1e-9, epoch);
+  }
+  return LORAKV_OK;
+}
+
+/* Status of the gathers enqueued so far (synchronises the ctx stream): fails if a handshake timed out. */
+int lorakv_gather_check(lorakv_gather* g) {
+  if (!g) return fail("gather_check: null argument");
+  LK_TRY(lk::gather_read_status(g));
+  LK_CUDA(cudaStreamSynchronize(g->ctx->stream));
+  if (*g->status_host != 0) return fail("peer gather: rank %d waited %.1f s for a peer that never arrived", g->rank, g->timeout_ns * 1e-9);
+  return LORAKV_OK;
 }
 
 int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer, int64_t agent,

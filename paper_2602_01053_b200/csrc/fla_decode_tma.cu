@@ -404,7 +404,21 @@ struct DecodeMergeParams {
   const float* scale;    // [n_layers][n_agents]
   int64_t n_agents;
   float* out;            // [layers][n_batch][n_q_local * d]
+  PeerOut peers;         // n > 0: the row goes to every rank's [layers][n_batch][n_q_total * d] buffer instead
 };
+
+// Address of the output row of (layer, batch entry, local q head): the local slab, or -- when the step ends in the
+// output gather -- the same row of the full-width buffer (the stores then fan out to every peer, store_row).
+__device__ __forceinline__ int64_t merge_row_offset(const DecodeMergeParams& p, int64_t layer_rel, int entry, int64_t head) {
+  if (p.peers.n == 0) return ((layer_rel * p.n_batch + entry) * p.n_q_local + head) * p.D;
+  return ((layer_rel * p.n_batch + entry) * p.peers.n_q_total + p.peers.q_head_begin + head) * p.D;
+}
+__device__ __forceinline__ void store_out(const DecodeMergeParams& p, int64_t off, float v) {
+  if (p.peers.n == 0) { p.out[off] = v; return; }
+#pragma unroll
+  for (int pe = 0; pe < kMaxPeers; ++pe)          // constant indices: the table stays in the parameter bank
+    if (pe < p.peers.n) p.peers.dst[pe][off] = v;
+}
 
 constexpr int kMergeWarps = 8;
 
@@ -494,7 +508,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   const int agent = p.agent_ids ? p.agent_ids[entry] : 0;
   const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
-  float* dst = p.out + ((layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * p.D;
+  const int64_t dst = merge_row_offset(p, layer_rel, entry, (int64_t)kvh * p.group + gi);
   const float inv_l = 1.0f / stat_s[1];
   auto total = [&](int c) {
     float t = 0.f;
@@ -504,7 +518,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   for (int c = tid; c < p.D; c += kMergeWarps * 32) {
     float o = total(c);
     for (int k = 0; k < p.r; ++k) o = fmaf(scale * total(p.D + k), b[k * dkv + c], o);
-    dst[c] = o * inv_l;
+    store_out(p, dst + c, o * inv_l);
   }
 }
 
@@ -621,7 +635,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   const int agent = p.agent_ids ? p.agent_ids[entry] : 0;
   const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
-  float* dst = p.out + ((layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * p.D;
+  const int64_t dst = merge_row_offset(p, layer_rel, entry, (int64_t)kvh * p.group + gi);
   const float inv_l = 1.0f / lsum;
 #pragma unroll
   for (int i = 0; i < kMaxCols; ++i) {
@@ -629,15 +643,17 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
     if (c < p.D) {
       float o = acc[i];
       for (int k = 0; k < p.r; ++k) o = fmaf(scale * olr_s[warp][k], b[k * dkv + c], o);
-      dst[c] = o * inv_l;
+      store_out(p, dst + c, o * inv_l);
     }
   }
 }
 
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
-                        const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers) {
+                        const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
+                        const PeerOut* peers) {
   DecodeMergeParams mp;
+  if (peers) mp.peers = *peers;
   mp.part = part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;
   mp.n_kv_local = n_kv_local; mp.n_batch = n_batch; mp.rows_total = rows_total;
   mp.row_blocks = row_blocks; mp.T = T; mp.G = G; mp.layer_begin = layer_begin; mp.n_q_local = n_q_local;
@@ -726,7 +742,7 @@ int launch_decode_tma(const PagedAttnCall& c) {
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));
 
   LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,
-                             T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers));
+                             T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers));
   ctx->last_kernel = "fla_decode_tma";
   return LORAKV_OK;
 }

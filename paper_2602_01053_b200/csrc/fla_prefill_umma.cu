@@ -653,7 +653,7 @@ int launch_decode_umma(const PagedAttnCall& c) {
   // T = splits * G tiles per unit and G tiles per worker, one segment per worker
   LK_TRY(launch_decode_merge(ctx, pp.part, d, rp, r, /*MW=*/8, pp.group, (int)pool->n_kv_local, (int)c.n_batch, pp.rows_total,
                              /*row_blocks=*/1, /*T=*/splits * tiles_per_split, /*G=*/tiles_per_split, c.layer_begin, c.n_q_local,
-                             /*max_seg=*/1, c.agent_ids_dev, c.adapters, c.out_dev, n_layers));
+                             /*max_seg=*/1, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers));
   ctx->last_kernel = "fla_decode_umma";
   return LORAKV_OK;
 }

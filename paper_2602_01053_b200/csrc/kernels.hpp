@@ -39,6 +39,17 @@ int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, in
 int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                        int64_t n_rows, float* dst_dev);
 
+// Where a finished output row goes when the step ends in the output gather of a kv-head-sharded run
+// (peer_gather.cu): the epilogue stores its slice of the FULL row [n_q_total * d] straight into every rank's
+// peer-mapped buffer over NVLink instead of a local slab that a collective would move afterwards.
+constexpr int kMaxPeers = 8;
+struct PeerOut {
+  float* dst[kMaxPeers];   // [layers][n_batch][n_q_total * d] on every rank (own rank included)
+  int n = 0;               // 0: plain local store
+  int64_t n_q_total = 0;   // q heads of the full output row
+  int64_t q_head_begin = 0;  // first q head this shard owns
+};
+
 // fla_paged_simt.cu ---------------------------------------------------------------------------
 struct PagedAttnCall {
   lorakv_pool* pool;
@@ -54,6 +65,7 @@ struct PagedAttnCall {
   int64_t L;                        // cached rows visible to the kernel (min over K, V, LR buffers)
   const float* q_dev;               // [layers][n_batch][rows_per_entry][n_q_local*d]
   float* out_dev;                   // same shape
+  const PeerOut* peers = nullptr;   // decode only: store finished rows into the peers' gather buffers as well
 };
 int launch_paged_simt(const PagedAttnCall& call);
 
@@ -63,7 +75,8 @@ int launch_decode_tma(const PagedAttnCall& call);
 // split merge + up-projection epilogue over the partial layout both decode kernels write
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
-                        const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers);
+                        const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
+                        const PeerOut* peers = nullptr);
 
 // fla_prefill_umma.cu (tcgen05 / TMEM / TMA; bf16 pages, prefill blocks) ---------------------------------
 bool prefill_umma_supported(const PagedAttnCall& call);
@@ -100,6 +113,9 @@ int launch_rows_q_project(lorakv_ctx* ctx, const void* wq_packed, int64_t d_mode
                           int64_t ld, bool rope, float* q_dev);
 int launch_rows_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set, int64_t row0,
                            const float* x_dev, int64_t n_rows, int64_t ld);
+
+// peer_gather.cu: local slab [layers][n_batch][n_q_local * d] -> every peer's full buffer (paths without the merge epilogue)
+int launch_peer_scatter(lorakv_ctx* ctx, const float* slab_dev, int64_t rows, int64_t n_q_local, int64_t d, const PeerOut& peers);
 
 // umma_selftest.cu ------------------------------------------------------------------------------------
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,

@@ -129,6 +129,29 @@ struct lorakv_adapters {
   std::vector<uint8_t> a_set, b_set, a_agent_set;
 };
 
+// End-of-step output gather of a kv-head-sharded run over peer memory (peer_gather.cu).  Every rank owns one
+// allocation {flags, full output x 2} and maps every other rank's through CUDA IPC; the decode epilogue stores
+// its slice of the output rows into all of them, a one-block kernel then publishes the step number to the
+// peers' flag words and waits for theirs.
+struct lorakv_gather {
+  lorakv_ctx* ctx = nullptr;
+  int rank = 0, world = 1;
+  int64_t full_elems = 0;            // floats of one full output [layers][n_batch][n_q * d]
+  size_t buf_bytes = 0;              // flags page + 2 * full output
+  char* local = nullptr;             // this rank's allocation
+  char* peer[8] = {};                // every rank's allocation as mapped here (peer[rank] == local)
+  bool connected = false;
+  uint32_t epoch = 0;                // steps gathered so far
+  uint32_t* status_host = nullptr;   // pinned word the status flag is read back into
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+};
+
+namespace lk {
+int gather_sync(lorakv_gather* g);                                         // peer_gather.cu
+float* gather_buffer(const lorakv_gather* g, int rank, uint32_t epoch);
+int gather_read_status(lorakv_gather* g);                                  // enqueue the status read-back
+}  // namespace lk
+
 // Projection weights of the step that feeds the cache (engine.hpp:376-403): Wk, Wv per layer, restricted to
 // the kv heads this shard holds.  bf16 pools with d_head 128 keep them packed for the tcgen05 kernel
 // (kv_project_umma.cu), every other case keeps the caller's float32 matrices.

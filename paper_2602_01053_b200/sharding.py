@@ -65,3 +65,16 @@ def gather_outputs(out_local, group=None):
     gathered = torch.empty((world,) + tuple(out_local.shape), dtype=out_local.dtype, device=out_local.device)
     dist.all_gather_into_tensor(gathered.view(-1), out_local.contiguous().view(-1), group=group)
     return gathered
+
+
+def exchange_handles(handle: bytes, group=None, device=None):
+    """All-gather one fixed-size byte blob per rank (the lorakv_gather_export handles) and return them in rank
+    order, ready for lorakv_gather_connect.  `device`: where the staging tensor lives (a CUDA device under NCCL,
+    None under gloo)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    mine = torch.tensor(list(handle), dtype=torch.uint8, device=device)
+    everyone = torch.empty((world, len(handle)), dtype=torch.uint8, device=device)
+    dist.all_gather_into_tensor(everyone.view(-1), mine, group=group)
+    return [bytes(row.tolist()) for row in everyone.cpu()]

@@ -35,9 +35,14 @@ def _worker(rank, world, port, out_dir):
             local[l, a] = orc.gqa_attention(shard.slice_q(q[a], d), shard.slice_kv(k, d), shard.slice_kv(v, d), v_lr,
                                             shard.slice_kv(b[a], d), s, L - 1, shard.n_q_local, shard.n_kv_local)[0]
             full[l, a] = orc.gqa_attention(q[a], k, v, v_lr, b[a], s, L - 1, n_q, n_kv)[0]
+    # the handle exchange of the peer-memory gather (lorakv_gather_export -> lorakv_gather_connect): rank order, bytes intact
+    from paper_2602_01053_b200.sharding import exchange_handles
+    blob = bytes((7 * rank + i) % 256 for i in range(64))
+    handles = exchange_handles(blob)
+    handles_ok = handles == [bytes((7 * p + i) % 256 for i in range(64)) for p in range(world)]
     gathered = gather_outputs(torch.from_numpy(local))
     got = assemble(gathered, d).numpy()
-    np.save(os.path.join(out_dir, f"ok_{rank}.npy"), np.array([np.array_equal(got, full), got.shape == full.shape]))
+    np.save(os.path.join(out_dir, f"ok_{rank}.npy"), np.array([np.array_equal(got, full), got.shape == full.shape, handles_ok]))
     dist.barrier()
     dist.destroy_process_group()
 

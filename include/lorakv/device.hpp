@@ -75,6 +75,47 @@ inline Matrix<float> decode_batched(KvStore<float>& store, const AdapterTable* t
   return out;
 }
 
+// End-of-step output gather of a kv-head-sharded decode over peer memory (lorakv_gather_*, csrc/peer_gather.cu):
+// every rank's decode epilogue stores its column slice of the output rows straight into all ranks' buffers.
+//   OutputGather g(rank, world, layers * batch * n_q_heads * d_head);
+//   exchange g.handle() with the other ranks (MPI_Allgather, a file, ...), g.connect(all handles in rank order);
+//   each step: Matrix<float> full = decode_batched_gather(store, tables, g, ...);   // rows x (n_q_heads * d_head)
+//   tear-down: g.disconnect(); barrier; destructor.
+class OutputGather {
+ public:
+  OutputGather(int rank, int world, idx full_elems) { b200::check(lorakv_gather_create(b200::Runtime::ctx(), rank, world, full_elems, &h_)); }
+  ~OutputGather() { lorakv_gather_destroy(h_); }
+  OutputGather(const OutputGather&) = delete;
+  OutputGather& operator=(const OutputGather&) = delete;
+  std::vector<unsigned char> handle() const {
+    std::vector<unsigned char> h(LORAKV_GATHER_HANDLE_BYTES);
+    b200::check(lorakv_gather_export(h_, h.data()));
+    return h;
+  }
+  void connect(const std::vector<unsigned char>& handles_in_rank_order) { b200::check(lorakv_gather_connect(h_, handles_in_rank_order.data())); }
+  void disconnect() { b200::check(lorakv_gather_disconnect(h_)); }
+  idx steps() const { std::int64_t n = 0; b200::check(lorakv_gather_steps(h_, &n)); return n; }
+  lorakv_gather* raw() const { return h_; }
+
+ private:
+  lorakv_gather* h_ = nullptr;
+};
+
+// q: this rank's heads, [(layer_end - layer_begin) * agents.size()] rows x (n_q_local * d_head);
+// result: the gathered rows of ALL heads, same row count x (n_q_heads * d_head)
+inline Matrix<float> decode_batched_gather(KvStore<float>& store, const AdapterTable* tables, OutputGather& gather, idx layer_begin,
+                                           idx layer_end, const std::vector<std::int32_t>& agents, idx n_q_heads, const Matrix<float>& q) {
+  const idx n_batch = static_cast<idx>(agents.size());
+  if (q.rows != (layer_end - layer_begin) * n_batch)
+    fail("decode_batched: q has " + std::to_string(q.rows) + " rows, expected layers x batch = " +
+         std::to_string((layer_end - layer_begin) * n_batch));
+  const DeviceOptions& o = store.device_options();
+  Matrix<float> out(q.rows, n_q_heads * (store.dims().d_kv / o.n_kv_heads));
+  b200::check(lorakv_fla_decode_batched_gather(store.handle(), tables ? tables->handle() : nullptr, gather.raw(), layer_begin, layer_end,
+                                               agents.data(), n_batch, n_q_heads, q.data.data(), LORAKV_HOST, out.data.data(), nullptr));
+  return out;
+}
+
 inline Matrix<float> prefill(KvStore<float>& store, const AdapterTable* tables, idx layer, idx agent, idx n_q_heads,
                              const Matrix<float>& q, idx query_offset) {
   Matrix<float> out(q.rows, q.cols);

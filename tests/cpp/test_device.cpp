@@ -71,6 +71,17 @@ void run_config(bool bf16, double tol, idx L, idx n_q, idx n_kv, idx d, idx r, i
       CHECK_LE(max_rel_error(got, want), tol);
     }
   }
+  // the same step ending in the peer-memory output gather: with one rank the gathered rows ARE the decode's rows
+  {
+    OutputGather gather(0, 1, layers * agents * n_q * d);
+    CHECK(gather.handle().size() == std::size_t(LORAKV_GATHER_HANDLE_BYTES));
+    for (int rep = 0; rep < 3; ++rep) {      // both buffers of the pair
+      const Matrix<float> full = decode_batched_gather(store, &tables, gather, 0, layers, batch, n_q, q);
+      REQUIRE(full.rows == out.rows); REQUIRE(full.cols == out.cols);
+      CHECK(full.data == out.data);
+    }
+    CHECK(gather.steps() == 3);
+  }
   // prefill block of agent 1 on layer 0 at the tail of the cache
   const idx L_c = std::min<idx>(L, 9);
   const Matrix<float> qp = rnd(Matrix<float>::gaussian(L_c, n_q * d, Rng(99), 1.0 / std::sqrt(double(d))));

@@ -1084,6 +1084,7 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   bool rows_at_peers = false;    // the decode kernels' merge epilogue stores straight into the gather buffers
   if (ctx->policy == 0 && decode_umma_supported(call)) { LK_TRY(launch_decode_umma(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && decode_tma_supported(call)) { LK_TRY(launch_decode_tma(call)); rows_at_peers = true; }
+  else if (ctx->policy != 1 && decode_f32_supported(call)) { LK_TRY(launch_decode_f32(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
   else LK_TRY(launch_paged_simt(call));
   if (peers) {

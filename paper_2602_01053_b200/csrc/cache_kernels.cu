@@ -69,9 +69,11 @@ __global__ void kv_append_scatter_kernel(PageAddr a, int64_t row0, const float* 
     pk.z = *reinterpret_cast<uint32_t*>(&p2); pk.w = *reinterpret_cast<uint32_t*>(&p3);
     *reinterpret_cast<uint4*>(dst) = pk;
   } else {
+    // fp32 pages swizzle 16-byte chunks (page_layout.cuh): the two halves are placed separately
     float* df = reinterpret_cast<float*>(dst);
+    float* df2 = df - page_offset(a.lay, (int)(row % a.P), c) + page_offset(a.lay, (int)(row % a.P), c + 4);
     *reinterpret_cast<float4*>(df) = make_float4(x[0], x[1], x[2], x[3]);
-    *reinterpret_cast<float4*>(df + 4) = make_float4(x[4], x[5], x[6], x[7]);
+    *reinterpret_cast<float4*>(df2) = make_float4(x[4], x[5], x[6], x[7]);
   }
 }
 

@@ -78,6 +78,10 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
                         const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
                         const PeerOut* peers = nullptr);
 
+// fla_decode_f32.cu (the same streaming decode over fp32 pages: 3 x TF32 mma.sync, fp32 accuracy) ----------
+bool decode_f32_supported(const PagedAttnCall& call);
+int launch_decode_f32(const PagedAttnCall& call);
+
 // fla_prefill_umma.cu (tcgen05 / TMEM / TMA; bf16 pages, prefill blocks) ---------------------------------
 bool prefill_umma_supported(const PagedAttnCall& call);
 int launch_prefill_umma(const PagedAttnCall& call);

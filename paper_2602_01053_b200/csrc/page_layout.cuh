@@ -3,8 +3,11 @@
 // The reference keeps each cache as a contiguous row-major GrowMat (proj/include/lorakv/kvcache.hpp:
 // 161-206); pages are this library's layout and are chosen for the kernels that read them:
 //
-//   fp32 pages, and bf16 pages whose row width is not a multiple of 8 elements:
-//       row-major [P tokens][width]
+//   fp32 pages: row-major [P tokens][width]; when the width is a multiple of 4 elements the 16-byte chunks of a
+//       row are XOR-swizzled with the token index -- chunk' = chunk ^ (t & swz), swz + 1 = the largest power of two
+//       <= 8 that divides the chunks per row -- so that a contiguous bulk copy of 8 tokens lands in shared memory
+//       as a tile whose TF32 MMA fragments (fla_decode_f32.cu) load without bank conflicts
+//   bf16 pages whose row width is not a multiple of 8 elements: row-major [P tokens][width]
 //   bf16 pages (the hot path):
 //       [width / bw column blocks][P tokens][bw elements], bw = 64 when width % 64 == 0, the width
 //       itself when it is 8, 16 or 32, and 8 otherwise.  Inside a block every token owns one row of
@@ -25,11 +28,18 @@ struct PageLayout {
   int width;    // elements per token row (d_head, or the padded rank)
   int bw;       // column-block width in elements; == width for row-major pages
   int swz;      // chunks_per_row - 1 when swizzled, 0 otherwise
+  int eb;       // bytes per element
 };
 
 __host__ __device__ inline PageLayout make_page_layout(int P, int width, int elem_bytes) {
   PageLayout l;
-  l.P = P; l.width = width; l.bw = width; l.swz = 0;
+  l.P = P; l.width = width; l.bw = width; l.swz = 0; l.eb = elem_bytes;
+  if (elem_bytes == 4 && width > 0 && width % 4 == 0) {
+    const int chunks = width / 4;
+    int s = 1;
+    while (s < 8 && chunks % (2 * s) == 0) s *= 2;
+    l.swz = s - 1;
+  }
   if (elem_bytes == 2 && width > 0 && width % 8 == 0) {
     if (width % 64 == 0) l.bw = 64;
     else if (width == 8 || width == 16 || width == 32) l.bw = width;
@@ -41,6 +51,7 @@ __host__ __device__ inline PageLayout make_page_layout(int P, int width, int ele
 
 // element offset of (token t, column c) from the start of the page
 __host__ __device__ inline int64_t page_offset(const PageLayout& l, int t, int c) {
+  if (l.eb == 4) return (int64_t)t * l.width + ((((c >> 2) ^ (t & l.swz)) << 2) | (c & 3));
   if (l.bw == l.width && l.swz == 0) return (int64_t)t * l.width + c;
   const int blk = c / l.bw, cc = c % l.bw;
   uint32_t byte = (uint32_t)t * (uint32_t)(2 * l.bw) + (uint32_t)(cc >> 3) * 16u;

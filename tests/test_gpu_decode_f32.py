@@ -1,0 +1,91 @@
+"""fp32 mode of the decode path (fla_decode_f32: TMA bulk-copy rings over swizzled fp32 pages + 3 x TF32 mma.sync)
+against the CPU oracle through the C ABI.  Oracle = gqa_attention per (agent, layer) (attention.hpp:332-363), as
+engine.hpp:440-443 calls it; tolerance 1e-4 on max_rel_error (BASELINE.json north_star, fp32 mode; cli.cpp:94).
+Needs a B200."""
+import numpy as np
+import pytest
+
+from tests.test_gpu_pool import build_pool
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2602_01053_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def check(ctx, orc, pool, ad, layers, batch, n_q, n_kv, L, amp_note=""):
+    n_layers = len(layers)
+    qs = np.stack([np.stack([layers[l][0][a][0] for a in batch]) for l in range(n_layers)])
+    outs = {}
+    for policy, kernel in ((0, "fla_decode_f32"), (1, "fla_paged_simt")):
+        ctx.set_kernel_policy(policy)
+        out = pool.decode(ad, 0, n_layers, batch, n_q, qs)
+        assert ctx.last_kernel() == kernel, (policy, ctx.last_kernel())
+        outs[policy] = out
+        worst = 0.0
+        for l in range(n_layers):
+            q, k, v, v_lr, b, s = layers[l]
+            for i, a in enumerate(batch):
+                bb = b[a] if len(b) else np.zeros((0, k.shape[1]), np.float32)
+                want = orc.gqa_attention(q[a], k, v, v_lr, bb, s, L - 1, n_q, n_kv)
+                worst = max(worst, orc.max_rel_error(out[l, i][None, :], want))
+        assert worst <= TOL, (policy, worst, amp_note)
+    ctx.set_kernel_policy(0)
+    assert orc.max_rel_error(outs[0].reshape(1, -1), outs[1].reshape(1, -1)) <= TOL
+
+
+# n_q, n_kv, d, r, agents, L, P, layers
+SHAPES = [
+    (8, 2, 128, 16, 3, 1000, 64, 2),    # 12 rows: one warp per worker (the Llama cfg-2 row count)
+    (32, 8, 128, 16, 3, 257, 64, 1),    # Llama head counts
+    (8, 2, 128, 64, 8, 777, 32, 1),     # 32 rows, rank 64: two warps per worker
+    (4, 1, 128, 32, 16, 530, 64, 1),    # 64 rows, rank 32: four warps per worker
+    (16, 2, 64, 8, 12, 300, 16, 1),     # 96 rows, d = 64, rank 8 padded to 16
+    (8, 1, 128, 4, 20, 211, 8, 1),      # 160 rows: two 128-row blocks; 8-token pages
+    (4, 2, 64, 24, 2, 130, 128, 3),     # rank 24 padded to 32, 128-token pages, 3 layers
+    (4, 2, 128, 0, 2, 333, 64, 1),      # rank 0: plain attention (FullShared contents)
+]
+
+
+@pytest.mark.parametrize("n_q,n_kv,d,r,A,L,P,n_layers", SHAPES)
+def test_decode_f32_matches_reference_path(ctx, orc, n_q, n_kv, d, r, A, L, P, n_layers):
+    from paper_2602_01053_b200 import abi
+    scheme = "BaseLRShared" if r > 0 else "FullShared"
+    pool, ad, layers = build_pool(ctx, orc, scheme, abi.F32, 2000 + L, L, n_layers, n_q, n_kv, d, r, A, P=P)
+    check(ctx, orc, pool, ad, layers, list(range(A)), n_q, n_kv, L)
+    pool.close()
+
+
+@pytest.mark.parametrize("L", [1, 7, 8, 9, 63, 64, 65, 4099])
+def test_decode_f32_ragged_lengths(ctx, orc, L):
+    """Single-token caches, tiles and pages that end mid-way; keys >= L must contribute exactly 0."""
+    from paper_2602_01053_b200 import abi
+    n_q, n_kv, d, r, A = 8, 2, 128, 16, 3
+    pool, ad, layers = build_pool(ctx, orc, "BaseLRShared", abi.F32, 70 + L, L, 1, n_q, n_kv, d, r, A, P=32)
+    check(ctx, orc, pool, ad, layers, [2, 0, 1, 1], n_q, n_kv, L)
+    pool.close()
+
+
+@pytest.mark.parametrize("amp", [5.0, 25.0])
+def test_decode_f32_large_scores(ctx, orc, amp):
+    """fuzz.hpp:30,40-43 amplitudes: scores of several hundred, near exp underflow -- the split-TF32 products must
+    keep the score error far below one ulp of the softmax."""
+    from paper_2602_01053_b200 import Adapters, Pool, abi
+    from tests.cases import synthetic_layer
+    n_q, n_kv, d, r, A, L = 8, 2, 128, 16, 3, 600
+    pool = Pool(ctx, "BaseLRShared", 1, n_kv, d, 64, r, A, max_tokens=L, dtype=abi.F32)
+    ad = Adapters(ctx, 1, A, 64, r, n_kv, d, dtype=abi.F32)
+    q, k, v, v_lr, b, s = synthetic_layer(orc, 4242, L, 1, n_q, n_kv, d, r, A, amp=amp)
+    pool.append_tokens(L)
+    pool.append_key(0, 0, 0, k); pool.append_value(0, 0, 0, v); pool.append_lr(0, 0, 0, v_lr)
+    for a in range(A):
+        ad.set_b(0, a, b[a], 16.0)
+    check(ctx, orc, pool, ad, [(q, k, v, v_lr, b, s)], list(range(A)), n_q, n_kv, L, amp_note=f"amp {amp}")
+    pool.close()

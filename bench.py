@@ -417,7 +417,7 @@ def main():
                 pool.append_device(abi.LR, layer, 0, c0, lbuf.data_ptr(), n, max(r, 1))
         torch.cuda.synchronize()
     host_rng = np.random.default_rng(7)
-    b_host = [[(host_rng.standard_normal((r, n_kv * d)).astype(np.float32) * (0.02 / np.sqrt(max(r, 1)))) for _ in range(A)]
+    b_host = [[(host_rng.standard_normal((r, n_kv * d)).astype(np.float32) * np.float32(0.02 / np.sqrt(max(r, 1)))) for _ in range(A)]
               for _ in range(n_layers)]
     bf16_round = (lambda x: torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()) if dtype == abi.BF16 else (lambda x: x)
     for layer in range(n_layers):

@@ -499,13 +499,13 @@ def main():
 
     # ---- dominant-kernel duration for the roofline: the library brackets the attention kernel alone
     # (not the merge epilogue) with events on its launch stream; averaged over the same K steps ----
+    # (one event pair per launch, no synchronisation between the steps: the kernel as it runs inside the step loop)
+    barrier()
     ctx.set_profiling(True)
-    k_ms = []
-    for _ in range(args.steps):
+    for _ in range(min(args.steps, 256 // (n_layers if args.per_layer_launch else 1))):
         step_device()
-        k_ms.append(ctx.last_kernel_ms())
+    kernel_ms, _n_prof = ctx.mean_kernel_ms()
     ctx.set_profiling(False)
-    kernel_ms = sum(k_ms) / len(k_ms)
 
     # ---- end to end through the C ABI with host buffers ------------------------------------------------
     q_pin = ctx.pinned_array(q_local_host.shape)

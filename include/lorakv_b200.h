@@ -325,6 +325,10 @@ int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* adapters, int64
  * stream; lorakv_ctx_last_kernel_ms waits for the second and returns the time between them. */
 int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled);
 int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms);
+/* Mean of that time over the fast-path calls made since profiling was switched on (or since the previous call of
+ * this function; up to 256 calls), without a synchronisation between the calls: the kernel timed inside an
+ * uninterrupted run of steps.  *n_calls (optional) = how many calls were averaged. */
+int lorakv_ctx_mean_kernel_ms(lorakv_ctx* ctx, float* ms, int* n_calls);
 
 /* One-tile tcgen05 self-test (diagnostics): D (128 x N) = A (128 x K) * B on the tensor cores with the
  * shared-memory operand layouts the prefill kernel uses; B is N x K row-major (b_mn_major = 0, the

@@ -138,6 +138,7 @@ SIGNATURES = {
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
     "lorakv_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "lorakv_ctx_last_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
+    "lorakv_ctx_mean_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     "lorakv_selftest_umma": (C.c_int, [_vp, _pf, _pf, C.c_int, C.c_int, C.c_int, C.c_float, C.c_int, C.c_int, _pf]),
     "lorakv_set_kernel_policy": (C.c_int, [_vp, C.c_int]),
     "lorakv_last_kernel": (C.c_char_p, [_vp]),
@@ -227,6 +228,12 @@ class Context:
         ms = C.c_float()
         _check(self.lib.lorakv_ctx_last_kernel_ms(self.h, C.byref(ms)))
         return float(ms.value)
+
+    def mean_kernel_ms(self):
+        """(mean device time of the dominant kernel over the profiled calls since set_profiling(True), calls averaged)"""
+        ms, n = C.c_float(), C.c_int()
+        _check(self.lib.lorakv_ctx_mean_kernel_ms(self.h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def selftest_umma(self, a, b, b_mn_major: bool, alpha: float = 1.0, rescale: bool = False, a_in_tmem: bool = False):
         a = np.ascontiguousarray(a, dtype=np.float32); b = np.ascontiguousarray(b, dtype=np.float32)

@@ -157,6 +157,7 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (cudaEvent_t e : ctx->prof_ev) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->prof_ring) if (e) cudaEventDestroy(e);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -244,8 +245,28 @@ int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled) {
     LK_CUDA(cudaEventCreate(&ctx->prof_ev[0]));
     LK_CUDA(cudaEventCreate(&ctx->prof_ev[1]));
   }
+  if (enabled && ctx->prof_ring.empty()) {
+    ctx->prof_ring.resize(2 * lorakv_ctx::kProfPairs, nullptr);
+    for (cudaEvent_t& e : ctx->prof_ring) LK_CUDA(cudaEventCreate(&e));
+  }
   ctx->profiling = enabled != 0;
   ctx->prof_valid = false;
+  ctx->prof_count = 0;
+  return LORAKV_OK;
+}
+int lorakv_ctx_mean_kernel_ms(lorakv_ctx* ctx, float* ms, int* n_calls) {
+  if (!ctx || !ms) return fail("null argument");
+  if (ctx->prof_count < 1) return fail("mean_kernel_ms: no profiled fast-path call yet");
+  LK_CUDA(cudaEventSynchronize(ctx->prof_ring[(size_t)(2 * ctx->prof_count - 1)]));
+  double sum = 0.0;
+  for (int i = 0; i < ctx->prof_count; ++i) {
+    float t = 0.f;
+    LK_CUDA(cudaEventElapsedTime(&t, ctx->prof_ring[(size_t)(2 * i)], ctx->prof_ring[(size_t)(2 * i + 1)]));
+    sum += t;
+  }
+  *ms = (float)(sum / ctx->prof_count);
+  if (n_calls) *n_calls = ctx->prof_count;
+  ctx->prof_count = 0;
   return LORAKV_OK;
 }
 int lorakv_ctx_last_kernel_ms(lorakv_ctx* ctx, float* ms) {

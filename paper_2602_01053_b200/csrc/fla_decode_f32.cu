@@ -34,11 +34,12 @@ namespace lk {
 
 namespace {
 
-constexpr int kWarps = 8;
 constexpr int kTK = 8;                      // keys per tile = one n8 tile of S = one k8 step of P V
 constexpr int kMaxStages = 24;
 constexpr int kRingBudget = 216 * 1024;
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
+
+constexpr int warps_per_cta(int mw) { return mw <= 8 ? 8 : 8; }   // 12 warps of 168 registers spill and leave two stages per ring: 2.2 ms vs 1.6 ms at cfg 2
 
 struct DecodeF32Params {
   const float *k_pages, *v_pages, *lr_pages;
@@ -88,9 +89,11 @@ __device__ __forceinline__ void mma_3x(float (&c)[4], const uint32_t (&ah)[4], c
   mma_tf32(c, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
 }
 
-template <int D, int RP, int MW>
-__global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_f32_kernel(const DecodeF32Params p) {
-  constexpr int kWorkers = kWarps / MW;
+// W = warps per CTA: 12 where the worker width divides it (their ~168 registers each still hold the Q fragments and
+// the O accumulators; four more warps per SM hide more of the MMA and shared-memory latency), else 8
+template <int D, int RP, int MW, int W>
+__global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF32Params p) {
+  constexpr int kWorkers = W / MW;
   constexpr uint32_t kRowBytes = D * 4;
   constexpr uint32_t kKvBytes = kTK * kRowBytes;
   constexpr uint32_t kLrRowBytes = RP * 4;
@@ -252,7 +255,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_f32_kernel(const De
     const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
 
     // ---- S = Q K^T : 16 rows x 8 keys, 3 x TF32 ------------------------------------------------------
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+    // three accumulators (hi*hi, lo*hi, hi*lo) so that the 3 * D / 8 MMAs form three chains, not one
+    float sc[4] = {0.f, 0.f, 0.f, 0.f}, sc_a[4] = {0.f, 0.f, 0.f, 0.f}, sc_b[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int kk = 0; kk < D / 8; ++kk) {
       const uint32_t line = sK + k_row + (uint32_t)((2 * kk) >> 3) * 128u;
@@ -263,8 +267,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_f32_kernel(const De
       for (int e = 0; e < 4; ++e) split_tf32(qf[kk][e], ah[e], al[e]);
       split_tf32(k0, bh0, bl0);
       split_tf32(k1, bh1, bl1);
-      mma_3x(sc, ah, al, bh0, bh1, bl0, bl1);
+      mma_tf32(sc_a, al[0], al[1], al[2], al[3], bh0, bh1);
+      mma_tf32(sc_b, ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+      mma_tf32(sc, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
     }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) sc[e] += sc_a[e] + sc_b[e];
 
     // ---- online softmax (exp2 domain), rows g and g + 8; this lane holds keys 2t, 2t + 1 -----------------
     const int64_t key_base = (int64_t)tl * kTK + 2 * t;
@@ -344,10 +352,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_f32_kernel(const De
 
 template <int D, int RP, int MW>
 int launch_t(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem) {
-  auto kern = fla_decode_f32_kernel<D, RP, MW>;
+  constexpr int W = warps_per_cta(MW);
+  auto kern = fla_decode_f32_kernel<D, RP, MW, W>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);
-  kern<<<grid, kWarps * 32, smem, ctx->stream>>>(dp);
+  kern<<<grid, W * 32, smem, ctx->stream>>>(dp);
   prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
@@ -401,7 +410,7 @@ int launch_decode_f32(const PagedAttnCall& c) {
   while (16 * mw < rows_total && mw < 8) mw *= 2;
   const int rows_blk = 16 * mw;
   const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
-  const int workers_per_cta = kWarps / mw;
+  const int workers_per_cta = warps_per_cta(mw) / mw;
   const uint32_t stage_bytes = kTK * (2 * d + rp) * 4;
   int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
   if (n_stages > kMaxStages) n_stages = kMaxStages;

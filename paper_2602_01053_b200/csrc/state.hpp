@@ -58,6 +58,11 @@ struct lorakv_ctx {
   bool profiling = false;             // bracket the dominant kernel of fast-path calls with events
   cudaEvent_t prof_ev[2] = {nullptr, nullptr};
   bool prof_valid = false;
+  // back-to-back profiling: one event pair per fast-path call since profiling was switched on (up to kProfPairs), so
+  // that the kernel can be timed inside an uninterrupted run of steps (lorakv_ctx_mean_kernel_ms)
+  static constexpr int kProfPairs = 256;
+  std::vector<cudaEvent_t> prof_ring;    // 2 * kProfPairs events, created with the first profiled call
+  int prof_count = 0;
 };
 
 namespace lk {
@@ -65,7 +70,9 @@ namespace lk {
 inline void prof_mark(lorakv_ctx* ctx, int which) {
   if (!ctx->profiling) return;
   cudaEventRecord(ctx->prof_ev[which], ctx->stream);
-  if (which == 1) ctx->prof_valid = true;
+  if (ctx->prof_count < lorakv_ctx::kProfPairs && !ctx->prof_ring.empty())
+    cudaEventRecord(ctx->prof_ring[(size_t)(2 * ctx->prof_count + which)], ctx->stream);
+  if (which == 1) { ctx->prof_valid = true; if (ctx->prof_count < lorakv_ctx::kProfPairs) ++ctx->prof_count; }
 }
 }  // namespace lk
 

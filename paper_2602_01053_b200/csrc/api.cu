@@ -1107,6 +1107,7 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   else if (ctx->policy != 1 && decode_tma_supported(call)) { LK_TRY(launch_decode_tma(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && decode_f32_supported(call)) { LK_TRY(launch_decode_f32(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
+  else if (ctx->policy != 1 && prefill_f32_supported(call)) LK_TRY(launch_prefill_f32(call));
   else LK_TRY(launch_paged_simt(call));
   if (peers) {
     if (!rows_at_peers)

@@ -350,6 +350,266 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF
   flush();
 }
 
+// ---- prefill blocks over fp32 pages ---------------------------------------------------------------------
+// gqa_attention for L_c rows of one agent on one layer (attention.hpp:332-363) with the causal rule of :44-46: key j is
+// hidden from the row at position query_offset + i iff j > query_offset + i.  Same fragments, same split-TF32
+// products and the same stage ring as the decode kernel, arranged as a flash-attention forward: one CTA = eight
+// warps = 128 query rows of one kv head (row = position * group + q head within the group), all eight warps consume
+// every 8-key stage of the ring warp 0 fills.  CTAs are ordered kv head by kv head (one head's K / V_base, 33 MB at
+// 32K tokens, stays in L2 while its row blocks run) and, inside a head, longest causal range first.  A CTA covers its
+// rows' whole key range, so it writes exactly one partial per row and fla_decode_merge (one "split") applies
+// B[agent] and the division by l.
+struct PrefillF32Params {
+  const float *k_pages, *v_pages, *lr_pages;
+  const int32_t *kv_table, *lr_table;
+  int64_t kv_head_stride, kv_page_stride, lr_page_stride;   // elements; layer offsets already applied to the page pointers
+  int P, group, n_kv_local, rows_total, row_blocks, n_pages, n_stages;
+  int64_t L_c, query_offset, n_q_local;
+  float scale_log2;
+  const float* q;        // [L_c][n_q_local * D]
+  float* part;           // [n_kv_local * row_blocks][128][4 + D + RP]
+};
+
+template <int D, int RP>
+__global__ void __launch_bounds__(256, 1) fla_prefill_f32_kernel(const PrefillF32Params p) {
+  constexpr int MW = 8;
+  constexpr uint32_t kRowBytes = D * 4;
+  constexpr uint32_t kKvBytes = kTK * kRowBytes;
+  constexpr uint32_t kLrRowBytes = RP * 4;
+  constexpr uint32_t kLrBytes = kTK * kLrRowBytes;
+  constexpr uint32_t kStageBytes = 2 * kKvBytes + kLrBytes;
+  constexpr int kLrSwz = RP >= 32 ? 7 : (RP / 4 - 1);
+  constexpr int kNO = D / 8, kNL = RP / 8;
+  constexpr int PS = 4 + D + RP;
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full[kMaxStages];
+  __shared__ uint64_t empty[kMaxStages];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wi = warp;
+  const int g = lane >> 2, t = lane & 3;
+  const int NS = p.n_stages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], MW); }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  const int kvh = (int)(blockIdx.x / p.row_blocks);
+  const int rb = p.row_blocks - 1 - (int)(blockIdx.x % p.row_blocks);     // longest key range first
+  const int64_t i_last = min(p.L_c - 1, (int64_t)((rb * 128 + 127) / p.group));
+  const int n = (int)((p.query_offset + i_last) / kTK + 1);                 // tiles holding keys 0 .. query_offset + i_last
+  const uint32_t ring = ptx::smem_u32(smem);
+  const bool producer = wi == 0;
+
+  int win_base = -(1 << 30), win_kv = 0, win_lr = 0;
+  int p_page = 0, p_tok = 0, p_stage = 0, p_wrap = 0, p_issued = 0;
+  auto issue_next = [&]() {
+    if (p_page < win_base || p_page >= win_base + 32) {
+      win_base = p_page;
+      const int pg = p_page + lane;
+      win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
+      if (RP > 0) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
+    }
+    const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
+    const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
+    if (ptx::elect_one()) {
+      const uint32_t dst = ring + (uint32_t)p_stage * kStageBytes;
+      const int64_t kv_off = (int64_t)kvh * p.kv_head_stride + (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * D;
+      ptx::mbar_arrive_expect_tx(&full[p_stage], kStageBytes);
+      bulk_g2s(dst, p.k_pages + kv_off, kKvBytes, &full[p_stage], ptx::kEvictLast);
+      bulk_g2s(dst + kKvBytes, p.v_pages + kv_off, kKvBytes, &full[p_stage], ptx::kEvictLast);
+      if (RP > 0) {
+        const int64_t lr_off = (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
+        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], ptx::kEvictLast);
+      }
+    }
+    ++p_issued;
+    if (++p_stage == NS) { p_stage = 0; ++p_wrap; }
+    p_tok += kTK;
+    if (p_tok == p.P) { p_tok = 0; ++p_page; }
+  };
+  if (producer) {
+    const int pre = n < NS ? n : NS;
+    for (int i = 0; i < pre; ++i) issue_next();
+  }
+
+  const float ninf = -std::numeric_limits<float>::infinity();
+  float qf[D / 8][4];
+  float o[kNO][4];
+  float olr[kNL > 0 ? kNL : 1][4];
+  float m_used[2], l_run[2];
+  int64_t vis[2];                  // last visible key of rows g and g + 8
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int rho = rb * 128 + wi * 16 + g + 8 * h;
+    const bool real = rho < p.rows_total;
+    const int64_t pos = real ? rho / p.group : i_last;
+    const int gi = real ? rho % p.group : 0;
+    const float* src = p.q + (pos * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
+#pragma unroll
+    for (int kk = 0; kk < D / 8; ++kk) {
+      qf[kk][h] = real ? __ldg(src + 8 * kk + t) : 0.f;
+      qf[kk][2 + h] = real ? __ldg(src + 8 * kk + 4 + t) : 0.f;
+    }
+    vis[h] = p.query_offset + pos;
+    m_used[h] = ninf; l_run[h] = 0.f;
+  }
+#pragma unroll
+  for (int nt = 0; nt < kNO; ++nt) { o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f; }
+#pragma unroll
+  for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
+  // keys beyond the last one any row of this warp may see are skipped (the stage is still released)
+  const int64_t warp_vis = p.query_offset + min(i_last, (int64_t)((rb * 128 + wi * 16 + 15) / p.group));
+
+  const uint32_t k_row = (uint32_t)g * kRowBytes + (uint32_t)t * 4u;
+  const uint32_t v_row0 = (uint32_t)(2 * t) * kRowBytes + (uint32_t)(g & 3) * 4u;
+  const uint32_t v_row1 = v_row0 + kRowBytes;
+  const uint32_t v_c0 = (uint32_t)((g >> 2) ^ (2 * t)), v_c1 = (uint32_t)((g >> 2) ^ (2 * t + 1));
+
+  int c_stage = 0, c_wrap = 0;
+  for (int i = 0; i < n; ++i) {
+    if (producer && i >= 1 && p_issued < n) {
+      ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
+      issue_next();
+    }
+    const int s = c_stage;
+    ptx::mbar_wait(&full[s], (uint32_t)(c_wrap & 1));
+    const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
+    const int64_t key_base = (int64_t)i * kTK + 2 * t;
+
+    if ((int64_t)i * kTK <= warp_vis) {
+      float sc[4] = {0.f, 0.f, 0.f, 0.f}, sc_a[4] = {0.f, 0.f, 0.f, 0.f}, sc_b[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int kk = 0; kk < D / 8; ++kk) {
+        const uint32_t line = sK + k_row + (uint32_t)((2 * kk) >> 3) * 128u;
+        const float k0 = lds32(line + ((uint32_t)(((2 * kk) & 7) ^ g) << 4));
+        const float k1 = lds32(line + ((uint32_t)(((2 * kk + 1) & 7) ^ g) << 4));
+        uint32_t ah[4], al[4], bh0, bl0, bh1, bl1;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_tf32(qf[kk][e], ah[e], al[e]);
+        split_tf32(k0, bh0, bl0);
+        split_tf32(k1, bh1, bl1);
+        mma_tf32(sc_a, al[0], al[1], al[2], al[3], bh0, bh1);
+        mma_tf32(sc_b, ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+        mma_tf32(sc, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[e] += sc_a[e] + sc_b[e];
+
+      // causal mask per row (attention.hpp:149-154); masked scores are never exponentiated (:171)
+      bool valid[2][2];
+      float tmax[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        valid[h][0] = key_base <= vis[h];
+        valid[h][1] = key_base + 1 <= vis[h];
+        const float v0 = valid[h][0] ? sc[2 * h] * p.scale_log2 : ninf;
+        const float v1 = valid[h][1] ? sc[2 * h + 1] * p.scale_log2 : ninf;
+        sc[2 * h] = v0; sc[2 * h + 1] = v1;
+        float mx = fmaxf(v0, v1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        tmax[h] = mx;
+      }
+      const bool grow = tmax[0] > m_used[0] + kRescaleThreshold || tmax[1] > m_used[1] + kRescaleThreshold;
+      if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float m_new = fmaxf(m_used[h], tmax[h]);
+          const float alpha = (m_used[h] == ninf) ? 0.f : ex2(m_used[h] - m_new);
+          m_used[h] = m_new;
+          l_run[h] *= alpha;
+#pragma unroll
+          for (int nt = 0; nt < kNO; ++nt) { o[nt][2 * h] *= alpha; o[nt][2 * h + 1] *= alpha; }
+#pragma unroll
+          for (int nt = 0; nt < kNL; ++nt) { olr[nt][2 * h] *= alpha; olr[nt][2 * h + 1] *= alpha; }
+        }
+      }
+      uint32_t ph[4], pl[4];
+      {
+        const float p00 = valid[0][0] ? ex2(sc[0] - m_used[0]) : 0.f;
+        const float p01 = valid[0][1] ? ex2(sc[1] - m_used[0]) : 0.f;
+        const float p10 = valid[1][0] ? ex2(sc[2] - m_used[1]) : 0.f;
+        const float p11 = valid[1][1] ? ex2(sc[3] - m_used[1]) : 0.f;
+        l_run[0] += p00 + p01;
+        l_run[1] += p10 + p11;
+        split_tf32(p00, ph[0], pl[0]);
+        split_tf32(p10, ph[1], pl[1]);
+        split_tf32(p01, ph[2], pl[2]);
+        split_tf32(p11, ph[3], pl[3]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < kNO; ++nt) {
+        const uint32_t line = (uint32_t)((2 * nt) >> 3) * 128u;
+        const float v0 = lds32(sV + v_row0 + line + ((((uint32_t)(2 * nt) & 7u) ^ v_c0) << 4));
+        const float v1 = lds32(sV + v_row1 + line + ((((uint32_t)(2 * nt) & 7u) ^ v_c1) << 4));
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(v0, bh0, bl0);
+        split_tf32(v1, bh1, bl1);
+        mma_3x(o[nt], ph, pl, bh0, bh1, bl0, bl1);
+      }
+      if (RP > 0) {
+#pragma unroll
+        for (int nt = 0; nt < kNL; ++nt) {
+          const uint32_t chunk = (uint32_t)(2 * nt + (g >> 2));
+          const uint32_t a0 = sLR + (uint32_t)(2 * t) * kLrRowBytes + ((chunk ^ ((uint32_t)(2 * t) & (uint32_t)kLrSwz)) << 4) + (uint32_t)(g & 3) * 4u;
+          const uint32_t a1 = sLR + (uint32_t)(2 * t + 1) * kLrRowBytes + ((chunk ^ ((uint32_t)(2 * t + 1) & (uint32_t)kLrSwz)) << 4) +
+                              (uint32_t)(g & 3) * 4u;
+          uint32_t bh0, bl0, bh1, bl1;
+          split_tf32(lds32(a0), bh0, bl0);
+          split_tf32(lds32(a1), bh1, bl1);
+          mma_3x(olr[nt], ph, pl, bh0, bh1, bl0, bl1);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (++c_stage == NS) { c_stage = 0; ++c_wrap; }
+  }
+
+  // one partial per row: slot = unit (fla_decode_merge with a single split per row)
+  const int64_t unit = (int64_t)kvh * p.row_blocks + rb;
+  float* base = p.part + (unit * 128 + wi * 16) * PS;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float l = l_run[h];
+    l += __shfl_xor_sync(0xffffffffu, l, 1);
+    l += __shfl_xor_sync(0xffffffffu, l, 2);
+    float* row = base + (g + 8 * h) * PS;
+    if (t == 0) { row[0] = m_used[h]; row[1] = l; }
+#pragma unroll
+    for (int nt = 0; nt < kNO; ++nt)
+      *reinterpret_cast<float2*>(row + 4 + 8 * nt + 2 * t) = make_float2(o[nt][2 * h], o[nt][2 * h + 1]);
+#pragma unroll
+    for (int nt = 0; nt < kNL; ++nt)
+      *reinterpret_cast<float2*>(row + 4 + D + 8 * nt + 2 * t) = make_float2(olr[nt][2 * h], olr[nt][2 * h + 1]);
+  }
+}
+
+template <int D, int RP>
+int launch_prefill_t(lorakv_ctx* ctx, const PrefillF32Params& pp, unsigned grid, size_t smem) {
+  auto kern = fla_prefill_f32_kernel<D, RP>;
+  LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  prof_mark(ctx, 0);
+  kern<<<grid, 256, smem, ctx->stream>>>(pp);
+  prof_mark(ctx, 1);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+template <int D>
+int launch_prefill_rp(lorakv_ctx* ctx, const PrefillF32Params& pp, unsigned grid, size_t smem, int rp) {
+  switch (rp) {
+    case 0: return launch_prefill_t<D, 0>(ctx, pp, grid, smem);
+    case 16: return launch_prefill_t<D, 16>(ctx, pp, grid, smem);
+    case 32: return launch_prefill_t<D, 32>(ctx, pp, grid, smem);
+    default: return launch_prefill_t<D, 64>(ctx, pp, grid, smem);
+  }
+}
+
 template <int D, int RP, int MW>
 int launch_t(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem) {
   constexpr int W = warps_per_cta(MW);
@@ -452,6 +712,60 @@ int launch_decode_f32(const PagedAttnCall& c) {
   LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,
                              T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers));
   ctx->last_kernel = "fla_decode_f32";
+  return LORAKV_OK;
+}
+
+bool prefill_f32_supported(const PagedAttnCall& c) {
+  const lorakv_pool* pool = c.pool;
+  const int64_t d = pool->dims.d_head, rp = pool->r_pad;
+  if (pool->dims.dtype != LORAKV_F32) return false;
+  if (c.n_batch != 1 || c.rows_per_entry < 2 || c.layer_end - c.layer_begin != 1) return false;   // prefill blocks only
+  if (d != 64 && d != 128) return false;
+  if (!(rp == 0 || rp == 16 || rp == 32 || rp == 64)) return false;
+  if (pool->P % kTK != 0) return false;
+  if (c.L < 1 || c.n_q_local % pool->n_kv_local != 0) return false;
+  return true;
+}
+
+int launch_prefill_f32(const PagedAttnCall& c) {
+  lorakv_pool* pool = c.pool;
+  lorakv_ctx* ctx = pool->ctx;
+  const int d = (int)pool->dims.d_head, r = (int)pool->dims.rank, rp = (int)pool->r_pad;
+  if (r > 0 && !c.adapters) return fail("paged attention: rank %lld cache needs adapter tables", (long long)r);
+  const int group = (int)(c.n_q_local / pool->n_kv_local);
+  const int64_t rows_total = c.rows_per_entry * group;
+  const int row_blocks = (int)((rows_total + 127) / 128);
+  const uint32_t stage_bytes = kTK * (2 * d + rp) * 4;
+  int n_stages = (int)(kRingBudget / stage_bytes);
+  if (n_stages > kMaxStages) n_stages = kMaxStages;
+  const size_t smem = (size_t)n_stages * stage_bytes;
+  const int64_t units = pool->n_kv_local * row_blocks;
+  const int PS = 4 + d + rp;
+  LK_TRY(scratch_reserve(ctx, ctx->work, (size_t)units * 128 * PS * sizeof(float)));
+
+  PrefillF32Params pp;
+  const int64_t layer = c.layer_begin;
+  pp.k_pages = static_cast<const float*>(pool->k_pages) + layer * pool->kv_layer_stride();
+  pp.v_pages = static_cast<const float*>(pool->v_pages) + layer * pool->kv_layer_stride();
+  pp.lr_pages = rp > 0 ? static_cast<const float*>(pool->lr_pages) + layer * pool->lr_layer_stride() : nullptr;
+  pp.kv_table = pool->kv_space.dev_table + c.kv_set * pool->kv_space.max_pages;
+  pp.lr_table = rp > 0 ? pool->lr_space.dev_table + c.lr_set * pool->lr_space.max_pages : nullptr;
+  pp.kv_head_stride = pool->kv_head_stride(); pp.kv_page_stride = pool->kv_page_stride(); pp.lr_page_stride = pool->lr_page_stride();
+  pp.P = (int)pool->P; pp.group = group; pp.n_kv_local = (int)pool->n_kv_local;
+  pp.rows_total = (int)rows_total; pp.row_blocks = row_blocks;
+  pp.n_pages = (int)((c.L + pool->P - 1) / pool->P); pp.n_stages = n_stages;
+  pp.L_c = c.rows_per_entry; pp.query_offset = c.query_offset; pp.n_q_local = c.n_q_local;
+  pp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
+  pp.q = c.q_dev; pp.part = static_cast<float*>(ctx->work.ptr);
+  const unsigned grid = (unsigned)units;
+  if (d == 128) LK_TRY(launch_prefill_rp<128>(ctx, pp, grid, smem, rp));
+  else LK_TRY(launch_prefill_rp<64>(ctx, pp, grid, smem, rp));
+
+  // one partial per row: the merge's closed form with T = G = 1 tile per unit, one segment per worker
+  LK_TRY(launch_decode_merge(ctx, pp.part, d, rp, r, /*MW=*/8, group, (int)pool->n_kv_local, /*n_batch=*/(int)c.rows_per_entry,
+                             (int)rows_total, row_blocks, /*T=*/1, /*G=*/1, c.layer_begin, c.n_q_local, /*max_seg=*/1,
+                             /*agent_ids_dev=*/nullptr, c.adapters, c.out_dev, /*n_layers=*/1, nullptr, /*agent_fixed=*/(int)c.agent_host));
+  ctx->last_kernel = "fla_prefill_f32";
   return LORAKV_OK;
 }
 

@@ -405,6 +405,7 @@ struct DecodeMergeParams {
   int64_t n_agents;
   float* out;            // [layers][n_batch][n_q_local * d]
   PeerOut peers;         // n > 0: the row goes to every rank's [layers][n_batch][n_q_total * d] buffer instead
+  int agent_fixed;       // >= 0: every row belongs to this agent (prefill blocks: the batch axis is the position)
 };
 
 // Address of the output row of (layer, batch entry, local q head): the local slab, or -- when the step ends in the
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   const int gi = rho % p.group, entry = rho / p.group;
   const int64_t layer = p.layer_begin + layer_rel;
   const int64_t dkv = (int64_t)p.n_kv_local * p.D;
-  const int agent = p.agent_ids ? p.agent_ids[entry] : 0;
+  const int agent = p.agent_fixed >= 0 ? p.agent_fixed : (p.agent_ids ? p.agent_ids[entry] : 0);
   const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
   const int64_t dst = merge_row_offset(p, layer_rel, entry, (int64_t)kvh * p.group + gi);
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   const int gi = rho % p.group, entry = rho / p.group;
   const int64_t layer = p.layer_begin + layer_rel;
   const int64_t dkv = (int64_t)p.n_kv_local * p.D;
-  const int agent = p.agent_ids ? p.agent_ids[entry] : 0;
+  const int agent = p.agent_fixed >= 0 ? p.agent_fixed : (p.agent_ids ? p.agent_ids[entry] : 0);
   const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
   const int64_t dst = merge_row_offset(p, layer_rel, entry, (int64_t)kvh * p.group + gi);
@@ -651,9 +652,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
                         const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
-                        const PeerOut* peers) {
+                        const PeerOut* peers, int agent_fixed) {
   DecodeMergeParams mp;
   if (peers) mp.peers = *peers;
+  mp.agent_fixed = agent_fixed;
   mp.part = part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;
   mp.n_kv_local = n_kv_local; mp.n_batch = n_batch; mp.rows_total = rows_total;
   mp.row_blocks = row_blocks; mp.T = T; mp.G = G; mp.layer_begin = layer_begin; mp.n_q_local = n_q_local;

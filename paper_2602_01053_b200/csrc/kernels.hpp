@@ -76,11 +76,13 @@ int launch_decode_tma(const PagedAttnCall& call);
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
                         const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
-                        const PeerOut* peers = nullptr);
+                        const PeerOut* peers = nullptr, int agent_fixed = -1);
 
 // fla_decode_f32.cu (the same streaming decode over fp32 pages: 3 x TF32 mma.sync, fp32 accuracy) ----------
 bool decode_f32_supported(const PagedAttnCall& call);
 int launch_decode_f32(const PagedAttnCall& call);
+bool prefill_f32_supported(const PagedAttnCall& call);     // prefill blocks of one agent on one layer
+int launch_prefill_f32(const PagedAttnCall& call);
 
 // fla_prefill_umma.cu (tcgen05 / TMEM / TMA; bf16 pages, prefill blocks) ---------------------------------
 bool prefill_umma_supported(const PagedAttnCall& call);

@@ -6,8 +6,10 @@ from paper_2602_01053_b200 import abi
 from tests.test_gpu_pool import build_pool
 orc = checker.oracle()
 ctx = pkg.Context(0)
+import os
+F32_ONLY = os.environ.get("LORAKV_SMOKE_F32_ONLY") == "1"    # synccheck: only the mbarrier rings of the fp32 kernels and the gather
 # decode MW=1 and MW=2/KT=2, prefill umma, lr_project, selftest
-for (n_q, n_kv, d, r, A, L, P) in [(8, 2, 128, 16, 3, 200, 64), (8, 2, 128, 32, 8, 150, 32), (16, 2, 64, 8, 12, 100, 16)]:
+for (n_q, n_kv, d, r, A, L, P) in ([] if F32_ONLY else [(8, 2, 128, 16, 3, 200, 64), (8, 2, 128, 32, 8, 150, 32), (16, 2, 64, 8, 12, 100, 16)]):
     pool, ad, layers = build_pool(ctx, orc, "BaseLRShared", abi.BF16, 7, L, 1, n_q, n_kv, d, r, A, P=P, project=True, d_model=192)
     q, k, v, v_lr, b, s = layers[0]
     out = pool.decode(ad, 0, 1, list(range(A)), n_q, np.stack([q[a][0] for a in range(A)])[None])
@@ -18,6 +20,29 @@ for (n_q, n_kv, d, r, A, L, P) in [(8, 2, 128, 16, 3, 200, 64), (8, 2, 128, 32, 
     want = orc.gqa_attention(qp, k, v, v_lr, b[1], s, L - 40, n_q, n_kv)
     print("prefill", ctx.last_kernel(), orc.max_rel_error(got, want))
     pool.close()
+# fp32 mode: split-TF32 decode (one- and two-warp workers) and prefill over chunk-swizzled fp32 pages; the peer-memory
+# output gather with one rank (merge epilogue storing into the gather buffer + handshake kernel)
+from paper_2602_01053_b200 import Gather
+for (n_q, n_kv, d, r, A, L, P) in [(8, 2, 128, 16, 3, 203, 64), (8, 2, 64, 32, 8, 150, 8)]:
+    pool, ad, layers = build_pool(ctx, orc, "BaseLRShared", abi.F32, 9, L, 1, n_q, n_kv, d, r, A, P=P)
+    q, k, v, v_lr, b, s = layers[0]
+    qs = np.stack([q[a][0] for a in range(A)])[None]
+    out = pool.decode(ad, 0, 1, list(range(A)), n_q, qs)
+    want = orc.gqa_attention(q[1], k, v, v_lr, b[1], s, L - 1, n_q, n_kv)
+    print("decode", ctx.last_kernel(), orc.max_rel_error(out[0, 1][None, :], want))
+    gth = Gather(ctx, 0, 1, qs.size)
+    for _ in range(2):
+        full, _dev = pool.decode_gather(ad, gth, 0, 1, list(range(A)), n_q, q=qs)
+    print("gather", ctx.last_kernel(), bool(np.array_equal(full, out)))
+    gth.close()
+    qp = orc.gaussian(40, n_q * d, 5, 1.0 / np.sqrt(d), np.float32)
+    got = pool.prefill(ad, 0, 1, n_q, qp, L - 40)
+    want = orc.gqa_attention(qp, k, v, v_lr, b[1], s, L - 40, n_q, n_kv)
+    print("prefill", ctx.last_kernel(), orc.max_rel_error(got, want))
+    pool.close()
+if F32_ONLY:
+    ctx.close()
+    sys.exit(0)
 # fused K / V projection + RoPE + append (tcgen05) and the tensor-core X * A projection
 from paper_2602_01053_b200 import Adapters, Pool, Projection
 for (L, d_model, n_kv, P) in [(200, 192, 1, 32), (300, 256, 2, 64)]:

@@ -50,7 +50,7 @@ struct DecodeF32Params {
   int64_t T, total_tiles, G;
   int max_seg, n_stages;
   float scale_log2;
-  uint64_t l2_policy;
+  uint64_t l2_policy, lr_policy;   // K / V stream evict-first; V_lr evict-last while the launch's low-rank cache fits in L2
   const float* q;
   float* part;           // [workers * max_seg][16 * MW][4 + D + RP]
 };
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF
       bulk_g2s(dst + kKvBytes, p.v_pages + kv_off, kKvBytes, &full[p_stage], p.l2_policy);
       if (RP > 0) {
         const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
-        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.l2_policy);
+        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.lr_policy);   // re-read by every kv head
       }
     }
     ++p_issued;
@@ -665,7 +665,6 @@ int launch_decode_f32(const PagedAttnCall& c) {
   const int group = (int)(c.n_q_local / pool->n_kv_local);
   const int64_t rows_total = c.n_batch * group;
   if (r > 0 && !c.adapters) return fail("paged attention: rank %lld cache needs adapter tables", (long long)r);
-
   int mw = 1;
   while (16 * mw < rows_total && mw < 8) mw *= 2;
   const int rows_blk = 16 * mw;
@@ -705,6 +704,7 @@ int launch_decode_f32(const PagedAttnCall& c) {
   dp.T = T; dp.total_tiles = total; dp.G = G; dp.max_seg = max_seg; dp.n_stages = n_stages;
   dp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
   dp.l2_policy = ptx::kEvictFirst;
+  dp.lr_policy = lr_fits_l2(c, c.L * rp * 4) ? ptx::kEvictLast : ptx::kEvictFirst;
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, rp));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, rp));

@@ -53,7 +53,8 @@ struct DecodeParams {
   int64_t G;             // tiles per worker
   int max_seg, n_stages;
   float scale_log2;      // (1/sqrt(d)) * log2(e)
-  uint64_t l2_policy;    // cache-hint operand of the bulk copies (0 = none)
+  uint64_t l2_policy;    // cache-hint operand of the K / V bulk copies (0 = none)
+  uint64_t lr_policy;    // ... and of the V_lr copies (evict-last while the launch's low-rank cache fits in L2)
   const float* q;        // [layers][n_batch][n_q_local * d]
   float* part;           // [workers * max_seg][16 * MW][4 + D + RP]
 };
@@ -174,7 +175,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
       }
       if (RP > 0) {
         const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
-        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.l2_policy);
+        // V_lr is per layer, not per head: the same tile is read once per kv head, at different times of the launch.
+        // Kept with evict-last while K / V stream through with evict-first, the whole low-rank cache of the step
+        // (33 MB at cfg 2) stays in L2 and DRAM serves it once instead of n_kv times.
+        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.lr_policy);
       }
     }
     // advance the cursor
@@ -697,7 +701,6 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const int group = (int)(c.n_q_local / pool->n_kv_local);
   const int64_t rows_total = c.n_batch * group;
   if (r > 0 && !c.adapters) return fail("paged attention: rank %lld cache needs adapter tables", (long long)r);
-
   int mw = 1;
   while (16 * mw < rows_total && mw < 8) mw *= 2;
   const int rows_blk = 16 * mw;
@@ -739,6 +742,7 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.T = T; dp.total_tiles = total; dp.G = G; dp.max_seg = max_seg; dp.n_stages = n_stages;
   dp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
   dp.l2_policy = ptx::kEvictFirst;      // the cache is streamed once per step: do not let it push the partials and q out of L2
+  dp.lr_policy = lr_fits_l2(c, c.L * rp * 2) ? ptx::kEvictLast : ptx::kEvictFirst;
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));

@@ -69,6 +69,17 @@ struct PagedAttnCall {
 };
 int launch_paged_simt(const PagedAttnCall& call);
 
+// V_lr is per layer, not per head (attention.hpp:353): a decode launch reads every low-rank tile once per kv head, at
+// different times of the launch.  While the low-rank cache of the whole launch fits in L2 beside the K / V stream, the
+// decode kernels load its tiles with an evict-last hint (K / V keep evict-first) and DRAM serves them once instead of
+// n_kv times (cfg 2: 4.56 -> 4.34 GB per step = the algorithmic bytes).  Larger ones (cfg 4: 268 MB) keep evict-first;
+// cutting the launch into L2-sized layer chunks was measured and does not pay (the chunks read exactly the algorithmic
+// bytes but six launch pairs cost more than the saved traffic: 1.60 vs 1.57 ms per cfg-4 step).
+constexpr int64_t kLrL2Budget = 80ll << 20;
+inline bool lr_fits_l2(const PagedAttnCall& c, int64_t lr_bytes_per_layer) {
+  return (c.layer_end - c.layer_begin) * lr_bytes_per_layer <= kLrL2Budget;
+}
+
 // fla_decode_tma.cu (TMA bulk-copy rings + tensor-core MMA; bf16 pages, decode) -------------------
 bool decode_tma_supported(const PagedAttnCall& call);
 int launch_decode_tma(const PagedAttnCall& call);

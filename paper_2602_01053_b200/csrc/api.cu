@@ -1042,7 +1042,7 @@ static int visible_rows(const lorakv_pool* pool, int64_t layer, int64_t kv_set, 
 static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer_begin, int64_t layer_end,
                      int64_t kv_set, int64_t lr_set, const int32_t* agent_ids, int64_t n_batch,
                      int64_t rows_per_entry, int64_t query_offset, int64_t n_q_heads, const float* q,
-                     float* out, int mem_kind, const lk::PeerOut* peers = nullptr) {
+                     float* out, int mem_kind, const lk::PeerOut* peers = nullptr, bool per_entry_lr = false) {
   lorakv_ctx* ctx = pool->ctx;
   LK_CUDA(cudaSetDevice(ctx->device));
   if (layer_begin < 0 || layer_end > pool->dims.n_layers || layer_begin >= layer_end) return fail("attention: bad layer range");
@@ -1055,6 +1055,16 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   for (int64_t l = layer_begin; l < layer_end; ++l) {
     int64_t Ll;
     LK_TRY(visible_rows(pool, l, kv_set, lr_set, &Ll));
+    if (per_entry_lr) {   // every entry reads its own agent's low-rank cache: all of them must have caught up
+      Ll = std::min(pool->key_rows[(size_t)kv_set][(size_t)l], pool->value_rows[(size_t)kv_set][(size_t)l]);
+      for (int64_t i = 0; i < n_batch; ++i) {
+        const int64_t a = agent_ids ? agent_ids[i] : 0;
+        if (a < 0 || a >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)a);
+        if (pool->lr_rows[(size_t)a][(size_t)l] < Ll)
+          return fail("fla_decode_batched: the per-agent low-rank cache of agent %lld holds %lld of %lld rows on layer %lld (its LR prefill "
+                      "is pending)", (long long)a, (long long)pool->lr_rows[(size_t)a][(size_t)l], (long long)Ll, (long long)l);
+      }
+    }
     if (L >= 0 && Ll != L) return fail("attention: layers %lld..%lld hold different row counts", (long long)layer_begin, (long long)layer_end);
     L = Ll;
   }
@@ -1102,8 +1112,15 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   call.L = L; call.q_dev = q_dev; call.out_dev = out_dev;
   call.agent_host = ids_host[0];
   call.peers = peers;
+  call.per_entry_lr = per_entry_lr;
   bool rows_at_peers = false;    // the decode kernels' merge epilogue stores straight into the gather buffers
-  if (ctx->policy == 0 && decode_umma_supported(call)) { LK_TRY(launch_decode_umma(call)); rows_at_peers = true; }
+  if (per_entry_lr) {
+    if (ctx->policy == 1 || !decode_tma_per_entry_lr_supported(call))
+      return fail("fla_decode_batched: scheme %s keeps per-agent caches; this shape has no batched kernel, batch one agent per call",
+                  kSchemeName[pool->dims.scheme]);
+    LK_TRY(launch_decode_tma(call));
+    rows_at_peers = true;
+  } else if (ctx->policy == 0 && decode_umma_supported(call)) { LK_TRY(launch_decode_umma(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && decode_tma_supported(call)) { LK_TRY(launch_decode_tma(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && decode_f32_supported(call)) { LK_TRY(launch_decode_f32(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
@@ -1130,18 +1147,26 @@ int lorakv_fla_decode_batched(lorakv_pool* pool, const lorakv_adapters* ad, int6
   // per-agent caches (NonShared K/V, BaseShared LR) can only serve one agent per launch
   int64_t kv_set = 0, lr_set = 0;
   const bool per_agent = pool->dims.scheme == LORAKV_NONSHARED || (pool->dims.scheme == LORAKV_BASESHARED && pool->r_pad > 0);
+  bool per_entry_lr = false;
   if (per_agent) {
+    bool mixed = false;
     for (int64_t i = 1; i < n_batch; ++i)
-      if (agent_ids && agent_ids[i] != agent_ids[0])
-        return fail("fla_decode_batched: scheme %s keeps per-agent caches; batch one agent per call", kSchemeName[pool->dims.scheme]);
+      if (agent_ids && agent_ids[i] != agent_ids[0]) mixed = true;
+    // BaseShared shares K / V_base: a batch of different agents still streams them once, every entry reading its own
+    // agent's V_lr page set (fla_decode_tma, PA).  NonShared has nothing to share between agents.
+    if (mixed && pool->dims.scheme == LORAKV_NONSHARED)
+      return fail("fla_decode_batched: scheme %s keeps per-agent caches; batch one agent per call", kSchemeName[pool->dims.scheme]);
+    per_entry_lr = mixed;
     const int64_t a = agent_ids ? agent_ids[0] : 0;
     if (a < 0 || a >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)a);
     if (pool->dims.scheme == LORAKV_NONSHARED) kv_set = a; else lr_set = a;
   }
   int64_t L;
   LK_TRY(visible_rows(pool, layer_begin, kv_set, lr_set, &L));
+  if (per_entry_lr) L = std::min(pool->key_rows[0][(size_t)layer_begin], pool->value_rows[0][(size_t)layer_begin]);
   if (L < 1) return fail("attention: query_offset 0 with L_c 1 exceeds L 0");
-  return run_paged(pool, ad, layer_begin, layer_end, kv_set, lr_set, agent_ids, n_batch, 1, L - 1, n_q_heads, q, out, mem_kind);
+  return run_paged(pool, ad, layer_begin, layer_end, kv_set, lr_set, agent_ids, n_batch, 1, L - 1, n_q_heads, q, out, mem_kind, nullptr,
+                   per_entry_lr);
 }
 
 // Sharded decode step ending in the output gather over peer memory (peer_gather.cu).

@@ -57,6 +57,11 @@ struct DecodeParams {
   uint64_t lr_policy;    // ... and of the V_lr copies (evict-last while the launch's low-rank cache fits in L2)
   const float* q;        // [layers][n_batch][n_q_local * d]
   float* part;           // [workers * max_seg][16 * MW][4 + D + RP]
+  // per-entry low-rank caches (template flag PA; BaseShared batches): entry i reads page set agent_ids[i]
+  const int32_t* lr_tables;   // [sets][lr_max_pages]
+  const int32_t* agent_ids;   // [n_batch]
+  int lr_max_pages;
+  int lr_per_block;           // entries of one row block = V_lr tiles per stage (16 * MW / group)
 };
 
 // The cache is streamed exactly once per step, so the copies carry an L2 evict-first policy: the lines
@@ -98,7 +103,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // D = d_head (64 / 128), RP = padded rank (0 / 16 / 32 / 64), MW = warps per worker, KT = 16-key
 // steps per tile (1 for single-warp workers whose eight rings must share the SM's shared memory; 2 for
 // the multi-warp workers, which halves their per-tile synchronisation and doubles the MMA ILP)
-template <int D, int RP, int MW, int KT>
+// PA: every batch entry has its own V_lr page set (BaseShared).  A stage then holds K, V_base and one V_lr tile per
+// entry of the row block; the lanes of the producer warp issue the V_lr copies in parallel (lane e -> entry e), and
+// a consumer warp runs the O_lr MMA once per entry its 16 rows touch with P masked to that entry's rows.
+template <int D, int RP, int MW, int KT, bool PA = false>
 __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
   constexpr int kTK = kKeyStep * KT;                    // keys per tile
   constexpr int kWorkers = kWarps / MW;
@@ -106,9 +114,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
   constexpr uint32_t kBlockBytes = kTK * 128;           // one block of one tile
   constexpr uint32_t kKvBytes = kBlocks * kBlockBytes;  // K (or V) tile
   constexpr uint32_t kLrBytes = kTK * RP * 2;
-  constexpr uint32_t kStageBytes = 2 * kKvBytes + kLrBytes;
   constexpr int kNO = D / 8, kNL = RP / 8;              // n8 tiles of O and O_lr
   constexpr int PS = 4 + D + RP;                        // floats per partial row
+  const uint32_t kStageBytes = 2 * kKvBytes + (PA ? (uint32_t)p.lr_per_block : 1u) * kLrBytes;
 
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full_bar[kWorkers][kMaxStages];
@@ -158,22 +166,34 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
       win_base = p_page;
       const int pg = p_page + lane;
       win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
-      if (RP > 0) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
+      if (RP > 0 && !PA) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
     }
     const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
-    const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
+    const int phys_lr = (RP > 0 && !PA) ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
+    int pa_entries = 0;         // PA: entries of this row block that exist (the last block may be ragged)
+    if (PA) {
+      const int e0 = (int)(p_unit % p.row_blocks) * p.lr_per_block;
+      pa_entries = min(p.lr_per_block, p.n_batch - e0);
+      if (lane < pa_entries) {  // lane e streams the V_lr tile of entry e0 + e from that entry's own page set
+        const int set = p.agent_ids[e0 + lane];
+        const int phys = p.lr_tables[(int64_t)set * p.lr_max_pages + p_page];
+        const int64_t lr_off = (p.layer_begin + p_layer) * p.lr_layer_stride + (int64_t)phys * p.lr_page_stride + (int64_t)p_tok * RP;
+        bulk_g2s(ring + (uint32_t)p_stage * kStageBytes + 2 * kKvBytes + (uint32_t)lane * kLrBytes, p.lr_pages + lr_off, kLrBytes,
+                 &full[p_stage], p.lr_policy);
+      }
+    }
     if (ptx::elect_one()) {     // not `lane == 0`: no ELECT / BRA.U.ANY waterfall loop around each UBLKCP
       const uint32_t dst = ring + (uint32_t)p_stage * kStageBytes;
       const int64_t layer = p.layer_begin + p_layer;
       const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride +
                              (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * 64;
-      ptx::mbar_arrive_expect_tx(&full[p_stage], kStageBytes);
+      ptx::mbar_arrive_expect_tx(&full[p_stage], PA ? 2 * kKvBytes + (uint32_t)pa_entries * kLrBytes : kStageBytes);
 #pragma unroll
       for (int b = 0; b < kBlocks; ++b) {
         bulk_g2s(dst + b * kBlockBytes, p.k_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[p_stage], p.l2_policy);
         bulk_g2s(dst + kKvBytes + b * kBlockBytes, p.v_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[p_stage], p.l2_policy);
       }
-      if (RP > 0) {
+      if (RP > 0 && !PA) {
         const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
         // V_lr is per layer, not per head: the same tile is read once per kv head, at different times of the launch.
         // Kept with evict-last while K / V stream through with evict-first, the whole low-rank cache of the step
@@ -371,7 +391,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
           mma_bf16(o[2 * np + 1], pa[kt], b2, b3);
         }
       }
-      if (RP >= 16) {
+      if (RP >= 16 && !PA) {
 #pragma unroll
         for (int np = 0; np < RP / 16; ++np) {
           const int chunk = 2 * np + (mi >> 1);
@@ -383,6 +403,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
             ldsm_x4_t(sLR + off, b0, b1, b2, b3);
             mma_bf16(olr[2 * np], pa[kt], b0, b1);
             mma_bf16(olr[2 * np + 1], pa[kt], b2, b3);
+          }
+        }
+      }
+      if (RP >= 16 && PA) {
+        // rows g and g + 8 of this warp belong to entries ent_lo / ent_hi of the row block; one masked MMA pass per entry
+        const int ent_lo = (wi * 16 + g) / p.group, ent_hi = (wi * 16 + g + 8) / p.group;
+        const int e_first = (wi * 16) / p.group, e_last = min((wi * 16 + 15) / p.group, p.lr_per_block - 1);
+        for (int e = e_first; e <= e_last; ++e) {
+          const uint32_t sE = sLR + (uint32_t)e * kLrBytes;
+          const uint32_t m_lo = ent_lo == e ? 0xffffffffu : 0u, m_hi = ent_hi == e ? 0xffffffffu : 0u;
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            const uint32_t pe[4] = {pa[kt][0] & m_lo, pa[kt][1] & m_hi, pa[kt][2] & m_lo, pa[kt][3] & m_hi};
+#pragma unroll
+            for (int np = 0; np < RP / 16; ++np) {
+              const int chunk = 2 * np + (mi >> 1);
+              uint32_t off = (uint32_t)(key + 16 * kt) * (2u * RP) + (uint32_t)chunk * 16u;
+              off ^= ((off >> 7) & (uint32_t)(RP / 8 - 1)) << 4;
+              uint32_t b0, b1, b2, b3;
+              ldsm_x4_t(sE + off, b0, b1, b2, b3);
+              mma_bf16(olr[2 * np], pe, b0, b1);
+              mma_bf16(olr[2 * np + 1], pe, b2, b3);
+            }
           }
         }
       }
@@ -527,9 +570,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   }
 }
 
-template <int D, int RP, int MW, int KT>
+template <int D, int RP, int MW, int KT, bool PA = false>
 int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
-  auto kern = fla_decode_tma_kernel<D, RP, MW, KT>;
+  auto kern = fla_decode_tma_kernel<D, RP, MW, KT, PA>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);
   kern<<<grid, kWarps * 32, smem, ctx->stream>>>(dp);
@@ -537,6 +580,26 @@ int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;
+}
+
+// per-entry V_lr tiles (BaseShared batches): 16-key tiles for every worker width (the stage already carries one V_lr tile
+// per entry)
+template <int D, int RP>
+int launch_mw_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw) {
+  switch (mw) {
+    case 1: return launch_t<D, RP, 1, 1, true>(ctx, dp, grid, smem);
+    case 2: return launch_t<D, RP, 2, 1, true>(ctx, dp, grid, smem);
+    case 4: return launch_t<D, RP, 4, 1, true>(ctx, dp, grid, smem);
+    default: return launch_t<D, RP, 8, 1, true>(ctx, dp, grid, smem);
+  }
+}
+template <int D>
+int launch_rp_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int rp) {
+  switch (rp) {
+    case 16: return launch_mw_pa<D, 16>(ctx, dp, grid, smem, mw);
+    case 32: return launch_mw_pa<D, 32>(ctx, dp, grid, smem, mw);
+    default: return launch_mw_pa<D, 64>(ctx, dp, grid, smem, mw);
+  }
 }
 
 template <int D, int RP>
@@ -681,6 +744,12 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
   return LORAKV_OK;
 }
 
+bool decode_tma_per_entry_lr_supported(const PagedAttnCall& c) {
+  if (!decode_tma_supported(c) || c.pool->r_pad < 16) return false;
+  const int64_t group = c.n_q_local / c.pool->n_kv_local;
+  return group >= 1 && (16 % group == 0 || group % 16 == 0) && group <= 128;   // a batch entry's rows never straddle a 16-row warp tile unevenly
+}
+
 bool decode_tma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
   const int64_t d = pool->dims.d_head, rp = pool->r_pad;
@@ -706,9 +775,13 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const int rows_blk = 16 * mw;
   const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
   const int workers_per_cta = kWarps / mw;
-  const int kt = (mw > 1 && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;   // 32-key tiles for multi-warp workers
+  const bool pa = c.per_entry_lr && rp > 0;
+  const int lr_per_block = pa ? (int)std::min<int64_t>(rows_blk / group, c.n_batch) : 1;   // V_lr tiles per stage
+  const int kt = (!pa && mw > 1 && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;   // 32-key tiles for multi-warp workers
   const int tk = kKeyStep * kt;
-  const uint32_t stage_bytes = tk * (4 * d + 2 * rp);
+  const uint32_t stage_bytes = tk * (4 * d + 2 * rp * lr_per_block);
+  if (pa && (size_t)workers_per_cta * 2 * stage_bytes > (size_t)kRingBudget)
+    return fail("decode over per-agent low-rank caches: %d entries x rank %d do not fit two stages per worker", lr_per_block, rp);
   int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
   if (n_stages > kMaxStages) n_stages = kMaxStages;
   const size_t smem = (size_t)workers_per_cta * n_stages * stage_bytes;
@@ -744,7 +817,13 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.l2_policy = ptx::kEvictFirst;      // the cache is streamed once per step: do not let it push the partials and q out of L2
   dp.lr_policy = lr_fits_l2(c, c.L * rp * 2) ? ptx::kEvictLast : ptx::kEvictFirst;
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
-  if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
+  dp.lr_tables = pool->lr_space.dev_table; dp.agent_ids = c.agent_ids_dev;
+  dp.lr_max_pages = (int)pool->lr_space.max_pages; dp.lr_per_block = lr_per_block;
+  if (pa) {
+    dp.lr_policy = ptx::kEvictFirst;     // every V_lr tile is read by one entry's rows of each kv head only
+    if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp));
+    else LK_TRY(launch_rp_pa<64>(ctx, dp, grid, smem, mw, rp));
+  } else if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));
 
   LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,

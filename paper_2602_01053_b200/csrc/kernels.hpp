@@ -66,7 +66,11 @@ struct PagedAttnCall {
   const float* q_dev;               // [layers][n_batch][rows_per_entry][n_q_local*d]
   float* out_dev;                   // same shape
   const PeerOut* peers = nullptr;   // decode only: store finished rows into the peers' gather buffers as well
+  // BaseShared batch (kvcache.hpp:127-130, 238-243: shared K / V_base, one V_lr cache PER AGENT): batch entry i reads the
+  // low-rank page set agent_ids[i] instead of lr_set, so that K / V_base are still streamed once for the whole batch
+  bool per_entry_lr = false;
 };
+bool decode_tma_per_entry_lr_supported(const PagedAttnCall& call);
 int launch_paged_simt(const PagedAttnCall& call);
 
 // V_lr is per layer, not per head (attention.hpp:353): a decode launch reads every low-rank tile once per kv head, at

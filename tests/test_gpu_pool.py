@@ -364,3 +364,57 @@ def test_baseshared_agent_switch_lr_prefill(ctx, orc):
     with pytest.raises(Exception, match="per-agent"):
         pool.decode(ad, 0, 1, [0, 1], n_q, np.concatenate([q, q])[None])
     pool.close(); ad.close()
+
+
+# n_q, n_kv, d, r, agents, batch, L, P, layers -- rows per kv head = len(batch) * n_q / n_kv
+BASESHARED_BATCHES = [
+    (8, 2, 128, 16, 3, [0, 1, 2], 300, 64, 2),           # 12 rows: one warp per worker, four entries per warp tile
+    (8, 2, 128, 32, 4, [3, 0, 0, 2, 1, 1, 3, 2], 257, 32, 1),   # 32 rows: two warps per worker, repeated agents
+    (32, 8, 128, 16, 3, [2, 0, 1], 130, 64, 1),          # Llama head counts
+    (4, 1, 128, 64, 6, [5, 4, 3, 2, 1, 0] * 6, 200, 16, 1),     # 144 rows: two row blocks, the second one ragged
+    (16, 1, 64, 8, 3, [1, 2, 0], 99, 16, 1),             # group 16: one entry per warp tile; d = 64, rank 8 padded to 16
+    (2, 2, 128, 16, 5, [4, 3, 2, 1, 0], 77, 16, 1),      # group 1: sixteen entries per warp tile (five used)
+]
+
+
+@pytest.mark.parametrize("n_q,n_kv,d,r,N,batch,L,P,n_layers", BASESHARED_BATCHES)
+def test_baseshared_batched_decode_reads_kv_once(ctx, orc, n_q, n_kv, d, r, N, batch, L, P, n_layers):
+    """BaseShared (kvcache.hpp:127-130, 238-243): K / V_base are shared, every agent has its OWN V_lr cache.  A batch of
+    different agents runs as ONE launch that streams K / V_base once, every entry reading its own agent's page set
+    (fla_decode_tma, per-entry V_lr tiles); each entry must equal gqa_attention with that agent's V_lr and B."""
+    from paper_2602_01053_b200 import Adapters, Pool, abi
+    rnd = orc.round_bf16
+    g = lambda rows, cols, seed, sc: rnd(orc.gaussian(rows, cols, seed, sc, np.float32))
+    pool = Pool(ctx, "BaseShared", n_layers, n_kv, d, 64, r, N, max_tokens=L + 8, dtype=abi.BF16, page_tokens=P)
+    ad = Adapters(ctx, n_layers, N, 64, r, n_kv, d, dtype=abi.BF16)
+    pool.append_tokens(L)
+    k, v, lr, B = [], [], [], []
+    for l in range(n_layers):
+        k.append(g(L, n_kv * d, 100 + l, 1.0 / np.sqrt(d))); v.append(g(L, n_kv * d, 200 + l, 1.0))
+        pool.append_key(l, 0, 0, k[l]); pool.append_value(l, 0, 0, v[l])
+        lr.append([g(L, r, 300 + 10 * l + a, 1.0) for a in range(N)])
+        B.append([g(r, n_kv * d, 400 + 10 * l + a, 0.02 / np.sqrt(r)) for a in range(N)])
+        for a in range(N):
+            # interleave the agents' appends so that their page sets are interleaved physically
+            half = L // 2
+            pool.append_lr(l, a, 0, lr[l][a][:half])
+        for a in reversed(range(N)):
+            pool.append_lr(l, a, L // 2, lr[l][a][L // 2:])
+            ad.set_b(l, a, B[l][a], 16.0)
+    q = np.stack([np.stack([g(1, n_q * d, 500 + 7 * l + i, 1.0 / np.sqrt(d))[0] for i in range(len(batch))]) for l in range(n_layers)])
+    launches = ctx.launch_count
+    out = pool.decode(ad, 0, n_layers, batch, n_q, q)
+    assert ctx.last_kernel() == "fla_decode_tma"
+    assert ctx.launch_count - launches == 2                      # attention + merge: one pass over K / V for the whole batch
+    for l in range(n_layers):
+        for i, a in enumerate(batch):
+            want = orc.gqa_attention(q[l, i][None, :], k[l], v[l], lr[l][a], B[l][a], 16.0 / r, L - 1, n_q, n_kv)
+            assert orc.max_rel_error(out[l, i][None, :], want) <= 2e-2, (l, i, a)
+            # and the same entry alone (the one-agent-per-call path) agrees far tighter
+            alone = pool.decode(ad, l, l + 1, [a], n_q, q[l, i][None, None, :])
+            assert orc.max_rel_error(out[l, i][None, :], alone[0]) <= 5e-3
+    ctx.set_kernel_policy(1)
+    with pytest.raises(Exception, match="per-agent"):           # the CUDA-core path has no batched kernel for it
+        pool.decode(ad, 0, n_layers, batch, n_q, q)
+    ctx.set_kernel_policy(0)
+    pool.close(); ad.close()

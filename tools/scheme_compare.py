@@ -8,7 +8,8 @@ measured exactly on one B200: rank 0's shard (n_kv / G kv heads, all layers, all
 Schemes (proj/include/lorakv/kvcache.hpp:15-21, Tables 3/4):
   BaseLRShared : one K/V_base cache + one rank-r V_lr cache for all agents, ONE batched launch per step
   FullShared   : one K/V cache, no adapter term (r = 0) -- the accuracy-losing lower bound on bytes
-  BaseShared   : shared K/V_base, one V_lr cache per agent  -> one launch per agent (per-agent caches)
+  BaseShared   : shared K/V_base, one V_lr cache per agent  -> ONE batched launch (every entry reads its own agent's V_lr
+                 page set); "BaseShared:per-agent" times the one-launch-per-agent alternative
   NonShared    : private K/V per agent (values carry the adapter), the multi-LoRA status quo -> one launch per agent
 Times are device times (events on the library's stream) of a whole step = all agents x all layers."""
 from __future__ import annotations
@@ -25,7 +26,7 @@ sys.path.insert(0, ROOT)
 from bench import WORKLOADS, load_peaks  # noqa: E402
 
 
-def run_scheme(torch, pkg, abi, ctx, scheme, wl, G, steps, warmup):
+def run_scheme(torch, pkg, abi, ctx, scheme, wl, G, steps, warmup, per_agent_launches=False):
     desc, n_layers, n_q, n_kv, d, r, A, L, d_model = wl
     dev = torch.device("cuda", 0)
     n_kv_local = n_kv // G
@@ -57,7 +58,8 @@ def run_scheme(torch, pkg, abi, ctx, scheme, wl, G, steps, warmup):
         for layer in range(n_layers):
             for a in range(A):
                 ad.set_b(layer, a, b, 16.0)
-    batched = scheme in ("BaseLRShared", "FullShared")
+    # BaseShared batches run as one launch too: K / V_base streamed once, every entry reading its own agent's V_lr set
+    batched = scheme in ("BaseLRShared", "FullShared") or (scheme == "BaseShared" and not per_agent_launches)
     q = torch.randn((n_layers, A, n_q_local * d), generator=gen, device=dev) * float(1.0 / np.sqrt(d))
     out = torch.zeros_like(q)
     q_agent = [q[:, a:a + 1].contiguous() for a in range(A)]
@@ -87,7 +89,7 @@ def run_scheme(torch, pkg, abi, ctx, scheme, wl, G, steps, warmup):
     step_bytes = n_layers * (kv_reads * 2 * L * n_kv_local * d * e + lr_reads * L * rank * e)
     cb = pool.bytes()
     key_b, val_b, lr_b = cb["key"], cb["value"], cb["lr"]
-    res = {"scheme": scheme, "ms_per_step": ms, "agent_tok_s": A / (ms * 1e-3), "launches_per_step": int(launches),
+    res = {"scheme": scheme + (" (one launch per agent)" if scheme == "BaseShared" and per_agent_launches else ""), "ms_per_step": ms, "agent_tok_s": A / (ms * 1e-3), "launches_per_step": int(launches),
            "kernel": ctx.last_kernel(), "streamed_bytes_per_step": int(step_bytes), "achieved_gbs": step_bytes / (ms * 1e-3) / 1e9,
            "cache_bytes": {"key": int(key_b), "value": int(val_b), "lr": int(lr_b)},
            "cache_gb": (key_b + val_b + lr_b) / 1e9, "reserved_hbm_gb": pool.reserved_bytes() / 1e9}
@@ -105,7 +107,7 @@ def main():
     ap.add_argument("--shard-of", type=int, default=8, help="G: time rank 0's shard of a G-GPU run")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--schemes", default="BaseLRShared,FullShared,BaseShared,NonShared")
+    ap.add_argument("--schemes", default="BaseLRShared,FullShared,BaseShared,BaseShared:per-agent,NonShared")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "schemes.json"))
     args = ap.parse_args()
     import torch
@@ -118,7 +120,8 @@ def main():
     peak, peak_src = load_peaks()
     rows = []
     for scheme in args.schemes.split(","):
-        res = run_scheme(torch, pkg, abi, ctx, scheme, wl, args.shard_of, args.steps, args.warmup)
+        per_agent = scheme.endswith(":per-agent")
+        res = run_scheme(torch, pkg, abi, ctx, scheme.split(":")[0], wl, args.shard_of, args.steps, args.warmup, per_agent)
         res["frac_of_hbm_peak"] = res["achieved_gbs"] / peak
         rows.append(res)
         print(json.dumps(res), flush=True)

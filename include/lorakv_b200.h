@@ -52,6 +52,10 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx);
 int lorakv_ctx_synchronize(lorakv_ctx* ctx);
 void* lorakv_ctx_stream(lorakv_ctx* ctx);
 int lorakv_ctx_sm_count(lorakv_ctx* ctx);
+/* L2 capacity the decode path plans with (default: the device's).  The low-rank cache V_lr is shared by the kv heads
+ * of a layer; the decode keeps it L2-resident (evict-last hint) when the launch's share fits, and otherwise walks the
+ * layers in equal chunks inside the kernel so that one chunk's share does.  Tests shrink it to force the chunked path. */
+int lorakv_ctx_set_l2_bytes(lorakv_ctx* ctx, int64_t bytes);
 /* number of kernels this library has launched on ctx since creation (bench.py's gpu_launches) */
 int64_t lorakv_ctx_launch_count(lorakv_ctx* ctx);
 

@@ -68,6 +68,7 @@ SIGNATURES = {
     "lorakv_ctx_stream": (_vp, [_vp]),
     "lorakv_ctx_sm_count": (C.c_int, [_vp]),
     "lorakv_ctx_launch_count": (_i64, [_vp]),
+    "lorakv_ctx_set_l2_bytes": (C.c_int, [_vp, _i64]),
     "lorakv_dev_alloc": (C.c_int, [_vp, _i64, C.POINTER(_vp)]),
     "lorakv_dev_free": (C.c_int, [_vp, _vp]),
     "lorakv_host_alloc": (C.c_int, [_vp, _i64, C.POINTER(_vp)]),
@@ -220,6 +221,10 @@ class Context:
 
     def set_kernel_policy(self, policy: int) -> int:
         return self.lib.lorakv_set_kernel_policy(self.h, policy)
+
+    def set_l2_bytes(self, nbytes: int):
+        """L2 capacity the decode plans its V_lr residency with (tests shrink it to force the layer-chunked path)."""
+        _check(self.lib.lorakv_ctx_set_l2_bytes(self.h, int(nbytes)))
 
     def set_profiling(self, enabled: bool):
         _check(self.lib.lorakv_ctx_set_profiling(self.h, int(enabled)))

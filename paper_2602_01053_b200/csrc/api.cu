@@ -138,6 +138,7 @@ int lorakv_ctx_create(int device, void* stream, lorakv_ctx** out) {
   if (!ctx) return fail("ctx_create: out of host memory");
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
+  ctx->l2_bytes = prop.l2CacheSize > 0 ? (int64_t)prop.l2CacheSize : (int64_t)126 << 20;
   if (stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -238,6 +239,11 @@ void lorakv_event_destroy(lorakv_event* ev) {
   delete ev;
 }
 
+int lorakv_ctx_set_l2_bytes(lorakv_ctx* ctx, int64_t bytes) {
+  if (!ctx || bytes < 1) return fail("ctx_set_l2_bytes: bad argument");
+  ctx->l2_bytes = bytes;
+  return LORAKV_OK;
+}
 int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled) {
   if (!ctx) return fail("null context");
   LK_CUDA(cudaSetDevice(ctx->device));

@@ -49,8 +49,10 @@ struct DecodeParams {
   int P, group, n_kv_local, n_batch, rows_total, row_blocks, n_pages;
   int64_t L, layer_begin, n_q_local;
   int64_t T;             // tiles per unit
-  int64_t total_tiles;   // units * T
-  int64_t G;             // tiles per worker
+  int64_t total_tiles;   // units * T of ONE layer chunk
+  int64_t G;             // tiles per worker and chunk
+  int n_chunks;          // equal layer chunks walked one after the other (1 = the whole launch at once)
+  int64_t n_workers;     // workers of the launch (partials are laid out [chunk][worker][segment])
   int max_seg, n_stages;
   float scale_log2;      // (1/sqrt(d)) * log2(e)
   uint64_t l2_policy;    // cache-hint operand of the K / V bulk copies (0 = none)
@@ -138,10 +140,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
   __syncthreads();
 
   const int64_t w = (int64_t)blockIdx.x * kWorkers + wk;
-  const int64_t g0 = w * p.G;
-  const int64_t g1 = min(g0 + p.G, p.total_tiles);
-  const int n = g1 > g0 ? (int)(g1 - g0) : 0;
-  if (n == 0) return;
+  // A launch whose low-rank cache does not fit in L2 is cut into p.n_chunks equal LAYER CHUNKS that every worker walks
+  // through one after the other (no grid barrier: all workers get the same share of every chunk and stay in step), so
+  // that at any time the kv heads of only a few layers are in flight and their shared V_lr tiles are served by L2.
+  // Inside a chunk the (unit, tile) pairs are cut into equal contiguous ranges as before (p.total_tiles per chunk).
+  int64_t g0 = 0;
+  int n = 0, chunk = 0;
 
   const uint32_t ring = ptx::smem_u32(smem) + (uint32_t)wk * (uint32_t)NS * kStageBytes;
   uint64_t* full = full_bar[wk];
@@ -155,13 +159,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
   // Producer cursor.  Everything the per-tile path needs is carried incrementally (unit, tile, page,
   // token, stage, wrap count): the only divisions happen here and at unit changes, never per tile.
   const int T32 = (int)p.T;
-  int64_t p_unit = g0 / p.T;
-  int p_tl = (int)(g0 - p_unit * p.T);
-  int p_page = (p_tl * kTK) / p.P, p_tok = (p_tl * kTK) % p.P;
-  int p_layer = (int)(p_unit / units_per_layer), p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
-  int p_stage = 0, p_wrap = 0, p_issued = 0;
+  int64_t p_unit = 0;
+  int p_tl = 0, p_page = 0, p_tok = 0, p_layer = 0, p_kvh = 0;
+  int p_stage = 0, p_wrap = 0, p_issued = 0;      // stage and wrap count run on across chunks, like the consumer's
 
   auto issue_next = [&]() {       // whole producer warp; lane 0 talks to the TMA engine
+    // the stage must have been released by every warp of the worker (a fresh barrier passes the parity-1 wait)
+    ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
     if (p_page < win_base || p_page >= win_base + 32) {
       win_base = p_page;
       const int pg = p_page + lane;
@@ -214,11 +218,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
     }
   };
 
-  if (producer) {
-    const int pre = n < NS ? n : NS;
-    for (int i = 0; i < pre; ++i) issue_next();
-  }
-
   const float ninf = -std::numeric_limits<float>::infinity();
   uint32_t qa[D / 16][4];
   float o[kNO][4];
@@ -228,7 +227,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
 
   auto flush = [&]() {            // partial of the unit just finished
     const int64_t first_unit = g0 / p.T;
-    const int64_t slot = w * p.max_seg + (cur_unit - first_unit);
+    const int64_t slot = ((int64_t)chunk * p.n_workers + w) * p.max_seg + (cur_unit - first_unit);
     float* base = p.part + (slot * (16 * MW) + wi * 16) * PS;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -250,9 +249,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
   const int mi = lane >> 3, rr = lane & 7;
 
   // consumer cursor, carried incrementally like the producer's
+  int c_stage = 0, c_wrap = 0;
+  for (chunk = 0; chunk < p.n_chunks; ++chunk) {
+  const int64_t chunk_base = (int64_t)chunk * p.total_tiles;
+  g0 = chunk_base + w * p.G;
+  const int64_t g1 = min(g0 + p.G, chunk_base + p.total_tiles);
+  n = g1 > g0 ? (int)(g1 - g0) : 0;
+  if (n == 0) continue;
+  p_unit = g0 / p.T;
+  p_tl = (int)(g0 - p_unit * p.T);
+  p_page = (p_tl * kTK) / p.P; p_tok = (p_tl * kTK) % p.P;
+  p_layer = (int)(p_unit / units_per_layer); p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
+  p_issued = 0;
+  if (producer) {
+    const int pre = n < NS ? n : NS;
+    for (int i = 0; i < pre; ++i) issue_next();
+  }
+  cur_unit = -1;
   int64_t u = g0 / p.T;
   int tl = (int)(g0 - u * p.T);
-  int c_stage = 0, c_wrap = 0;
   for (int i = 0; i < n; ++i) {
     if (u != cur_unit) {
       if (cur_unit >= 0) flush();
@@ -285,10 +300,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
     }
 
     // refill the stage released one iteration ago (tile p_issued goes where tile p_issued - NS was)
-    if (producer && i >= 1 && p_issued < n) {
-      ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
-      issue_next();
-    }
+    if (producer && i >= 1 && p_issued < n) issue_next();
     const int s = c_stage;
     ptx::mbar_wait(&full[s], (uint32_t)(c_wrap & 1));
 
@@ -438,6 +450,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const De
     if (++tl == T32) { tl = 0; ++u; }
   }
   flush();
+  }   // layer chunks
 }
 
 // ---- merge of the per-worker partials + up-projection epilogue -----------------------------------
@@ -453,6 +466,7 @@ struct DecodeMergeParams {
   float* out;            // [layers][n_batch][n_q_local * d]
   PeerOut peers;         // n > 0: the row goes to every rank's [layers][n_batch][n_q_total * d] buffer instead
   int agent_fixed;       // >= 0: every row belongs to this agent (prefill blocks: the batch axis is the position)
+  int64_t units_per_chunk, n_workers;   // layer chunks of fla_decode_tma: partials are [chunk][worker][segment]
 };
 
 // Address of the output row of (layer, batch entry, local q head): the local slab, or -- when the step ends in the
@@ -485,7 +499,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   const int rows_blk = 16 * p.MW;
   const int rb = rho / rows_blk, r_in = rho % rows_blk;
   const int64_t u = (layer_rel * p.n_kv_local + kvh) * p.row_blocks + rb;
-  const int64_t w_lo = (u * p.T) / p.G, w_hi = ((u + 1) * p.T - 1) / p.G;
+  const int64_t ch = u / p.units_per_chunk, u_loc = u % p.units_per_chunk;    // layer chunk of the unit, unit inside it
+  const int64_t w_lo = (u_loc * p.T) / p.G, w_hi = ((u_loc + 1) * p.T - 1) / p.G;
   const int ns = (int)(w_hi - w_lo + 1);
   const int PS = 4 + p.D + p.RP, C = p.D + p.RP;
   float* w_s = sm;
@@ -493,7 +508,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   const float ninf = -std::numeric_limits<float>::infinity();
   auto row_of = [&](int s) -> const float* {
     const int64_t w = w_lo + s;
-    const int64_t slot = w * p.max_seg + (u - (w * p.G) / p.T);
+    const int64_t slot = (ch * p.n_workers + w) * p.max_seg + (u_loc - (w * p.G) / p.T);
     return p.part + (slot * rows_blk + r_in) * PS;
   };
   // ---- row max over the splits ----
@@ -647,13 +662,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   const int rows_blk = 16 * p.MW;
   const int rb = rho / rows_blk, r_in = rho % rows_blk;
   const int64_t u = (layer_rel * p.n_kv_local + kvh) * p.row_blocks + rb;
-  const int64_t w_lo = (u * p.T) / p.G, w_hi = ((u + 1) * p.T - 1) / p.G;
+  const int64_t ch = u / p.units_per_chunk, u_loc = u % p.units_per_chunk;    // layer chunk of the unit, unit inside it
+  const int64_t w_lo = (u_loc * p.T) / p.G, w_hi = ((u_loc + 1) * p.T - 1) / p.G;
   const int ns = (int)(w_hi - w_lo + 1);                     // <= 32, checked by the launcher
   const int PS = 4 + p.D + p.RP, C = p.D + p.RP;
   const float ninf = -std::numeric_limits<float>::infinity();
   auto row_of = [&](int s) -> const float* {
     const int64_t w = w_lo + s;
-    const int64_t slot = w * p.max_seg + (u - (w * p.G) / p.T);
+    const int64_t slot = (ch * p.n_workers + w) * p.max_seg + (u_loc - (w * p.G) / p.T);
     return p.part + (slot * rows_blk + r_in) * PS;
   };
   float m = ninf, l = 0.f;
@@ -719,10 +735,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
                         const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
-                        const PeerOut* peers, int agent_fixed) {
+                        const PeerOut* peers, int agent_fixed, int64_t units_per_chunk, int64_t n_workers) {
   DecodeMergeParams mp;
   if (peers) mp.peers = *peers;
   mp.agent_fixed = agent_fixed;
+  mp.units_per_chunk = units_per_chunk > 0 ? units_per_chunk : (int64_t)n_layers * n_kv_local * row_blocks;   // one chunk
+  mp.n_workers = n_workers;
   mp.part = part; mp.D = d; mp.RP = rp; mp.r = r; mp.MW = mw; mp.group = group;
   mp.n_kv_local = n_kv_local; mp.n_batch = n_batch; mp.rows_total = rows_total;
   mp.row_blocks = row_blocks; mp.T = T; mp.G = G; mp.layer_begin = layer_begin; mp.n_q_local = n_q_local;
@@ -743,6 +761,11 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
   LK_CUDA(cudaGetLastError());
   return LORAKV_OK;
 }
+
+bool lr_fits_l2(const PagedAttnCall& c, int64_t lr_bytes_per_layer) {
+  return (c.layer_end - c.layer_begin) * lr_bytes_per_layer <= c.pool->ctx->l2_bytes * 6 / 10;
+}
+int64_t lr_chunk_budget(const PagedAttnCall& c) { return c.pool->ctx->l2_bytes * 28 / 100; }
 
 bool decode_tma_per_entry_lr_supported(const PagedAttnCall& c) {
   if (!decode_tma_supported(c) || c.pool->r_pad < 16) return false;
@@ -787,8 +810,19 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const size_t smem = (size_t)workers_per_cta * n_stages * stage_bytes;
 
   const int64_t T = (c.L + tk - 1) / tk;
+  // V_lr is shared by the kv heads of a layer (kernels.hpp: lr_fits_l2).  When the launch's low-rank cache does not
+  // fit in L2, the layers are cut into the fewest equal chunks whose share does; every worker walks the chunks in
+  // order, so only a chunk's V_lr is live at a time and DRAM serves it once instead of once per kv head.
+  int n_chunks = 1;
+  const int64_t lr_layer_bytes = c.L * rp * 2;
+  if (!pa && rp > 0 && pool->n_kv_local > 1 && !lr_fits_l2(c, lr_layer_bytes)) {
+    n_chunks = (int)n_layers;
+    for (int64_t nc = 2; nc <= n_layers; ++nc)
+      if (n_layers % nc == 0 && (n_layers / nc) * lr_layer_bytes <= lr_chunk_budget(c)) { n_chunks = (int)nc; break; }
+  }
   const int64_t units = n_layers * pool->n_kv_local * row_blocks;
-  const int64_t total = units * T;
+  const int64_t units_per_chunk = units / n_chunks;
+  const int64_t total = units_per_chunk * T;             // tiles of one chunk
   const int64_t max_workers = (int64_t)ctx->sm_count * workers_per_cta;
   int64_t G = (total + max_workers - 1) / max_workers;
   if (G < 4) G = 4;
@@ -796,7 +830,7 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const unsigned grid = (unsigned)((n_workers + workers_per_cta - 1) / workers_per_cta);
   const int max_seg = (int)((G + T - 2) / T + 1);
   const int PS = 4 + d + rp;
-  const size_t part_bytes = (size_t)grid * workers_per_cta * max_seg * rows_blk * PS * sizeof(float);
+  const size_t part_bytes = (size_t)n_chunks * n_workers * max_seg * rows_blk * PS * sizeof(float);
   LK_TRY(scratch_reserve(ctx, ctx->work, part_bytes));
 
   DecodeParams dp;
@@ -813,9 +847,10 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.n_pages = (int)((c.L + pool->P - 1) / pool->P);
   dp.L = c.L; dp.layer_begin = c.layer_begin; dp.n_q_local = c.n_q_local;
   dp.T = T; dp.total_tiles = total; dp.G = G; dp.max_seg = max_seg; dp.n_stages = n_stages;
+  dp.n_chunks = n_chunks; dp.n_workers = n_workers;
   dp.scale_log2 = (float)((1.0 / sqrt((double)d)) * 1.4426950408889634);
   dp.l2_policy = ptx::kEvictFirst;      // the cache is streamed once per step: do not let it push the partials and q out of L2
-  dp.lr_policy = lr_fits_l2(c, c.L * rp * 2) ? ptx::kEvictLast : ptx::kEvictFirst;
+  dp.lr_policy = (n_chunks > 1 || lr_fits_l2(c, lr_layer_bytes)) ? ptx::kEvictLast : ptx::kEvictFirst;
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   dp.lr_tables = pool->lr_space.dev_table; dp.agent_ids = c.agent_ids_dev;
   dp.lr_max_pages = (int)pool->lr_space.max_pages; dp.lr_per_block = lr_per_block;
@@ -827,7 +862,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));
 
   LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,
-                             T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers));
+                             T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers, -1,
+                             units_per_chunk, n_workers));
   ctx->last_kernel = "fla_decode_tma";
   return LORAKV_OK;
 }

@@ -76,13 +76,13 @@ int launch_paged_simt(const PagedAttnCall& call);
 // V_lr is per layer, not per head (attention.hpp:353): a decode launch reads every low-rank tile once per kv head, at
 // different times of the launch.  While the low-rank cache of the whole launch fits in L2 beside the K / V stream, the
 // decode kernels load its tiles with an evict-last hint (K / V keep evict-first) and DRAM serves them once instead of
-// n_kv times (cfg 2: 4.56 -> 4.34 GB per step = the algorithmic bytes).  Larger ones (cfg 4: 268 MB) keep evict-first;
-// cutting the launch into L2-sized layer chunks was measured and does not pay (the chunks read exactly the algorithmic
-// bytes but six launch pairs cost more than the saved traffic: 1.60 vs 1.57 ms per cfg-4 step).
-constexpr int64_t kLrL2Budget = 80ll << 20;
-inline bool lr_fits_l2(const PagedAttnCall& c, int64_t lr_bytes_per_layer) {
-  return (c.layer_end - c.layer_begin) * lr_bytes_per_layer <= kLrL2Budget;
-}
+// n_kv times (cfg 2: 4.56 -> 4.34 GB per step = the algorithmic bytes).  Larger ones (cfg 4: 268 MB) are cut into layer
+// chunks INSIDE the kernel (fla_decode_tma: n_chunks); separate launches per chunk were measured first and do not pay
+// (six launch pairs cost more than the saved traffic: 1.60 vs 1.57 ms per cfg-4 step).
+// Budgets are fractions of the device's L2 (lorakv_ctx::l2_bytes, 126 MB on B200; lorakv_ctx_set_l2_bytes overrides it):
+// a whole launch may keep 0.6 of it for V_lr, one in-kernel layer chunk 0.28 (two chunks can be live at once).
+bool lr_fits_l2(const PagedAttnCall& c, int64_t lr_bytes_per_layer);
+int64_t lr_chunk_budget(const PagedAttnCall& c);
 
 // fla_decode_tma.cu (TMA bulk-copy rings + tensor-core MMA; bf16 pages, decode) -------------------
 bool decode_tma_supported(const PagedAttnCall& call);
@@ -91,7 +91,7 @@ int launch_decode_tma(const PagedAttnCall& call);
 int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r, int mw, int group, int n_kv_local, int n_batch,
                         int rows_total, int row_blocks, int64_t T, int64_t G, int64_t layer_begin, int64_t n_q_local, int max_seg,
                         const int32_t* agent_ids_dev, const lorakv_adapters* adapters, float* out_dev, int64_t n_layers,
-                        const PeerOut* peers = nullptr, int agent_fixed = -1);
+                        const PeerOut* peers = nullptr, int agent_fixed = -1, int64_t units_per_chunk = 0, int64_t n_workers = 0);
 
 // fla_decode_f32.cu (the same streaming decode over fp32 pages: 3 x TF32 mma.sync, fp32 accuracy) ----------
 bool decode_f32_supported(const PagedAttnCall& call);

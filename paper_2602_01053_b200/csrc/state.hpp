@@ -48,6 +48,7 @@ struct lorakv_ctx {
   cudaStream_t stream = nullptr;
   bool owns_stream = false;
   int sm_count = 0;
+  int64_t l2_bytes = 0;               // device L2 size (cudaDevAttrL2CacheSize); sizes the V_lr residency decisions of the decode
   int64_t launches = 0;
   int policy = 0;
   const char* last_kernel = "none";

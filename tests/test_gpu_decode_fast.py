@@ -138,25 +138,27 @@ def test_swizzled_pages_read_back_bit_exact(ctx, orc, d, r, P):
     pool.close()
 
 
-@pytest.mark.parametrize("n_layers,l2_kb", [(4, 64), (6, 48), (3, 8), (8, 200)])
-def test_decode_tma_layer_chunks_keep_results(ctx, orc, n_layers, l2_kb):
+def test_decode_tma_layer_chunks_keep_results(ctx, orc):
     """A launch whose low-rank cache exceeds the L2 budget walks the layers in equal chunks inside the kernel (so that a
-    chunk's V_lr, shared by the kv heads of a layer, is served by L2).  Shrinking the planning L2 forces that path on a
-    small cache; the chunking only reorders which worker computes which (unit, tile) range, so the result must agree with
-    the unchunked launch to split-merge rounding and with the reference path to the bf16 tolerance."""
+    chunk's V_lr, shared by the kv heads of a layer, is served by L2).  The chunked path needs >= 4 kv heads and a few
+    dozen tiles per worker and chunk, so the case is 12 layers x 4 kv heads x 40 000 tokens with the planning L2 shrunk to
+    20 MB (15.4 MB of V_lr: three chunks of four layers).  Chunking only changes which worker computes which (unit, tile)
+    range, so the result must agree with the unchunked launch to split-merge rounding and with the reference path to the
+    bf16 tolerance."""
     from paper_2602_01053_b200 import abi
-    n_q, n_kv, d, r, A, L = 8, 2, 128, 16, 3, 530
-    pool, ad, layers = build_pool(ctx, orc, "BaseLRShared", abi.BF16, 3000 + n_layers, L, n_layers, n_q, n_kv, d, r, A, P=32)
+    n_layers, n_q, n_kv, d, r, A, L = 12, 4, 4, 64, 16, 3, 40000
+    pool, ad, layers = build_pool(ctx, orc, "BaseLRShared", abi.BF16, 3100, L, n_layers, n_q, n_kv, d, r, A)
     qs = np.stack([np.stack([layers[l][0][a][0] for a in range(A)]) for l in range(n_layers)])
     whole = pool.decode(ad, 0, n_layers, list(range(A)), n_q, qs)
-    ctx.set_l2_bytes(l2_kb * 1024)            # L * r_pad * 2 B = 17 KB of V_lr per layer
+    assert ctx.last_kernel() == "fla_decode_tma"
+    ctx.set_l2_bytes(20 << 20)
     try:
         chunked = pool.decode(ad, 0, n_layers, list(range(A)), n_q, qs)
-        assert ctx.last_kernel() == "fla_decode_tma"
+        assert ctx.last_kernel() == "fla_decode_tma (layer chunks)"
     finally:
         ctx.set_l2_bytes(126 << 20)
     assert orc.max_rel_error(chunked.reshape(1, -1), whole.reshape(1, -1)) <= 5e-3
-    for l in range(n_layers):
+    for l in (0, 3, 4, 11):                       # first and last layer of a chunk
         q, k, v, v_lr, b, s = layers[l]
         for a in range(A):
             want = orc.gqa_attention(q[a], k, v, v_lr, b[a], s, L - 1, n_q, n_kv)

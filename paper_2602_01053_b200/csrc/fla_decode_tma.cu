@@ -506,11 +506,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   float* w_s = sm;
   float* acc_s = sm + ns;
   const float ninf = -std::numeric_limits<float>::infinity();
-  auto row_of = [&](int s) -> const float* {
-    const int64_t w = w_lo + s;
-    const int64_t slot = (ch * p.n_workers + w) * p.max_seg + (u_loc - (w * p.G) / p.T);
-    return p.part + (slot * rows_blk + r_in) * PS;
-  };
+  // partial of split s: worker w_lo + s, segment = unit minus the worker's first unit.  Only the FIRST worker of a unit can
+  // have started in an earlier unit (every later one starts inside it: segment 0), so one 64-bit division serves the row
+  // instead of one per split (they were half of the instructions this kernel executed)
+  const int64_t seg_lo = u_loc - (w_lo * p.G) / p.T;
+  const float* part0 = p.part + ((ch * p.n_workers + w_lo) * p.max_seg * rows_blk + r_in) * PS;
+  const int64_t split_stride = (int64_t)p.max_seg * rows_blk * PS;
+  const int64_t seg_off = seg_lo * rows_blk * PS;
+  auto row_of = [&](int s) -> const float* { return part0 + s * split_stride + (s == 0 ? seg_off : 0); };
   // ---- row max over the splits ----
   float mx = ninf;
   for (int s = tid; s < ns; s += kMergeWarps * 32) mx = fmaxf(mx, row_of(s)[0]);
@@ -667,11 +670,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   const int ns = (int)(w_hi - w_lo + 1);                     // <= 32, checked by the launcher
   const int PS = 4 + p.D + p.RP, C = p.D + p.RP;
   const float ninf = -std::numeric_limits<float>::infinity();
-  auto row_of = [&](int s) -> const float* {
-    const int64_t w = w_lo + s;
-    const int64_t slot = (ch * p.n_workers + w) * p.max_seg + (u_loc - (w * p.G) / p.T);
-    return p.part + (slot * rows_blk + r_in) * PS;
-  };
+  // partial of split s: worker w_lo + s, segment = unit minus the worker's first unit.  Only the FIRST worker of a unit can
+  // have started in an earlier unit (every later one starts inside it: segment 0), so one 64-bit division serves the row
+  // instead of one per split (they were half of the instructions this kernel executed)
+  const int64_t seg_lo = u_loc - (w_lo * p.G) / p.T;
+  const float* part0 = p.part + ((ch * p.n_workers + w_lo) * p.max_seg * rows_blk + r_in) * PS;
+  const int64_t split_stride = (int64_t)p.max_seg * rows_blk * PS;
+  const int64_t seg_off = seg_lo * rows_blk * PS;
+  auto row_of = [&](int s) -> const float* { return part0 + s * split_stride + (s == 0 ? seg_off : 0); };
   float m = ninf, l = 0.f;
   if (lane < ns) { const float2 ml = *reinterpret_cast<const float2*>(row_of(lane)); m = ml.x; l = ml.y; }
   float mx = m;
@@ -721,14 +727,20 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
   const int64_t dst = merge_row_offset(p, layer_rel, entry, (int64_t)kvh * p.group + gi);
   const float inv_l = 1.0f / lsum;
+  // k outermost: one shared-memory read and one multiply per rank index, the (up to four) columns of a lane as
+  // independent loads of the same B row -- the column-outer form re-read olr_s and recomputed the 64-bit row address per
+  // (column, k) and was most of the ~5000 instructions a warp executed at rank 64
+  const float* bp = b + lane;
+  for (int k = 0; k < p.r; ++k, bp += dkv) {
+    const float sk = scale * olr_s[warp][k];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (lane + 32 * i < p.D) acc[i] = fmaf(sk, __ldg(bp + 32 * i), acc[i]);
+  }
 #pragma unroll
   for (int i = 0; i < kMaxCols; ++i) {
     const int c = lane + 32 * i;
-    if (c < p.D) {
-      float o = acc[i];
-      for (int k = 0; k < p.r; ++k) o = fmaf(scale * olr_s[warp][k], b[k * dkv + c], o);
-      store_out(p, dst + c, o * inv_l);
-    }
+    if (c < p.D) store_out(p, dst + c, acc[i] * inv_l);
   }
 }
 

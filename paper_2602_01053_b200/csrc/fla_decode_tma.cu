@@ -37,6 +37,7 @@ namespace lk {
 namespace {
 
 constexpr int kWarps = 8;           // warps per CTA
+constexpr int kWideWorkers = 3;     // single-warp workers per CTA when they take 32-key tiles (d_head 128)
 constexpr int kKeyStep = 16;        // keys per MMA k-step; a tile is KT of them
 constexpr int kMaxStages = 24;      // ring depth limit per worker
 constexpr int kRingBudget = 216 * 1024;   // of the 227 KB a CTA may own
@@ -108,10 +109,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // PA: every batch entry has its own V_lr page set (BaseShared).  A stage then holds K, V_base and one V_lr tile per
 // entry of the row block; the lanes of the producer warp issue the V_lr copies in parallel (lane e -> entry e), and
 // a consumer warp runs the O_lr MMA once per entry its 16 rows touch with P masked to that entry's rows.
-template <int D, int RP, int MW, int KT, bool PA = false>
-__global__ void __launch_bounds__(kWarps * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
+// NW = warps per CTA.  Eight, except for single-warp workers at d_head 128 (kWideWorkers): three workers with 32-key tiles
+// and four-stage rings stream faster than eight with 16-key tiles and three-stage rings (cfg 2: 0.695 -> 0.617 ms per
+// step, 7.1 TB/s) -- the bulk copies are twice as large and every worker prefetches deeper, and three warps still cover
+// the few MMAs a <= 16-row tile needs.  d_head 64 and the multi-warp workers lose with fewer warps (measured).
+template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps>
+__global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
   constexpr int kTK = kKeyStep * KT;                    // keys per tile
-  constexpr int kWorkers = kWarps / MW;
+  constexpr int kWorkers = NW / MW;
   constexpr int kBlocks = D / 64;                       // 64-column blocks of a K / V page
   constexpr uint32_t kBlockBytes = kTK * 128;           // one block of one tile
   constexpr uint32_t kKvBytes = kBlocks * kBlockBytes;  // K (or V) tile
@@ -588,12 +593,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   }
 }
 
-template <int D, int RP, int MW, int KT, bool PA = false>
+template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps>
 int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
-  auto kern = fla_decode_tma_kernel<D, RP, MW, KT, PA>;
+  auto kern = fla_decode_tma_kernel<D, RP, MW, KT, PA, NW>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);
-  kern<<<grid, kWarps * 32, smem, ctx->stream>>>(dp);
+  kern<<<grid, NW * 32, smem, ctx->stream>>>(dp);
   prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
@@ -622,7 +627,12 @@ int launch_rp_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t 
 
 template <int D, int RP>
 int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt) {
-  if (mw == 1) return launch_t<D, RP, 1, 1>(ctx, dp, grid, smem);
+  if (mw == 1) {
+    if constexpr (D == 128) {
+      if (kt == 2) return launch_t<D, RP, 1, 2, false, kWideWorkers>(ctx, dp, grid, smem);
+    }
+    return launch_t<D, RP, 1, 1>(ctx, dp, grid, smem);
+  }
   if (kt == 2) {
     switch (mw) {
       case 2: return launch_t<D, RP, 2, 2>(ctx, dp, grid, smem);
@@ -809,10 +819,11 @@ int launch_decode_tma(const PagedAttnCall& c) {
   while (16 * mw < rows_total && mw < 8) mw *= 2;
   const int rows_blk = 16 * mw;
   const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
-  const int workers_per_cta = kWarps / mw;
   const bool pa = c.per_entry_lr && rp > 0;
   const int lr_per_block = pa ? (int)std::min<int64_t>(rows_blk / group, c.n_batch) : 1;   // V_lr tiles per stage
-  const int kt = (!pa && mw > 1 && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;   // 32-key tiles for multi-warp workers
+  // 32-key tiles for multi-warp workers and, at d_head 128, for single-warp workers (then three per CTA, see the kernel)
+  const int kt = (!pa && (mw > 1 || d == 128) && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;
+  const int workers_per_cta = (mw == 1 && kt == 2) ? kWideWorkers : kWarps / mw;
   const int tk = kKeyStep * kt;
   const uint32_t stage_bytes = tk * (4 * d + 2 * rp * lr_per_block);
   if (pa && (size_t)workers_per_cta * 2 * stage_bytes > (size_t)kRingBudget)

@@ -268,6 +268,20 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
                         "peak_sustained": peak_sustained,
                         "frac_of_sustained": (flops / (attn_ms * 1e-3) / 1e12 / peak_sustained) if peak_sustained else None},
            "clocks": prefill_clocks}
+    # cold prefill ("also report cold L_p = 0"): the same L_c rows attending only to themselves
+    try:
+        pool.prefill_device(ad, 0, 1, n_q, q.data_ptr(), L_c, 0, out.data_ptr())
+        c0, c1 = ctx.event(), ctx.event()
+        c0.record()
+        for i in range(steps):
+            pool.prefill_device(ad, i % n_layers, 1, n_q, q.data_ptr(), L_c, 0, out.data_ptr())
+        c1.record()
+        cold_ms = c0.elapsed_ms(c1) / steps
+        cold_flops = 2 * n_q * (L_c * (L_c + 1) // 2) * (2 * d + r) + 2 * n_q * L_c * r * d
+        res["cold"] = {"L_c": L_c, "query_offset": 0, "attention_ms_per_layer": cold_ms, "algorithmic_flops": cold_flops,
+                       "attention_tflops": cold_flops / (cold_ms * 1e-3) / 1e12, "frac": cold_flops / (cold_ms * 1e-3) / 1e12 / peak}
+    except Exception as e:
+        res["cold"] = {"error": str(e)[:200]}
     # parity: a seeded sample of query rows against the reference CPU path (rows via L_c = 1)
     if not args.no_cpu_baseline:
         from oracle import checker

@@ -298,7 +298,8 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
             want = chk.gqa_attention(np.ascontiguousarray(qh[i][None, :]), k0[:pos + 1], v0[:pos + 1], lr0[:pos + 1], b1,
                                      16.0 / r if r else 1.0, pos, n_q, n_kv, threads=host_threads())
             worst = max(worst, chk.max_rel_error(got[i][None, :], want))
-        res["parity"] = {"sampled_rows": rows, "max_rel_error": worst, "tolerance": 2e-2, "oracle": chk.kind}
+        res["parity"] = {"sampled_rows": rows, "max_rel_error": worst, "tolerance": 2e-2 if args.dtype == "bf16" else 1e-4,
+                         "oracle": chk.kind}
     # the X*A projection + LR append of the same L_c rows (scratch pool, one layer)
     try:
         x = torch.randn((L_c, d_model), generator=gen, device=dev, dtype=torch.float32)

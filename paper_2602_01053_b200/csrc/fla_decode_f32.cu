@@ -81,6 +81,22 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) 
   hi = __float_as_uint(x) & 0xffffe000u;
   lo = __float_as_uint(x - __uint_as_float(hi));
 }
+// acc += a * b with the running sum kept OUT of the tensor-core accumulator: the MMA adds its products into C with
+// truncation, a bias of up to 2^-24 per instruction that grows linearly with the length of the chain (4096 key tiles of a
+// 32K-token row: 2e-4 -- measured, and over the 1e-4 contract).  The tile's product therefore starts from zero and
+// is added to the running sum with an ordinary round-to-nearest FADD, whose error grows only as the square root.
+__device__ __forceinline__ void mma_3x_add(float (&acc)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
+                                           uint32_t bl0, uint32_t bl1) {
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  mma_tf32(d, al[0], al[1], al[2], al[3], bh0, bh1);
+  mma_tf32(d, ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+  mma_tf32(d, ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+  // two packed adds (add.rn.f32x2, sm_100) instead of four scalar ones: the adds are pure issue pressure here
+  asm("{\n\t.reg .b64 a, b;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 b, {%4, %5};\n\tadd.rn.f32x2 a, a, b;\n\tmov.b64 {%0, %1}, a;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%6, %7};\n\tadd.rn.f32x2 a, a, b;\n\tmov.b64 {%2, %3}, a;\n\t}"
+      : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
+      : "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]));
+}
 // c += a * b for full-precision fragments: small terms first
 __device__ __forceinline__ void mma_3x(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
                                        uint32_t bl0, uint32_t bl1) {
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF
       uint32_t bh0, bl0, bh1, bl1;
       split_tf32(v0, bh0, bl0);
       split_tf32(v1, bh1, bl1);
-      mma_3x(o[nt], ph, pl, bh0, bh1, bl0, bl1);
+      mma_3x_add(o[nt], ph, pl, bh0, bh1, bl0, bl1);
     }
     if (RP > 0) {
 #pragma unroll
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF
         uint32_t bh0, bl0, bh1, bl1;
         split_tf32(lds32(a0), bh0, bl0);
         split_tf32(lds32(a1), bh1, bl1);
-        mma_3x(olr[nt], ph, pl, bh0, bh1, bl0, bl1);
+        mma_3x_add(olr[nt], ph, pl, bh0, bh1, bl0, bl1);
       }
     }
 
@@ -548,7 +564,7 @@ __global__ void __launch_bounds__(256, 1) fla_prefill_f32_kernel(const PrefillF3
         uint32_t bh0, bl0, bh1, bl1;
         split_tf32(v0, bh0, bl0);
         split_tf32(v1, bh1, bl1);
-        mma_3x(o[nt], ph, pl, bh0, bh1, bl0, bl1);
+        mma_3x_add(o[nt], ph, pl, bh0, bh1, bl0, bl1);
       }
       if (RP > 0) {
 #pragma unroll
@@ -560,7 +576,7 @@ __global__ void __launch_bounds__(256, 1) fla_prefill_f32_kernel(const PrefillF3
           uint32_t bh0, bl0, bh1, bl1;
           split_tf32(lds32(a0), bh0, bl0);
           split_tf32(lds32(a1), bh1, bl1);
-          mma_3x(olr[nt], ph, pl, bh0, bh1, bl0, bl1);
+          mma_3x_add(olr[nt], ph, pl, bh0, bh1, bl0, bl1);
         }
       }
     }

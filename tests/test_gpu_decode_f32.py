@@ -159,3 +159,27 @@ def test_prefill_f32_masked_keys_contribute_exactly_zero(ctx, orc):
         assert ctx.last_kernel() == "fla_prefill_f32"
         pool.close(); ad.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_prefill_f32_long_rows_stay_at_fp32_accuracy(ctx, orc):
+    """A 32K-token row is 4096 key tiles.  Tensor-core MMAs add into their accumulator with truncation, a bias that grows
+    linearly with the chain (2e-4 at this length when the running sums lived in the MMA accumulators); the kernels keep the
+    running sums in ordinary fp32 adds instead.  Checked against the float64 reference path, far inside the 1e-4 contract."""
+    from paper_2602_01053_b200 import Adapters, Pool, abi
+    from tests.cases import synthetic_layer
+    n_q, n_kv, d, r, A, L, L_c = 4, 2, 128, 16, 2, 32768, 16
+    _, k, v, v_lr, b, s = synthetic_layer(orc, 11, L, 1, n_q, n_kv, d, r, A)
+    q = orc.gaussian(L_c, n_q * d, 99, 1.0 / np.sqrt(d), np.float32)
+    pool = Pool(ctx, "BaseLRShared", 1, n_kv, d, 64, r, A, max_tokens=L, dtype=abi.F32)
+    ad = Adapters(ctx, 1, A, 64, r, n_kv, d, dtype=abi.F32)
+    pool.append_tokens(L)
+    pool.append_key(0, 0, 0, k); pool.append_value(0, 0, 0, v); pool.append_lr(0, 0, 0, v_lr)
+    for a in range(A):
+        ad.set_b(0, a, b[a], 16.0)
+    got = pool.prefill(ad, 0, 1, n_q, q, L - L_c)
+    assert ctx.last_kernel() == "fla_prefill_f32"
+    f64 = lambda x: np.asarray(x, np.float64)
+    want = orc.gqa_attention(f64(q), f64(k), f64(v), f64(v_lr), f64(b[1]), float(s), L - L_c, n_q, n_kv)
+    err = float(np.max(np.abs(f64(got) - want)) / np.max(np.abs(want)))
+    assert err <= 2e-5, err
+    pool.close(); ad.close()

@@ -164,3 +164,25 @@ def test_decode_tma_layer_chunks_keep_results(ctx, orc):
             want = orc.gqa_attention(q[a], k, v, v_lr, b[a], s, L - 1, n_q, n_kv)
             assert orc.max_rel_error(chunked[l, a][None, :], want) <= TOL, (l, a)
     pool.close()
+
+
+def test_kernel_timing_api_averages_back_to_back_calls(ctx, orc):
+    """lorakv_ctx_mean_kernel_ms: one event pair per fast-path call since profiling was switched on, no synchronisation
+    between the calls (bench.py's roofline denominator)."""
+    from paper_2602_01053_b200 import abi
+    n_q, n_kv, d, r, A, L = 8, 2, 128, 16, 3, 2048
+    pool, ad, layers = build_pool(ctx, orc, "BaseLRShared", abi.BF16, 5, L, 1, n_q, n_kv, d, r, A)
+    qs = np.stack([layers[0][0][a][0] for a in range(A)])[None]
+    ctx.set_profiling(True)
+    with pytest.raises(abi.LorakvError, match="no profiled"):
+        ctx.mean_kernel_ms()
+    for _ in range(3):
+        pool.decode(ad, 0, 1, list(range(A)), n_q, qs)
+    ms, n = ctx.mean_kernel_ms()
+    assert n == 3 and 0.0 < ms < 5.0
+    assert 0.0 < ctx.last_kernel_ms() < 5.0
+    pool.decode(ad, 0, 1, list(range(A)), n_q, qs)
+    ms, n = ctx.mean_kernel_ms()             # the counter restarts after a read
+    assert n == 1
+    ctx.set_profiling(False)
+    pool.close()

@@ -522,7 +522,7 @@ def main():
     n_prof_steps = min(args.steps, 256 // (n_layers if args.per_layer_launch else 1))
     kernel_ms, n_prof = ctx.mean_kernel_ms()
     ctx.set_profiling(False)
-    launches_per_step = max(1, round(n_prof / n_prof_steps))     # the library may cut a step into layer chunks (L2-resident V_lr)
+    launches_per_step = max(1, round(n_prof / n_prof_steps))     # attention launches the library made per step (1 today)
     if not args.per_layer_launch:
         kernel_ms *= launches_per_step                            # attention-kernel time per step = per algorithmic_bytes_per_launch
 
@@ -603,7 +603,7 @@ def main():
                    "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "launch": "per-layer" if args.per_layer_launch else
                              ("one launch per step over all layers" if launches_per_step == 1 else
-                              f"{launches_per_step} layer-chunk launches per step (V_lr of a chunk stays in L2)"),
+                              f"{launches_per_step} attention launches per step"),
                    "l2": f"inputs ({alg / 1e9:.2f} GB per step) larger than L2; no flush needed",
                    "kernel": ctx.last_kernel(), "output_gather": gather_mode, "output_gather_check": gather_check},
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": d2h_bytes,

@@ -37,7 +37,9 @@ namespace lk {
 namespace {
 
 constexpr int kWarps = 8;           // warps per CTA
-constexpr int kWideWorkers = 3;     // single-warp workers per CTA when they take 32-key tiles (d_head 128)
+// single-warp workers per CTA when they take 32-key tiles: three at d_head 128, four at d_head 64 (half the bytes per
+// key for the same softmax work: 3 x 32 loses there, 0.253 vs 0.204 ms on a 16-layer probe, 4 x 32 gains 4 %)
+constexpr int wide_workers(int d) { return d == 128 ? 3 : 4; }
 constexpr int kKeyStep = 16;        // keys per MMA k-step; a tile is KT of them
 constexpr int kMaxStages = 24;      // ring depth limit per worker
 constexpr int kRingBudget = 216 * 1024;   // of the 227 KB a CTA may own
@@ -109,10 +111,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // PA: every batch entry has its own V_lr page set (BaseShared).  A stage then holds K, V_base and one V_lr tile per
 // entry of the row block; the lanes of the producer warp issue the V_lr copies in parallel (lane e -> entry e), and
 // a consumer warp runs the O_lr MMA once per entry its 16 rows touch with P masked to that entry's rows.
-// NW = warps per CTA.  Eight, except for single-warp workers at d_head 128 (kWideWorkers): three workers with 32-key tiles
+// NW = warps per CTA.  Eight, except for single-warp workers (wide_workers): at d_head 128 three workers with 32-key tiles
 // and four-stage rings stream faster than eight with 16-key tiles and three-stage rings (cfg 2: 0.695 -> 0.617 ms per
 // step, 7.1 TB/s) -- the bulk copies are twice as large and every worker prefetches deeper, and three warps still cover
-// the few MMAs a <= 16-row tile needs.  d_head 64 and the multi-warp workers lose with fewer warps (measured).
+// the few MMAs a <= 16-row tile needs.  d_head 64 wants four (three lose there) and the multi-warp workers keep eight warps
+// (fewer lose: cfg 4 with 6 warps 1.87 ms vs 1.41 ms).
 template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps>
 __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
   constexpr int kTK = kKeyStep * KT;                    // keys per tile
@@ -628,9 +631,7 @@ int launch_rp_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t 
 template <int D, int RP>
 int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt) {
   if (mw == 1) {
-    if constexpr (D == 128) {
-      if (kt == 2) return launch_t<D, RP, 1, 2, false, kWideWorkers>(ctx, dp, grid, smem);
-    }
+    if (kt == 2) return launch_t<D, RP, 1, 2, false, wide_workers(D)>(ctx, dp, grid, smem);
     return launch_t<D, RP, 1, 1>(ctx, dp, grid, smem);
   }
   if (kt == 2) {
@@ -821,9 +822,9 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
   const bool pa = c.per_entry_lr && rp > 0;
   const int lr_per_block = pa ? (int)std::min<int64_t>(rows_blk / group, c.n_batch) : 1;   // V_lr tiles per stage
-  // 32-key tiles for multi-warp workers and, at d_head 128, for single-warp workers (then three per CTA, see the kernel)
-  const int kt = (!pa && (mw > 1 || d == 128) && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;
-  const int workers_per_cta = (mw == 1 && kt == 2) ? kWideWorkers : kWarps / mw;
+  // 32-key tiles whenever a page holds them; single-warp workers then run three (d_head 128) or four (64) per CTA
+  const int kt = (!pa && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;
+  const int workers_per_cta = (mw == 1 && kt == 2) ? wide_workers(d) : kWarps / mw;
   const int tk = kKeyStep * kt;
   const uint32_t stage_bytes = tk * (4 * d + 2 * rp * lr_per_block);
   if (pa && (size_t)workers_per_cta * 2 * stage_bytes > (size_t)kRingBudget)

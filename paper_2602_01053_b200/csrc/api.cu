@@ -3,6 +3,7 @@
 // adapter tables (proj/include/lorakv/lora.hpp:13-87) and the dispatch into the kernels.
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "kernels.hpp"
@@ -44,6 +45,36 @@ int pinned_reserve(lorakv_ctx* ctx, size_t bytes) {
   ctx->pinned = nullptr; ctx->pinned_bytes = 0;
   LK_CUDA(cudaMallocHost(&ctx->pinned, bytes));
   ctx->pinned_bytes = bytes;
+  return LORAKV_OK;
+}
+
+int stage_agent_ids(lorakv_ctx* ctx, const int32_t* ids, int64_t n, const int32_t** dev) {
+  for (IdSlot& s : ctx->id_slots)
+    if (s.dev && (int64_t)s.ids.size() == n && std::memcmp(s.ids.data(), ids, (size_t)n * sizeof(int32_t)) == 0) {
+      *dev = s.dev;
+      return LORAKV_OK;
+    }
+  IdSlot& s = ctx->id_slots[ctx->id_next];
+  ctx->id_next = (ctx->id_next + 1) % lorakv_ctx::kIdSlots;
+  if (!s.copied) LK_CUDA(cudaEventCreateWithFlags(&s.copied, cudaEventDisableTiming));
+  if ((size_t)n > s.cap) {
+    LK_CUDA(cudaStreamSynchronize(ctx->stream));     // kernels reading the old device buffer are done
+    if (s.host) LK_CUDA(cudaFreeHost(s.host));
+    if (s.dev) LK_CUDA(cudaFree(s.dev));
+    s.host = nullptr; s.dev = nullptr; s.cap = 0; s.ids.clear();
+    const size_t cap = std::max<size_t>(64, (size_t)n * 2);
+    LK_CUDA(cudaMallocHost(&s.host, cap * sizeof(int32_t)));
+    LK_CUDA(cudaMalloc(&s.dev, cap * sizeof(int32_t)));
+    s.cap = cap;
+  } else {
+    LK_CUDA(cudaEventSynchronize(s.copied));         // the previous copy out of this pinned buffer has completed
+  }
+  std::memcpy(s.host, ids, (size_t)n * sizeof(int32_t));
+  s.ids.assign(ids, ids + n);
+  // stream order protects the device buffer: kernels of earlier calls that read it run before this copy
+  LK_CUDA(cudaMemcpyAsync(s.dev, s.host, (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  LK_CUDA(cudaEventRecord(s.copied, ctx->stream));
+  *dev = s.dev;
   return LORAKV_OK;
 }
 
@@ -139,6 +170,8 @@ int lorakv_ctx_create(int device, void* stream, lorakv_ctx** out) {
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
   ctx->l2_bytes = prop.l2CacheSize > 0 ? (int64_t)prop.l2CacheSize : (int64_t)126 << 20;
+  const char* no_pdl = std::getenv("LORAKV_NO_PDL");       // A/B switch for the programmatic dependent launches
+  ctx->pdl = !(no_pdl && no_pdl[0] == '1');
   if (stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -157,6 +190,11 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
   for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj})
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (IdSlot& s : ctx->id_slots) {
+    if (s.host) cudaFreeHost(s.host);
+    if (s.dev) cudaFree(s.dev);
+    if (s.copied) cudaEventDestroy(s.copied);
+  }
   for (cudaEvent_t e : ctx->prof_ev) if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->prof_ring) if (e) cudaEventDestroy(e);
   if (ctx->owns_stream) cudaStreamDestroy(ctx->stream);
@@ -1081,27 +1119,26 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   const int64_t n_elems = n_layers * n_batch * rows_per_entry * n_q_local * pool->dims.d_head;
   if (n_elems == 0) return LORAKV_OK;
 
-  // agent ids -> device (tiny), staged through pinned memory
-  LK_TRY(pinned_reserve(ctx, 4096 + (size_t)n_batch * sizeof(int32_t)));
-  int32_t* ids_host = static_cast<int32_t*>(ctx->pinned);
+  // agent ids -> device: staged once per distinct list (stage_agent_ids), no copy when the batch repeats
+  std::vector<int32_t> ids_host((size_t)n_batch);
   for (int64_t i = 0; i < n_batch; ++i) {
     const int32_t a = agent_ids ? agent_ids[i] : 0;
     if (a < 0 || a >= pool->dims.n_agents) return fail("unknown agent %d", a);
     if (ad && pool->r_pad > 0)
       for (int64_t l = layer_begin; l < layer_end; ++l)
         if (!ad->b_set[(size_t)(l * ad->n_agents + a)]) return fail("attention: B of layer %lld agent %d was never uploaded", (long long)l, a);
-    ids_host[i] = a;
+    ids_host[(size_t)i] = a;
   }
-  const size_t ids_bytes = ((size_t)n_batch * sizeof(int32_t) + 255) / 256 * 256;
   const size_t q_bytes = (size_t)n_elems * sizeof(float);
   const bool host = mem_kind == LORAKV_HOST;
   if (!host && mem_kind != LORAKV_DEVICE) return fail("bad mem_kind %d", mem_kind);
   // with a peer gather the rows go to the gather buffers; the local slab only serves the paths without a merge epilogue
   const bool local_slab = host || peers;
-  LK_TRY(scratch_reserve(ctx, ctx->out, ids_bytes + (local_slab ? 2 * ((q_bytes + 255) / 256 * 256) : 0)));
+  if (local_slab) LK_TRY(scratch_reserve(ctx, ctx->out, 2 * ((q_bytes + 255) / 256 * 256)));
   char* base = static_cast<char*>(ctx->out.ptr);
-  int32_t* ids_dev = reinterpret_cast<int32_t*>(base);
-  LK_CUDA(cudaMemcpyAsync(ids_dev, ids_host, (size_t)n_batch * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+  const size_t ids_bytes = 0;
+  const int32_t* ids_dev = nullptr;
+  LK_TRY(stage_agent_ids(ctx, ids_host.data(), n_batch, &ids_dev));
   const float* q_dev = q;
   float* out_dev = out;
   if (local_slab) out_dev = reinterpret_cast<float*>(base + ids_bytes + (q_bytes + 255) / 256 * 256);

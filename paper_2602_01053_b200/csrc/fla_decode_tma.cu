@@ -45,6 +45,21 @@ constexpr int kMaxStages = 24;      // ring depth limit per worker
 constexpr int kRingBudget = 216 * 1024;   // of the 227 KB a CTA may own
 constexpr float kRescaleThreshold = 8.0f;   // log2 units: p stays <= 2^8 between rescales
 
+#ifdef LK_DECODE_TRACE
+// debug build only (make EXTRA=-DLK_DECODE_TRACE): per-warp phase timestamps of the last launch, tools/probe_decode_trace.py
+__device__ unsigned long long g_decode_trace[1024 * 16];
+__device__ __forceinline__ void trace_mark(int64_t warp_global, int slot) {
+  if ((threadIdx.x & 31) == 0 && warp_global < 1024) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_decode_trace[warp_global * 16 + slot] = t;
+  }
+}
+#define LK_TRACE(slot) trace_mark((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), slot)
+#else
+#define LK_TRACE(slot)
+#endif
+
 struct DecodeParams {
   const __nv_bfloat16 *k_pages, *v_pages, *lr_pages;
   const int32_t *kv_table, *lr_table;
@@ -67,6 +82,7 @@ struct DecodeParams {
   const int32_t* agent_ids;   // [n_batch]
   int lr_max_pages;
   int lr_per_block;           // entries of one row block = V_lr tiles per stage (16 * MW / group)
+  int identity;               // bit 0 / 1: the K-V / V_lr page table is the identity (PageSpace::identity): no table load
 };
 
 // The cache is streamed exactly once per step, so the copies carry an L2 evict-first policy: the lines
@@ -136,6 +152,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   const int wk = warp / MW, wi = warp % MW;
   const int g = lane >> 2, t = lane & 3;
   const int NS = p.n_stages;
+  LK_TRACE(0);
 
   if (threadIdx.x == 0) {
     for (int a = 0; a < kWorkers; ++a)
@@ -146,13 +163,17 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
     ptx::fence_barrier_init();
   }
   __syncthreads();
+  LK_TRACE(1);
 
-  const int64_t w = (int64_t)blockIdx.x * kWorkers + wk;
+  // (unit, tile) arithmetic in 32 bits: the launcher checks that the tile count of the launch fits.  The 64-bit divisions
+  // of the first version cost a lone warp ~2 us before its first bulk copy went out (a one-layer launch lasts ~25).
+  const int w = (int)blockIdx.x * kWorkers + wk;
+  const int T32 = (int)p.T, G32 = (int)p.G, total32 = (int)p.total_tiles;
   // A launch whose low-rank cache does not fit in L2 is cut into p.n_chunks equal LAYER CHUNKS that every worker walks
   // through one after the other (no grid barrier: all workers get the same share of every chunk and stay in step), so
   // that at any time the kv heads of only a few layers are in flight and their shared V_lr tiles are served by L2.
   // Inside a chunk the (unit, tile) pairs are cut into equal contiguous ranges as before (p.total_tiles per chunk).
-  int64_t g0 = 0;
+  int g0 = 0, first_unit = 0;
   int n = 0, chunk = 0;
 
   const uint32_t ring = ptx::smem_u32(smem) + (uint32_t)wk * (uint32_t)NS * kStageBytes;
@@ -166,22 +187,23 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
 
   // Producer cursor.  Everything the per-tile path needs is carried incrementally (unit, tile, page,
   // token, stage, wrap count): the only divisions happen here and at unit changes, never per tile.
-  const int T32 = (int)p.T;
-  int64_t p_unit = 0;
+  int p_unit = 0;
   int p_tl = 0, p_page = 0, p_tok = 0, p_layer = 0, p_kvh = 0;
   int p_stage = 0, p_wrap = 0, p_issued = 0;      // stage and wrap count run on across chunks, like the consumer's
 
   auto issue_next = [&]() {       // whole producer warp; lane 0 talks to the TMA engine
     // the stage must have been released by every warp of the worker (a fresh barrier passes the parity-1 wait)
     ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
-    if (p_page < win_base || p_page >= win_base + 32) {
+    if (p_issued == 1) LK_TRACE(11);
+    const bool id_kv = (p.identity & 1) != 0, id_lr = (p.identity & 2) != 0 || RP == 0 || PA;
+    if (!(id_kv && id_lr) && (p_page < win_base || p_page >= win_base + 32)) {
       win_base = p_page;
       const int pg = p_page + lane;
-      win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
-      if (RP > 0 && !PA) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
+      if (!id_kv) win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
+      if (!id_lr) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
     }
-    const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
-    const int phys_lr = (RP > 0 && !PA) ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
+    const int phys_kv = id_kv ? p_page : __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
+    const int phys_lr = id_lr ? p_page : __shfl_sync(0xffffffffu, win_lr, p_page - win_base);
     int pa_entries = 0;         // PA: entries of this row block that exist (the last block may be ragged)
     if (PA) {
       const int e0 = (int)(p_unit % p.row_blocks) * p.lr_per_block;
@@ -200,6 +222,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
       const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride +
                              (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * 64;
       ptx::mbar_arrive_expect_tx(&full[p_stage], PA ? 2 * kKvBytes + (uint32_t)pa_entries * kLrBytes : kStageBytes);
+      if (p_issued == 1) LK_TRACE(12);
 #pragma unroll
       for (int b = 0; b < kBlocks; ++b) {
         bulk_g2s(dst + b * kBlockBytes, p.k_pages + kv_off + (int64_t)b * p.P * 64, kBlockBytes, &full[p_stage], p.l2_policy);
@@ -213,6 +236,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
         bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.lr_policy);
       }
     }
+    if (p_issued == 1) LK_TRACE(13);
     // advance the cursor
     ++p_issued;
     if (++p_stage == NS) { p_stage = 0; ++p_wrap; }
@@ -221,8 +245,8 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
     if (++p_tl == T32) {
       p_tl = 0; p_page = 0; p_tok = 0;
       ++p_unit;
-      p_layer = (int)(p_unit / units_per_layer);
-      p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
+      p_layer = p_unit / units_per_layer;
+      p_kvh = (p_unit / p.row_blocks) % p.n_kv_local;
     }
   };
 
@@ -231,10 +255,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   float o[kNO][4];
   float olr[kNL > 0 ? kNL : 1][4];
   float m_used[2], l_run[2];
-  int64_t cur_unit = -1;
+  int cur_unit = -1;
 
   auto flush = [&]() {            // partial of the unit just finished
-    const int64_t first_unit = g0 / p.T;
     const int64_t slot = ((int64_t)chunk * p.n_workers + w) * p.max_seg + (cur_unit - first_unit);
     float* base = p.part + (slot * (16 * MW) + wi * 16) * PS;
 #pragma unroll
@@ -256,61 +279,91 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   // ldmatrix lane roles
   const int mi = lane >> 3, rr = lane & 7;
 
+  // first rows of a unit: Q fragments (bf16, registers) and empty accumulators.  Two phases, so that the launch's first
+  // bulk copies can be issued while the query loads are in flight: load_q only ISSUES the loads (volatile asm keeps them
+  // ahead of the copies in program order), pack_q consumes them.
+  float2 qraw[2][D / 16][2];
+  auto load_q = [&](int u) {
+    const int layer_rel = u / units_per_layer;
+    const int kvh = (u / p.row_blocks) % p.n_kv_local;
+    const int rb = u % p.row_blocks;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rho = rb * 16 * MW + wi * 16 + g + 8 * h;
+      const bool real = rho < p.rows_total;
+      const int entry = real ? rho / p.group : 0, gi = real ? rho % p.group : 0;
+      const float* src = p.q + (((int64_t)layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          float2 v = make_float2(0.f, 0.f);
+          if (real)
+            asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(src + 16 * kk + 8 * part + 2 * t));
+          qraw[h][kk][part] = v;
+        }
+    }
+  };
+  auto pack_q = [&]() {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) {
+        qa[kk][h] = pack_bf16(qraw[h][kk][0].x, qraw[h][kk][0].y);
+        qa[kk][2 + h] = pack_bf16(qraw[h][kk][1].x, qraw[h][kk][1].y);
+      }
+      m_used[h] = ninf; l_run[h] = 0.f;
+    }
+#pragma unroll
+    for (int nt = 0; nt < kNO; ++nt) { o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f; }
+#pragma unroll
+    for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
+  };
+
+  // Everything above overlaps the tail of the previous kernel of the stream when this one was launched as a programmatic
+  // dependent (the merge of the previous layer, the projections of this one); from here on its results are read.
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
+  LK_TRACE(8);
+
   // consumer cursor, carried incrementally like the producer's
   int c_stage = 0, c_wrap = 0;
   for (chunk = 0; chunk < p.n_chunks; ++chunk) {
-  const int64_t chunk_base = (int64_t)chunk * p.total_tiles;
-  g0 = chunk_base + w * p.G;
-  const int64_t g1 = min(g0 + p.G, chunk_base + p.total_tiles);
-  n = g1 > g0 ? (int)(g1 - g0) : 0;
+  const int chunk_base = chunk * total32;
+  g0 = chunk_base + w * G32;
+  const int g1 = min(g0 + G32, chunk_base + total32);
+  n = g1 > g0 ? g1 - g0 : 0;
   if (n == 0) continue;
-  p_unit = g0 / p.T;
-  p_tl = (int)(g0 - p_unit * p.T);
+  p_unit = g0 / T32;
+  first_unit = p_unit;
+  p_tl = g0 - p_unit * T32;
   p_page = (p_tl * kTK) / p.P; p_tok = (p_tl * kTK) % p.P;
-  p_layer = (int)(p_unit / units_per_layer); p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
+  p_layer = p_unit / units_per_layer; p_kvh = (p_unit / p.row_blocks) % p.n_kv_local;
   p_issued = 0;
-  if (producer) {
-    const int pre = n < NS ? n : NS;
-    for (int i = 0; i < pre; ++i) issue_next();
-  }
-  cur_unit = -1;
-  int64_t u = g0 / p.T;
-  int tl = (int)(g0 - u * p.T);
+  int u = p_unit;
+  int tl = p_tl;
+  // Start-up order (measured with the phase trace of tools/probe_decode_trace.py): the query loads go out first -- once
+  // every SM's bulk copies are in flight the memory system is saturated and a plain load waits ~2.4 us behind them, 1.1 us
+  // on an idle one --, two stages are issued while they fly (0.4 us of issue work per stage: five bulk copies), then the
+  // fragments are packed and the rest of the ring goes out.  First tile consumed ~1 us earlier than "Q, then four stages".
+  cur_unit = u;
+  load_q(u);
+  LK_TRACE(14);
+  const int pre = n < NS ? n : NS;
+  if (producer)
+    for (int i = 0; i < (pre < 2 ? pre : 2); ++i) { issue_next(); if (i == 0) LK_TRACE(10); }
+  pack_q();
+  LK_TRACE(9);
+  if (producer)
+    for (int i = 2; i < pre; ++i) issue_next();
+  LK_TRACE(2);
   for (int i = 0; i < n; ++i) {
-    if (u != cur_unit) {
-      if (cur_unit >= 0) flush();
-      cur_unit = u;
-      const int layer_rel = (int)(u / units_per_layer);
-      const int kvh = (int)((u / p.row_blocks) % p.n_kv_local);
-      const int rb = (int)(u % p.row_blocks);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rho = rb * 16 * MW + wi * 16 + g + 8 * h;
-        const bool real = rho < p.rows_total;
-        const int entry = real ? rho / p.group : 0, gi = real ? rho % p.group : 0;
-        const float* src = p.q + (((int64_t)layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          float2 lo = make_float2(0.f, 0.f), hi = make_float2(0.f, 0.f);
-          if (real) {
-            lo = __ldg(reinterpret_cast<const float2*>(src + 16 * kk + 2 * t));
-            hi = __ldg(reinterpret_cast<const float2*>(src + 16 * kk + 8 + 2 * t));
-          }
-          qa[kk][h] = pack_bf16(lo.x, lo.y);
-          qa[kk][2 + h] = pack_bf16(hi.x, hi.y);
-        }
-        m_used[h] = ninf; l_run[h] = 0.f;
-      }
-#pragma unroll
-      for (int nt = 0; nt < kNO; ++nt) { o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f; }
-#pragma unroll
-      for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
-    }
-
     // refill the stage released one iteration ago (tile p_issued goes where tile p_issued - NS was)
     if (producer && i >= 1 && p_issued < n) issue_next();
     const int s = c_stage;
+    if (i == 0) LK_TRACE(3);
     ptx::mbar_wait(&full[s], (uint32_t)(c_wrap & 1));
+    if (i == 0) LK_TRACE(4);
 
     const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
 
@@ -455,9 +508,15 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&empty[s]);
     if (++c_stage == NS) { c_stage = 0; ++c_wrap; }
-    if (++tl == T32) { tl = 0; ++u; }
+    if (++tl == T32) {
+      tl = 0; ++u;
+      if (i + 1 < n) { flush(); cur_unit = u; load_q(u); pack_q(); }
+    }
+    if (i == 0) LK_TRACE(5);
   }
+  LK_TRACE(6);
   flush();
+  LK_TRACE(7);
   }   // layer chunks
 }
 
@@ -492,14 +551,19 @@ __device__ __forceinline__ void store_out(const DecodeMergeParams& p, int64_t of
 
 constexpr int kMergeWarps = 8;
 
-// One CTA per (query row, layer x kv head).  The splits of the row are spread over the warps (warp w takes
-// splits w, w + 8, ...), the 4 + D + RP columns of a partial over the lanes, so every global read is a
-// coalesced 128-byte line and a row with ~150 partials (one layer per launch) costs ~20 dependent steps,
-// not 150.
+// One CTA per (query row, layer x kv head): the latency-optimised merge of a launch with few rows (one layer per launch:
+// ~55 splits per row at cfg 2).  ONE global round trip after the attention kernel completes: warp w takes splits w, w + 8,
+// ... and issues the loads of up to eight of them -- (m, l) and its lanes' columns of O / O_lr -- before using any; it
+// reduces them relative to its own maximum, the warps' results meet in shared memory.  Everything that does not depend on
+// the attention kernel happens BEFORE pdl_wait(): address arithmetic and this thread's column of B[agent] (static data), so
+// under a programmatic dependent launch the CTA is resident and set up when the partials arrive.
 __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(const DecodeMergeParams p) {
-  extern __shared__ float sm[];          // [ns] weights | [kMergeWarps][D + RP] per-warp sums
-  __shared__ float red_s[kMergeWarps];
-  __shared__ float stat_s[2];            // row max, row denominator
+  constexpr int kMaxCols = 6;            // (D + RP) <= 192 columns / 32 lanes
+  constexpr int kBatch = 8;              // splits of a warp in flight together
+  constexpr int kMaxRank = 64;
+  __shared__ float m_s[kMergeWarps], l_s[kMergeWarps];
+  __shared__ float acc_s[kMergeWarps][192];
+  __shared__ float tot_s[192];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rho = blockIdx.x;
   const int kvh = blockIdx.y % p.n_kv_local;
@@ -511,71 +575,15 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   const int64_t w_lo = (u_loc * p.T) / p.G, w_hi = ((u_loc + 1) * p.T - 1) / p.G;
   const int ns = (int)(w_hi - w_lo + 1);
   const int PS = 4 + p.D + p.RP, C = p.D + p.RP;
-  float* w_s = sm;
-  float* acc_s = sm + ns;
   const float ninf = -std::numeric_limits<float>::infinity();
   // partial of split s: worker w_lo + s, segment = unit minus the worker's first unit.  Only the FIRST worker of a unit can
   // have started in an earlier unit (every later one starts inside it: segment 0), so one 64-bit division serves the row
-  // instead of one per split (they were half of the instructions this kernel executed)
   const int64_t seg_lo = u_loc - (w_lo * p.G) / p.T;
   const float* part0 = p.part + ((ch * p.n_workers + w_lo) * p.max_seg * rows_blk + r_in) * PS;
   const int64_t split_stride = (int64_t)p.max_seg * rows_blk * PS;
   const int64_t seg_off = seg_lo * rows_blk * PS;
   auto row_of = [&](int s) -> const float* { return part0 + s * split_stride + (s == 0 ? seg_off : 0); };
-  // ---- row max over the splits ----
-  float mx = ninf;
-  for (int s = tid; s < ns; s += kMergeWarps * 32) mx = fmaxf(mx, row_of(s)[0]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (lane == 0) red_s[warp] = mx;
-  __syncthreads();
-  if (tid == 0) {
-    float m = red_s[0];
-    for (int i = 1; i < kMergeWarps; ++i) m = fmaxf(m, red_s[i]);
-    stat_s[0] = m;
-  }
-  __syncthreads();
-  mx = stat_s[0];
-  // ---- weights and the denominator ----
-  float l = 0.f;
-  for (int s = tid; s < ns; s += kMergeWarps * 32) {
-    const float* row = row_of(s);
-    const float wgt = (row[0] == ninf) ? 0.f : exp2f(row[0] - mx);
-    w_s[s] = wgt;
-    l += wgt * row[1];
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-  __syncthreads();                       // red_s reused; w_s complete
-  if (lane == 0) red_s[warp] = l;
-  __syncthreads();
-  if (tid == 0) {
-    float t = 0.f;
-    for (int i = 0; i < kMergeWarps; ++i) t += red_s[i];
-    stat_s[1] = t;
-  }
-  // ---- weighted sums of O and O_lr: warps over splits, lanes over columns ----
-  constexpr int kMaxCols = 6;            // (D + RP) <= 192 columns / 32 lanes
-  float acc[kMaxCols];
-#pragma unroll
-  for (int i = 0; i < kMaxCols; ++i) acc[i] = 0.f;
-  for (int s = warp; s < ns; s += kMergeWarps) {
-    const float wgt = w_s[s];
-    if (wgt == 0.f) continue;            // an empty split carries no accumulators
-    const float* row = row_of(s) + 4;
-#pragma unroll
-    for (int i = 0; i < kMaxCols; ++i) {
-      const int c = lane + 32 * i;
-      if (c < C) acc[i] = fmaf(wgt, row[c], acc[i]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kMaxCols; ++i) {
-    const int c = lane + 32 * i;
-    if (c < C) acc_s[warp * C + c] = acc[i];
-  }
-  __syncthreads();
-  // ---- epilogue: o += (lr_scale * o_lr[k]) * B[agent][k,:], out = o / l (attention.hpp:244-259) ----
+  // ---- epilogue operands that do not depend on the attention kernel ----
   const int gi = rho % p.group, entry = rho / p.group;
   const int64_t layer = p.layer_begin + layer_rel;
   const int64_t dkv = (int64_t)p.n_kv_local * p.D;
@@ -583,25 +591,94 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   const float* b = p.r > 0 ? p.b + ((layer * p.n_agents + agent) * p.r) * dkv + (int64_t)kvh * p.D : nullptr;
   const float scale = p.r > 0 ? p.scale[layer * p.n_agents + agent] : 0.f;
   const int64_t dst = merge_row_offset(p, layer_rel, entry, (int64_t)kvh * p.group + gi);
-  const float inv_l = 1.0f / stat_s[1];
-  auto total = [&](int c) {
+  float bcol[kMaxRank];                  // B[agent][k][tid] for the output column this thread finishes (r <= 64, launcher)
+  if (tid < p.D) {
+#pragma unroll
+    for (int k = 0; k < kMaxRank; ++k) bcol[k] = k < p.r ? __ldg(b + (int64_t)k * dkv + tid) : 0.f;
+  }
+  ptx::pdl_launch_dependents();          // the next layer's kernels may set themselves up under this epilogue
+  ptx::pdl_wait();                       // the partials of the attention kernel are complete and visible from here on
+  // ---- this warp's splits, kBatch at a time, all loads first ----
+  float m_w = ninf, l_w = 0.f;
+  float acc[kMaxCols];
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) acc[i] = 0.f;
+  for (int s0 = warp; s0 < ns; s0 += kBatch * kMergeWarps) {
+    float2 ml[kBatch];
+    float v[kBatch][kMaxCols];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int sidx = s0 + j * kMergeWarps;
+      const float* row = row_of(sidx < ns ? sidx : s0);
+      ml[j] = sidx < ns ? *reinterpret_cast<const float2*>(row) : make_float2(ninf, 0.f);
+#pragma unroll
+      for (int i = 0; i < kMaxCols; ++i) {
+        const int c = lane + 32 * i;
+        v[j][i] = (sidx < ns && c < C) ? row[4 + c] : 0.f;
+      }
+    }
+    float m_new = m_w;
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) m_new = fmaxf(m_new, ml[j].x);
+    if (m_new == ninf) continue;         // only empty splits so far
+    const float keep = (m_w == ninf) ? 0.f : exp2f(m_w - m_new);
+    l_w *= keep;
+#pragma unroll
+    for (int i = 0; i < kMaxCols; ++i) acc[i] *= keep;
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      if (ml[j].x == ninf) continue;     // an empty split carries no accumulators: its values are never used
+      const float wgt = exp2f(ml[j].x - m_new);
+      l_w = fmaf(wgt, ml[j].y, l_w);
+#pragma unroll
+      for (int i = 0; i < kMaxCols; ++i) acc[i] = fmaf(wgt, v[j][i], acc[i]);
+    }
+    m_w = m_new;
+  }
+  if (lane == 0) { m_s[warp] = m_w; l_s[warp] = l_w; }
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) {
+    const int c = lane + 32 * i;
+    if (c < C) acc_s[warp][c] = acc[i];
+  }
+  __syncthreads();
+  // ---- the warps' results relative to the row maximum ----
+  float mx = m_s[0];
+#pragma unroll
+  for (int i = 1; i < kMergeWarps; ++i) mx = fmaxf(mx, m_s[i]);
+  float wq[kMergeWarps], lsum = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMergeWarps; ++i) {
+    wq[i] = (m_s[i] == ninf) ? 0.f : exp2f(m_s[i] - mx);
+    lsum = fmaf(wq[i], l_s[i], lsum);
+  }
+  if (tid < C) {
     float t = 0.f;
-    for (int wq = 0; wq < kMergeWarps; ++wq) t += acc_s[wq * C + c];
-    return t;
-  };
-  for (int c = tid; c < p.D; c += kMergeWarps * 32) {
-    float o = total(c);
-    for (int k = 0; k < p.r; ++k) o = fmaf(scale * total(p.D + k), b[k * dkv + c], o);
-    store_out(p, dst + c, o * inv_l);
+#pragma unroll
+    for (int i = 0; i < kMergeWarps; ++i) t = fmaf(wq[i], acc_s[i][tid], t);
+    tot_s[tid] = t;
+  }
+  __syncthreads();
+  // ---- epilogue: o += (lr_scale * o_lr[k]) * B[agent][k,:], out = o / l (attention.hpp:244-259) ----
+  if (tid < p.D) {
+    float o = tot_s[tid];
+#pragma unroll
+    for (int k = 0; k < kMaxRank; ++k)
+      if (k < p.r) o = fmaf(scale * tot_s[p.D + k], bcol[k], o);
+    store_out(p, dst + tid, o / lsum);
   }
 }
 
 template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps>
 int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
   auto kern = fla_decode_tma_kernel<D, RP, MW, KT, PA, NW>;
-  LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static int attr_device = -1;         // once per instantiation: the attribute call costs more than the launch
+  if (attr_device != ctx->device) {
+    LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBudget));
+    attr_device = ctx->device;
+  }
   prof_mark(ctx, 0);
-  kern<<<grid, NW * 32, smem, ctx->stream>>>(dp);
+  LK_CUDA(launch_kernel(ctx, kern, dim3(grid), dim3(NW * 32), smem, true, dp));
   prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
@@ -689,6 +766,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_warp_kernel
   const int64_t split_stride = (int64_t)p.max_seg * rows_blk * PS;
   const int64_t seg_off = seg_lo * rows_blk * PS;
   auto row_of = [&](int s) -> const float* { return part0 + s * split_stride + (s == 0 ? seg_off : 0); };
+  ptx::pdl_launch_dependents();          // the next layer's kernels may set themselves up under this epilogue
+  ptx::pdl_wait();                       // the partials of the attention kernel are complete and visible from here on
   float m = ninf, l = 0.f;
   if (lane < ns) { const float2 ml = *reinterpret_cast<const float2*>(row_of(lane)); m = ml.x; l = ml.y; }
   float mx = m;
@@ -774,11 +853,23 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
   const int ns_max = (int)((T - 1) / G + 2);
   dim3 mgrid((unsigned)rows_total, (unsigned)(n_layers * n_kv_local));
   if (d + rp > 192) return fail("decode merge: d_head + padded rank %d exceeds 192 columns", d + rp);
-  if (ns_max <= 32 && rp <= 64) {
+  // the same shared-memory carve-out as the attention kernels, so that the SMs are not reconfigured between the two
+  // launches of every layer-step (and the merge CTAs can become resident beside the attention CTAs they wait for)
+  static int carve_device = -1;
+  if (carve_device != ctx->device) {
+    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_warp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    carve_device = ctx->device;
+  }
+  if (r > 64) return fail("decode merge: rank %d exceeds 64", r);
+  // many rows (a whole step per launch): one warp per row, throughput; few rows (a layer per launch) or many splits: one CTA
+  // per row, one global round trip
+  if (ns_max <= 32 && rp <= 64 && (int64_t)rows_total * n_layers * n_kv_local > 1024) {
     const int64_t n = (int64_t)rows_total * n_layers * n_kv_local;
-    fla_decode_merge_warp_kernel<<<(unsigned)((n + kMergeWarps - 1) / kMergeWarps), kMergeWarps * 32, 0, ctx->stream>>>(mp, n);
+    LK_CUDA(launch_kernel(ctx, fla_decode_merge_warp_kernel, dim3((unsigned)((n + kMergeWarps - 1) / kMergeWarps)), dim3(kMergeWarps * 32), 0,
+                          true, mp, n));
   } else {
-    fla_decode_merge_kernel<<<mgrid, kMergeWarps * 32, (size_t)(ns_max + kMergeWarps * (d + rp)) * sizeof(float), ctx->stream>>>(mp);
+    LK_CUDA(launch_kernel(ctx, fla_decode_merge_kernel, mgrid, dim3(kMergeWarps * 32), 0, true, mp));
   }
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
@@ -858,6 +949,7 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const int64_t n_workers = (total + G - 1) / G;
   const unsigned grid = (unsigned)((n_workers + workers_per_cta - 1) / workers_per_cta);
   const int max_seg = (int)((G + T - 2) / T + 1);
+  if ((total + G) * n_chunks >= ((int64_t)1 << 31)) return fail("decode: %lld key tiles in one launch exceed the kernel's 32-bit tile arithmetic", (long long)(total * n_chunks));
   const int PS = 4 + d + rp;
   const size_t part_bytes = (size_t)n_chunks * n_workers * max_seg * rows_blk * PS * sizeof(float);
   LK_TRY(scratch_reserve(ctx, ctx->work, part_bytes));
@@ -883,6 +975,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   dp.lr_tables = pool->lr_space.dev_table; dp.agent_ids = c.agent_ids_dev;
   dp.lr_max_pages = (int)pool->lr_space.max_pages; dp.lr_per_block = lr_per_block;
+  dp.identity = (pool->kv_space.identity(c.kv_set, dp.n_pages) ? 1 : 0) | ((rp > 0 && !pa && pool->lr_space.identity(c.lr_set, dp.n_pages)) ? 2 : 0);
+  if (const char* e = std::getenv("LORAKV_NO_PAGE_IDENTITY")) if (e[0] == '1') dp.identity = 0;
   if (pa) {
     dp.lr_policy = ptx::kEvictFirst;     // every V_lr tile is read by one entry's rows of each kv head only
     if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp));
@@ -898,3 +992,9 @@ int launch_decode_tma(const PagedAttnCall& c) {
 }
 
 }  // namespace lk
+
+#ifdef LK_DECODE_TRACE
+extern "C" int lorakv_debug_decode_trace(unsigned long long* out, int n_words) {
+  return cudaMemcpyFromSymbol(out, lk::g_decode_trace, sizeof(unsigned long long) * (size_t)n_words) == cudaSuccess ? 0 : 1;
+}
+#endif

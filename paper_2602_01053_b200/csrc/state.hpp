@@ -12,6 +12,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "lorakv_b200.h"
@@ -43,6 +44,20 @@ struct Scratch {            // grow-only device buffer
 
 }  // namespace lk
 
+namespace lk {
+// Agent-id lists of the batched calls, staged once: a small ring of {pinned host, device} buffers keyed by content.  A call
+// whose list equals a staged one reuses the device copy (a decode loop passes the same batch every layer and step: no
+// copy at all); a new list takes the next slot, and the slot's event makes sure the pinned buffer is not rewritten while
+// an earlier host-to-device copy of it is still pending.
+struct IdSlot {
+  int32_t* host = nullptr;
+  int32_t* dev = nullptr;
+  size_t cap = 0;                 // entries
+  std::vector<int32_t> ids;       // what the device buffer holds (or will, in stream order)
+  cudaEvent_t copied = nullptr;
+};
+}  // namespace lk
+
 struct lorakv_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -51,9 +66,13 @@ struct lorakv_ctx {
   int64_t l2_bytes = 0;               // device L2 size (cudaDevAttrL2CacheSize); sizes the V_lr residency decisions of the decode
   int64_t launches = 0;
   int policy = 0;
+  bool pdl = true;                    // chain the decode kernels with programmatic dependent launches (LORAKV_NO_PDL=1 disables)
   const char* last_kernel = "none";
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
   lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection
+  static constexpr int kIdSlots = 8;
+  lk::IdSlot id_slots[kIdSlots];
+  int id_next = 0;
   void* pinned = nullptr;             // small pinned staging buffer
   size_t pinned_bytes = 0;
   bool profiling = false;             // bracket the dominant kernel of fast-path calls with events
@@ -67,6 +86,18 @@ struct lorakv_ctx {
 };
 
 namespace lk {
+// Kernel launch on the ctx stream, optionally as a programmatic dependent launch (umma.cuh: pdl_wait): the kernels of a
+// decode layer-step chain this way so that each one's launch latency and prologue hide under its predecessor's tail.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_kernel(lorakv_ctx* ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr; cfg.numAttrs = (pdl && ctx->pdl) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, KArgs(std::forward<Args>(args))...);
+}
 // record the start (which = 0) / end (which = 1) of the dominant kernel when profiling is on
 inline void prof_mark(lorakv_ctx* ctx, int which) {
   if (!ctx->profiling) return;
@@ -81,6 +112,8 @@ namespace lk {
 
 int scratch_reserve(lorakv_ctx* ctx, Scratch& s, size_t bytes);
 int pinned_reserve(lorakv_ctx* ctx, size_t bytes);
+// device copy of an agent-id list (see IdSlot); valid for every kernel enqueued on the ctx stream after this call
+int stage_agent_ids(lorakv_ctx* ctx, const int32_t* ids, int64_t n, const int32_t** dev);
 
 // One page space: page ids handed out in first-touch order to the logical pages of its sets.
 struct PageSpace {
@@ -89,6 +122,17 @@ struct PageSpace {
   std::vector<std::vector<int32_t>> table;    // [set][logical page] -> physical page
   int32_t* dev_table = nullptr;               // [n_sets][max_pages], mirrors `table`
   int64_t total_pages() const { return n_sets * max_pages; }
+  // True when logical page i of `set` is physical page i for every i < n_pages (one trajectory appended in order: the
+  // common case).  The decode kernel then skips the page-table load that its first bulk copy would otherwise wait for.
+  // Tables are append-only, so the verified prefix is remembered.
+  std::vector<int64_t> ident_upto;            // [set] pages verified so far; -1 once a mismatch was found
+  bool identity(int64_t set, int64_t n_pages) {
+    if (ident_upto.size() != table.size()) ident_upto.assign(table.size(), 0);
+    int64_t& c = ident_upto[(size_t)set];
+    const auto& tab = table[(size_t)set];
+    while (c >= 0 && c < n_pages && c < (int64_t)tab.size()) c = tab[(size_t)c] == c ? c + 1 : -1;
+    return c >= n_pages;
+  }
 };
 
 }  // namespace lk

@@ -34,6 +34,11 @@ def test_two_rank_bench_line(gather):
     assert d["n_gpus"] == 2 and d["config"]["workload"] == "cfg1" and d["config"]["parallelism"] == "kv-head shard x2"
     assert d["gpu_launches"] > 0 and d["value"] > 0 and d["e2e"]["value"] > 0
     assert d["e2e"]["d2h_bytes_per_step"] == 2 * d["e2e"]["h2d_bytes_per_step"]      # every rank reads the gathered rows back
+    # the cost of the end-of-step gather per mode, and every rank's own kernel / step time
+    comm = d["comm"]
+    assert [r["rank"] for r in comm["per_rank"]] == [0, 1] and all(r["kernel_ms"] > 0 and r["step_ms"] > 0 for r in comm["per_rank"])
+    assert comm["attention_only_ms"] > 0 and comm["nccl_all_gather"]["step_ms"] > 0 and comm["bytes_per_rank"] > 0
+    assert (comm["peer_memory"]["step_ms"] is not None) == (gather == "peer")
     if gather == "peer":
         assert d["config"]["output_gather"] == "peer"
         assert d["config"]["output_gather_check"] == "bit-exact vs all_gather on every rank"

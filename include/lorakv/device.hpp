@@ -50,8 +50,19 @@ class AdapterTable {
     else if (upload_a) b200::check(lorakv_adapters_set_a(h_, layer, adapter.a.data.data()));
     b200::check(lorakv_adapters_set_b(h_, layer, agent, adapter.b.data.data(), adapter.alpha));
   }
+  // A MultiLoraSet without shared_a may carry a different down-projection per agent (legal for NonShared / FullShared,
+  // engine.hpp:375-379 reads adapter(agent).a): every agent's A is then kept on the device, not only agent 0's.
   void set_layer(idx layer, const MultiLoraSet<float>& set) {
-    for (idx a = 0; a < set.num_agents(); ++a) this->set(layer, a, set.adapter(a), a == 0);
+    for (idx a = 0; a < set.num_agents(); ++a) {
+      const LoraAdapter<float>& ad = set.adapter(a);
+      if (per_agent_a_ || !set.shared_a) {
+        b200::check(lorakv_adapters_set_a_agent(h_, layer, a, ad.a.data.data()));
+        if (a == 0 && !per_agent_a_) b200::check(lorakv_adapters_set_a(h_, layer, ad.a.data.data()));
+        b200::check(lorakv_adapters_set_b(h_, layer, a, ad.b.data.data(), ad.alpha));
+      } else {
+        this->set(layer, a, ad, a == 0);
+      }
+    }
   }
   lorakv_adapters* handle() const { return h_; }
   idx n_q_heads() const { return n_q_heads_; }

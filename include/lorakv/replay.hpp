@@ -160,6 +160,15 @@ inline ReplayReport replay_trace(const std::vector<SublayerWeights>& layers, idx
     timer.start();
     for (idx l = 0; l < n_layers; ++l) {
       const Interval kv = plan.kv_project_at(l, scheme);
+      // A decode step (a handful of fresh rows, every cache of the layer ending where they begin) is ONE library call:
+      // lorakv_step_layer chains the projections, the appends, the attention and its epilogue as four dependent
+      // launches.  Anything else (prefills, agent switches that re-project a longer range) takes the calls below.
+      const Interval lr_iv = (lr_cached && has_lora) ? plan.lr_project_at(l, scheme) : plan.hidden_pass;
+      if (n <= 8 && kv.begin == p0 && kv.end == p1 && lr_iv.begin == p0 && lr_iv.end == p1 && (has_lora || !lr_cached)) {
+        b200::check(lorakv_step_layer(store.handle(), weights.handle(), has_lora ? tables.handle() : nullptr, l, agent, p0, xbuf.f(), n,
+                                      d_model, rope ? 1 : 0, n_q_heads, qbuf.f(), obuf.f(), LORAKV_DEVICE));
+        continue;
+      }
       if (!kv.empty()) {
         const float* xkv = xbuf.f() + (kv.begin - p0) * d_model;
         if (full_values && has_lora)

@@ -24,7 +24,8 @@
 extern "C" {
 #endif
 
-#define LORAKV_ABI_VERSION 3   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory */
+#define LORAKV_ABI_VERSION 4   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory;
+                                  4: lorakv_step_layer, lorakv_snapshot_tokens */
 
 typedef struct lorakv_ctx lorakv_ctx;           /* device + stream + scratch */
 typedef struct lorakv_pool lorakv_pool;         /* paged cache of one trajectory (KvStore<T>) */
@@ -228,6 +229,8 @@ int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const i
 int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int64_t n_kv_heads,
                               int64_t page_tokens, int64_t max_tokens, lorakv_pool** out,
                               int32_t* tokens_out, int64_t tokens_cap, int64_t* n_tokens);
+/* The token ids a snapshot file holds, from its header alone: writes min(cap, n) ids, *n_tokens = n (both may be NULL). */
+int lorakv_snapshot_tokens(const char* path, int32_t* tokens_out, int64_t cap, int64_t* n_tokens);
 /* The "full values" variant of engine.hpp:385-393 (NonShared, FullShared): the stored value rows are
  * v_base + (alpha/rank) * ((x * A_v) * B_v[agent]) with A_v, B_v, alpha from the adapter table. */
 int lorakv_pool_append_kv_project_full(lorakv_pool* pool, const lorakv_proj* proj,
@@ -323,6 +326,24 @@ int lorakv_fla_decode_batched_gather(lorakv_pool* pool, const lorakv_adapters* a
 int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* adapters, int64_t layer,
                        int64_t agent, int64_t n_q_heads, const float* q, int64_t L_c,
                        int64_t query_offset, float* out, int mem_kind);
+
+/* One decode layer-step of step() restricted to the attention sublayer (proj/include/lorakv/engine.hpp:331-443): for the rows
+ * x (n_rows x d_model float32, logical rows [row_begin, row_begin + n_rows) of the trajectory, the positions of the new
+ * tokens)
+ *     q = rope(x Wq + (alpha/rank) (x A_q) B_q[agent])                                         (:352-373, :422-427)
+ *     append_key(rope(x Wk)); append_value(x Wv [+ (alpha/rank) (x A_v) B_v[agent] under NonShared / FullShared])  (:376-403)
+ *     append_lr(x A_v)                             (BaseShared / BaseLRShared, :411-419)
+ *     out = gqa_attention(q, key_view, value_view, lr_view, B_v[agent], alpha/rank, query_offset = row_begin)    (:429-443)
+ * i.e. lorakv_pool_append_kv_project[_full] + lorakv_pool_append_lr_project + lorakv_proj_query + lorakv_fla_prefill.  The q
+ * adapter of (layer, agent) is applied when one was uploaded (lorakv_proj_set_q_lora).  adapters: the value-side tables
+ * (required by the schemes with an LR cache; NonShared / FullShared merge them into the stored rows when given, NULL = none).
+ * With DEVICE operands, a bf16 pool, d_head 128 and <= 8 fresh rows -- a decode step -- the whole call is four chained
+ * kernel launches with no host synchronisation and no copy (all projections in two launches, attention, merge epilogue).
+ *   q_scratch: NULL, or n_rows x (n_q_local*d_head) float32 in the same memory kind as x: receives the projected queries
+ *   out      : n_rows x (n_q_local*d_head) float32 */
+int lorakv_step_layer(lorakv_pool* pool, const lorakv_proj* proj, const lorakv_adapters* adapters, int64_t layer, int64_t agent,
+                      int64_t row_begin, const float* x, int64_t n_rows, int64_t ld, int rope, int64_t n_q_heads,
+                      float* q_scratch, float* out, int mem_kind);
 
 /* Device time of the dominant kernel alone.  With profiling on, every fast-path call brackets its
  * main attention kernel (not the merge epilogue, not the staging copies) with two events on the ctx

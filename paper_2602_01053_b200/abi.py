@@ -137,6 +137,8 @@ SIGNATURES = {
     "lorakv_fla_decode_batched_gather": (C.c_int, [_vp, _vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, C.c_int, _vp,
                                                    C.POINTER(_vp)]),
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
+    "lorakv_step_layer": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, _i64, _vp, _vp, C.c_int]),
+    "lorakv_snapshot_tokens": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _i64, C.POINTER(_i64)]),
     "lorakv_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "lorakv_ctx_last_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "lorakv_ctx_mean_kernel_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
@@ -161,7 +163,7 @@ def load_library(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lorakv_abi_version() != 3:
+    if lib.lorakv_abi_version() != 4:
         raise LorakvError("liblorakv_b200.so ABI version mismatch")
     if path is None:
         _lib = lib
@@ -756,6 +758,24 @@ class Pool:
                                                n_q_heads, q.ctypes.data_as(_vp), q.shape[0], query_offset,
                                                out.ctypes.data_as(_vp), HOST))
         return out
+
+    def step_layer(self, proj, adapters, layer, agent, row_begin, x, n_q_heads, rope=True):
+        """One decode layer-step (projections + appends + attention) on HOST rows x; returns (q rows, attention output)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        group = n_q_heads // self.dims.n_kv_heads
+        n_kv_local = self.dims.n_kv_local or self.dims.n_kv_heads
+        dq = group * n_kv_local * self.dims.d_head
+        q = np.zeros((x.shape[0], dq), dtype=np.float32)
+        out = np.zeros_like(q)
+        _check(self.ctx.lib.lorakv_step_layer(self.h, proj.h, adapters.h if adapters else None, layer, agent, row_begin,
+                                              x.ctypes.data_as(_vp), x.shape[0], x.shape[1], 1 if rope else 0, n_q_heads,
+                                              q.ctypes.data_as(_vp), out.ctypes.data_as(_vp), HOST))
+        return q, out
+
+    def step_layer_device(self, proj, adapters, layer, agent, row_begin, x_dev, n_rows, ld, n_q_heads, out_dev, q_dev=0, rope=True):
+        _check(self.ctx.lib.lorakv_step_layer(self.h, proj.h, adapters.h if adapters else None, layer, agent, row_begin,
+                                              _vp(x_dev), n_rows, ld, 1 if rope else 0, n_q_heads, _vp(q_dev) if q_dev else None,
+                                              _vp(out_dev), DEVICE))
 
     def prefill_device(self, adapters, layer, agent, n_q_heads, q_dev, L_c, query_offset, out_dev):
         _check(self.ctx.lib.lorakv_fla_prefill(self.h, adapters.h if adapters else None, layer, agent,

@@ -187,7 +187,7 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj})
+  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj, &ctx->qrows})
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (IdSlot& s : ctx->id_slots) {
@@ -867,11 +867,17 @@ static int append_kv_project_impl(lorakv_pool* pool, const lorakv_proj* pr, cons
         layer >= merge->n_layers)
       return fail("append_kv_project_full: adapter table does not match the projection (rank %lld)", (long long)merge->rank);
     if (agent < 0 || agent >= merge->n_agents) return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)merge->n_agents);
-    if (!merge->a_set[(size_t)layer] || !merge->b_set[(size_t)(layer * merge->n_agents + agent)])
+    const bool has_a = merge->a_set[(size_t)layer] ||
+                       (merge->a_agent && merge->a_agent_set[(size_t)(layer * merge->n_agents + agent)]);
+    if (!has_a || !merge->b_set[(size_t)(layer * merge->n_agents + agent)])
       return fail("append_kv_project_full: A / B of layer %lld agent %lld were never uploaded", (long long)layer, (long long)agent);
     rank = merge->rank;
     if (rank > 64) return fail("append_kv_project_full: rank %lld > 64 is not supported", (long long)rank);
-    av = merge->a + layer * merge->d_model * rank;
+    // the agent's own down-projection when one was uploaded (engine.hpp:375-379 uses v_lora->adapter(agent).a: NonShared
+    // and FullShared adapters need not share A), else the layer's shared A
+    const bool own_a = merge->a_agent && merge->a_agent_set[(size_t)(layer * merge->n_agents + agent)];
+    av = own_a ? merge->a_agent + (size_t)(layer * merge->n_agents + agent) * (size_t)(merge->d_model * rank)
+               : merge->a + layer * merge->d_model * rank;
     bv = merge->b + ((layer * merge->n_agents + agent) * rank) * (merge->n_kv_local * merge->d_head);
     v_scale = merge->scale_host[(size_t)(layer * merge->n_agents + agent)];
     if (pr->fused) {
@@ -1076,10 +1082,18 @@ static int check_adapters(const lorakv_pool* pool, const lorakv_adapters* ad) {
 }
 
 // rows every buffer the call reads has materialised (K, V and -- when present -- LR)
-static int visible_rows(const lorakv_pool* pool, int64_t layer, int64_t kv_set, int64_t lr_set, int64_t* L) {
-  int64_t n = std::min(pool->key_rows[(size_t)kv_set][(size_t)layer], pool->value_rows[(size_t)kv_set][(size_t)layer]);
-  if (pool->r_pad > 0) n = std::min(n, pool->lr_rows[(size_t)lr_set][(size_t)layer]);
-  *L = n;
+// validate_attention_inputs (attention.hpp:58-76) rejects k, v_base and v_lr views of different row counts; so does this
+// (a cache that lags -- e.g. a BaseShared agent whose LR prefill is pending -- is an error, never a silently shorter context)
+static int visible_rows(const lorakv_pool* pool, int64_t layer, int64_t kv_set, int64_t lr_set, int64_t* L, bool with_lr = true) {
+  const int64_t nk = pool->key_rows[(size_t)kv_set][(size_t)layer], nv = pool->value_rows[(size_t)kv_set][(size_t)layer];
+  if (nk != nv) return fail("attention: k is %lldx%lld but v_base has %lld rows (layer %lld)", (long long)nk,
+                            (long long)pool->d_kv_local(), (long long)nv, (long long)layer);
+  if (pool->r_pad > 0 && with_lr) {     // (a batch over per-agent low-rank caches checks every entry's own cache instead)
+    const int64_t nl = pool->lr_rows[(size_t)lr_set][(size_t)layer];
+    if (nl != nk) return fail("attention: v_lr has %lld rows, k has %lld (layer %lld; the low-rank cache of this agent lags: its LR prefill "
+                              "is pending)", (long long)nl, (long long)nk, (long long)layer);
+  }
+  *L = nk;
   return LORAKV_OK;
 }
 
@@ -1098,7 +1112,7 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   int64_t L = -1;
   for (int64_t l = layer_begin; l < layer_end; ++l) {
     int64_t Ll;
-    LK_TRY(visible_rows(pool, l, kv_set, lr_set, &Ll));
+    LK_TRY(visible_rows(pool, l, kv_set, lr_set, &Ll, !per_entry_lr));
     if (per_entry_lr) {   // every entry reads its own agent's low-rank cache: all of them must have caught up
       Ll = std::min(pool->key_rows[(size_t)kv_set][(size_t)l], pool->value_rows[(size_t)kv_set][(size_t)l]);
       for (int64_t i = 0; i < n_batch; ++i) {
@@ -1205,8 +1219,7 @@ int lorakv_fla_decode_batched(lorakv_pool* pool, const lorakv_adapters* ad, int6
     if (pool->dims.scheme == LORAKV_NONSHARED) kv_set = a; else lr_set = a;
   }
   int64_t L;
-  LK_TRY(visible_rows(pool, layer_begin, kv_set, lr_set, &L));
-  if (per_entry_lr) L = std::min(pool->key_rows[0][(size_t)layer_begin], pool->value_rows[0][(size_t)layer_begin]);
+  LK_TRY(visible_rows(pool, layer_begin, kv_set, lr_set, &L, !per_entry_lr));
   if (L < 1) return fail("attention: query_offset 0 with L_c 1 exceeds L 0");
   return run_paged(pool, ad, layer_begin, layer_end, kv_set, lr_set, agent_ids, n_batch, 1, L - 1, n_q_heads, q, out, mem_kind, nullptr,
                    per_entry_lr);
@@ -1274,6 +1287,95 @@ int lorakv_fla_prefill(lorakv_pool* pool, const lorakv_adapters* ad, int64_t lay
   int64_t lr_set = pool->dims.scheme == LORAKV_BASESHARED ? agent : 0;
   const int32_t id = (int32_t)agent;
   return run_paged(pool, ad, layer, layer + 1, kv_set, lr_set, &id, 1, L_c, query_offset, n_q_heads, q, out, mem_kind);
+}
+
+// ---- one decode layer-step of step() on the attention sublayer (engine.hpp:331-443) ----------------------------------
+// == lorakv_pool_append_kv_project[_full] + lorakv_pool_append_lr_project + lorakv_proj_query + lorakv_fla_prefill on rows
+// [row_begin, row_begin + n_rows).  A decode step's handful of fresh rows on a bf16 pool runs as FOUR chained launches
+// (step_layer.cu: all projections in two; attention; merge epilogue); anything else goes through those entry points.
+int lorakv_step_layer(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_adapters* ad, int64_t layer, int64_t agent,
+                      int64_t row_begin, const float* x, int64_t n_rows, int64_t ld, int rope, int64_t n_q_heads, float* q_scratch,
+                      float* out, int mem_kind) {
+  if (!pool || !pr || !x || !out) return fail("step_layer: null argument");
+  if (n_rows < 1) return fail("step_layer: no rows");
+  if (layer < 0 || layer >= pool->dims.n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (agent < 0 || agent >= pool->dims.n_agents) return fail("unknown agent %lld", (long long)agent);
+  const int scheme = pool->dims.scheme;
+  const bool full_values = scheme == LORAKV_NONSHARED || scheme == LORAKV_FULLSHARED;
+  const bool lr_cached = pool->lr_sets() > 0 && pool->r_pad > 0;
+  if (lr_cached && !ad) return fail("step_layer: the pool keeps a rank-%lld cache but no adapter tables were given", (long long)pool->dims.rank);
+  const bool merge_v = full_values && ad != nullptr;
+  const bool q_lora = pr->aq != nullptr && agent < pr->q_agents && layer < pr->n_layers &&
+                      pr->q_lora_set[(size_t)(layer * pr->q_agents + agent)];
+  lorakv_ctx* ctx = pool->ctx;
+  const int64_t r_q = q_lora ? pr->q_rank : 0, r_v = (merge_v || lr_cached) ? ad->rank : 0;
+  int64_t kv_set = 0, lr_set = 0; bool none;
+  LK_TRY(resolve(pool, LORAKV_KEY, layer, agent, &kv_set, &none));
+  if (lr_cached) LK_TRY(resolve(pool, LORAKV_LR, layer, agent, &lr_set, &none));
+  // the fused path wants fresh rows only (every cache of the step ends exactly at row_begin): the decode case
+  const bool fresh = pool->key_rows[(size_t)kv_set][(size_t)layer] == row_begin && pool->value_rows[(size_t)kv_set][(size_t)layer] == row_begin &&
+                     (!lr_cached || pool->lr_rows[(size_t)lr_set][(size_t)layer] == row_begin);
+  const bool fast = mem_kind == LORAKV_DEVICE && ctx->policy != 1 && fresh && pr->fused && pr->q_fused &&
+                    pool->dims.dtype == LORAKV_BF16 && step_layer_supported(n_rows, pr->d_model, pr->d_head, r_q, r_v) &&
+                    n_q_heads == pr->n_q_heads && layer < pr->n_layers && pr->set[(size_t)layer] && pr->q_set[(size_t)layer];
+  const int64_t group = pr->n_kv_heads > 0 ? n_q_heads / pr->n_kv_heads : 0;
+  const int64_t dq = group * pr->n_kv_local * pr->d_head;
+  if (!fast) {
+    int64_t added = 0;
+    if (merge_v) LK_TRY(lorakv_pool_append_kv_project_full(pool, pr, ad, layer, agent, row_begin, x, n_rows, ld, mem_kind, rope, &added));
+    else LK_TRY(lorakv_pool_append_kv_project(pool, pr, layer, agent, row_begin, x, n_rows, ld, mem_kind, rope, &added));
+    if (lr_cached) LK_TRY(lorakv_pool_append_lr_project(pool, ad, layer, agent, row_begin, x, n_rows, ld, mem_kind, &added));
+    float* q = q_scratch;
+    std::vector<float> q_host;
+    if (!q) {
+      if (mem_kind == LORAKV_HOST) { q_host.resize((size_t)(n_rows * dq)); q = q_host.data(); }
+      else { LK_TRY(scratch_reserve(ctx, ctx->qrows, (size_t)(n_rows * dq) * sizeof(float))); q = static_cast<float*>(ctx->qrows.ptr); }
+    }
+    LK_TRY(lorakv_proj_query(const_cast<lorakv_proj*>(pr), layer, q_lora ? agent : -1, row_begin, x, n_rows, ld, rope, q, mem_kind));
+    return lorakv_fla_prefill(pool, lr_cached ? ad : nullptr, layer, agent, n_q_heads, q, n_rows, row_begin, out, mem_kind);
+  }
+  // ---- fused path ----
+  if (pr->d_model != pool->dims.d_model || pr->n_kv_heads != pool->dims.n_kv_heads || pr->d_head != pool->dims.d_head ||
+      pr->kv_head_begin != pool->dims.kv_head_begin || pr->n_kv_local != pool->n_kv_local || pr->dtype != pool->dims.dtype)
+    return fail("append_kv_project: projection weights do not match the pool (d_model %lld vs %lld, d_kv %lld vs %lld)",
+                (long long)pr->d_model, (long long)pool->dims.d_model, (long long)(pr->n_kv_heads * pr->d_head),
+                (long long)(pool->dims.n_kv_heads * pool->dims.d_head));
+  const float *a_v = nullptr, *b_v = nullptr; float s_v = 0.f;
+  if (merge_v || lr_cached) {
+    if (ad->d_model != pr->d_model || ad->n_kv_local != pr->n_kv_local || ad->d_head != pr->d_head || layer >= ad->n_layers ||
+        agent >= ad->n_agents)
+      return fail("step_layer: adapter table does not match the projection (rank %lld)", (long long)ad->rank);
+    const size_t la = (size_t)(layer * ad->n_agents + agent);
+    const bool own_a = ad->a_agent && ad->a_agent_set[la];
+    if (!own_a && !ad->a_set[(size_t)layer]) return fail("lr_append_project: A of layer %lld was never uploaded", (long long)layer);
+    if (!ad->b_set[la]) return fail("attention: B of layer %lld agent %lld was never uploaded", (long long)layer, (long long)agent);
+    a_v = own_a ? ad->a_agent + la * (size_t)(ad->d_model * ad->rank) : ad->a + layer * ad->d_model * ad->rank;
+    b_v = ad->b + (la * ad->rank) * (size_t)(ad->n_kv_local * ad->d_head);
+    s_v = ad->scale_host[la];
+  }
+  LK_CUDA(cudaSetDevice(ctx->device));
+  LK_TRY(ensure_pages(pool, pool->kv_space, kv_set, row_begin + n_rows));
+  if (lr_cached) LK_TRY(ensure_pages(pool, pool->lr_space, lr_set, row_begin + n_rows));
+  float* q_dev = q_scratch;
+  if (!q_dev) { LK_TRY(scratch_reserve(ctx, ctx->qrows, (size_t)(n_rows * dq) * sizeof(float))); q_dev = static_cast<float*>(ctx->qrows.ptr); }
+  const int64_t dq_full = pr->n_q_heads * pr->d_head, col0 = pr->kv_head_begin * group * pr->d_head;
+  StepLayerCall c;
+  c.layer = layer; c.kv_set = kv_set; c.lr_set = lr_set; c.row0 = row_begin; c.n_rows = n_rows; c.x_dev = x; c.ld = ld;
+  c.wq_packed = static_cast<const char*>(pr->wq_packed) + (size_t)(layer * pr->d_model * dq) * 2;
+  c.wkv_packed = static_cast<const char*>(pr->packed) + (size_t)(layer * kv_project_packed_elems(pr->d_model, pr->n_kv_local, pr->d_head)) * 2;
+  c.dq = dq;
+  c.a_q = q_lora ? pr->aq + (size_t)(layer * pr->d_model * r_q) : nullptr;
+  c.b_q = q_lora ? pr->bq + (size_t)((layer * pr->q_agents + agent) * r_q * dq_full) + col0 : nullptr;
+  c.ldb_q = dq_full; c.r_q = r_q; c.s_q = q_lora ? pr->q_scale[(size_t)(layer * pr->q_agents + agent)] : 0.f;
+  c.a_v = a_v; c.b_v = b_v; c.r_v = r_v; c.s_v = s_v;
+  c.merge_v = merge_v; c.append_lr = lr_cached; c.rope = rope != 0; c.q_dev = q_dev;
+  LK_TRY(launch_step_layer(pool, c));
+  pool->key_rows[(size_t)kv_set][(size_t)layer] += n_rows;
+  pool->value_rows[(size_t)kv_set][(size_t)layer] += n_rows;
+  if (lr_cached) pool->lr_rows[(size_t)lr_set][(size_t)layer] += n_rows;
+  const int32_t id = (int32_t)agent;
+  return run_paged(pool, lr_cached ? ad : nullptr, layer, layer + 1, kv_set, lr_set, &id, 1, n_rows, row_begin, n_q_heads, q_dev, out,
+                   LORAKV_DEVICE);
 }
 
 }  // extern "C"

@@ -135,6 +135,23 @@ int launch_rows_q_project(lorakv_ctx* ctx, const void* wq_packed, int64_t d_mode
 int launch_rows_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set, int64_t row0,
                            const float* x_dev, int64_t n_rows, int64_t ld);
 
+// step_layer.cu: all projections of one decode layer-step (<= 8 rows) in two launches: q (+ q-LoRA, RoPE) into float32
+// rows, K (RoPE) / V (+ merged value adapter) into their pages, V_lr = x A_v into its LR page
+struct StepLayerCall {
+  int64_t layer, kv_set, lr_set, row0, n_rows;
+  const float* x_dev; int64_t ld;
+  const void* wq_packed; const void* wkv_packed;   // this layer's packed bf16 weights
+  int64_t dq;                                      // q columns of this shard
+  const float* a_q; const float* b_q; int64_t ldb_q, r_q; float s_q;   // q adapter (a_q null: none); b_q already at the shard's first column
+  const float* a_v; const float* b_v; int64_t r_v; float s_v;          // value adapter: A for V_lr / the merge, B (shard-local width) for the merge
+  bool merge_v;                                    // full-values schemes: v += s_v (x A_v) B_v
+  bool append_lr;                                  // schemes with an LR cache: V_lr row = x A_v
+  bool rope;
+  float* q_dev;                                    // [n_rows][dq] float32
+};
+bool step_layer_supported(int64_t n_rows, int64_t d_model, int64_t d_head, int64_t r_q, int64_t r_v);
+int launch_step_layer(lorakv_pool* pool, const StepLayerCall& call);
+
 // peer_gather.cu: local slab [layers][n_batch][n_q_local * d] -> every peer's full buffer (paths without the merge epilogue)
 int launch_peer_scatter(lorakv_ctx* ctx, const float* slab_dev, int64_t rows, int64_t n_q_local, int64_t d, const PeerOut& peers);
 

@@ -101,7 +101,9 @@ struct Parser {
     } else if (c == '-' || (c >= '0' && c <= '9')) {
       size_t q = p; if (t[q] == '-') ++q;
       while (q < t.size() && t[q] >= '0' && t[q] <= '9') ++q;
-      j.kind = Json::Int; j.i = std::stoll(t.substr(p, q - p)); p = q;
+      j.kind = Json::Int;
+      if (q - p > 18 || q == p + (t[p] == '-' ? 1u : 0u)) { ok = false; return j; }   // fits int64 without overflow; at least one digit
+      j.i = std::stoll(t.substr(p, q - p)); p = q;
     } else {
       ok = false;
     }
@@ -171,22 +173,33 @@ int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const i
   return LORAKV_OK;
 }
 
-int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int64_t n_kv_heads, int64_t page_tokens,
-                              int64_t max_tokens, lorakv_pool** out_pool, int32_t* tokens_out, int64_t tokens_cap,
-                              int64_t* n_tokens) {
-  if (!ctx || !path || !out_pool) return fail("null argument");
-  *out_pool = nullptr;
-  std::ifstream in(path, std::ios::binary);
+}  // extern "C"
+
+// header of a snapshot file: length-prefixed JSON; the length is checked against the file size before anything is allocated
+static int read_header(std::ifstream& in, const char* path, Json* header) {
   if (!in) return fail("cannot open snapshot file: %s", path);
+  in.seekg(0, std::ios::end);
+  const std::streamoff file_size = in.tellg();
+  in.seekg(0, std::ios::beg);
   uint64_t hlen = 0;
   in.read(reinterpret_cast<char*>(&hlen), sizeof hlen);
-  if (!in || hlen > ((uint64_t)1 << 32)) return fail("snapshot header truncated: %s", path);
+  if (!in || file_size < (std::streamoff)sizeof hlen || hlen > (uint64_t)(file_size - (std::streamoff)sizeof hlen))
+    return fail("snapshot header truncated: %s", path);
   std::string hs((size_t)hlen, '\0');
   in.read(&hs[0], (std::streamsize)hlen);
   if (!in) return fail("snapshot header truncated: %s", path);
   Parser ps(hs);
-  const Json header = ps.value();
-  if (!ps.ok || header.kind != Json::Obj) return fail("snapshot header is not valid JSON: %s", path);
+  *header = ps.value();
+  if (!ps.ok || header->kind != Json::Obj) return fail("snapshot header is not valid JSON: %s", path);
+  return LORAKV_OK;
+}
+
+static int load_snapshot_impl(lorakv_ctx* ctx, const char* path, int dtype, int64_t n_kv_heads, int64_t page_tokens,
+                              int64_t max_tokens, lorakv_pool** out_pool, int32_t* tokens_out, int64_t tokens_cap,
+                              int64_t* n_tokens) {
+  std::ifstream in(path, std::ios::binary);
+  Json header;
+  LK_TRY(read_header(in, path, &header));
   const Json* fmt = header.get("format");
   if (!fmt || fmt->s != "lorakv-cache-snapshot") return fail("not a cache snapshot: %s", path);
   const Json* dt = header.get("dtype");
@@ -203,6 +216,9 @@ int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int6
   LK_TRY(need_int(header, "rank", &dims.rank, path));
   LK_TRY(need_int(header, "n_agents", &dims.n_agents, path));
   LK_TRY(need_int(header, "length", &length, path));
+  if (dims.n_layers < 1 || dims.n_layers > 4096 || d_kv < 1 || dims.d_model < 1 || dims.rank < 0 || dims.n_agents < 1 ||
+      dims.n_agents > 65536 || length < 0 || length > ((int64_t)1 << 40))
+    return fail("snapshot header holds implausible dimensions: %s", path);
   if (n_kv_heads < 1 || d_kv % n_kv_heads != 0)
     return fail("load_snapshot: d_kv %lld is not divisible by n_kv_heads %lld", (long long)d_kv, (long long)n_kv_heads);
   dims.scheme = scheme; dims.dtype = dtype; dims.n_kv_heads = n_kv_heads; dims.d_head = d_kv / n_kv_heads;
@@ -227,6 +243,9 @@ int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int6
     if (!nm || !rj || !cj || nm->s != tensors[i].name) return bail(fail("snapshot tensor order mismatch at %s", tensors[i].name.c_str()));
     if (cj->i != tensors[i].cols) return bail(fail("snapshot tensor width mismatch at %s", tensors[i].name.c_str()));
     const int64_t rows = rj->i;
+    if (rows < 0 || rows > dims.max_tokens)
+      return bail(fail("snapshot tensor %s claims %lld rows; the trajectory holds at most %lld", tensors[i].name.c_str(), (long long)rows,
+                       (long long)dims.max_tokens));
     const size_t n = (size_t)(rows * tensors[i].cols);
     buf.resize(std::max<size_t>(n, 1));
     in.read(reinterpret_cast<char*>(buf.data()), (std::streamsize)(n * sizeof(float)));
@@ -241,6 +260,40 @@ int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int6
     for (size_t i = 0; i < toks->arr.size() && (int64_t)i < tokens_cap; ++i) tokens_out[i] = (int32_t)toks->arr[i].i;
   *out_pool = pool;
   return LORAKV_OK;
+}
+
+extern "C" {
+
+// No C++ exception may cross the C ABI: a malformed file (absurd sizes -> bad_alloc, ...) becomes a status + message.
+int lorakv_pool_load_snapshot(lorakv_ctx* ctx, const char* path, int dtype, int64_t n_kv_heads, int64_t page_tokens,
+                              int64_t max_tokens, lorakv_pool** out_pool, int32_t* tokens_out, int64_t tokens_cap,
+                              int64_t* n_tokens) {
+  if (!ctx || !path || !out_pool) return fail("null argument");
+  *out_pool = nullptr;
+  try {
+    return load_snapshot_impl(ctx, path, dtype, n_kv_heads, page_tokens, max_tokens, out_pool, tokens_out, tokens_cap, n_tokens);
+  } catch (const std::exception& e) {
+    if (*out_pool) { lorakv_pool_destroy(*out_pool); *out_pool = nullptr; }
+    return fail("load_snapshot: %s: %s", path, e.what());
+  }
+}
+
+// Token ids of a snapshot without loading it (header only): writes min(cap, n) ids, *n_tokens = how many the file holds.
+int lorakv_snapshot_tokens(const char* path, int32_t* tokens_out, int64_t cap, int64_t* n_tokens) {
+  if (!path) return fail("null argument");
+  try {
+    std::ifstream in(path, std::ios::binary);
+    Json header;
+    LK_TRY(read_header(in, path, &header));
+    const Json* toks = header.get("tokens");
+    if (!toks || toks->kind != Json::Arr) return fail("snapshot header truncated: %s", path);
+    if (n_tokens) *n_tokens = (int64_t)toks->arr.size();
+    if (tokens_out)
+      for (size_t i = 0; i < toks->arr.size() && (int64_t)i < cap; ++i) tokens_out[i] = (int32_t)toks->arr[i].i;
+    return LORAKV_OK;
+  } catch (const std::exception& e) {
+    return fail("snapshot_tokens: %s: %s", path, e.what());
+  }
 }
 
 }  // extern "C"

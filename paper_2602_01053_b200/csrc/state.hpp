@@ -69,7 +69,8 @@ struct lorakv_ctx {
   bool pdl = true;                    // chain the decode kernels with programmatic dependent launches (LORAKV_NO_PDL=1 disables)
   const char* last_kernel = "none";
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
-  lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection
+  lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection; partial sums of a fused layer-step
+  lk::Scratch qrows;                  // query rows of a fused layer-step when the caller passes no scratch
   static constexpr int kIdSlots = 8;
   lk::IdSlot id_slots[kIdSlots];
   int id_next = 0;

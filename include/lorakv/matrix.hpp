@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstdint>
 #include <cstdlib>
 #include <stdexcept>
@@ -150,6 +151,61 @@ inline Matrix<T> matmul(Span2D<const T> a, Span2D<const T> b) {
 template <class T>
 inline Matrix<T> matmul(const Matrix<T>& a, const Matrix<T>& b) {
   return matmul(a.view(), b.view());
+}
+
+// out += a * b (matrix.hpp:101-111).  The product runs on the device like matmul; into a zero `out` -- the only way the
+// reference itself calls it (matmul, :114-121) -- the result carries the reference's bits, into anything else the product
+// is added with one rounding per element instead of being threaded through the reference's running sum.
+template <class T>
+inline void matmul_accumulate(Span2D<const T> a, Span2D<const T> b, Matrix<T>& out) {
+  if (a.cols != b.rows || out.rows != a.rows || out.cols != b.cols)
+    fail("matmul dimension mismatch: " + shape_str(a.rows, a.cols) + " x " + shape_str(b.rows, b.cols));
+  const Matrix<T> product = matmul(a, b);
+  std::transform(out.data.begin(), out.data.end(), product.data.begin(), out.data.begin(), [](T x, T y) { return x + y; });
+}
+
+// ---- host statistics the reference's analysis tools and its naive oracle use (matrix.hpp:138-186).  Not on the device
+// path: a few scalar passes over host matrices. ----
+
+// softmax of every row after subtracting its maximum; -inf entries (masked scores) are fine, a row of nothing else is not
+template <class T>
+inline Matrix<T> row_softmax(const Matrix<T>& s) {
+  const T ninf = -std::numeric_limits<T>::infinity();
+  Matrix<T> out(s.rows, s.cols);
+  for (idx i = 0; i < s.rows; ++i) {
+    const T* in = s.data.data() + i * s.cols;
+    T* o = out.data.data() + i * s.cols;
+    const T top = s.cols > 0 ? *std::max_element(in, in + s.cols) : ninf;
+    if (!(top > ninf)) fail("row_softmax: row " + std::to_string(i) + " has no finite entry");
+    T total = T(0);
+    for (idx j = 0; j < s.cols; ++j) total += (o[j] = std::exp(in[j] - top));
+    for (idx j = 0; j < s.cols; ++j) o[j] /= total;
+  }
+  ensure_finite(out, "row_softmax");
+  return out;
+}
+
+// cosine of the angle between two matrices seen as vectors, accumulated in double and clamped to [-1, 1]
+template <class T>
+inline double cosine_similarity(const Matrix<T>& a, const Matrix<T>& b) {
+  if (!a.same_shape(b))
+    fail("cosine_similarity shape mismatch: " + shape_str(a.rows, a.cols) + " vs " + shape_str(b.rows, b.cols));
+  double ab = 0.0, aa = 0.0, bb = 0.0;
+  for (std::size_t i = 0; i < a.data.size(); ++i) {
+    const double x = static_cast<double>(a.data[i]), y = static_cast<double>(b.data[i]);
+    ab += x * y; aa += x * x; bb += y * y;
+  }
+  if (aa == 0.0 || bb == 0.0) fail("cosine_similarity: zero-norm input");
+  return std::clamp(ab / (std::sqrt(aa) * std::sqrt(bb)), -1.0, 1.0);
+}
+
+// mean absolute entry (0 for an empty matrix)
+template <class T>
+inline double l1_norm_mean(const Matrix<T>& a) {
+  if (a.data.empty()) return 0.0;
+  double total = 0.0;
+  for (const T& v : a.data) total += std::abs(static_cast<double>(v));
+  return total / static_cast<double>(a.data.size());
 }
 
 template <class T>

@@ -34,14 +34,16 @@ typedef struct lorakv_adapters lorakv_adapters; /* shared A per layer, B per (la
 enum { LORAKV_OK = 0, LORAKV_ERR = 1 };
 
 /* storage / arithmetic modes */
-enum { LORAKV_F32 = 0, LORAKV_BF16 = 1 };
+enum { LORAKV_F32 = 0, LORAKV_BF16 = 1,
+       LORAKV_F64 = 2 };  /* fp64 pages: KvStore<double> of the reference API (exact rows, lorakv_pool_append_f64 / _read_f64);
+                             storage only -- attention over such a store goes through the views and lorakv_gqa_forward_f64 */
 /* where a caller buffer lives */
 enum { LORAKV_HOST = 0, LORAKV_DEVICE = 1 };
 /* SchemeKind, kvcache.hpp:15-21 (SelectiveRecompute is outside the hot path) */
 enum { LORAKV_NONSHARED = 0, LORAKV_FULLSHARED = 1, LORAKV_BASESHARED = 2, LORAKV_BASELRSHARED = 3,
        LORAKV_SELECTIVE = 4 };
-/* which cache */
-enum { LORAKV_KEY = 0, LORAKV_VALUE = 1, LORAKV_LR = 2 };
+/* which cache (LORAKV_HIDDEN: the hidden-state cache of SelectiveRecompute, kvcache.hpp:245-246, 289-293; layer ignored) */
+enum { LORAKV_KEY = 0, LORAKV_VALUE = 1, LORAKV_LR = 2, LORAKV_HIDDEN = 3 };
 
 int lorakv_abi_version(void);
 const char* lorakv_last_error(void);
@@ -237,6 +239,21 @@ int lorakv_pool_append_kv_project_full(lorakv_pool* pool, const lorakv_proj* pro
                                        const lorakv_adapters* adapters, int64_t layer, int64_t agent,
                                        int64_t row_begin, const float* x, int64_t n_rows, int64_t ld,
                                        int mem_kind, int rope, int64_t* appended);
+/* The same two calls for fp64 pools (dtype LORAKV_F64): rows / out are float64. */
+int lorakv_pool_append_f64(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin, const double* rows,
+                           int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended);
+int lorakv_pool_read_f64(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin, int64_t n_rows,
+                         double* out);
+/* SelectiveRecompute (kvcache.hpp:53-58): the sorted, unique layers whose cached K / V rows a returning agent recomputes */
+int lorakv_pool_set_recompute_layers(lorakv_pool* pool, const int64_t* layers, int64_t n);
+int lorakv_pool_get_recompute_layers(const lorakv_pool* pool, int64_t* out, int64_t cap, int64_t* n);   /* writes min(cap, n) */
+/* recompute_overwrite, kvcache.hpp:298-305 / GrowMat::overwrite :184-193: replace already materialised rows
+ * [row_begin, row_begin + n_rows) of the key or value cache of a recompute layer (anything else is the reference's
+ * "overwrite ... forbidden" error).  rows: float32 (lorakv_pool_overwrite) or float64 (_f64, fp64 pools). */
+int lorakv_pool_overwrite(lorakv_pool* pool, int which, int64_t layer, int64_t row_begin, const float* rows, int64_t n_rows,
+                          int64_t ld, int mem_kind);
+int lorakv_pool_overwrite_f64(lorakv_pool* pool, int which, int64_t layer, int64_t row_begin, const double* rows, int64_t n_rows,
+                              int64_t ld, int mem_kind);
 /* rows currently materialised in the buffer (layer, agent) resolves to (GrowMat::rows) */
 int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* rows);
 /* key_view / value_view / lr_view, :307-324: de-paginate rows [row_begin, row_begin+n_rows) into a

@@ -61,6 +61,19 @@ def build_ref() -> str | None:
     return REF_SO if os.path.exists(REF_SO) else None
 
 
+REF_TESTS = os.path.join(HERE, "_ref", "ref_tests_on_b200")
+
+
+def build_ref_tests() -> str | None:
+    """The reference's own doctest suites compiled against include/lorakv and linked with the product library
+    (oracle/Makefile ref_tests); built where /root/reference exists and the product library is there, else the prebuilt
+    binary (if any) is kept.  make rebuilds only when a header or the library is newer."""
+    lib = os.path.join(os.path.dirname(HERE), "paper_2602_01053_b200", "lib", "liblorakv_b200.so")
+    if os.path.isdir("/root/reference/proj/tests") and os.path.exists(lib):
+        subprocess.run(["make", "-C", HERE, "ref_tests"], check=True, capture_output=True)
+    return REF_TESTS if os.path.exists(REF_TESTS) else None
+
+
 class Checker:
     """One loaded checker library; ``kind`` is "port" (C restatement) or "reference"."""
 

@@ -137,6 +137,12 @@ SIGNATURES = {
     "lorakv_fla_decode_batched_gather": (C.c_int, [_vp, _vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, C.c_int, _vp,
                                                    C.POINTER(_vp)]),
     "lorakv_fla_prefill": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, C.c_int]),
+    "lorakv_pool_append_f64": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _pd, _i64, _i64, C.c_int, C.POINTER(_i64)]),
+    "lorakv_pool_read_f64": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _i64, _pd]),
+    "lorakv_pool_set_recompute_layers": (C.c_int, [_vp, C.POINTER(_i64), _i64]),
+    "lorakv_pool_get_recompute_layers": (C.c_int, [_vp, C.POINTER(_i64), _i64, C.POINTER(_i64)]),
+    "lorakv_pool_overwrite": (C.c_int, [_vp, C.c_int, _i64, _i64, _pf, _i64, _i64, C.c_int]),
+    "lorakv_pool_overwrite_f64": (C.c_int, [_vp, C.c_int, _i64, _i64, _pd, _i64, _i64, C.c_int]),
     "lorakv_step_layer": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, C.c_int, _i64, _vp, _vp, C.c_int]),
     "lorakv_snapshot_tokens": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), _i64, C.POINTER(_i64)]),
     "lorakv_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),

@@ -87,6 +87,10 @@ static const char* kWhat[3] = {"key", "value", "lr"};
 static int resolve(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t* set,
                    bool* none) {
   *none = false; *set = 0;
+  if (which == LORAKV_HIDDEN) {      // one hidden-state cache for the trajectory (kvcache.hpp:245-246); no layer, no agent
+    if (pool->dims.scheme != LORAKV_SELECTIVE) return fail("KvStore: scheme %s has no hidden-state cache", kSchemeName[pool->dims.scheme]);
+    return LORAKV_OK;
+  }
   if (which < LORAKV_KEY || which > LORAKV_LR) return fail("bad cache selector %d", which);
   const bool per_agent = (which != LORAKV_LR && pool->dims.scheme == LORAKV_NONSHARED) ||
                          (which == LORAKV_LR && pool->dims.scheme == LORAKV_BASESHARED);
@@ -102,6 +106,18 @@ static int resolve(const lorakv_pool* pool, int which, int64_t layer, int64_t ag
   return LORAKV_OK;
 }
 
+// row counter of the buffer (which, set, layer)
+static int64_t& row_counter(lorakv_pool* pool, int which, int64_t set, int64_t layer) {
+  if (which == LORAKV_HIDDEN) return pool->hidden_rows;
+  auto& t = which == LORAKV_KEY ? pool->key_rows : which == LORAKV_VALUE ? pool->value_rows : pool->lr_rows;
+  return t[(size_t)set][(size_t)layer];
+}
+static int64_t cache_cols_full(const lorakv_pool* pool, int which) {      // width of a caller's row
+  return which == LORAKV_HIDDEN ? pool->dims.d_model : which == LORAKV_LR ? pool->dims.rank : pool->dims.n_kv_heads * pool->dims.d_head;
+}
+static int64_t cache_cols_local(const lorakv_pool* pool, int which) {     // width of a stored / returned row
+  return which == LORAKV_HIDDEN ? pool->dims.d_model : which == LORAKV_LR ? pool->dims.rank : pool->d_kv_local();
+}
 static std::vector<std::vector<int64_t>>& rows_of(lorakv_pool* pool, int which) {
   return which == LORAKV_KEY ? pool->key_rows : which == LORAKV_VALUE ? pool->value_rows : pool->lr_rows;
 }
@@ -127,15 +143,16 @@ static int ensure_pages(lorakv_pool* pool, PageSpace& sp, int64_t set, int64_t r
   return LORAKV_OK;
 }
 
-static int stage_rows(lorakv_ctx* ctx, const float* rows, int64_t n, int64_t cols, int64_t ld,
-                      int mem_kind, const float** dev, int64_t* dev_ld) {
+template <class E>
+static int stage_rows(lorakv_ctx* ctx, const E* rows, int64_t n, int64_t cols, int64_t ld,
+                      int mem_kind, const E** dev, int64_t* dev_ld) {
   if (mem_kind == LORAKV_DEVICE) { *dev = rows; *dev_ld = ld; return LORAKV_OK; }
   if (mem_kind != LORAKV_HOST) return fail("bad mem_kind %d", mem_kind);
-  LK_TRY(scratch_reserve(ctx, ctx->in, (size_t)std::max<int64_t>(n * cols, 1) * sizeof(float)));
+  LK_TRY(scratch_reserve(ctx, ctx->in, (size_t)std::max<int64_t>(n * cols, 1) * sizeof(E)));
   if (n > 0 && cols > 0)
-    LK_CUDA(cudaMemcpy2DAsync(ctx->in.ptr, cols * sizeof(float), rows, ld * sizeof(float),
-                              cols * sizeof(float), n, cudaMemcpyHostToDevice, ctx->stream));
-  *dev = static_cast<const float*>(ctx->in.ptr);
+    LK_CUDA(cudaMemcpy2DAsync(ctx->in.ptr, cols * sizeof(E), rows, ld * sizeof(E),
+                              cols * sizeof(E), n, cudaMemcpyHostToDevice, ctx->stream));
+  *dev = static_cast<const E*>(ctx->in.ptr);
   *dev_ld = cols;
   return LORAKV_OK;
 }
@@ -422,10 +439,10 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   if (dims->n_layers < 1 || dims->n_kv_heads < 1 || dims->d_head < 1 || dims->d_model < 1 || dims->n_agents < 1)
     return fail("KvStore: invalid dims");
   if (dims->rank < 0) return fail("KvStore: negative rank");
-  if (dims->scheme < LORAKV_NONSHARED || dims->scheme > LORAKV_BASELRSHARED)
-    return fail("KvStore: scheme %s is outside the B200 hot path",
-                dims->scheme == LORAKV_SELECTIVE ? kSchemeName[4] : "?");
-  if (dims->dtype != LORAKV_F32 && dims->dtype != LORAKV_BF16) return fail("KvStore: unknown dtype %d", dims->dtype);
+  // SelectiveRecompute is a baseline scheme outside the Flash-LoRA-Attention path; its store (shared K / V, the hidden-state
+  // cache, the overwrite of recompute layers) exists so that the reference's callers and tests run against this library
+  if (dims->scheme < LORAKV_NONSHARED || dims->scheme > LORAKV_SELECTIVE) return fail("KvStore: unknown scheme %d", dims->scheme);
+  if (dims->dtype != LORAKV_F32 && dims->dtype != LORAKV_BF16 && dims->dtype != LORAKV_F64) return fail("KvStore: unknown dtype %d", dims->dtype);
   if (dims->max_tokens < 1) return fail("KvStore: max_tokens must be >= 1");
   lorakv_pool* p = new (std::nothrow) lorakv_pool();
   if (!p) return fail("pool_create: out of host memory");
@@ -440,7 +457,7 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
     return fail("KvStore: kv head shard [%lld,+%lld) outside [0,%lld)", (long long)dims->kv_head_begin,
                 (long long)dims->n_kv_local, (long long)dims->n_kv_heads);
   }
-  p->elem = dims->dtype == LORAKV_BF16 ? 2 : 4;
+  p->elem = dims->dtype == LORAKV_BF16 ? 2 : dims->dtype == LORAKV_F64 ? 8 : 4;
   const bool has_lr = p->lr_sets() > 0 && dims->rank > 0;
   // LR row width in HBM: the rank padded with zero columns (exact) to 16/32/64 or a multiple of
   // 64, the widths page_layout.cuh can swizzle
@@ -479,6 +496,8 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   int rc = alloc_zero(&p->k_pages, kv_bytes);
   if (rc == LORAKV_OK) rc = alloc_zero(&p->v_pages, kv_bytes);
   if (rc == LORAKV_OK) rc = alloc_zero(&p->lr_pages, lr_bytes);
+  if (rc == LORAKV_OK && dims->scheme == LORAKV_SELECTIVE)
+    rc = alloc_zero(&p->hidden_pages, (size_t)(p->kv_space.total_pages() * p->P * dims->d_model) * (size_t)p->elem);
   auto alloc_table = [&](PageSpace& sp) -> int {
     if (sp.total_pages() == 0) return LORAKV_OK;
     LK_CUDA(cudaMalloc(&sp.dev_table, (size_t)sp.total_pages() * sizeof(int32_t)));
@@ -496,7 +515,7 @@ void lorakv_pool_destroy(lorakv_pool* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
   cudaStreamSynchronize(p->ctx->stream);
-  for (void* q : {p->k_pages, p->v_pages, p->lr_pages, (void*)p->kv_space.dev_table, (void*)p->lr_space.dev_table})
+  for (void* q : {p->k_pages, p->v_pages, p->lr_pages, p->hidden_pages, (void*)p->kv_space.dev_table, (void*)p->lr_space.dev_table})
     if (q) cudaFree(q);
   delete p;
 }
@@ -544,28 +563,35 @@ static int fww(const char* what, int64_t rows, int64_t row_begin, int64_t n, int
   return LORAKV_OK;
 }
 
-int lorakv_pool_append(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin,
-                       const float* rows, int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended) {
+}  // extern "C"
+
+static const char* kWhat4[4] = {"key", "value", "lr", "hidden"};
+
+template <class E>
+static int pool_append_impl(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin,
+                            const E* rows, int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended) {
   if (!pool) return fail("null pool");
   if (appended) *appended = 0;
   int64_t set; bool none;
   LK_TRY(resolve(pool, which, layer, agent, &set, &none));
   if (none) return fail("KvStore: scheme %s has no LR cache", kSchemeName[pool->dims.scheme]);
   if (n_rows < 0) return fail("append: negative row count");
-  int64_t& have = rows_of(pool, which)[(size_t)set][(size_t)layer];
+  if ((sizeof(E) == 8) != (pool->dims.dtype == LORAKV_F64))
+    return fail("append: %s rows into a pool of another element type (fp64 pools take float64 rows, the others float32)",
+                sizeof(E) == 8 ? "float64" : "float32");
+  int64_t& have = row_counter(pool, which, set, layer);
   int64_t skip, add;
-  LK_TRY(fww(kWhat[which], have, row_begin, n_rows, &skip, &add));
+  LK_TRY(fww(kWhat4[which], have, row_begin, n_rows, &skip, &add));
   if (add == 0) return LORAKV_OK;
-  const bool is_lr = which == LORAKV_LR;
-  const int64_t full_cols = is_lr ? pool->dims.rank : pool->dims.n_kv_heads * pool->dims.d_head;
+  const int64_t full_cols = cache_cols_full(pool, which);
   if (full_cols > 0) {
     if (!rows) return fail("append: null rows");
     lorakv_ctx* ctx = pool->ctx;
     LK_CUDA(cudaSetDevice(ctx->device));
-    LK_TRY(ensure_pages(pool, is_lr ? pool->lr_space : pool->kv_space, set, have + add));
-    const float* dev; int64_t dev_ld;
+    LK_TRY(ensure_pages(pool, which == LORAKV_LR ? pool->lr_space : pool->kv_space, set, have + add));
+    const E* dev; int64_t dev_ld;
     LK_TRY(stage_rows(ctx, rows + skip * ld, add, full_cols, ld, mem_kind, &dev, &dev_ld));
-    const int64_t col0 = is_lr ? 0 : pool->dims.kv_head_begin * pool->dims.d_head;
+    const int64_t col0 = (which == LORAKV_KEY || which == LORAKV_VALUE) ? pool->dims.kv_head_begin * pool->dims.d_head : 0;
     LK_TRY(launch_append_scatter(pool, which, layer, set, have, dev + col0, add, dev_ld));
     if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));  // staging is reused
   }
@@ -574,11 +600,98 @@ int lorakv_pool_append(lorakv_pool* pool, int which, int64_t layer, int64_t agen
   return LORAKV_OK;
 }
 
+// recompute_overwrite (kvcache.hpp:298-305): same scatter as an append, over rows that exist, counters untouched
+template <class E>
+static int pool_overwrite_impl(lorakv_pool* pool, int which, int64_t layer, int64_t row_begin, const E* rows, int64_t n_rows,
+                               int64_t ld, int mem_kind) {
+  if (!pool) return fail("null pool");
+  if (which != LORAKV_KEY && which != LORAKV_VALUE) return fail("bad cache selector %d", which);
+  const bool allowed = pool->dims.scheme == LORAKV_SELECTIVE &&
+                       std::binary_search(pool->recompute_layers.begin(), pool->recompute_layers.end(), layer);
+  if (!allowed)
+    return fail("KvStore: overwrite of existing cache rows is forbidden (scheme %s, layer %lld)", kSchemeName[pool->dims.scheme], (long long)layer);
+  if (layer < 0 || layer >= pool->dims.n_layers) return fail("layer %lld out of range", (long long)layer);
+  if ((sizeof(E) == 8) != (pool->dims.dtype == LORAKV_F64)) return fail("overwrite: rows of another element type than the pool's");
+  const int64_t have = row_counter(pool, which, 0, layer);
+  if (row_begin < 0 || n_rows < 0 || row_begin + n_rows > have)
+    return fail("GrowMat::overwrite: rows [%lld,%lld) not materialized", (long long)row_begin, (long long)(row_begin + n_rows));
+  if (n_rows == 0) return LORAKV_OK;
+  if (!rows) return fail("overwrite: null rows");
+  lorakv_ctx* ctx = pool->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  const E* dev; int64_t dev_ld;
+  LK_TRY(stage_rows(ctx, rows, n_rows, cache_cols_full(pool, which), ld, mem_kind, &dev, &dev_ld));
+  LK_TRY(launch_append_scatter(pool, which, layer, 0, row_begin, dev + pool->dims.kv_head_begin * pool->dims.d_head, n_rows, dev_ld));
+  if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LORAKV_OK;
+}
+
+template <class E>
+static int pool_read_impl(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin, int64_t n_rows, E* out) {
+  if (!pool) return fail("null pool");
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, which, layer, agent, &set, &none));
+  if (none) return LORAKV_OK;   // zero columns
+  if ((sizeof(E) == 8) != (pool->dims.dtype == LORAKV_F64)) return fail("read: rows of another element type than the pool's");
+  const int64_t have = row_counter(const_cast<lorakv_pool*>(pool), which, set, layer);
+  if (row_begin < 0 || n_rows < 0 || row_begin + n_rows > have)
+    return fail("row_range [%lld,%lld) out of bounds for %lld rows", (long long)row_begin,
+                (long long)(row_begin + n_rows), (long long)have);
+  const int64_t cols = cache_cols_local(pool, which);
+  if (n_rows == 0 || cols == 0) return LORAKV_OK;
+  if (!out) return fail("read: null out");
+  lorakv_ctx* ctx = pool->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  LK_TRY(scratch_reserve(ctx, ctx->out, (size_t)(n_rows * cols) * sizeof(E)));
+  LK_TRY(launch_gather_rows(pool, which, layer, set, row_begin, n_rows, static_cast<E*>(ctx->out.ptr)));
+  LK_CUDA(cudaMemcpyAsync(out, ctx->out.ptr, (size_t)(n_rows * cols) * sizeof(E), cudaMemcpyDeviceToHost, ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LORAKV_OK;
+}
+
+extern "C" {
+
+int lorakv_pool_append(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin,
+                       const float* rows, int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended) {
+  return pool_append_impl(pool, which, layer, agent, row_begin, rows, n_rows, ld, mem_kind, appended);
+}
+int lorakv_pool_append_f64(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin,
+                           const double* rows, int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended) {
+  return pool_append_impl(pool, which, layer, agent, row_begin, rows, n_rows, ld, mem_kind, appended);
+}
+int lorakv_pool_overwrite(lorakv_pool* pool, int which, int64_t layer, int64_t row_begin, const float* rows, int64_t n_rows,
+                          int64_t ld, int mem_kind) {
+  return pool_overwrite_impl(pool, which, layer, row_begin, rows, n_rows, ld, mem_kind);
+}
+int lorakv_pool_overwrite_f64(lorakv_pool* pool, int which, int64_t layer, int64_t row_begin, const double* rows, int64_t n_rows,
+                              int64_t ld, int mem_kind) {
+  return pool_overwrite_impl(pool, which, layer, row_begin, rows, n_rows, ld, mem_kind);
+}
+int lorakv_pool_read_f64(const lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin, int64_t n_rows,
+                         double* out) {
+  return pool_read_impl(pool, which, layer, agent, row_begin, n_rows, out);
+}
+int lorakv_pool_get_recompute_layers(const lorakv_pool* pool, int64_t* out, int64_t cap, int64_t* n) {
+  if (!pool) return fail("null pool");
+  if (n) *n = (int64_t)pool->recompute_layers.size();
+  for (int64_t i = 0; out && i < cap && i < (int64_t)pool->recompute_layers.size(); ++i) out[i] = pool->recompute_layers[(size_t)i];
+  return LORAKV_OK;
+}
+int lorakv_pool_set_recompute_layers(lorakv_pool* pool, const int64_t* layers, int64_t n) {
+  if (!pool || (n > 0 && !layers)) return fail("null argument");
+  for (int64_t i = 0; i < n; ++i)
+    if (layers[i] < 0 || layers[i] >= pool->dims.n_layers) return fail("KvStore: recompute layer %lld out of range", (long long)layers[i]);
+  pool->recompute_layers.assign(layers, layers + n);
+  std::sort(pool->recompute_layers.begin(), pool->recompute_layers.end());
+  return LORAKV_OK;
+}
+
 int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer,
                                   int64_t agent, int64_t row_begin, const float* x, int64_t n_rows,
                                   int64_t ld, int mem_kind, int64_t* appended) {
   if (!pool || !ad) return fail("null argument");
   if (appended) *appended = 0;
+  if (pool->dims.dtype == LORAKV_F64) return fail("lr_append_project: fp64 pools are storage only (append_lr takes the rows)");
   int64_t set; bool none;
   LK_TRY(resolve(pool, LORAKV_LR, layer, agent, &set, &none));
   if (none) return fail("KvStore: scheme %s has no LR cache", kSchemeName[pool->dims.scheme]);
@@ -915,30 +1028,13 @@ int lorakv_pool_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t 
     *rows = pool->key_rows[(size_t)set][(size_t)layer];
     return LORAKV_OK;
   }
-  *rows = rows_of(pool, which)[(size_t)set][(size_t)layer];
+  *rows = row_counter(const_cast<lorakv_pool*>(pool), which, set, layer);
   return LORAKV_OK;
 }
 
 int lorakv_pool_read(const lorakv_pool* pool, int which, int64_t layer, int64_t agent,
                      int64_t row_begin, int64_t n_rows, float* out) {
-  if (!pool) return fail("null pool");
-  int64_t set; bool none;
-  LK_TRY(resolve(pool, which, layer, agent, &set, &none));
-  if (none) return LORAKV_OK;   // zero columns
-  const int64_t have = rows_of(pool, which)[(size_t)set][(size_t)layer];
-  if (row_begin < 0 || n_rows < 0 || row_begin + n_rows > have)
-    return fail("row_range [%lld,%lld) out of bounds for %lld rows", (long long)row_begin,
-                (long long)(row_begin + n_rows), (long long)have);
-  const int64_t cols = which == LORAKV_LR ? pool->dims.rank : pool->d_kv_local();
-  if (n_rows == 0 || cols == 0) return LORAKV_OK;
-  if (!out) return fail("read: null out");
-  lorakv_ctx* ctx = pool->ctx;
-  LK_CUDA(cudaSetDevice(ctx->device));
-  LK_TRY(scratch_reserve(ctx, ctx->out, (size_t)(n_rows * cols) * sizeof(float)));
-  LK_TRY(launch_gather_rows(pool, which, layer, set, row_begin, n_rows, static_cast<float*>(ctx->out.ptr)));
-  LK_CUDA(cudaMemcpyAsync(out, ctx->out.ptr, (size_t)(n_rows * cols) * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-  LK_CUDA(cudaStreamSynchronize(ctx->stream));
-  return LORAKV_OK;
+  return pool_read_impl(pool, which, layer, agent, row_begin, n_rows, out);
 }
 
 int lorakv_pool_bytes(const lorakv_pool* pool, uint64_t out[4]) {
@@ -951,13 +1047,14 @@ int lorakv_pool_bytes(const lorakv_pool* pool, uint64_t out[4]) {
   for (const auto& per : pool->value_rows) for (int64_t n : per) v += (uint64_t)n * dkv;
   if (pool->lr_sets() > 0)
     for (const auto& per : pool->lr_rows) for (int64_t n : per) l += (uint64_t)n * r;
-  out[0] = k * sz; out[1] = v * sz; out[2] = l * sz; out[3] = 0;
+  out[0] = k * sz; out[1] = v * sz; out[2] = l * sz;
+  out[3] = (uint64_t)pool->hidden_rows * (uint64_t)pool->dims.d_model * sz;
   return LORAKV_OK;
 }
 uint64_t lorakv_pool_allocated_elements(const lorakv_pool* pool) {
   uint64_t b[4];
   if (lorakv_pool_bytes(pool, b) != LORAKV_OK) return 0;
-  return (b[0] + b[1] + b[2]) / (uint64_t)pool->elem;
+  return (b[0] + b[1] + b[2] + b[3]) / (uint64_t)pool->elem;
 }
 uint64_t lorakv_pool_reserved_bytes(const lorakv_pool* pool) { return pool ? pool->reserved_bytes : 0; }
 
@@ -1103,6 +1200,9 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
                      float* out, int mem_kind, const lk::PeerOut* peers = nullptr, bool per_entry_lr = false) {
   lorakv_ctx* ctx = pool->ctx;
   LK_CUDA(cudaSetDevice(ctx->device));
+  if (pool->dims.dtype == LORAKV_F64)
+    return fail("attention: fp64 pages are storage only; attend over the views with gqa_attention<double> (lorakv_gqa_forward_f64), "
+                "as the reference's step() does");
   if (layer_begin < 0 || layer_end > pool->dims.n_layers || layer_begin >= layer_end) return fail("attention: bad layer range");
   if (n_q_heads < 1 || n_q_heads % pool->dims.n_kv_heads != 0)
     return fail("gqa_attention: n_q_heads %lld not divisible by n_kv_heads %lld", (long long)n_q_heads, (long long)pool->dims.n_kv_heads);

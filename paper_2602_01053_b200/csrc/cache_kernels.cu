@@ -32,6 +32,8 @@ struct PageAddr {
 template <class S> __device__ __forceinline__ S to_store(float x);
 template <> __device__ __forceinline__ float to_store<float>(float x) { return x; }
 template <> __device__ __forceinline__ __nv_bfloat16 to_store<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <class S> __device__ __forceinline__ S to_store(double x);
+template <> __device__ __forceinline__ double to_store<double>(double x) { return x; }       // fp64 pages: exact
 template <class S> __device__ __forceinline__ float from_store(S x);
 template <> __device__ __forceinline__ float from_store<float>(float x) { return x; }
 template <> __device__ __forceinline__ float from_store<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
@@ -78,8 +80,8 @@ __global__ void kv_append_scatter_kernel(PageAddr a, int64_t row0, const float* 
 }
 
 // scalar variant for head dims that are not a multiple of 8
-template <class S>
-__global__ void kv_append_scatter_scalar_kernel(PageAddr a, int64_t row0, const float* __restrict__ src,
+template <class S, class Src = float>
+__global__ void kv_append_scatter_scalar_kernel(PageAddr a, int64_t row0, const Src* __restrict__ src,
                                                 int64_t n_rows, int64_t ld) {
   const int64_t per_row = (int64_t)a.width * a.n_heads;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -87,10 +89,22 @@ __global__ void kv_append_scatter_scalar_kernel(PageAddr a, int64_t row0, const 
   const int64_t i = idx / per_row;
   const int v = (int)(idx % per_row);
   const int head = v / a.width, c = v % a.width;
-  const float x = c < a.src_cols ? src[i * ld + (int64_t)head * a.src_cols + c] : 0.f;
+  const Src x = c < a.src_cols ? src[i * ld + (int64_t)head * a.src_cols + c] : Src(0);
   const int64_t row = row0 + i;
   const int64_t phys = a.table[row / a.P];
   static_cast<S*>(a.base)[(int64_t)head * a.head_stride + phys * a.page_stride + page_offset(a.lay, (int)(row % a.P), c)] = to_store<S>(x);
+}
+
+__global__ void gather_rows_f64_kernel(PageAddr a, int64_t row0, int64_t n_rows, double* __restrict__ dst) {
+  const int64_t per_row = (int64_t)a.src_cols * a.n_heads;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_rows * per_row) return;
+  const int64_t i = idx / per_row;
+  const int v = (int)(idx % per_row);
+  const int head = v / a.src_cols, c = v % a.src_cols;
+  const int64_t row = row0 + i;
+  const int64_t phys = a.table[row / a.P];
+  dst[idx] = static_cast<const double*>(a.base)[(int64_t)head * a.head_stride + phys * a.page_stride + page_offset(a.lay, (int)(row % a.P), c)];
 }
 
 template <class S>
@@ -349,7 +363,15 @@ __global__ void __launch_bounds__(kMmaProjWarps * 32) lr_append_project_mma_kern
 PageAddr make_addr(const lorakv_pool* pool, int which, int64_t layer, int64_t set) {
   PageAddr a;
   const int64_t elem = pool->elem;
-  if (which == LORAKV_LR) {
+  if (which == LORAKV_HIDDEN) {          // one cache for the trajectory, paged through the K / V table
+    a.base = pool->hidden_pages;
+    a.table = pool->kv_space.dev_table;
+    a.head_stride = 0;
+    a.page_stride = pool->P * pool->dims.d_model;
+    a.width = (int)pool->dims.d_model;
+    a.n_heads = 1;
+    a.src_cols = (int)pool->dims.d_model;
+  } else if (which == LORAKV_LR) {
     a.base = static_cast<char*>(pool->lr_pages) + layer * pool->lr_layer_stride() * elem;
     a.table = pool->lr_space.dev_table + set * pool->lr_space.max_pages;
     a.head_stride = 0;
@@ -375,8 +397,37 @@ PageAddr make_addr(const lorakv_pool* pool, int which, int64_t layer, int64_t se
 }  // namespace
 
 int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
+                          const double* src_dev, int64_t n_rows, int64_t ld) {
+  if (n_rows == 0) return LORAKV_OK;
+  if (pool->dims.dtype != LORAKV_F64) return fail("append: float64 rows need an fp64 pool");
+  lorakv_ctx* ctx = pool->ctx;
+  const PageAddr a = make_addr(pool, which, layer, set);
+  if (a.width == 0) return LORAKV_OK;
+  const int64_t n = n_rows * a.width * a.n_heads;
+  kv_append_scatter_scalar_kernel<double, double><<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(a, row0, src_dev, n_rows, ld);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
+                       int64_t n_rows, double* dst_dev) {
+  if (n_rows == 0) return LORAKV_OK;
+  if (pool->dims.dtype != LORAKV_F64) return fail("read: float64 rows need an fp64 pool");
+  lorakv_ctx* ctx = pool->ctx;
+  const PageAddr a = make_addr(pool, which, layer, set);
+  if (a.src_cols == 0) return LORAKV_OK;
+  const int64_t n = n_rows * a.src_cols * a.n_heads;
+  gather_rows_f64_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(a, row0, n_rows, dst_dev);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                           const float* src_dev, int64_t n_rows, int64_t ld) {
   if (n_rows == 0) return LORAKV_OK;
+  if (pool->dims.dtype == LORAKV_F64) return fail("append: an fp64 pool takes float64 rows (lorakv_pool_append_f64)");
   lorakv_ctx* ctx = pool->ctx;
   const PageAddr a = make_addr(pool, which, layer, set);
   if (a.width == 0) return LORAKV_OK;   // rank-0 cache tracks row counts only (kvcache.hpp:173-176)
@@ -400,6 +451,7 @@ int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t s
 int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                        int64_t n_rows, float* dst_dev) {
   if (n_rows == 0) return LORAKV_OK;
+  if (pool->dims.dtype == LORAKV_F64) return fail("read: an fp64 pool returns float64 rows (lorakv_pool_read_f64)");
   lorakv_ctx* ctx = pool->ctx;
   const PageAddr a = make_addr(pool, which, layer, set);
   if (a.src_cols == 0) return LORAKV_OK;

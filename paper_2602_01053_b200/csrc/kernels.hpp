@@ -32,12 +32,16 @@ int matmul_forward(lorakv_ctx* ctx, const T* a, int64_t lda, const T* b, int64_t
 // into pages, starting at logical row `row0` of the page set `set`.
 int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                           const float* src_dev, int64_t n_rows, int64_t ld);
+int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
+                          const double* src_dev, int64_t n_rows, int64_t ld);          // fp64 pools
 // V_lr rows = X * A for one layer, written into the LR pages of `set` from logical row `row0`.
 int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set,
                       int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld);
 // De-paginate rows [row0, row0+n_rows) into a dense float32 device matrix.
 int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                        int64_t n_rows, float* dst_dev);
+int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
+                       int64_t n_rows, double* dst_dev);                                // fp64 pools
 
 // Where a finished output row goes when the step ends in the output gather of a kv-head-sharded run
 // (peer_gather.cu): the epilogue stores its slice of the FULL row [n_q_total * d] straight into every rank's

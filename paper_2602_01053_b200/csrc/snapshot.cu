@@ -24,7 +24,7 @@ const char* kSchemeName[5] = {"NonShared", "FullShared", "BaseShared", "BaseLRSh
 struct TensorRef { std::string name; int which; int64_t layer, agent, cols; };
 
 // SnapshotAccess::collect (kvcache.hpp:523-544)
-std::vector<TensorRef> collect(int scheme, int64_t n_layers, int64_t n_agents, int64_t d_kv, int64_t rank) {
+std::vector<TensorRef> collect(int scheme, int64_t n_layers, int64_t n_agents, int64_t d_kv, int64_t rank, int64_t d_model) {
   std::vector<TensorRef> out;
   for (int64_t l = 0; l < n_layers; ++l) {
     const std::string tag = "layer" + std::to_string(l);
@@ -41,6 +41,7 @@ std::vector<TensorRef> collect(int scheme, int64_t n_layers, int64_t n_agents, i
       for (int64_t a = 0; a < n_agents; ++a) out.push_back({tag + ".lr.agent" + std::to_string(a), LORAKV_LR, l, a, rank});
     if (scheme == LORAKV_BASELRSHARED) out.push_back({tag + ".lr", LORAKV_LR, l, 0, rank});
   }
+  if (scheme == LORAKV_SELECTIVE) out.push_back({"hidden", LORAKV_HIDDEN, 0, 0, d_model});
   return out;
 }
 
@@ -133,7 +134,8 @@ int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const i
                 (long long)pool->n_kv_local, (long long)pool->dims.n_kv_heads);
   const lorakv_pool_dims& d = pool->dims;
   const int64_t d_kv = d.n_kv_heads * d.d_head;
-  const std::vector<TensorRef> tensors = collect(d.scheme, d.n_layers, d.n_agents, d_kv, d.rank);
+  const std::vector<TensorRef> tensors = collect(d.scheme, d.n_layers, d.n_agents, d_kv, d.rank, d.d_model);
+  const bool f64 = d.dtype == LORAKV_F64;      // KvStore<double>: dtype "f64", float64 payloads (detail::dtype_name, kvcache.hpp:431-435)
   std::vector<int64_t> rows(tensors.size());
   for (size_t i = 0; i < tensors.size(); ++i)
     LK_TRY(lorakv_pool_rows(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, &rows[i]));
@@ -141,12 +143,13 @@ int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const i
   std::string h = "{";
   h += "\"d_kv\":" + std::to_string((long long)d_kv);
   h += ",\"d_model\":" + std::to_string((long long)d.d_model);
-  h += ",\"dtype\":\"f32\",\"format\":\"lorakv-cache-snapshot\"";
+  h += std::string(",\"dtype\":\"") + (f64 ? "f64" : "f32") + "\",\"format\":\"lorakv-cache-snapshot\"";
   h += ",\"length\":" + std::to_string((long long)pool->length);
   h += ",\"n_agents\":" + std::to_string((long long)d.n_agents);
   h += ",\"n_layers\":" + std::to_string((long long)d.n_layers);
   h += ",\"rank\":" + std::to_string((long long)d.rank);
-  h += ",\"recompute_layers\":[],\"scheme\":\"" + std::string(kSchemeName[d.scheme]) + "\"";
+  h += ",\"recompute_layers\":" + int_array(pool->recompute_layers, pool->recompute_layers.size()) + ",\"scheme\":\"" +
+       std::string(kSchemeName[d.scheme]) + "\"";
   h += ",\"seen_upto\":" + int_array(pool->seen, pool->seen.size());
   h += ",\"tensors\":[";
   for (size_t i = 0; i < tensors.size(); ++i) {
@@ -162,12 +165,19 @@ int lorakv_pool_save_snapshot(const lorakv_pool* pool, const char* path, const i
   out.write(reinterpret_cast<const char*>(&hlen), sizeof hlen);
   out.write(h.data(), (std::streamsize)h.size());
   std::vector<float> buf;
+  std::vector<double> buf64;
   for (size_t i = 0; i < tensors.size(); ++i) {
     const size_t n = (size_t)(rows[i] * tensors[i].cols);
     if (n == 0) continue;
-    buf.resize(n);
-    LK_TRY(lorakv_pool_read(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, 0, rows[i], buf.data()));
-    out.write(reinterpret_cast<const char*>(buf.data()), (std::streamsize)(n * sizeof(float)));
+    if (f64) {
+      buf64.resize(n);
+      LK_TRY(lorakv_pool_read_f64(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, 0, rows[i], buf64.data()));
+      out.write(reinterpret_cast<const char*>(buf64.data()), (std::streamsize)(n * sizeof(double)));
+    } else {
+      buf.resize(n);
+      LK_TRY(lorakv_pool_read(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, 0, rows[i], buf.data()));
+      out.write(reinterpret_cast<const char*>(buf.data()), (std::streamsize)(n * sizeof(float)));
+    }
   }
   if (!out) return fail("snapshot write failed: %s", path);
   return LORAKV_OK;
@@ -203,7 +213,9 @@ static int load_snapshot_impl(lorakv_ctx* ctx, const char* path, int dtype, int6
   const Json* fmt = header.get("format");
   if (!fmt || fmt->s != "lorakv-cache-snapshot") return fail("not a cache snapshot: %s", path);
   const Json* dt = header.get("dtype");
-  if (!dt || dt->s != "f32") return fail("snapshot dtype %s does not match build dtype f32", dt ? dt->s.c_str() : "?");
+  const bool f64 = dtype == LORAKV_F64;
+  const char* want_dt = f64 ? "f64" : "f32";
+  if (!dt || dt->s != want_dt) return fail("snapshot dtype %s does not match build dtype %s", dt ? dt->s.c_str() : "?", want_dt);
   const Json* sch = header.get("scheme");
   int scheme = -1;
   for (int k = 0; k < 5; ++k) if (sch && sch->s == kSchemeName[k]) scheme = k;
@@ -234,9 +246,16 @@ static int load_snapshot_impl(lorakv_ctx* ctx, const char* path, int dtype, int6
   if ((int64_t)seen->arr.size() != dims.n_agents) return bail(fail("snapshot seen_upto has %zu entries for %lld agents", seen->arr.size(), (long long)dims.n_agents));
   pool->length = length;
   for (size_t a = 0; a < seen->arr.size(); ++a) pool->seen[a] = seen->arr[a].i;
-  const std::vector<TensorRef> tensors = collect(scheme, dims.n_layers, dims.n_agents, d_kv, dims.rank);
+  if (const Json* rl = header.get("recompute_layers")) {
+    std::vector<int64_t> layers;
+    if (rl->kind == Json::Arr) for (const Json& x : rl->arr) layers.push_back(x.i);
+    const int rc = lorakv_pool_set_recompute_layers(pool, layers.data(), (int64_t)layers.size());
+    if (rc != LORAKV_OK) return bail(rc);
+  }
+  const std::vector<TensorRef> tensors = collect(scheme, dims.n_layers, dims.n_agents, d_kv, dims.rank, dims.d_model);
   if (tj->arr.size() != tensors.size()) return bail(fail("snapshot tensor list mismatch: %s", path));
   std::vector<float> buf;
+  std::vector<double> buf64;
   for (size_t i = 0; i < tensors.size(); ++i) {
     const Json& meta = tj->arr[i];
     const Json *nm = meta.get("name"), *rj = meta.get("rows"), *cj = meta.get("cols");
@@ -247,12 +266,21 @@ static int load_snapshot_impl(lorakv_ctx* ctx, const char* path, int dtype, int6
       return bail(fail("snapshot tensor %s claims %lld rows; the trajectory holds at most %lld", tensors[i].name.c_str(), (long long)rows,
                        (long long)dims.max_tokens));
     const size_t n = (size_t)(rows * tensors[i].cols);
-    buf.resize(std::max<size_t>(n, 1));
-    in.read(reinterpret_cast<char*>(buf.data()), (std::streamsize)(n * sizeof(float)));
-    if (!in) return bail(fail("snapshot payload truncated: %s", path));
     int64_t added = 0;
-    const int rc = lorakv_pool_append(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, 0, buf.data(), rows,
-                                      tensors[i].cols, LORAKV_HOST, &added);
+    int rc;
+    if (f64) {
+      buf64.resize(std::max<size_t>(n, 1));
+      in.read(reinterpret_cast<char*>(buf64.data()), (std::streamsize)(n * sizeof(double)));
+      if (!in) return bail(fail("snapshot payload truncated: %s", path));
+      rc = lorakv_pool_append_f64(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, 0, buf64.data(), rows, tensors[i].cols,
+                                  LORAKV_HOST, &added);
+    } else {
+      buf.resize(std::max<size_t>(n, 1));
+      in.read(reinterpret_cast<char*>(buf.data()), (std::streamsize)(n * sizeof(float)));
+      if (!in) return bail(fail("snapshot payload truncated: %s", path));
+      rc = lorakv_pool_append(pool, tensors[i].which, tensors[i].layer, tensors[i].agent, 0, buf.data(), rows, tensors[i].cols,
+                              LORAKV_HOST, &added);
+    }
     if (rc != LORAKV_OK) return bail(rc);
   }
   if (n_tokens) *n_tokens = (int64_t)toks->arr.size();

@@ -153,6 +153,11 @@ struct lorakv_pool {
   void* k_pages = nullptr;   // [n_layers][n_kv_local][kv_total_pages] pages; inside a page: page_layout.cuh
   void* v_pages = nullptr;
   void* lr_pages = nullptr;  // [n_layers][lr_total_pages][P][r_pad]
+  // SelectiveRecompute (kvcache.hpp:53-58, 245-246, 289-305): one hidden-state cache of the trajectory (rows x d_model,
+  // paged through the K / V page table) and the layers whose cached rows a returning agent may overwrite
+  void* hidden_pages = nullptr;          // [kv_total_pages][P][d_model]
+  int64_t hidden_rows = 0;
+  std::vector<int64_t> recompute_layers;
   uint64_t reserved_bytes = 0;
   int64_t kv_sets() const { return dims.scheme == LORAKV_NONSHARED ? dims.n_agents : 1; }
   int64_t lr_sets() const {

@@ -112,7 +112,32 @@ TEST_CASE("overwrites are forbidden; schemes without a hidden cache say so") {
   const Matrix<float> rows = fill_rows(2, 8, 0.f);
   CHECK_THROWS_WITH_AS(st.recompute_overwrite(0, 0, rows.view(), rows.view()), "forbidden", std::runtime_error);
   CHECK_THROWS_WITH_AS(st.append_hidden(0, rows.view()), "no hidden-state cache", std::runtime_error);
-  CHECK_THROWS_AS(KvStore<float>(CacheScheme{SchemeKind::SelectiveRecompute, {0}}, StoreDims{1, 8, 16, 2, 2}), std::runtime_error);
+  // SelectiveRecompute (kvcache.hpp:229-246, 289-305): needs a recompute set; keeps one hidden-state cache; only its recompute
+  // layers may overwrite rows that exist (the rest stays first-writer-wins)
+  CHECK_THROWS_WITH_AS(KvStore<float>(CacheScheme{SchemeKind::SelectiveRecompute, {}}, StoreDims{1, 8, 16, 2, 2}), "non-empty recompute set",
+                       std::runtime_error);
+  KvStore<float> sel(CacheScheme{SchemeKind::SelectiveRecompute, {1}}, StoreDims{2, 8, 16, 0, 2}, DeviceOptions{1, 64});
+  const Matrix<float> hid = fill_rows(2, 16, 50.f), other = fill_rows(2, 8, 7.f);
+  for (idx l = 0; l < 2; ++l) { sel.append_key(l, 0, 0, rows.view()); sel.append_value(l, 0, 0, rows.view()); }
+  sel.append_hidden(0, hid.view());
+  CHECK(sel.hidden_size() == 2);
+  CHECK(same(sel.hidden_rows(0, 2), hid));
+  CHECK(sel.bytes().hidden == 2u * 16u * sizeof(float));
+  CHECK_THROWS_WITH_AS(sel.recompute_overwrite(0, 0, other.view(), other.view()), "forbidden", std::runtime_error);
+  sel.recompute_overwrite(1, 0, other.view(), other.view());
+  CHECK(same(sel.key_view(1, 0), other)); CHECK(same(sel.value_view(1, 1), other)); CHECK(same(sel.key_view(0, 0), rows));
+  CHECK_THROWS_WITH_AS(sel.recompute_overwrite(1, 1, other.view(), other.view()), "not materialized", std::runtime_error);
+  // KvStore<double>: fp64 pages keep every bit; a copy is a second pool with equal contents
+  KvStore<double> dbl(scheme(SchemeKind::BaseLRShared), StoreDims{1, 8, 16, 2, 2}, DeviceOptions{1, 64});
+  Matrix<double> fine(3, 8);
+  for (std::size_t i = 0; i < fine.data.size(); ++i) fine.data[i] = 1.0 / 3.0 + 1e-13 * double(i);
+  dbl.append_tokens({1, 2, 3}); dbl.append_key(0, 0, 0, fine.view()); dbl.mark_seen(1);
+  const auto kv = dbl.key_view(0, 0);
+  CHECK(kv.rows == 3);
+  for (idx i = 0; i < 3; ++i) for (idx j = 0; j < 8; ++j) CHECK(kv(i, j) == fine(i, j));
+  CHECK(dbl.bytes().key == 3u * 8u * sizeof(double));
+  const KvStore<double> twin = dbl;
+  CHECK(twin == dbl); CHECK(twin.seen(1) == 3); CHECK(twin.seen(0) == 0);
   CHECK_THROWS_WITH_AS(CacheScheme::parse("Shared"), "unknown cache scheme", std::runtime_error);
   CHECK(CacheScheme::parse("BaseLRShared").kind == SchemeKind::BaseLRShared);
 }

@@ -13,11 +13,50 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box with -m gpu)")
 
 
+class _Prefer:
+    """Checker that answers from `first` and falls back to `second` for the few helpers only the C restatement has."""
+
+    def __init__(self, first, second):
+        self._first, self._second = first, second
+        self.kind = first.kind
+
+    def __getattr__(self, name):
+        attr = getattr(self._first, name)
+        if not callable(attr):
+            return attr
+        fallback = getattr(self._second, name, None)
+
+        def call(*a, **kw):
+            try:
+                return attr(*a, **kw)
+            except AttributeError:          # the reference shim does not export this helper (append_fww)
+                if fallback is None:
+                    raise
+                return fallback(*a, **kw)
+        return call
+
+
 @pytest.fixture(scope="session")
 def orc():
-    """The C restatement of the reference path (oracle/liblorakv_oracle.so)."""
+    """The CPU checker the parity tests compare with.  Without a GPU (the `-m "not gpu"` suite): the C restatement of the
+    reference path (oracle/liblorakv_oracle.so), which tests/test_oracle_vs_ref.py pins bit for bit to the reference.  On the
+    GPU box: the reference's OWN code (oracle/_ref/libref_lorakv.so, its headers compiled by oracle/Makefile ref) whenever
+    that library travelled with the tree, so that the CUDA path is compared with the reference itself, not only with its
+    restatement.  LORAKV_TEST_CHECKER=port|reference overrides."""
     from oracle import checker
-    return checker.oracle()
+    port = checker.oracle()
+    want = os.environ.get("LORAKV_TEST_CHECKER")
+    if want == "port":
+        return port
+    use_ref = want == "reference"
+    if want is None:
+        try:
+            import torch
+            use_ref = torch.cuda.is_available()
+        except Exception:
+            use_ref = False
+    ref_chk = checker.reference() if use_ref else None
+    return _Prefer(ref_chk, port) if ref_chk is not None else port
 
 
 @pytest.fixture(scope="session")

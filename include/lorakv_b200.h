@@ -24,8 +24,9 @@
 extern "C" {
 #endif
 
-#define LORAKV_ABI_VERSION 4   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory;
-                                  4: lorakv_step_layer, lorakv_snapshot_tokens */
+#define LORAKV_ABI_VERSION 5   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory;
+                                  4: lorakv_step_layer, lorakv_snapshot_tokens, fp64 pools, SelectiveRecompute store;
+                                  5: key-side low-rank term (lorakv_pool_dims.rank_k, lorakv_adapters_*_k, *_keylr_*) */
 
 typedef struct lorakv_ctx lorakv_ctx;           /* device + stream + scratch */
 typedef struct lorakv_pool lorakv_pool;         /* paged cache of one trajectory (KvStore<T>) */
@@ -43,7 +44,8 @@ enum { LORAKV_HOST = 0, LORAKV_DEVICE = 1 };
 enum { LORAKV_NONSHARED = 0, LORAKV_FULLSHARED = 1, LORAKV_BASESHARED = 2, LORAKV_BASELRSHARED = 3,
        LORAKV_SELECTIVE = 4 };
 /* which cache (LORAKV_HIDDEN: the hidden-state cache of SelectiveRecompute, kvcache.hpp:245-246, 289-293; layer ignored) */
-enum { LORAKV_KEY = 0, LORAKV_VALUE = 1, LORAKV_LR = 2, LORAKV_HIDDEN = 3 };
+enum { LORAKV_KEY = 0, LORAKV_VALUE = 1, LORAKV_LR = 2, LORAKV_HIDDEN = 3,
+       LORAKV_LK = 4 };   /* the key-side low-rank cache L_k = X A_k (extension; lorakv_pool_dims.rank_k > 0; layer-wide, no agent) */
 
 int lorakv_abi_version(void);
 const char* lorakv_last_error(void);
@@ -130,6 +132,24 @@ int lorakv_gqa_forward_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const 
                            int64_t n_q_heads, int64_t n_kv_heads, int64_t d_head, int64_t r,
                            int64_t query_offset, double* out);
 
+/* gqa_attention with a KEY-side low-rank term (the north star's "q K_base^T + (q B_k^T) L_k^T"): the effective keys are
+ * K_base + k_scale * L_k B_k with l_k: L x r_k (shared by all heads, like v_lr) and b_k: r_k x (n_kv_heads*d_head); the
+ * full-width adapter keys are never formed.  The reference has NO key adapter (engine.hpp:129-130, attention.hpp:47-56;
+ * ruled out under RoPE): this is an extension, parity unpinned (the checker materialises K_eff and calls the
+ * reference's attention); r_k = 0 is exactly lorakv_gqa_forward_*.  n_q_heads = n_kv_heads = 1 gives the per-head operator. */
+int lorakv_gqa_forward_keylr_f32(lorakv_ctx* ctx, const float* q, int64_t ldq, const float* k, int64_t ldk,
+                                 const float* v_base, int64_t ldv, const float* v_lr, int64_t ldlr, const float* b_up,
+                                 int64_t ldb, float lr_scale, const float* l_k, int64_t ld_lk, const float* b_k,
+                                 int64_t ld_bk, float k_scale, int64_t L_c, int64_t L, int64_t n_q_heads,
+                                 int64_t n_kv_heads, int64_t d_head, int64_t r, int64_t r_k, int64_t query_offset,
+                                 float* out);
+int lorakv_gqa_forward_keylr_f64(lorakv_ctx* ctx, const double* q, int64_t ldq, const double* k, int64_t ldk,
+                                 const double* v_base, int64_t ldv, const double* v_lr, int64_t ldlr,
+                                 const double* b_up, int64_t ldb, double lr_scale, const double* l_k, int64_t ld_lk,
+                                 const double* b_k, int64_t ld_bk, double k_scale, int64_t L_c, int64_t L,
+                                 int64_t n_q_heads, int64_t n_kv_heads, int64_t d_head, int64_t r, int64_t r_k,
+                                 int64_t query_offset, double* out);
+
 /* matmul, matrix.hpp:101-135: out (M x N, dense) = a (M x K, stride lda) * b (K x N, stride ldb) over
  * HOST pointers.  Ascending-k accumulation with separately rounded multiply and add, i.e. the bits the
  * reference's triple loop produces under -ffp-contract=off.  Used by expand_lr / forward_decomposed
@@ -166,6 +186,7 @@ typedef struct {
   int64_t max_tokens;    /* capacity of the trajectory, rounded up to whole pages */
   int64_t kv_head_begin; /* this pool stores kv heads [kv_head_begin, kv_head_begin + n_kv_local) */
   int64_t n_kv_local;    /* 0 = all heads (single GPU) */
+  int64_t rank_k;        /* key-side low-rank cache L_k (extension, lorakv_gqa_forward_keylr_*); 0 = none, the reference */
 } lorakv_pool_dims;
 
 int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_pool** out);
@@ -287,6 +308,16 @@ int lorakv_adapters_set_a_agent(lorakv_adapters* ad, int64_t layer, int64_t agen
  * the effective scale alpha/rank travels with B (lora.hpp:9-11,34) */
 int lorakv_adapters_set_b(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* b,
                           double alpha);
+
+/* Key-side adapter tables (extension; see lorakv_gqa_forward_keylr_*): shared down-projection A_k (d_model x rank_k) per
+ * layer, per-agent up-projection B_k (rank_k x n_kv_heads*d_head, FULL width) with alpha_k; scale alpha_k / rank_k.  A pool
+ * with rank_k > 0 attends with S = (q K_base^T + (k_scale q B_k[agent]^T) L_k^T) / sqrt(d). */
+int lorakv_adapters_enable_key(lorakv_adapters* ad, int64_t rank_k);
+int lorakv_adapters_set_a_k(lorakv_adapters* ad, int64_t layer, const float* a_k);
+int lorakv_adapters_set_b_k(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* b_k, double alpha_k);
+/* L_k rows = X * A_k computed on the device and written into the L_k pages (the key-side twin of lorakv_pool_append_lr_project) */
+int lorakv_pool_append_lk_project(lorakv_pool* pool, const lorakv_adapters* adapters, int64_t layer, int64_t row_begin,
+                                  const float* x, int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended);
 
 /* ---- device-resident fast paths --------------------------------------------------------------
  * Batched decode = one gqa_attention call (attention.hpp:332) per (layer, batch entry), every

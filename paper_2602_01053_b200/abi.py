@@ -25,7 +25,7 @@ class PoolDims(C.Structure):
     _fields_ = [("scheme", C.c_int32), ("dtype", C.c_int32), ("n_layers", C.c_int64),
                 ("n_kv_heads", C.c_int64), ("d_head", C.c_int64), ("d_model", C.c_int64),
                 ("rank", C.c_int64), ("n_agents", C.c_int64), ("page_tokens", C.c_int64),
-                ("max_tokens", C.c_int64), ("kv_head_begin", C.c_int64), ("n_kv_local", C.c_int64)]
+                ("max_tokens", C.c_int64), ("kv_head_begin", C.c_int64), ("n_kv_local", C.c_int64), ("rank_k", C.c_int64)]
 
 
 def lib_path() -> str:
@@ -88,6 +88,14 @@ SIGNATURES = {
     "lorakv_naive_forward_f64": (C.c_int, _attn_sig(_d, _pd, False)),
     "lorakv_gqa_forward_f32": (C.c_int, _gqa_sig(_f, _pf)),
     "lorakv_gqa_forward_f64": (C.c_int, _gqa_sig(_d, _pd)),
+    "lorakv_gqa_forward_keylr_f32": (C.c_int, [_vp, _pf, _i64, _pf, _i64, _pf, _i64, _pf, _i64, _pf, _i64, _f, _pf, _i64, _pf, _i64, _f,
+                                               _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _pf]),
+    "lorakv_gqa_forward_keylr_f64": (C.c_int, [_vp, _pd, _i64, _pd, _i64, _pd, _i64, _pd, _i64, _pd, _i64, _d, _pd, _i64, _pd, _i64, _d,
+                                               _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _pd]),
+    "lorakv_adapters_enable_key": (C.c_int, [_vp, _i64]),
+    "lorakv_adapters_set_a_k": (C.c_int, [_vp, _i64, _pf]),
+    "lorakv_adapters_set_b_k": (C.c_int, [_vp, _i64, _i64, _pf, _d]),
+    "lorakv_pool_append_lk_project": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, C.POINTER(_i64)]),
     "lorakv_matmul_f32": (C.c_int, [_vp, _pf, _i64, _pf, _i64, _i64, _i64, _i64, _pf]),
     "lorakv_matmul_f64": (C.c_int, [_vp, _pd, _i64, _pd, _i64, _i64, _i64, _i64, _pd]),
     "lorakv_lr_mac_counts": (None, [_i64, _i64, _i64, _i64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -169,7 +177,7 @@ def load_library(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lorakv_abi_version() != 4:
+    if lib.lorakv_abi_version() != 5:
         raise LorakvError("liblorakv_b200.so ABI version mismatch")
     if path is None:
         _lib = lib
@@ -343,6 +351,21 @@ class Context:
                                                         b.shape[1], out.ctypes.data_as(C.POINTER(T))))
         return out
 
+    def gqa_attention_keylr(self, q, k, v, v_lr, b_up, lr_scale, l_k, b_k, k_scale, query_offset, n_q, n_kv):
+        """gqa_attention over K_eff = K_base + k_scale * L_k B_k without forming K_eff (extension, parity unpinned)."""
+        T = np.float64 if q.dtype == np.float64 else np.float32
+        arrs = [np.ascontiguousarray(a, dtype=T) for a in (q, k, v, v_lr, b_up, l_k, b_k)]
+        q, k, v, v_lr, b_up, l_k, b_k = arrs
+        P, fn = (_pd, self.lib.lorakv_gqa_forward_keylr_f64) if T == np.float64 else (_pf, self.lib.lorakv_gqa_forward_keylr_f32)
+        d = q.shape[1] // n_q
+        out = np.zeros((q.shape[0], q.shape[1]), dtype=T)
+        ld = lambda a: max(a.shape[1], 1)
+        ptr = lambda a: a.ctypes.data_as(P)
+        _check(fn(self.h, ptr(q), ld(q), ptr(k), ld(k), ptr(v), ld(v), ptr(v_lr), ld(v_lr), ptr(b_up), ld(b_up), T(lr_scale),
+                  ptr(l_k), ld(l_k), ptr(b_k), ld(b_k), T(k_scale), q.shape[0], k.shape[0], n_q, n_kv, d, v_lr.shape[1], l_k.shape[1],
+                  query_offset, ptr(out)))
+        return out
+
     def gqa_attention(self, q, k, v, v_lr, b_up, lr_scale, query_offset, n_q, n_kv):
         suf, T = ("f32", _f) if q.dtype == np.float32 else ("f64", _d)
         if n_q < 1 or n_kv < 1 or n_q % n_kv or q.shape[1] % n_q:
@@ -438,6 +461,17 @@ class Adapters:
     def set_a_agent(self, layer, agent, a):
         a = np.ascontiguousarray(a, dtype=np.float32)
         _check(self.ctx.lib.lorakv_adapters_set_a_agent(self.h, layer, agent, a.ctypes.data_as(_pf)))
+
+    def enable_key(self, rank_k):
+        _check(self.ctx.lib.lorakv_adapters_enable_key(self.h, rank_k))
+
+    def set_a_k(self, layer, a_k):
+        a_k = np.ascontiguousarray(a_k, dtype=np.float32)
+        _check(self.ctx.lib.lorakv_adapters_set_a_k(self.h, layer, a_k.ctypes.data_as(_pf)))
+
+    def set_b_k(self, layer, agent, b_k, alpha_k):
+        b_k = np.ascontiguousarray(b_k, dtype=np.float32)
+        _check(self.ctx.lib.lorakv_adapters_set_b_k(self.h, layer, agent, b_k.ctypes.data_as(_pf), float(alpha_k)))
 
     def set_b(self, layer, agent, b, alpha):
         b = np.ascontiguousarray(b, dtype=np.float32)
@@ -548,11 +582,11 @@ class Pool:
     """lorakv_pool: the paged HBM cache of one trajectory with KvStore's interface (kvcache.hpp:213)."""
 
     def __init__(self, ctx: Context, scheme, n_layers, n_kv_heads, d_head, d_model, rank, n_agents,
-                 max_tokens, dtype=F32, page_tokens=0, kv_head_begin=0, n_kv_local=0):
+                 max_tokens, dtype=F32, page_tokens=0, kv_head_begin=0, n_kv_local=0, rank_k=0):
         self.ctx = ctx
         dims = PoolDims(SCHEMES[scheme] if isinstance(scheme, str) else scheme, dtype, n_layers,
                         n_kv_heads, d_head, d_model, rank, n_agents, page_tokens, max_tokens,
-                        kv_head_begin, n_kv_local)
+                        kv_head_begin, n_kv_local, rank_k)
         h = _vp()
         _check(ctx.lib.lorakv_pool_create(ctx.h, C.byref(dims), C.byref(h)))
         self.h = h
@@ -629,6 +663,20 @@ class Pool:
     def append_value(self, layer, agent, row_begin, rows):
         return self._append(VALUE, layer, agent, row_begin, rows)
 
+    def append_lk(self, layer, row_begin, rows):
+        """key-side low-rank rows L_k (n x rank_k), the extension of lorakv_gqa_forward_keylr_*"""
+        return self._append(4, layer, 0, row_begin, rows)
+
+    def append_lk_project(self, adapters, layer, row_begin, x):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        n = _i64()
+        _check(self.ctx.lib.lorakv_pool_append_lk_project(self.h, adapters.h, layer, row_begin, x.ctypes.data_as(_vp), x.shape[0],
+                                                          x.shape[1], HOST, C.byref(n)))
+        return n.value
+
+    def lk_view(self, layer):
+        return self._view(4, layer, 0)
+
     def append_lr(self, layer, agent, row_begin, rows):
         return self._append(LR, layer, agent, row_begin, rows)
 
@@ -680,7 +728,7 @@ class Pool:
 
     def _view(self, which, layer, agent):
         n = self.rows(which, layer, agent)
-        cols = self.dims.rank if which == LR else self.dims.n_kv_local * self.dims.d_head
+        cols = self.dims.rank if which == LR else self.dims.rank_k if which == 4 else self.dims.n_kv_local * self.dims.d_head
         if which == LR and self.dims.scheme not in (2, 3):
             cols = 0
         out = np.zeros((n, cols), dtype=np.float32)

@@ -91,6 +91,11 @@ static int resolve(const lorakv_pool* pool, int which, int64_t layer, int64_t ag
     if (pool->dims.scheme != LORAKV_SELECTIVE) return fail("KvStore: scheme %s has no hidden-state cache", kSchemeName[pool->dims.scheme]);
     return LORAKV_OK;
   }
+  if (which == LORAKV_LK) {          // key-side low-rank cache (extension): one per layer, shared by all agents
+    if (pool->rk_pad == 0) return fail("KvStore: this store keeps no key-side low-rank cache (rank_k = 0)");
+    if (layer < 0 || layer >= pool->dims.n_layers) return fail("layer %lld out of range", (long long)layer);
+    return LORAKV_OK;
+  }
   if (which < LORAKV_KEY || which > LORAKV_LR) return fail("bad cache selector %d", which);
   const bool per_agent = (which != LORAKV_LR && pool->dims.scheme == LORAKV_NONSHARED) ||
                          (which == LORAKV_LR && pool->dims.scheme == LORAKV_BASESHARED);
@@ -109,13 +114,16 @@ static int resolve(const lorakv_pool* pool, int which, int64_t layer, int64_t ag
 // row counter of the buffer (which, set, layer)
 static int64_t& row_counter(lorakv_pool* pool, int which, int64_t set, int64_t layer) {
   if (which == LORAKV_HIDDEN) return pool->hidden_rows;
+  if (which == LORAKV_LK) return pool->lk_rows[(size_t)layer];
   auto& t = which == LORAKV_KEY ? pool->key_rows : which == LORAKV_VALUE ? pool->value_rows : pool->lr_rows;
   return t[(size_t)set][(size_t)layer];
 }
 static int64_t cache_cols_full(const lorakv_pool* pool, int which) {      // width of a caller's row
+  if (which == LORAKV_LK) return pool->dims.rank_k;
   return which == LORAKV_HIDDEN ? pool->dims.d_model : which == LORAKV_LR ? pool->dims.rank : pool->dims.n_kv_heads * pool->dims.d_head;
 }
 static int64_t cache_cols_local(const lorakv_pool* pool, int which) {     // width of a stored / returned row
+  if (which == LORAKV_LK) return pool->dims.rank_k;
   return which == LORAKV_HIDDEN ? pool->dims.d_model : which == LORAKV_LR ? pool->dims.rank : pool->d_kv_local();
 }
 static std::vector<std::vector<int64_t>>& rows_of(lorakv_pool* pool, int which) {
@@ -204,7 +212,7 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj, &ctx->qrows})
+  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj, &ctx->qrows, &ctx->qk})
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (IdSlot& s : ctx->id_slots) {
@@ -387,6 +395,22 @@ const char* lorakv_last_kernel(lorakv_ctx* ctx) { return ctx ? ctx->last_kernel 
 LK_OPS(f32, float)
 LK_OPS(f64, double)
 
+// gqa_attention with the key-side low-rank term (KeyLowRank, kernels.hpp): n_q = n_kv = 1 is the per-head operator
+#define LK_KEY_OPS(SUF, T)                                                                                             \
+  int lorakv_gqa_forward_keylr_##SUF(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t ldk, const T* v,    \
+                                     int64_t ldv, const T* vlr, int64_t ldlr, const T* b, int64_t ldb, T s,            \
+                                     const T* l_k, int64_t ld_lk, const T* b_k, int64_t ld_bk, T k_scale, int64_t Lc,  \
+                                     int64_t L, int64_t n_q, int64_t n_kv, int64_t d, int64_t r, int64_t r_k,          \
+                                     int64_t off, T* out) {                                                            \
+    if (n_q < 1 || n_kv < 1 || n_q % n_kv != 0)                                                                        \
+      return fail("gqa_attention: n_q_heads %lld not divisible by n_kv_heads %lld", (long long)n_q, (long long)n_kv);  \
+    const KeyLowRank<T> key{l_k, ld_lk, b_k, ld_bk, k_scale, r_k};                                                     \
+    return generic_forward<T>(ctx, "flash_lora_attention", 0, q, ldq, k, ldk, v, ldv, vlr, ldlr, b, ldb, s, Lc, L,     \
+                              (int)n_q, (int)n_kv, d, r, off, out, nullptr, nullptr, r_k > 0 ? &key : nullptr);        \
+  }
+LK_KEY_OPS(f32, float)
+LK_KEY_OPS(f64, double)
+
 int lorakv_matmul_f32(lorakv_ctx* ctx, const float* a, int64_t lda, const float* b, int64_t ldb, int64_t M,
                       int64_t K, int64_t N, float* out) {
   return matmul_forward<float>(ctx, a, lda, b, ldb, M, K, N, out);
@@ -467,6 +491,11 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
     while (p->r_pad < dims->rank && p->r_pad < 64) p->r_pad *= 2;
     if (p->r_pad < dims->rank) p->r_pad = (dims->rank + 63) / 64 * 64;
   }
+  if (dims->rank_k < 0 || dims->rank_k > 64) { delete p; return fail("KvStore: key rank %lld outside [0,64]", (long long)dims->rank_k); }
+  if (dims->rank_k > 0) {
+    p->rk_pad = 16;
+    while (p->rk_pad < dims->rank_k) p->rk_pad *= 2;
+  }
   p->seen.assign((size_t)dims->n_agents, 0);
   const int64_t max_pages = (dims->max_tokens + p->P - 1) / p->P;
   p->dims.max_tokens = max_pages * p->P;
@@ -476,6 +505,8 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   };
   init_space(p->kv_space, p->kv_sets());
   init_space(p->lr_space, p->lr_sets());
+  init_space(p->lk_space, p->rk_pad > 0 ? 1 : 0);
+  p->lk_rows.assign((size_t)dims->n_layers, 0);
   p->key_rows.assign((size_t)p->kv_sets(), std::vector<int64_t>((size_t)dims->n_layers, 0));
   p->value_rows = p->key_rows;
   p->lr_rows.assign((size_t)std::max<int64_t>(p->lr_sets(), 1), std::vector<int64_t>((size_t)dims->n_layers, 0));
@@ -496,6 +527,7 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   int rc = alloc_zero(&p->k_pages, kv_bytes);
   if (rc == LORAKV_OK) rc = alloc_zero(&p->v_pages, kv_bytes);
   if (rc == LORAKV_OK) rc = alloc_zero(&p->lr_pages, lr_bytes);
+  if (rc == LORAKV_OK) rc = alloc_zero(&p->lk_pages, (size_t)(dims->n_layers * p->lk_layer_stride()) * (size_t)p->elem);
   if (rc == LORAKV_OK && dims->scheme == LORAKV_SELECTIVE)
     rc = alloc_zero(&p->hidden_pages, (size_t)(p->kv_space.total_pages() * p->P * dims->d_model) * (size_t)p->elem);
   auto alloc_table = [&](PageSpace& sp) -> int {
@@ -506,6 +538,7 @@ int lorakv_pool_create(lorakv_ctx* ctx, const lorakv_pool_dims* dims, lorakv_poo
   };
   if (rc == LORAKV_OK) rc = alloc_table(p->kv_space);
   if (rc == LORAKV_OK) rc = alloc_table(p->lr_space);
+  if (rc == LORAKV_OK) rc = alloc_table(p->lk_space);
   if (rc != LORAKV_OK) return cleanup(rc);
   *out = p;
   return LORAKV_OK;
@@ -515,7 +548,8 @@ void lorakv_pool_destroy(lorakv_pool* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
   cudaStreamSynchronize(p->ctx->stream);
-  for (void* q : {p->k_pages, p->v_pages, p->lr_pages, p->hidden_pages, (void*)p->kv_space.dev_table, (void*)p->lr_space.dev_table})
+  for (void* q : {p->k_pages, p->v_pages, p->lr_pages, p->hidden_pages, p->lk_pages, (void*)p->kv_space.dev_table,
+                  (void*)p->lr_space.dev_table, (void*)p->lk_space.dev_table})
     if (q) cudaFree(q);
   delete p;
 }
@@ -565,7 +599,7 @@ static int fww(const char* what, int64_t rows, int64_t row_begin, int64_t n, int
 
 }  // extern "C"
 
-static const char* kWhat4[4] = {"key", "value", "lr", "hidden"};
+static const char* kWhat4[5] = {"key", "value", "lr", "hidden", "key-lr"};
 
 template <class E>
 static int pool_append_impl(lorakv_pool* pool, int which, int64_t layer, int64_t agent, int64_t row_begin,
@@ -588,7 +622,7 @@ static int pool_append_impl(lorakv_pool* pool, int which, int64_t layer, int64_t
     if (!rows) return fail("append: null rows");
     lorakv_ctx* ctx = pool->ctx;
     LK_CUDA(cudaSetDevice(ctx->device));
-    LK_TRY(ensure_pages(pool, which == LORAKV_LR ? pool->lr_space : pool->kv_space, set, have + add));
+    LK_TRY(ensure_pages(pool, which == LORAKV_LR ? pool->lr_space : which == LORAKV_LK ? pool->lk_space : pool->kv_space, set, have + add));
     const E* dev; int64_t dev_ld;
     LK_TRY(stage_rows(ctx, rows + skip * ld, add, full_cols, ld, mem_kind, &dev, &dev_ld));
     const int64_t col0 = (which == LORAKV_KEY || which == LORAKV_VALUE) ? pool->dims.kv_head_begin * pool->dims.d_head : 0;
@@ -1047,6 +1081,7 @@ int lorakv_pool_bytes(const lorakv_pool* pool, uint64_t out[4]) {
   for (const auto& per : pool->value_rows) for (int64_t n : per) v += (uint64_t)n * dkv;
   if (pool->lr_sets() > 0)
     for (const auto& per : pool->lr_rows) for (int64_t n : per) l += (uint64_t)n * r;
+  for (int64_t n : pool->lk_rows) l += (uint64_t)n * (uint64_t)pool->dims.rank_k;     // key-side low-rank rows count as low-rank bytes
   out[0] = k * sz; out[1] = v * sz; out[2] = l * sz;
   out[3] = (uint64_t)pool->hidden_rows * (uint64_t)pool->dims.d_model * sz;
   return LORAKV_OK;
@@ -1064,7 +1099,7 @@ int lorakv_pool_page_table(const lorakv_pool* pool, int which, int64_t agent, in
   int64_t set; bool none;
   LK_TRY(resolve(pool, which, 0, agent, &set, &none));
   if (none) { if (n_pages) *n_pages = 0; return LORAKV_OK; }
-  const auto& tab = (which == LORAKV_LR ? pool->lr_space : pool->kv_space).table[(size_t)set];
+  const auto& tab = (which == LORAKV_LR ? pool->lr_space : which == LORAKV_LK ? pool->lk_space : pool->kv_space).table[(size_t)set];
   if (n_pages) *n_pages = (int64_t)tab.size();
   for (int64_t i = 0; i < cap && i < (int64_t)tab.size(); ++i) out[i] = tab[(size_t)i];
   return LORAKV_OK;
@@ -1115,6 +1150,8 @@ void lorakv_adapters_destroy(lorakv_adapters* ad) {
   if (ad->a_agent) cudaFree(ad->a_agent);
   if (ad->b) cudaFree(ad->b);
   if (ad->scale) cudaFree(ad->scale);
+  for (float* q : {ad->a_k, ad->b_k, ad->scale_k})
+    if (q) cudaFree(q);
   delete ad;
 }
 
@@ -1165,6 +1202,91 @@ int lorakv_adapters_set_b(lorakv_adapters* ad, int64_t layer, int64_t agent, con
                           sizeof(float), cudaMemcpyHostToDevice, ad->ctx->stream));
   LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
   ad->b_set[(size_t)(layer * ad->n_agents + agent)] = 1;
+  return LORAKV_OK;
+}
+
+// ---- key-side adapter tables (extension; kernels.hpp: KeyLowRank) ------------------------------------------------------
+int lorakv_adapters_enable_key(lorakv_adapters* ad, int64_t rank_k) {
+  if (!ad) return fail("null argument");
+  if (rank_k < 1 || rank_k > 64) return fail("LoraAdapter: key rank must be in [1,64], got %lld", (long long)rank_k);
+  if (ad->rank_k == rank_k) return LORAKV_OK;
+  if (ad->rank_k != 0) return fail("adapters: the key-side tables were already created with rank %lld", (long long)ad->rank_k);
+  LK_CUDA(cudaSetDevice(ad->ctx->device));
+  const size_t a_bytes = (size_t)(ad->n_layers * ad->d_model * rank_k) * sizeof(float);
+  const size_t b_bytes = (size_t)(ad->n_layers * ad->n_agents * rank_k * ad->n_kv_local * ad->d_head) * sizeof(float);
+  LK_CUDA(cudaMalloc(&ad->a_k, a_bytes));
+  LK_CUDA(cudaMalloc(&ad->b_k, b_bytes));
+  LK_CUDA(cudaMalloc(&ad->scale_k, (size_t)(ad->n_layers * ad->n_agents) * sizeof(float)));
+  LK_CUDA(cudaMemsetAsync(ad->a_k, 0, a_bytes, ad->ctx->stream));
+  LK_CUDA(cudaMemsetAsync(ad->b_k, 0, b_bytes, ad->ctx->stream));
+  LK_CUDA(cudaMemsetAsync(ad->scale_k, 0, (size_t)(ad->n_layers * ad->n_agents) * sizeof(float), ad->ctx->stream));
+  ad->rank_k = rank_k;
+  ad->scale_k_host.assign((size_t)(ad->n_layers * ad->n_agents), 0.f);
+  ad->a_k_set.assign((size_t)ad->n_layers, 0);
+  ad->b_k_set.assign((size_t)(ad->n_layers * ad->n_agents), 0);
+  return LORAKV_OK;
+}
+
+int lorakv_adapters_set_a_k(lorakv_adapters* ad, int64_t layer, const float* a_k) {
+  if (!ad || !a_k) return fail("null argument");
+  if (ad->rank_k == 0) return fail("adapters: no key-side tables (lorakv_adapters_enable_key)");
+  if (layer < 0 || layer >= ad->n_layers) return fail("layer %lld out of range", (long long)layer);
+  LK_CUDA(cudaSetDevice(ad->ctx->device));
+  LK_CUDA(cudaMemcpyAsync(ad->a_k + layer * ad->d_model * ad->rank_k, a_k, (size_t)(ad->d_model * ad->rank_k) * sizeof(float),
+                          cudaMemcpyHostToDevice, ad->ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
+  ad->a_k_set[(size_t)layer] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_adapters_set_b_k(lorakv_adapters* ad, int64_t layer, int64_t agent, const float* b_k, double alpha_k) {
+  if (!ad || !b_k) return fail("null argument");
+  if (ad->rank_k == 0) return fail("adapters: no key-side tables (lorakv_adapters_enable_key)");
+  if (layer < 0 || layer >= ad->n_layers) return fail("layer %lld out of range", (long long)layer);
+  if (agent < 0 || agent >= ad->n_agents)
+    return fail("agent index %lld out of range [0,%lld)", (long long)agent, (long long)ad->n_agents);
+  const double s = alpha_k / (double)ad->rank_k;
+  if (!(std::isfinite(s) && s > 0.0)) return fail("LoraAdapter: effective scale alpha/rank must be finite and positive");
+  LK_CUDA(cudaSetDevice(ad->ctx->device));
+  const int64_t dkv_full = ad->n_kv_heads * ad->d_head, dkv = ad->n_kv_local * ad->d_head;
+  const size_t la = (size_t)(layer * ad->n_agents + agent);
+  float* dst = ad->b_k + (la * ad->rank_k) * dkv;
+  LK_CUDA(cudaMemcpy2DAsync(dst, dkv * sizeof(float), b_k + ad->kv_head_begin * ad->d_head, dkv_full * sizeof(float),
+                            dkv * sizeof(float), ad->rank_k, cudaMemcpyHostToDevice, ad->ctx->stream));
+  ad->scale_k_host[la] = (float)s;
+  LK_CUDA(cudaMemcpyAsync(ad->scale_k + la, &ad->scale_k_host[la], sizeof(float), cudaMemcpyHostToDevice, ad->ctx->stream));
+  LK_CUDA(cudaStreamSynchronize(ad->ctx->stream));
+  ad->b_k_set[la] = 1;
+  return LORAKV_OK;
+}
+
+int lorakv_pool_append_lk_project(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer, int64_t row_begin, const float* x,
+                                  int64_t n_rows, int64_t ld, int mem_kind, int64_t* appended) {
+  if (!pool || !ad) return fail("null argument");
+  if (appended) *appended = 0;
+  if (pool->dims.dtype == LORAKV_F64) return fail("lk_append_project: fp64 pools are storage only");
+  int64_t set; bool none;
+  LK_TRY(resolve(pool, LORAKV_LK, layer, 0, &set, &none));
+  if (ad->rank_k != pool->dims.rank_k || ad->d_model != pool->dims.d_model || layer >= ad->n_layers)
+    return fail("lk_append_project: adapter table does not match the pool (key rank %lld vs %lld)", (long long)ad->rank_k,
+                (long long)pool->dims.rank_k);
+  if (!ad->a_k_set[(size_t)layer]) return fail("lk_append_project: A_k of layer %lld was never uploaded", (long long)layer);
+  if (n_rows < 0) return fail("append: negative row count");
+  int64_t& have = pool->lk_rows[(size_t)layer];
+  int64_t skip, add;
+  LK_TRY(fww("key-lr", have, row_begin, n_rows, &skip, &add));
+  if (add == 0) return LORAKV_OK;
+  if (!x) return fail("append: null rows");
+  lorakv_ctx* ctx = pool->ctx;
+  LK_CUDA(cudaSetDevice(ctx->device));
+  LK_TRY(ensure_pages(pool, pool->lk_space, 0, have + add));
+  const float* dev; int64_t dev_ld;
+  LK_TRY(stage_rows(ctx, x + skip * ld, add, pool->dims.d_model, ld, mem_kind, &dev, &dev_ld));
+  LK_TRY(launch_lr_project(pool, ad->a_k + layer * ad->d_model * ad->rank_k, ad->d_model, ad->rank_k, layer, 0, have, dev, add, dev_ld,
+                           LORAKV_LK));
+  if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  have += add;
+  if (appended) *appended = add;
   return LORAKV_OK;
 }
 
@@ -1262,6 +1384,21 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
     q_dev = qd;
   }
 
+  // key-side low-rank term: every layer's L_k must have caught up, the agents' B_k must be there; the queries are projected
+  // through B_k once (r_k numbers per row and head) before the attention kernel
+  if (pool->rk_pad > 0) {
+    if (!ad || ad->rank_k != pool->dims.rank_k)
+      return fail("attention: the pool keeps a rank-%lld key-side cache but the adapter tables carry key rank %lld", (long long)pool->dims.rank_k,
+                  (long long)(ad ? ad->rank_k : 0));
+    for (int64_t l = layer_begin; l < layer_end; ++l) {
+      if (pool->lk_rows[(size_t)l] != L)
+        return fail("attention: l_k has %lld rows, k has %lld (layer %lld)", (long long)pool->lk_rows[(size_t)l], (long long)L, (long long)l);
+      for (int64_t i = 0; i < n_batch; ++i)
+        if (!ad->b_k_set[(size_t)(l * ad->n_agents + ids_host[(size_t)i])])
+          return fail("attention: B_k of layer %lld agent %d was never uploaded", (long long)l, ids_host[(size_t)i]);
+    }
+  }
+
   PagedAttnCall call;
   call.pool = pool; call.adapters = ad; call.layer_begin = layer_begin; call.layer_end = layer_end;
   call.kv_set = kv_set; call.lr_set = lr_set; call.agent_ids_dev = ids_dev; call.n_batch = n_batch;
@@ -1270,6 +1407,11 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   call.agent_host = ids_host[0];
   call.peers = peers;
   call.per_entry_lr = per_entry_lr;
+  if (pool->rk_pad > 0) {
+    LK_TRY(scratch_reserve(ctx, ctx->qk, (size_t)(n_layers * n_batch * rows_per_entry * n_q_local * pool->rk_pad) * sizeof(float)));
+    LK_TRY(launch_qk_project(call, static_cast<float*>(ctx->qk.ptr)));
+    call.qk_dev = static_cast<const float*>(ctx->qk.ptr);
+  }
   bool rows_at_peers = false;    // the decode kernels' merge epilogue stores straight into the gather buffers
   if (per_entry_lr) {
     if (ctx->policy == 1 || !decode_tma_per_entry_lr_supported(call))
@@ -1415,7 +1557,7 @@ int lorakv_step_layer(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_ada
   // the fused path wants fresh rows only (every cache of the step ends exactly at row_begin): the decode case
   const bool fresh = pool->key_rows[(size_t)kv_set][(size_t)layer] == row_begin && pool->value_rows[(size_t)kv_set][(size_t)layer] == row_begin &&
                      (!lr_cached || pool->lr_rows[(size_t)lr_set][(size_t)layer] == row_begin);
-  const bool fast = mem_kind == LORAKV_DEVICE && ctx->policy != 1 && fresh && pr->fused && pr->q_fused &&
+  const bool fast = mem_kind == LORAKV_DEVICE && ctx->policy != 1 && fresh && pr->fused && pr->q_fused && pool->rk_pad == 0 &&
                     pool->dims.dtype == LORAKV_BF16 && step_layer_supported(n_rows, pr->d_model, pr->d_head, r_q, r_v) &&
                     n_q_heads == pr->n_q_heads && layer < pr->n_layers && pr->set[(size_t)layer] && pr->q_set[(size_t)layer];
   const int64_t group = pr->n_kv_heads > 0 ? n_q_heads / pr->n_kv_heads : 0;
@@ -1425,6 +1567,10 @@ int lorakv_step_layer(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_ada
     if (merge_v) LK_TRY(lorakv_pool_append_kv_project_full(pool, pr, ad, layer, agent, row_begin, x, n_rows, ld, mem_kind, rope, &added));
     else LK_TRY(lorakv_pool_append_kv_project(pool, pr, layer, agent, row_begin, x, n_rows, ld, mem_kind, rope, &added));
     if (lr_cached) LK_TRY(lorakv_pool_append_lr_project(pool, ad, layer, agent, row_begin, x, n_rows, ld, mem_kind, &added));
+    if (pool->rk_pad > 0) {      // key-side low-rank cache (extension): L_k rows = x A_k
+      if (!ad) return fail("step_layer: the pool keeps a key-side low-rank cache but no adapter tables were given");
+      LK_TRY(lorakv_pool_append_lk_project(pool, ad, layer, row_begin, x, n_rows, ld, mem_kind, &added));
+    }
     float* q = q_scratch;
     std::vector<float> q_host;
     if (!q) {
@@ -1432,7 +1578,7 @@ int lorakv_step_layer(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_ada
       else { LK_TRY(scratch_reserve(ctx, ctx->qrows, (size_t)(n_rows * dq) * sizeof(float))); q = static_cast<float*>(ctx->qrows.ptr); }
     }
     LK_TRY(lorakv_proj_query(const_cast<lorakv_proj*>(pr), layer, q_lora ? agent : -1, row_begin, x, n_rows, ld, rope, q, mem_kind));
-    return lorakv_fla_prefill(pool, lr_cached ? ad : nullptr, layer, agent, n_q_heads, q, n_rows, row_begin, out, mem_kind);
+    return lorakv_fla_prefill(pool, (lr_cached || pool->rk_pad > 0) ? ad : nullptr, layer, agent, n_q_heads, q, n_rows, row_begin, out, mem_kind);
   }
   // ---- fused path ----
   if (pr->d_model != pool->dims.d_model || pr->n_kv_heads != pool->dims.n_kv_heads || pr->d_head != pool->dims.d_head ||

@@ -371,6 +371,14 @@ PageAddr make_addr(const lorakv_pool* pool, int which, int64_t layer, int64_t se
     a.width = (int)pool->dims.d_model;
     a.n_heads = 1;
     a.src_cols = (int)pool->dims.d_model;
+  } else if (which == LORAKV_LK) {       // key-side low-rank cache: layer-wide like the shared V_lr cache
+    a.base = static_cast<char*>(pool->lk_pages) + layer * pool->lk_layer_stride() * elem;
+    a.table = pool->lk_space.dev_table;
+    a.head_stride = 0;
+    a.page_stride = pool->lk_page_stride();
+    a.width = (int)pool->rk_pad;
+    a.n_heads = 1;
+    a.src_cols = (int)pool->dims.rank_k;
   } else if (which == LORAKV_LR) {
     a.base = static_cast<char*>(pool->lr_pages) + layer * pool->lr_layer_stride() * elem;
     a.table = pool->lr_space.dev_table + set * pool->lr_space.max_pages;
@@ -465,17 +473,17 @@ int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_
 }
 
 int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set,
-                      int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld) {
+                      int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld, int which) {
   if (n_rows == 0) return LORAKV_OK;
   lorakv_ctx* ctx = pool->ctx;
-  const PageAddr a = make_addr(pool, LORAKV_LR, layer, set);
+  const PageAddr a = make_addr(pool, which, layer, set);
   if (a.width == 0) return LORAKV_OK;
   if (a.width > 128) return fail("lr_append_project: rank %lld > 128 is not supported", (long long)pool->dims.rank);
   const float* A = a_dev;
   const bool bf16 = pool->dims.dtype == LORAKV_BF16;
   const bool vec_ok = (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(x_dev) & 15) == 0);
   // a decode step's handful of rows: one CTA per row streams A (rows_project.cu) instead of a latency-bound MMA tile
-  if (bf16 && ctx->policy != 1 && rows_project_supported(n_rows, d_model, rank) && a.width <= 64 && a.lay.bw == a.width && a.width % 8 == 0) {
+  if (which == LORAKV_LR && bf16 && ctx->policy != 1 && rows_project_supported(n_rows, d_model, rank) && a.width <= 64 && a.lay.bw == a.width && a.width % 8 == 0) {
     LK_TRY(launch_rows_lr_project(pool, A, d_model, rank, layer, set, row0, x_dev, n_rows, ld));
     return LORAKV_OK;
   }

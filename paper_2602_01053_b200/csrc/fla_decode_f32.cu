@@ -663,6 +663,7 @@ int launch_rp(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t 
 
 bool decode_f32_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
+  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
   const int64_t d = pool->dims.d_head, rp = pool->r_pad;
   if (pool->dims.dtype != LORAKV_F32) return false;
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1) return false;   // decode only
@@ -733,6 +734,7 @@ int launch_decode_f32(const PagedAttnCall& c) {
 
 bool prefill_f32_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
+  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
   const int64_t d = pool->dims.d_head, rp = pool->r_pad;
   if (pool->dims.dtype != LORAKV_F32) return false;
   if (c.n_batch != 1 || c.rows_per_entry < 2 || c.layer_end - c.layer_begin != 1) return false;   // prefill blocks only

@@ -889,6 +889,7 @@ bool decode_tma_per_entry_lr_supported(const PagedAttnCall& c) {
 
 bool decode_tma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
+  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
   const int64_t d = pool->dims.d_head, rp = pool->r_pad;
   if (pool->dims.dtype != LORAKV_BF16) return false;       // fp32 pages keep the 1e-4 contract on FFMA
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1) return false;   // decode only

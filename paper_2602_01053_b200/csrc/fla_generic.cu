@@ -50,6 +50,10 @@ struct GenericArgs {
   int64_t chunk;                         // keys per split (multiple of 32)
   T* part;                               // [heads][Lc][splits][2 + d + r + (extra ? d : 0)]
   int64_t part_stride;
+  // key-side low-rank term (an extension the reference does not have, see KeyLowRank in kernels.hpp):
+  // score = (q . k_base[j] + qk . l_k[j]) / sqrt(d), qk = k_scale * (q B_k^T) computed once per (row, head)
+  const T *lk, *qk;                      // L x r_k; [Lc][heads][r_k]; null when r_k == 0
+  int64_t r_k;
 };
 
 // Stage 1: one warp per (query row, q head, key split); lanes own keys for the scores and
@@ -58,7 +62,8 @@ struct GenericArgs {
 template <class T, bool kExtra>
 __global__ void __launch_bounds__(kWarps * 32) fla_generic_partial(GenericArgs<T> a) {
   extern __shared__ unsigned char smem_raw[];
-  T* q_s = reinterpret_cast<T*>(smem_raw) + (threadIdx.x / 32) * a.d;
+  T* q_s = reinterpret_cast<T*>(smem_raw) + (threadIdx.x / 32) * (a.d + a.r_k);
+  T* qk_s = q_s + a.d;
   const int lane = threadIdx.x & 31;
   const int64_t i = (int64_t)blockIdx.x * kWarps + threadIdx.x / 32;
   const int h = blockIdx.y, split = blockIdx.z;
@@ -66,6 +71,7 @@ __global__ void __launch_bounds__(kWarps * 32) fla_generic_partial(GenericArgs<T
   const int kvh = h / a.group;
   const T* q_row = a.q + i * a.ldq + (int64_t)h * a.d;
   for (int64_t c = lane; c < a.d; c += 32) q_s[c] = q_row[c];
+  for (int64_t c = lane; c < a.r_k; c += 32) qk_s[c] = a.qk[(i * a.n_heads + h) * a.r_k + c];
   __syncwarp();
 
   const T* k_base = a.k + (int64_t)kvh * a.d;
@@ -99,6 +105,10 @@ __global__ void __launch_bounds__(kWarps * 32) fla_generic_partial(GenericArgs<T
       const T* k_row = k_base + j * a.ldk;
       T dot = T(0);
       for (int64_t c = 0; c < a.d; ++c) dot += q_s[c] * k_row[c];
+      if (a.r_k > 0) {
+        const T* lk_row = a.lk + j * a.r_k;
+        for (int64_t c = 0; c < a.r_k; ++c) dot += qk_s[c] * lk_row[c];
+      }
       s = dot * inv_sqrt_d;
     }
     const T tile_max = warp_max(s);
@@ -237,6 +247,21 @@ __global__ void __launch_bounds__(128) fla_generic_merge(MergeArgs<T> a) {
 }
 
 // expanded[j, c] = lr_scale * sum_p v_lr[j,p] * b_up[p,c]   (attention.hpp:281-285)
+// qk[i][h][p] = k_scale * sum_c q[i][h d + c] * b_k[p][kvh d + c]: the query seen through the key adapter, r_k numbers per
+// (row, head), so that the full-width adapter keys k_scale * L_k B_k are never formed
+template <class T>
+__global__ void qk_generic_kernel(const T* q, int64_t ldq, const T* bk, int64_t ldbk, T k_scale, int64_t Lc, int n_heads, int group,
+                                  int64_t d, int64_t r_k, T* qk) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Lc * n_heads * r_k) return;
+  const int64_t p = idx % r_k, h = (idx / r_k) % n_heads, i = idx / (r_k * n_heads);
+  const T* q_row = q + i * ldq + h * d;
+  const T* b_row = bk + p * ldbk + (h / group) * d;
+  T acc = T(0);
+  for (int64_t c = 0; c < d; ++c) acc += q_row[c] * b_row[c];
+  qk[idx] = k_scale * acc;
+}
+
 template <class T>
 __global__ void expand_lr_kernel(const T* vlr, int64_t ldlr, const T* b, int64_t ldb, T scale,
                                  int64_t L, int64_t width, int64_t r, T* out) {
@@ -343,9 +368,13 @@ template <class T>
 int generic_forward(lorakv_ctx* ctx, const char* op, int mode, const T* q, int64_t ldq, const T* k,
                     int64_t ldk, const T* v, int64_t ldv, const T* vlr, int64_t ldlr, const T* b,
                     int64_t ldb, T lr_scale, int64_t Lc, int64_t L, int n_q, int n_kv, int64_t d,
-                    int64_t r, int64_t off, T* out, T* row_max, T* row_denom) {
+                    int64_t r, int64_t off, T* out, T* row_max, T* row_denom, const KeyLowRank<T>* key) {
   if (!ctx) return fail("%s: null context", op);
   LK_TRY(check_shapes<T>(op, Lc, L, d, r, off));
+  const int64_t r_k = key ? key->r_k : 0;
+  if (r_k < 0 || r_k > 128) return fail("%s: key rank %lld outside [0,128]", op, (long long)r_k);
+  if (r_k > 0 && (!key->l_k || !key->b_k)) return fail("%s: key-side low-rank operands are null", op);
+  if (r_k > 0 && mode == 1) return fail("expand_first_attention has no key-side low-rank variant");
   if (Lc == 0) return LORAKV_OK;
   LK_CUDA(cudaSetDevice(ctx->device));
   const int group = n_q / n_kv;
@@ -361,7 +390,10 @@ int generic_forward(lorakv_ctx* ctx, const char* op, int mode, const T* q, int64
   size_t off_out = align_up(off_ex + (extra ? L * wkv * sizeof(T) : 0), 256);
   size_t off_st = align_up(off_out + Lc * wq * sizeof(T), 256);
   size_t off_flag = align_up(off_st + 2 * n_q * Lc * sizeof(T), 256);
-  size_t total = off_flag + 256;
+  size_t off_lk = align_up(off_flag + 256, 256);
+  size_t off_bk = align_up(off_lk + L * r_k * sizeof(T), 256);
+  size_t off_qk = align_up(off_bk + r_k * wkv * sizeof(T), 256);
+  size_t total = off_qk + Lc * n_q * r_k * sizeof(T) + 256;
   LK_TRY(scratch_reserve(ctx, ctx->in, total));
   char* base = static_cast<char*>(ctx->in.ptr);
   T* dq = reinterpret_cast<T*>(base + off_q);
@@ -382,6 +414,16 @@ int generic_forward(lorakv_ctx* ctx, const char* op, int mode, const T* q, int64
   }
   const int init_flag = 0x7fffffff;
   LK_CUDA(cudaMemcpyAsync(dflag, &init_flag, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  T* dlk = reinterpret_cast<T*>(base + off_lk);
+  T* dbk = reinterpret_cast<T*>(base + off_bk);
+  T* dqk = reinterpret_cast<T*>(base + off_qk);
+  if (r_k > 0) {
+    LK_TRY(upload2d(ctx, dlk, key->l_k, L, r_k, key->ld_lk));
+    LK_TRY(upload2d(ctx, dbk, key->b_k, r_k, wkv, key->ld_bk));
+    const int64_t n = Lc * n_q * r_k;
+    qk_generic_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(dq, wq, dbk, wkv, key->k_scale, Lc, n_q, group, d, r_k, dqk);
+    ctx->launches++;
+  }
 
   if (extra) {
     const int64_t n = L * wkv;
@@ -414,8 +456,9 @@ int generic_forward(lorakv_ctx* ctx, const char* op, int mode, const T* q, int64
   ga.Lc = Lc; ga.L = L; ga.d = d; ga.r = r_part; ga.query_offset = off;
   ga.n_heads = n_q; ga.group = group; ga.splits = splits; ga.chunk = chunk;
   ga.part = static_cast<T*>(ctx->work.ptr); ga.part_stride = part_stride;
+  ga.lk = r_k > 0 ? dlk : nullptr; ga.qk = r_k > 0 ? dqk : nullptr; ga.r_k = r_k;
   dim3 grid((unsigned)((Lc + kWarps - 1) / kWarps), (unsigned)n_q, (unsigned)splits);
-  const size_t smem = kWarps * d * sizeof(T);
+  const size_t smem = kWarps * (d + r_k) * sizeof(T);
   if (extra) fla_generic_partial<T, true><<<grid, kWarps * 32, smem, ctx->stream>>>(ga);
   else fla_generic_partial<T, false><<<grid, kWarps * 32, smem, ctx->stream>>>(ga);
   ctx->launches++;
@@ -498,11 +541,11 @@ int naive_forward(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t 
 template int generic_forward<float>(lorakv_ctx*, const char*, int, const float*, int64_t, const float*,
                                     int64_t, const float*, int64_t, const float*, int64_t, const float*,
                                     int64_t, float, int64_t, int64_t, int, int, int64_t, int64_t, int64_t,
-                                    float*, float*, float*);
+                                    float*, float*, float*, const KeyLowRank<float>*);
 template int generic_forward<double>(lorakv_ctx*, const char*, int, const double*, int64_t, const double*,
                                      int64_t, const double*, int64_t, const double*, int64_t,
                                      const double*, int64_t, double, int64_t, int64_t, int, int, int64_t,
-                                     int64_t, int64_t, double*, double*, double*);
+                                     int64_t, int64_t, double*, double*, double*, const KeyLowRank<double>*);
 template int naive_forward<float>(lorakv_ctx*, const float*, int64_t, const float*, int64_t, const float*,
                                   int64_t, const float*, int64_t, const float*, int64_t, float, int64_t,
                                   int64_t, int64_t, int64_t, int64_t, float*);

@@ -43,6 +43,9 @@ struct SimtParams {
   const float* q;                           // [layers][n_batch][rows_per_entry][n_q_local*d]
   float* part;                              // [layers][kv heads][rows_total][splits][2 + d + r_pad]
   int64_t part_stride;
+  // key-side low-rank term: the head dimension is extended by rk_pad columns -- q' = [q | qk], K' tile = [K_base | L_k]
+  const void* lk_pages; const int32_t* lk_table; int64_t lk_layer_stride, lk_page_stride; int rk_pad; PageLayout lk_lay;
+  const float* qk;                          // [layers][n_batch][rows_per_entry][n_q_local][rk_pad]
 };
 
 template <class S> struct Elem;
@@ -81,11 +84,12 @@ __device__ __forceinline__ float wsum(float v) {
 template <class S, int RW, int QD>
 __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int d = p.d, rp = p.r_pad;
-  const int kd = d + 4, kr = rp + 4;             // padded pitches (floats): conflict-free LDS.128
-  float* q_s = reinterpret_cast<float*>(smem_raw);          // [8*RW][d]
-  float* k_s = q_s + 8 * RW * d;                            // [kTile][kd]
-  float* v_s = k_s + kTile * kd;                            // [kTile][kd]
+  const int d = p.d, rp = p.r_pad, rk = p.rk_pad;
+  const int dx = d + rk;                         // extended head dimension of the score product
+  const int kd = d + 4, kr = rp + 4, kx = dx + 4;   // padded pitches (floats): conflict-free LDS.128
+  float* q_s = reinterpret_cast<float*>(smem_raw);          // [8*RW][dx]
+  float* k_s = q_s + 8 * RW * dx;                           // [kTile][kx]
+  float* v_s = k_s + kTile * kx;                            // [kTile][kd]
   float* lr_s = v_s + kTile * kd;                           // [kTile][kr]
   float* p_s = lr_s + kTile * kr;                           // [8*RW][kTile]
 
@@ -122,7 +126,17 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
                                 (int64_t)kvh * p.group + gi) * d;
       v = *reinterpret_cast<const float4*>(src + 4 * c4);
     }
-    *reinterpret_cast<float4*>(q_s + lr_ * d + 4 * c4) = v;
+    *reinterpret_cast<float4*>(q_s + lr_ * dx + 4 * c4) = v;
+  }
+  for (int idx = tid; idx < 8 * RW * (rk / 4); idx += kThreads) {      // qk = k_scale * (q B_k^T), columns [d, d + rk)
+    const int lr_ = idx / (rk / 4), c4 = idx % (rk / 4);
+    const int64_t rho = rho0 + lr_;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rho < p.rows_total) {
+      const int64_t gi = rho % p.group, et = rho / p.group;
+      v = *reinterpret_cast<const float4*>(p.qk + ((layer_rel * p.n_batch * p.rows_per_entry + et) * n_q_local + (int64_t)kvh * p.group + gi) * rk + 4 * c4);
+    }
+    *reinterpret_cast<float4*>(q_s + lr_ * dx + d + 4 * c4) = v;
   }
 
   float o[RW][QD][4], olr[RW][4], m_run[RW], l_run[RW];
@@ -154,8 +168,9 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
   const S* kp = static_cast<const S*>(p.k_pages) + layer * p.kv_layer_stride + (int64_t)kvh * p.kv_head_stride;
   const S* vp = static_cast<const S*>(p.v_pages) + layer * p.kv_layer_stride + (int64_t)kvh * p.kv_head_stride;
   const S* lp = rp > 0 ? static_cast<const S*>(p.lr_pages) + layer * p.lr_layer_stride : nullptr;
+  const S* lkp = rk > 0 ? static_cast<const S*>(p.lk_pages) + layer * p.lk_layer_stride : nullptr;
   constexpr int EPC = Elem<S>::kPerChunk;
-  const int kv_chunks = d / EPC, lr_chunks = rp / EPC;
+  const int kv_chunks = d / EPC, lr_chunks = rp / EPC, lk_chunks = rk / EPC;
 
   for (int64_t j0 = j_begin; j0 < j_end; j0 += kTile) {
     __syncthreads();   // previous tile fully consumed (also orders the q_s staging on iteration 0)
@@ -175,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
       }
 #pragma unroll
       for (int u = 0; u < EPC; u += 4) {
-        *reinterpret_cast<float4*>(k_s + jj * kd + c * EPC + u) = make_float4(tmp_k[u], tmp_k[u + 1], tmp_k[u + 2], tmp_k[u + 3]);
+        *reinterpret_cast<float4*>(k_s + jj * kx + c * EPC + u) = make_float4(tmp_k[u], tmp_k[u + 1], tmp_k[u + 2], tmp_k[u + 3]);
         *reinterpret_cast<float4*>(v_s + jj * kd + c * EPC + u) = make_float4(tmp_v[u], tmp_v[u + 1], tmp_v[u + 2], tmp_v[u + 3]);
       }
     }
@@ -194,18 +209,33 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
       for (int u = 0; u < EPC; u += 4)
         *reinterpret_cast<float4*>(lr_s + jj * kr + c * EPC + u) = make_float4(tmp[u], tmp[u + 1], tmp[u + 2], tmp[u + 3]);
     }
+    for (int idx = tid; idx < kTile * lk_chunks; idx += kThreads) {       // L_k tile into columns [d, d + rk) of the key tile
+      const int jj = idx / lk_chunks, c = idx % lk_chunks;
+      const int64_t j = j0 + jj;
+      float tmp[EPC];
+      if (j < j_end) {
+        const int64_t phys = p.lk_table[j / p.P];
+        Elem<S>::load_chunk(lkp + phys * p.lk_page_stride + page_offset(p.lk_lay, (int)(j % p.P), c * EPC), tmp);
+      } else {
+#pragma unroll
+        for (int u = 0; u < EPC; ++u) tmp[u] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < EPC; u += 4)
+        *reinterpret_cast<float4*>(k_s + jj * kx + d + c * EPC + u) = make_float4(tmp[u], tmp[u + 1], tmp[u + 2], tmp[u + 3]);
+    }
     __syncthreads();
 
     // ---- scores: lane = key --------------------------------------------------------------
     float dot[RW];
 #pragma unroll
     for (int t = 0; t < RW; ++t) dot[t] = 0.f;
-    const float* k_row = k_s + lane * kd;
-    for (int c = 0; c < d; c += 4) {
+    const float* k_row = k_s + lane * kx;
+    for (int c = 0; c < dx; c += 4) {             // q . K_base[j] + qk . L_k[j]: one product over the extended dimension
       const float4 kv = *reinterpret_cast<const float4*>(k_row + c);
 #pragma unroll
       for (int t = 0; t < RW; ++t) {
-        const float4 qv = *reinterpret_cast<const float4*>(q_s + (warp + 8 * t) * d + c);
+        const float4 qv = *reinterpret_cast<const float4*>(q_s + (warp + 8 * t) * dx + c);
         dot[t] = fmaf(qv.x, kv.x, dot[t]);
         dot[t] = fmaf(qv.y, kv.y, dot[t]);
         dot[t] = fmaf(qv.z, kv.z, dot[t]);
@@ -289,7 +319,48 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
   }
 }
 
+// qk[row][head][p] = scale_k[agent] * sum_c q[row][head d + c] * B_k[agent][p][kvh d + c]; one thread per output, zero padding
+__global__ void qk_project_kernel(const float* __restrict__ q, const float* __restrict__ bk, const float* __restrict__ scale_k,
+                                  const int32_t* __restrict__ agent_ids, int64_t layer_begin, int64_t n_agents, int64_t n_batch,
+                                  int64_t rows_per_entry, int n_q_local, int group, int d, int r_k, int rk_pad, int n_kv_local,
+                                  int64_t total, float* __restrict__ qk) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int p = (int)(idx % rk_pad);
+  const int64_t hrow = idx / rk_pad;                 // (layer, entry, token, head)
+  const int h = (int)(hrow % n_q_local);
+  const int64_t et = hrow / n_q_local;               // layer_rel * n_batch * rows_per_entry + entry * rows_per_entry + token
+  const int64_t layer_rel = et / (n_batch * rows_per_entry);
+  const int64_t entry = (et / rows_per_entry) % n_batch;
+  float acc = 0.f;
+  if (p < r_k) {
+    const int agent = agent_ids ? agent_ids[entry] : 0;
+    const int64_t layer = layer_begin + layer_rel;
+    const float* q_row = q + hrow * d;
+    const float* b_row = bk + (((layer * n_agents + agent) * r_k) + p) * ((int64_t)n_kv_local * d) + (int64_t)(h / group) * d;
+    for (int c = 0; c < d; ++c) acc = fmaf(q_row[c], b_row[c], acc);
+    acc *= scale_k[layer * n_agents + agent];
+  }
+  qk[idx] = acc;
+}
+
 }  // namespace
+
+int launch_qk_project(const PagedAttnCall& c, float* qk_out) {
+  lorakv_pool* pool = c.pool;
+  lorakv_ctx* ctx = pool->ctx;
+  const lorakv_adapters* ad = c.adapters;
+  const int64_t n_layers = c.layer_end - c.layer_begin;
+  const int64_t total = n_layers * c.n_batch * c.rows_per_entry * c.n_q_local * pool->rk_pad;
+  if (total == 0) return LORAKV_OK;
+  const int group = (int)(c.n_q_local / pool->n_kv_local);
+  qk_project_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+      c.q_dev, ad->b_k, ad->scale_k, c.agent_ids_dev, c.layer_begin, ad->n_agents, c.n_batch, c.rows_per_entry, (int)c.n_q_local, group,
+      (int)pool->dims.d_head, (int)pool->dims.rank_k, (int)pool->rk_pad, (int)pool->n_kv_local, total, qk_out);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
 
 // ---- split merge + up-projection epilogue, shared by every paged path --------------------------
 // part: [layers][kv heads][rows_total][splits][4 + d + r_pad]  (slot 0 = m, 1 = l; 2,3 unused so
@@ -369,7 +440,8 @@ int launch_paged_merge(lorakv_ctx* ctx, const MergeParams& mp, int64_t n_layers)
 template <class S, int RW, int QD>
 static int launch_simt_t(lorakv_ctx* ctx, const SimtParams& sp, dim3 grid) {
   const int d = sp.d, rp = sp.r_pad;
-  const size_t smem = sizeof(float) * ((size_t)8 * RW * d + 2 * kTile * (d + 4) + kTile * (rp + 4) + (size_t)8 * RW * kTile);
+  const int rk = sp.rk_pad;
+  const size_t smem = sizeof(float) * ((size_t)8 * RW * (d + rk) + kTile * (d + rk + 4) + kTile * (d + 4) + kTile * (rp + 4) + (size_t)8 * RW * kTile);
   auto kern = fla_paged_simt_kernel<S, RW, QD>;
   LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   prof_mark(ctx, 0);
@@ -435,6 +507,11 @@ int launch_paged_simt(const PagedAttnCall& c) {
   sp.n_batch = c.n_batch; sp.rows_per_entry = c.rows_per_entry; sp.query_offset = c.query_offset;
   sp.rows_total = rows_total; sp.splits = splits; sp.chunk = chunk;
   sp.q = c.q_dev; sp.part = static_cast<float*>(ctx->work.ptr); sp.part_stride = part_stride;
+  sp.lk_pages = pool->lk_pages; sp.lk_table = pool->lk_space.dev_table; sp.lk_layer_stride = pool->lk_layer_stride();
+  sp.lk_page_stride = pool->lk_page_stride(); sp.rk_pad = (int)pool->rk_pad;
+  sp.lk_lay = make_page_layout((int)pool->P, (int)std::max<int64_t>(pool->rk_pad, 8), (int)pool->elem);
+  sp.qk = c.qk_dev;
+  if (pool->rk_pad > 0 && !c.qk_dev) return fail("paged attention: the key-side low-rank term needs the projected queries (launch_qk_project)");
   dim3 grid((unsigned)row_blocks, (unsigned)(n_layers * pool->n_kv_local), (unsigned)splits);
   if (pool->dims.dtype == LORAKV_BF16) LK_TRY(launch_simt_s<__nv_bfloat16>(ctx, sp, grid, rw));
   else LK_TRY(launch_simt_s<float>(ctx, sp, grid, rw));

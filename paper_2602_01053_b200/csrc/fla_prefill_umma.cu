@@ -585,6 +585,7 @@ bool umma_shape_ok(const lorakv_pool* pool) {
 
 bool prefill_umma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
+  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
   if (!umma_shape_ok(pool)) return false;
   if (c.n_batch != 1 || c.rows_per_entry < 2 || c.layer_end - c.layer_begin != 1) return false;
   const int64_t group = c.n_q_local / pool->n_kv_local;
@@ -618,6 +619,7 @@ int launch_prefill_umma(const PagedAttnCall& c) {
 // fla_decode_tma.
 bool decode_umma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
+  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
   if (!umma_shape_ok(pool)) return false;
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1 || c.L < 1 || c.n_batch < 1) return false;
   const int64_t rows_total = c.n_batch * (c.n_q_local / pool->n_kv_local);

@@ -11,12 +11,24 @@ struct lorakv_adapters;
 
 namespace lk {
 
+// Key-side low-rank term of the north star: K_eff = K_base + k_scale * L_k B_k with L_k = X A_k (L x r_k, one per layer like
+// V_lr) and B_k (r_k x n_kv d, per agent).  The kernels never form K_eff: q . K_eff[j] = q . K_base[j] + (k_scale q B_k^T) . L_k[j].
+// The reference has no key adapter (engine.hpp:129-130; the paper rules it out under RoPE), so this is an
+// extension whose parity is UNPINNED: the checker materialises K_eff and calls the reference's attention.  r_k = 0 is the reference.
+template <class T>
+struct KeyLowRank {
+  const T* l_k; int64_t ld_lk;     // L x r_k
+  const T* b_k; int64_t ld_bk;     // r_k x (n_kv * d)
+  T k_scale;                       // alpha_k / r_k
+  int64_t r_k;
+};
+
 // fla_generic.cu ------------------------------------------------------------------------------
 template <class T>
 int generic_forward(lorakv_ctx* ctx, const char* op, int mode, const T* q, int64_t ldq, const T* k,
                     int64_t ldk, const T* v, int64_t ldv, const T* vlr, int64_t ldlr, const T* b,
                     int64_t ldb, T lr_scale, int64_t Lc, int64_t L, int n_q, int n_kv, int64_t d,
-                    int64_t r, int64_t off, T* out, T* row_max, T* row_denom);
+                    int64_t r, int64_t off, T* out, T* row_max, T* row_denom, const KeyLowRank<T>* key = nullptr);
 template <class T>
 int naive_forward(lorakv_ctx* ctx, const T* q, int64_t ldq, const T* k, int64_t ldk, const T* v,
                   int64_t ldv, const T* vlr, int64_t ldlr, const T* b, int64_t ldb, T lr_scale,
@@ -35,8 +47,9 @@ int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t s
 int launch_append_scatter(lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                           const double* src_dev, int64_t n_rows, int64_t ld);          // fp64 pools
 // V_lr rows = X * A for one layer, written into the LR pages of `set` from logical row `row0`.
+// (which = LORAKV_LK writes L_k = X * A_k into the key-side low-rank pages instead)
 int launch_lr_project(lorakv_pool* pool, const float* a_dev, int64_t d_model, int64_t rank, int64_t layer, int64_t set,
-                      int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld);
+                      int64_t row0, const float* x_dev, int64_t n_rows, int64_t ld, int which = LORAKV_LR);
 // De-paginate rows [row0, row0+n_rows) into a dense float32 device matrix.
 int launch_gather_rows(const lorakv_pool* pool, int which, int64_t layer, int64_t set, int64_t row0,
                        int64_t n_rows, float* dst_dev);
@@ -73,7 +86,12 @@ struct PagedAttnCall {
   // BaseShared batch (kvcache.hpp:127-130, 238-243: shared K / V_base, one V_lr cache PER AGENT): batch entry i reads the
   // low-rank page set agent_ids[i] instead of lr_set, so that K / V_base are still streamed once for the whole batch
   bool per_entry_lr = false;
+  // key-side low-rank term (KeyLowRank above; pool->rk_pad > 0): qk = k_scale * (q B_k[agent]^T) per query row and q head,
+  // [layers][n_batch][rows_per_entry][n_q_local][rk_pad] float32 (zero-padded), written by launch_qk_project before the
+  // attention kernel; the kernels add qk . L_k[j] to q . K_base[j]
+  const float* qk_dev = nullptr;
 };
+int launch_qk_project(const PagedAttnCall& call, float* qk_out);
 bool decode_tma_per_entry_lr_supported(const PagedAttnCall& call);
 int launch_paged_simt(const PagedAttnCall& call);
 

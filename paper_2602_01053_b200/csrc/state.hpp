@@ -70,6 +70,7 @@ struct lorakv_ctx {
   const char* last_kernel = "none";
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
   lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection; partial sums of a fused layer-step
+  lk::Scratch qk;                     // queries seen through the key adapter (launch_qk_project)
   lk::Scratch qrows;                  // query rows of a fused layer-step when the caller passes no scratch
   static constexpr int kIdSlots = 8;
   lk::IdSlot id_slots[kIdSlots];
@@ -155,6 +156,14 @@ struct lorakv_pool {
   void* lr_pages = nullptr;  // [n_layers][lr_total_pages][P][r_pad]
   // SelectiveRecompute (kvcache.hpp:53-58, 245-246, 289-305): one hidden-state cache of the trajectory (rows x d_model,
   // paged through the K / V page table) and the layers whose cached rows a returning agent may overwrite
+  // key-side low-rank cache L_k = X A_k (an extension, kernels.hpp: KeyLowRank): one L x rank_k cache per layer shared by
+  // every agent and kv head, laid out like the shared V_lr cache, own page table
+  int64_t rk_pad = 0;                    // row width in HBM (rank_k zero-padded to 16 / 32 / 64); 0: no such cache
+  void* lk_pages = nullptr;              // [n_layers][lk_total_pages][P][rk_pad]
+  lk::PageSpace lk_space;
+  std::vector<int64_t> lk_rows;          // [layer]
+  int64_t lk_page_stride() const { return P * rk_pad; }
+  int64_t lk_layer_stride() const { return lk_space.total_pages() * lk_page_stride(); }
   void* hidden_pages = nullptr;          // [kv_total_pages][P][d_model]
   int64_t hidden_rows = 0;
   std::vector<int64_t> recompute_layers;
@@ -185,6 +194,13 @@ struct lorakv_adapters {
   float* scale = nullptr;  // [n_layers][n_agents] device copy of alpha/rank
   std::vector<float> scale_host;
   std::vector<uint8_t> a_set, b_set, a_agent_set;
+  // key-side adapter (extension): shared down-projection A_k per layer, B_k and alpha_k / rank_k per (layer, agent)
+  int64_t rank_k = 0;
+  float* a_k = nullptr;      // [n_layers][d_model][rank_k]
+  float* b_k = nullptr;      // [n_layers][n_agents][rank_k][n_kv_local*d_head]
+  float* scale_k = nullptr;  // [n_layers][n_agents]
+  std::vector<float> scale_k_host;
+  std::vector<uint8_t> a_k_set, b_k_set;
 };
 
 // End-of-step output gather of a kv-head-sharded run over peer memory (peer_gather.cu).  Every rank owns one

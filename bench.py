@@ -405,6 +405,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill / TTFT leg")
     ap.add_argument("--policy", type=int, default=0, help="0 auto (tcgen05 where supported), 1 CUDA-core kernels")
+    ap.add_argument("--rank-k", type=int, default=0,
+                    help="key-side low-rank term (extension, parity unpinned): adds an L x rank_k cache L_k per layer and per-agent B_k; "
+                         "0 = the reference's operator (the BASELINE configuration)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -450,9 +453,20 @@ def main():
     assert stream.cuda_stream != 0
     ctx = pkg.Context(local_rank, stream=stream.cuda_stream)
     ctx.set_kernel_policy(args.policy)
+    r_k = args.rank_k
     pool = pkg.Pool(ctx, "BaseLRShared", n_layers, n_kv, d, d_model, r, A, max_tokens=L, dtype=dtype,
-                    kv_head_begin=kv_begin, n_kv_local=n_kv_local)
+                    kv_head_begin=kv_begin, n_kv_local=n_kv_local, rank_k=r_k)
     ad = pkg.Adapters(ctx, n_layers, A, d_model, r, n_kv, d, kv_head_begin=kv_begin, n_kv_local=n_kv_local, dtype=dtype)
+    if r_k > 0:
+        if args.no_cpu_baseline is False or not args.no_prefill:
+            print("[bench] --rank-k: the parity / prefill legs cover the reference's operator only; run with --no-cpu-baseline --no-prefill",
+                  file=sys.stderr)
+            args.no_cpu_baseline, args.no_prefill = True, True
+        ad.enable_key(r_k)
+        krng = np.random.default_rng(11)
+        for layer in range(n_layers):
+            for a in range(A):
+                ad.set_b_k(layer, a, (krng.standard_normal((r_k, n_kv * d)) * (0.5 / np.sqrt(d))).astype(np.float32), 16.0)
 
     # ---- synthetic cache of the named shape, generated on the device (same seed on every rank so
     # that head shards are slices of one logical cache) ----------------------------------------
@@ -496,6 +510,14 @@ def main():
         for a in range(A):
             b_host[layer][a] = shared_inputs[layer][1][a] if layer in shared_inputs else bf16_round(b_host[layer][a])
             ad.set_b(layer, a, b_host[layer][a], 16.0)
+    if r_k > 0:
+        for layer in range(n_layers):
+            gen.manual_seed(5000 + layer)
+            for c0 in range(0, L, rows_per_chunk):
+                n = min(rows_per_chunk, L - c0)
+                lk = torch.randn((n, r_k), generator=gen, device=dev, dtype=torch.float32)
+                pool.append_device(4, layer, 0, c0, lk.data_ptr(), n, r_k)
+        torch.cuda.synchronize()
     bench_prefill.b_host = b_host
     q_full = bf16_round((host_rng.standard_normal((n_layers, A, n_q * d)).astype(np.float32) * sc))
     for layer, (q_h, _b) in shared_inputs.items():
@@ -707,7 +729,7 @@ def main():
 
     main_kernel = ctx.last_kernel()
     peak, peak_src = load_peaks()
-    alg = algorithmic_bytes(n_layers, n_q, n_kv_local, n_kv, d, r, A, L, e)
+    alg = algorithmic_bytes(n_layers, n_q, n_kv_local, n_kv, d, r, A, L, e) + n_layers * (L * r_k * e + A * r_k * n_kv_local * d * 4)
     alg_launch = alg / n_layers if args.per_layer_launch else alg   # last_kernel_ms covers one launch
     achieved = alg_launch / (kernel_ms * 1e-3) / 1e9
     traffic = None
@@ -721,7 +743,7 @@ def main():
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.dtype if args.dtype != "f32" else "f32", "data": "synthetic",
         "config": {"workload": args.workload, "description": desc, "n_layers": n_layers, "agents": A, "context": L,
-                   "rank": r, "page_tokens": int(pool.dims.page_tokens), "scheme": "BaseLRShared",
+                   "rank": r, "rank_k": r_k, "page_tokens": int(pool.dims.page_tokens), "scheme": "BaseLRShared",
                    "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "launch": "per-layer" if args.per_layer_launch else
                              ("one launch per step over all layers" if launches_per_step == 1 else

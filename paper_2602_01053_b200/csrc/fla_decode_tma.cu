@@ -82,7 +82,11 @@ struct DecodeParams {
   const int32_t* agent_ids;   // [n_batch]
   int lr_max_pages;
   int lr_per_block;           // entries of one row block = V_lr tiles per stage (16 * MW / group)
-  int identity;               // bit 0 / 1: the K-V / V_lr page table is the identity (PageSpace::identity): no table load
+  int identity;               // bit 0 / 1 / 2: the K-V / V_lr / L_k page table is the identity (PageSpace::identity): no table load
+  // key-side low-rank term (template RK > 0; kernels.hpp: KeyLowRank): L_k tiles ride in the stage behind V_lr, the queries
+  // projected through B_k (launch_qk_project) extend the Q fragments, S = Q K^T + Qk L_k^T in the same accumulators
+  const __nv_bfloat16* lk_pages; const int32_t* lk_table; int64_t lk_layer_stride, lk_page_stride;
+  const float* qk;            // [layers][n_batch][n_q_local][RK]
 };
 
 // The cache is streamed exactly once per step, so the copies carry an L2 evict-first policy: the lines
@@ -132,8 +136,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // step, 7.1 TB/s) -- the bulk copies are twice as large and every worker prefetches deeper, and three warps still cover
 // the few MMAs a <= 16-row tile needs.  d_head 64 wants four (three lose there) and the multi-warp workers keep eight warps
 // (fewer lose: cfg 4 with 6 warps 1.87 ms vs 1.41 ms).
-template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps>
+template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps, int RK = 0>
 __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const DecodeParams p) {
+  static_assert(RK == 0 || (MW == 1 && !PA), "the key-side low-rank term is built for single-warp workers");
+  constexpr uint32_t kLkBytes = kKeyStep * KT * RK * 2;
   constexpr int kTK = kKeyStep * KT;                    // keys per tile
   constexpr int kWorkers = NW / MW;
   constexpr int kBlocks = D / 64;                       // 64-column blocks of a K / V page
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   constexpr uint32_t kLrBytes = kTK * RP * 2;
   constexpr int kNO = D / 8, kNL = RP / 8;              // n8 tiles of O and O_lr
   constexpr int PS = 4 + D + RP;                        // floats per partial row
-  const uint32_t kStageBytes = 2 * kKvBytes + (PA ? (uint32_t)p.lr_per_block : 1u) * kLrBytes;
+  const uint32_t kStageBytes = 2 * kKvBytes + (PA ? (uint32_t)p.lr_per_block : 1u) * kLrBytes + kLkBytes;
 
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t full_bar[kWorkers][kMaxStages];
@@ -183,7 +189,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   const int units_per_layer = p.n_kv_local * p.row_blocks;
 
   // page-table window held across the lanes of the producer warp: lane i caches logical page base + i
-  int win_base = -(1 << 30), win_kv = 0, win_lr = 0;
+  int win_base = -(1 << 30), win_kv = 0, win_lr = 0, win_lk = 0;
 
   // Producer cursor.  Everything the per-tile path needs is carried incrementally (unit, tile, page,
   // token, stage, wrap count): the only divisions happen here and at unit changes, never per tile.
@@ -195,15 +201,17 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
     // the stage must have been released by every warp of the worker (a fresh barrier passes the parity-1 wait)
     ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
     if (p_issued == 1) LK_TRACE(11);
-    const bool id_kv = (p.identity & 1) != 0, id_lr = (p.identity & 2) != 0 || RP == 0 || PA;
-    if (!(id_kv && id_lr) && (p_page < win_base || p_page >= win_base + 32)) {
+    const bool id_kv = (p.identity & 1) != 0, id_lr = (p.identity & 2) != 0 || RP == 0 || PA, id_lk = (p.identity & 4) != 0 || RK == 0;
+    if (!(id_kv && id_lr && id_lk) && (p_page < win_base || p_page >= win_base + 32)) {
       win_base = p_page;
       const int pg = p_page + lane;
       if (!id_kv) win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
       if (!id_lr) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
+      if (!id_lk) win_lk = pg < p.n_pages ? p.lk_table[pg] : 0;
     }
     const int phys_kv = id_kv ? p_page : __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
     const int phys_lr = id_lr ? p_page : __shfl_sync(0xffffffffu, win_lr, p_page - win_base);
+    const int phys_lk = id_lk ? p_page : __shfl_sync(0xffffffffu, win_lk, p_page - win_base);
     int pa_entries = 0;         // PA: entries of this row block that exist (the last block may be ragged)
     if (PA) {
       const int e0 = (int)(p_unit % p.row_blocks) * p.lr_per_block;
@@ -235,6 +243,10 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
         // (33 MB at cfg 2) stays in L2 and DRAM serves it once instead of n_kv times.
         bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.lr_policy);
       }
+      if (RK > 0) {     // L_k is per layer like V_lr: every kv head of the layer reads the same tile, so it gets the same L2 hint
+        const int64_t lk_off = layer * p.lk_layer_stride + (int64_t)phys_lk * p.lk_page_stride + (int64_t)p_tok * RK;
+        bulk_g2s(dst + 2 * kKvBytes + kLrBytes, p.lk_pages + lk_off, kLkBytes, &full[p_stage], p.lr_policy);
+      }
     }
     if (p_issued == 1) LK_TRACE(13);
     // advance the cursor
@@ -252,6 +264,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
 
   const float ninf = -std::numeric_limits<float>::infinity();
   uint32_t qa[D / 16][4];
+  uint32_t qka[RK > 0 ? RK / 16 : 1][4];          // the queries through B_k: RK / 16 more k-steps of the score product
   float o[kNO][4];
   float olr[kNL > 0 ? kNL : 1][4];
   float m_used[2], l_run[2];
@@ -283,6 +296,7 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   // bulk copies can be issued while the query loads are in flight: load_q only ISSUES the loads (volatile asm keeps them
   // ahead of the copies in program order), pack_q consumes them.
   float2 qraw[2][D / 16][2];
+  float2 qkraw[2][RK > 0 ? RK / 16 : 1][2];
   auto load_q = [&](int u) {
     const int layer_rel = u / units_per_layer;
     const int kvh = (u / p.row_blocks) % p.n_kv_local;
@@ -302,6 +316,18 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
             asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(src + 16 * kk + 8 * part + 2 * t));
           qraw[h][kk][part] = v;
         }
+      if (RK > 0) {
+        const float* srck = p.qk + (((int64_t)layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * RK;
+#pragma unroll
+        for (int kk = 0; kk < RK / 16; ++kk)
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            float2 v = make_float2(0.f, 0.f);
+            if (real)
+              asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(srck + 16 * kk + 8 * part + 2 * t));
+            qkraw[h][kk][part] = v;
+          }
+      }
     }
   };
   auto pack_q = [&]() {
@@ -311,6 +337,13 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
       for (int kk = 0; kk < D / 16; ++kk) {
         qa[kk][h] = pack_bf16(qraw[h][kk][0].x, qraw[h][kk][0].y);
         qa[kk][2 + h] = pack_bf16(qraw[h][kk][1].x, qraw[h][kk][1].y);
+      }
+      if (RK > 0) {
+#pragma unroll
+        for (int kk = 0; kk < RK / 16; ++kk) {
+          qka[kk][h] = pack_bf16(qkraw[h][kk][0].x, qkraw[h][kk][0].y);
+          qka[kk][2 + h] = pack_bf16(qkraw[h][kk][1].x, qkraw[h][kk][1].y);
+        }
       }
       m_used[h] = ninf; l_run[h] = 0.f;
     }
@@ -385,6 +418,22 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
           ldsm_x4(addr, b0, b1, b2, b3);
           mma_bf16(sc[2 * kt], qa[kk], b0, b1);
           mma_bf16(sc[2 * kt + 1], qa[kk], b2, b3);
+        }
+      }
+      if (RK > 0) {     // + Qk L_k^T: the L_k tile is [keys][RK] with 2 RK-byte rows, swizzled like every narrow page row
+        const uint32_t sLK = sLR + kLrBytes;
+#pragma unroll
+        for (int kk = 0; kk < RK / 16; ++kk) {
+          const int chunk = 2 * kk + (mi & 1);
+#pragma unroll
+          for (int kt = 0; kt < KT; ++kt) {
+            uint32_t off = (uint32_t)(key + 16 * kt) * (2u * RK) + (uint32_t)chunk * 16u;
+            off ^= ((off >> 7) & (uint32_t)(RK / 8 - 1)) << 4;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(sLK + off, b0, b1, b2, b3);
+            mma_bf16(sc[2 * kt], qka[kk], b0, b1);
+            mma_bf16(sc[2 * kt + 1], qka[kk], b2, b3);
+          }
         }
       }
     }
@@ -669,9 +718,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
   }
 }
 
-template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps>
+template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps, int RK = 0>
 int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem) {
-  auto kern = fla_decode_tma_kernel<D, RP, MW, KT, PA, NW>;
+  auto kern = fla_decode_tma_kernel<D, RP, MW, KT, PA, NW, RK>;
   static int attr_device = -1;         // once per instantiation: the attribute call costs more than the launch
   if (attr_device != ctx->device) {
     LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingBudget));
@@ -706,7 +755,9 @@ int launch_rp_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t 
 }
 
 template <int D, int RP>
-int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt) {
+int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt, int rk = 0) {
+  if (rk == 16) return launch_t<D, RP, 1, 2, false, wide_workers(D), 16>(ctx, dp, grid, smem);     // key-side low-rank term:
+  if (rk == 32) return launch_t<D, RP, 1, 2, false, wide_workers(D), 32>(ctx, dp, grid, smem);     // single-warp wide workers only
   if (mw == 1) {
     if (kt == 2) return launch_t<D, RP, 1, 2, false, wide_workers(D)>(ctx, dp, grid, smem);
     return launch_t<D, RP, 1, 1>(ctx, dp, grid, smem);
@@ -726,12 +777,12 @@ int launch_mw(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t sme
 }
 
 template <int D>
-int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt, int rp) {
+int launch_rp(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt, int rp, int rk) {
   switch (rp) {
-    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw, kt);
-    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw, kt);
-    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw, kt);
-    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw, kt);
+    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw, kt, rk);
+    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw, kt, rk);
+    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw, kt, rk);
+    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw, kt, rk);
   }
 }
 
@@ -889,7 +940,10 @@ bool decode_tma_per_entry_lr_supported(const PagedAttnCall& c) {
 
 bool decode_tma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
-  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
+  if (pool->rk_pad > 0) {      // key-side low-rank term: built for the single-warp wide workers (<= 16 query rows per kv head)
+    const int64_t group = pool->n_kv_local > 0 ? c.n_q_local / pool->n_kv_local : 0;
+    if (c.per_entry_lr || c.n_batch * group > 16 || pool->P % (2 * kKeyStep) != 0 || (pool->rk_pad != 16 && pool->rk_pad != 32)) return false;
+  }
   const int64_t d = pool->dims.d_head, rp = pool->r_pad;
   if (pool->dims.dtype != LORAKV_BF16) return false;       // fp32 pages keep the 1e-4 contract on FFMA
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1) return false;   // decode only
@@ -918,7 +972,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const int kt = (!pa && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;
   const int workers_per_cta = (mw == 1 && kt == 2) ? wide_workers(d) : kWarps / mw;
   const int tk = kKeyStep * kt;
-  const uint32_t stage_bytes = tk * (4 * d + 2 * rp * lr_per_block);
+  const int rk = (int)pool->rk_pad;
+  const uint32_t stage_bytes = tk * (4 * d + 2 * rp * lr_per_block + 2 * rk);
   if (pa && (size_t)workers_per_cta * 2 * stage_bytes > (size_t)kRingBudget)
     return fail("decode over per-agent low-rank caches: %d entries x rank %d do not fit two stages per worker", lr_per_block, rp);
   int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
@@ -976,14 +1031,18 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
   dp.lr_tables = pool->lr_space.dev_table; dp.agent_ids = c.agent_ids_dev;
   dp.lr_max_pages = (int)pool->lr_space.max_pages; dp.lr_per_block = lr_per_block;
-  dp.identity = (pool->kv_space.identity(c.kv_set, dp.n_pages) ? 1 : 0) | ((rp > 0 && !pa && pool->lr_space.identity(c.lr_set, dp.n_pages)) ? 2 : 0);
+  dp.identity = (pool->kv_space.identity(c.kv_set, dp.n_pages) ? 1 : 0) | ((rp > 0 && !pa && pool->lr_space.identity(c.lr_set, dp.n_pages)) ? 2 : 0) |
+                ((rk > 0 && pool->lk_space.identity(0, dp.n_pages)) ? 4 : 0);
+  dp.lk_pages = static_cast<const __nv_bfloat16*>(pool->lk_pages); dp.lk_table = pool->lk_space.dev_table;
+  dp.lk_layer_stride = pool->lk_layer_stride(); dp.lk_page_stride = pool->lk_page_stride(); dp.qk = c.qk_dev;
+  if (rk > 0 && !c.qk_dev) return fail("decode: the key-side low-rank term needs the projected queries (launch_qk_project)");
   if (const char* e = std::getenv("LORAKV_NO_PAGE_IDENTITY")) if (e[0] == '1') dp.identity = 0;
   if (pa) {
     dp.lr_policy = ptx::kEvictFirst;     // every V_lr tile is read by one entry's rows of each kv head only
     if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp));
     else LK_TRY(launch_rp_pa<64>(ctx, dp, grid, smem, mw, rp));
-  } else if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp));
-  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp));
+  } else if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp, rk));
+  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp, rk));
 
   LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,
                              T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers, -1,

@@ -19,6 +19,7 @@
 #include "kernels.hpp"
 #include "page_layout.cuh"
 #include "state.hpp"
+#include "umma.cuh"
 
 namespace lk {
 
@@ -319,29 +320,38 @@ __global__ void __launch_bounds__(kThreads) fla_paged_simt_kernel(SimtParams p) 
   }
 }
 
-// qk[row][head][p] = scale_k[agent] * sum_c q[row][head d + c] * B_k[agent][p][kvh d + c]; one thread per output, zero padding
-__global__ void qk_project_kernel(const float* __restrict__ q, const float* __restrict__ bk, const float* __restrict__ scale_k,
-                                  const int32_t* __restrict__ agent_ids, int64_t layer_begin, int64_t n_agents, int64_t n_batch,
-                                  int64_t rows_per_entry, int n_q_local, int group, int d, int r_k, int rk_pad, int n_kv_local,
-                                  int64_t total, float* __restrict__ qk) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int p = (int)(idx % rk_pad);
-  const int64_t hrow = idx / rk_pad;                 // (layer, entry, token, head)
+// qk[row][head][p] = scale_k[agent] * sum_c q[row][head d + c] * B_k[agent][p][kvh d + c], zero-padded to rk_pad columns.
+// One CTA of four warps per (row, head): the query row sits in shared memory, warp w takes p = w, w + 4, ..., its lanes the
+// columns (coalesced B_k rows), a shuffle tree finishes each dot product.
+__global__ void __launch_bounds__(128) qk_project_kernel(const float* __restrict__ q, const float* __restrict__ bk,
+                                                         const float* __restrict__ scale_k, const int32_t* __restrict__ agent_ids,
+                                                         int64_t layer_begin, int64_t n_agents, int64_t n_batch, int64_t rows_per_entry,
+                                                         int n_q_local, int group, int d, int r_k, int rk_pad, int n_kv_local,
+                                                         float* __restrict__ qk) {
+  extern __shared__ float q_s[];                     // [d]
+  const int64_t hrow = blockIdx.x;                   // (layer, entry, token, head)
   const int h = (int)(hrow % n_q_local);
   const int64_t et = hrow / n_q_local;               // layer_rel * n_batch * rows_per_entry + entry * rows_per_entry + token
   const int64_t layer_rel = et / (n_batch * rows_per_entry);
   const int64_t entry = (et / rows_per_entry) % n_batch;
-  float acc = 0.f;
-  if (p < r_k) {
-    const int agent = agent_ids ? agent_ids[entry] : 0;
-    const int64_t layer = layer_begin + layer_rel;
-    const float* q_row = q + hrow * d;
-    const float* b_row = bk + (((layer * n_agents + agent) * r_k) + p) * ((int64_t)n_kv_local * d) + (int64_t)(h / group) * d;
-    for (int c = 0; c < d; ++c) acc = fmaf(q_row[c], b_row[c], acc);
-    acc *= scale_k[layer * n_agents + agent];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ptx::pdl_wait();                                   // q comes from the previous kernel of the stream
+  ptx::pdl_launch_dependents();
+  for (int c = threadIdx.x; c < d; c += 128) q_s[c] = q[hrow * d + c];
+  __syncthreads();
+  const int agent = agent_ids ? agent_ids[entry] : 0;
+  const int64_t layer = layer_begin + layer_rel;
+  const float sc = scale_k[layer * n_agents + agent];
+  for (int p = warp; p < rk_pad; p += 4) {
+    float acc = 0.f;
+    if (p < r_k) {
+      const float* b_row = bk + (((layer * n_agents + agent) * r_k) + p) * ((int64_t)n_kv_local * d) + (int64_t)(h / group) * d;
+      for (int c = lane; c < d; c += 32) acc = fmaf(q_s[c], __ldg(b_row + c), acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    }
+    if (lane == 0) qk[hrow * rk_pad + p] = sc * acc;
   }
-  qk[idx] = acc;
 }
 
 }  // namespace
@@ -351,14 +361,15 @@ int launch_qk_project(const PagedAttnCall& c, float* qk_out) {
   lorakv_ctx* ctx = pool->ctx;
   const lorakv_adapters* ad = c.adapters;
   const int64_t n_layers = c.layer_end - c.layer_begin;
-  const int64_t total = n_layers * c.n_batch * c.rows_per_entry * c.n_q_local * pool->rk_pad;
-  if (total == 0) return LORAKV_OK;
+  const int64_t rows = n_layers * c.n_batch * c.rows_per_entry * c.n_q_local;
+  if (rows == 0) return LORAKV_OK;
   const int group = (int)(c.n_q_local / pool->n_kv_local);
-  qk_project_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
-      c.q_dev, ad->b_k, ad->scale_k, c.agent_ids_dev, c.layer_begin, ad->n_agents, c.n_batch, c.rows_per_entry, (int)c.n_q_local, group,
-      (int)pool->dims.d_head, (int)pool->dims.rank_k, (int)pool->rk_pad, (int)pool->n_kv_local, total, qk_out);
+  const int d = (int)pool->dims.d_head;
+  LK_CUDA(launch_kernel(ctx, qk_project_kernel, dim3((unsigned)rows), dim3(128), (size_t)d * sizeof(float), true, c.q_dev,
+                        (const float*)ad->b_k, (const float*)ad->scale_k, c.agent_ids_dev, c.layer_begin, ad->n_agents, c.n_batch,
+                        c.rows_per_entry, (int)c.n_q_local, group, d, (int)pool->dims.rank_k, (int)pool->rk_pad, (int)pool->n_kv_local,
+                        qk_out));
   ctx->launches++;
-  LK_CUDA(cudaGetLastError());
   return LORAKV_OK;
 }
 

@@ -42,7 +42,7 @@ def test_generic_operator_against_materialised_keys(ctx, orc, dtype, tol, L, L_c
     assert np.array_equal(none, ctx.gqa_attention(q, k, v, v_lr, b_up, 0.25, off, n_q, n_kv))
 
 
-def build(ctx, orc, dtype_name, scheme, n_layers, L, n_q, n_kv, d, r, r_k, A, d_model, seed, P=16):
+def build(ctx, orc, dtype_name, scheme, n_layers, L, n_q, n_kv, d, r, r_k, A, d_model, seed, P=32):
     from paper_2602_01053_b200 import Adapters, Pool, abi
     dt = abi.BF16 if dtype_name == "bf16" else abi.F32
     rnd = orc.round_bf16 if dtype_name == "bf16" else (lambda a: a)
@@ -80,6 +80,16 @@ def test_paged_decode_and_prefill_with_the_key_term(ctx, orc, dtype_name, tol, n
     q = np.stack([np.stack([g(1, n_q * d, 7000 + 10 * l + a, d ** -0.5)[0] for a in range(A)]) for l in range(n_layers)])
     out = pool.decode(ad, 0, n_layers, list(range(A)), n_q, q)
     kernel = ctx.last_kernel()
+    # bf16 pages with <= 16 query rows per kv head: the TMA / tensor-core decode kernel carries the term (one more k block of
+    # the score MMA); everything else runs on the CUDA-core paged kernel
+    assert kernel == ("fla_decode_tma" if dtype_name == "bf16" else "fla_paged_simt")
+    ctx.set_kernel_policy(1)
+    try:
+        cross = pool.decode(ad, 0, n_layers, list(range(A)), n_q, q)
+        assert ctx.last_kernel() == "fla_paged_simt"
+    finally:
+        ctx.set_kernel_policy(0)
+    assert orc.max_rel_error(out.reshape(1, -1), cross.reshape(1, -1)) <= tol
     for l in range(n_layers):
         lay = layers[l]
         for a in range(A):

@@ -540,6 +540,7 @@ def main():
             try:
                 gather = pkg.Gather(ctx, rank, world, n_layers * A * n_q * d)
                 gather.connect(exchange_handles(gather.export(), device=dev))
+                gather.set_overlap(True)      # the handshake of step s runs beside the attention of step s + 1
                 flag = torch.ones(1, device=dev)
             except abi.LorakvError as e_:
                 print(f"[bench] rank {rank}: peer gather unavailable ({e_}); using the NCCL all_gather", file=sys.stderr)

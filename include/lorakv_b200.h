@@ -356,6 +356,13 @@ int lorakv_gather_connect(lorakv_gather* g, const unsigned char* handles);
 /* how long a rank waits for its peers before the step fails instead of hanging (default 20 s) */
 int lorakv_gather_set_timeout_ms(lorakv_gather* g, int64_t ms);
 int lorakv_gather_steps(const lorakv_gather* g, int64_t* steps);
+/* Overlapped handshake (off by default).  On: the handshake kernel of a step runs on a side stream behind that step's
+ * epilogue, so the ctx stream goes straight on with the next step's attention kernel; the library makes the ctx stream
+ * wait for it only before the NEXT step's epilogue stores into the peers' buffers (the reuse guard of the buffer pair).
+ * The gathered rows of a step are then complete on the ctx stream only after lorakv_gather_wait(g): call it before
+ * enqueueing a reader of the pointer lorakv_fla_decode_batched_gather returned (the out_host path does it itself). */
+int lorakv_gather_set_overlap(lorakv_gather* g, int enabled);
+int lorakv_gather_wait(lorakv_gather* g);
 /* synchronises the ctx stream and fails if a handshake enqueued so far timed out */
 int lorakv_gather_check(lorakv_gather* g);
 /* lorakv_fla_decode_batched on this rank's shard, ending in the gather.

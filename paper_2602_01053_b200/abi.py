@@ -140,6 +140,8 @@ SIGNATURES = {
     "lorakv_gather_export": (C.c_int, [_vp, C.POINTER(C.c_ubyte)]),
     "lorakv_gather_connect": (C.c_int, [_vp, C.POINTER(C.c_ubyte)]),
     "lorakv_gather_set_timeout_ms": (C.c_int, [_vp, _i64]),
+    "lorakv_gather_set_overlap": (C.c_int, [_vp, C.c_int]),
+    "lorakv_gather_wait": (C.c_int, [_vp]),
     "lorakv_gather_steps": (C.c_int, [_vp, C.POINTER(_i64)]),
     "lorakv_gather_check": (C.c_int, [_vp]),
     "lorakv_fla_decode_batched_gather": (C.c_int, [_vp, _vp, _vp, _i64, _i64, C.POINTER(C.c_int32), _i64, _i64, _vp, C.c_int, _vp,
@@ -515,6 +517,12 @@ class Gather:
             raise LorakvError(f"gather_connect: {len(blob)} handle bytes for world size {self.world}")
         buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
         _check(self.ctx.lib.lorakv_gather_connect(self.h, buf))
+
+    def set_overlap(self, enabled: bool):
+        _check(self.ctx.lib.lorakv_gather_set_overlap(self.h, 1 if enabled else 0))
+
+    def wait(self):
+        _check(self.ctx.lib.lorakv_gather_wait(self.h))
 
     def set_timeout_ms(self, ms: int):
         _check(self.ctx.lib.lorakv_gather_set_timeout_ms(self.h, ms))

@@ -1493,6 +1493,9 @@ int lorakv_fla_decode_batched_gather(lorakv_pool* pool, const lorakv_adapters* a
   for (int i = 0; i < g->world; ++i) peers.dst[i] = lk::gather_buffer(g, i, epoch);
   peers.n_q_total = n_q_heads;
   peers.q_head_begin = pool->dims.kv_head_begin * (n_q_heads / pool->dims.n_kv_heads);
+  // overlapped handshake: the previous step's handshake still runs beside this step's attention kernel; only the kernel
+  // that stores into the peers' buffers (the reuse of the buffer pair) has to wait for it
+  if (g->overlap && g->sync_pending) { peers.wait_event = g->ev_synced; g->sync_pending = false; }
   LK_TRY(run_paged(pool, ad, layer_begin, layer_end, 0, 0, agent_ids, n_batch, 1, L - 1, n_q_heads, q, nullptr, q_mem_kind, &peers));
   g->epoch = epoch;
   LK_TRY(lk::gather_sync(g));
@@ -1500,6 +1503,7 @@ int lorakv_fla_decode_batched_gather(lorakv_pool* pool, const lorakv_adapters* a
   if (out_dev) *out_dev = mine;
   if (out_host) {
     lorakv_ctx* ctx = pool->ctx;
+    LK_TRY(lk::gather_wait(g));
     LK_CUDA(cudaMemcpyAsync(out_host, mine, (size_t)full * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
     LK_TRY(lk::gather_read_status(g));
     LK_CUDA(cudaStreamSynchronize(ctx->stream));

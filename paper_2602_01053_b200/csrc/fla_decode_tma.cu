@@ -913,6 +913,8 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
     carve_device = ctx->device;
   }
   if (r > 64) return fail("decode merge: rank %d exceeds 64", r);
+  // the output gather's overlapped handshake of the previous step guards the peers' buffers this epilogue stores into
+  if (peers && peers->wait_event) LK_CUDA(cudaStreamWaitEvent(ctx->stream, static_cast<cudaEvent_t>(peers->wait_event), 0));
   // many rows (a whole step per launch): one warp per row, throughput; few rows (a layer per launch) or many splits: one CTA
   // per row, one global round trip
   if (ns_max <= 32 && rp <= 64 && (int64_t)rows_total * n_layers * n_kv_local > 1024) {

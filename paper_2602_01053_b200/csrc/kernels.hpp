@@ -65,6 +65,7 @@ struct PeerOut {
   int n = 0;               // 0: plain local store
   int64_t n_q_total = 0;   // q heads of the full output row
   int64_t q_head_begin = 0;  // first q head this shard owns
+  void* wait_event = nullptr;  // cudaEvent_t the launch stream waits for before the kernel that stores into the peers (or null)
 };
 
 // fla_paged_simt.cu ---------------------------------------------------------------------------

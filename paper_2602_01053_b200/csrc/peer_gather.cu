@@ -80,6 +80,7 @@ int launch_peer_scatter(lorakv_ctx* ctx, const float* slab_dev, int64_t rows, in
   if (n4 == 0) return LORAKV_OK;
   int64_t blocks = (n4 + 255) / 256;
   if (blocks > 4 * ctx->sm_count) blocks = 4 * ctx->sm_count;
+  if (peers.wait_event) LK_CUDA(cudaStreamWaitEvent(ctx->stream, static_cast<cudaEvent_t>(peers.wait_event), 0));
   peer_scatter_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(slab_dev, rows, w_local, w_full, peers.q_head_begin * d, peers);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
@@ -92,13 +93,33 @@ int gather_sync(lorakv_gather* g) {
   for (int i = 0; i < g->world; ++i) sp.peer_flags[i] = reinterpret_cast<uint32_t*>(g->peer[i]);
   sp.my_flags = reinterpret_cast<uint32_t*>(g->local);
   sp.rank = g->rank; sp.world = g->world; sp.epoch = g->epoch; sp.timeout_ns = g->timeout_ns;
-  gather_sync_kernel<<<1, 32, 0, g->ctx->stream>>>(sp);
+  if (g->overlap) {
+    // side stream: behind this step's epilogue (ev_merged), beside whatever the ctx stream does next
+    LK_CUDA(cudaEventRecord(g->ev_merged, g->ctx->stream));
+    LK_CUDA(cudaStreamWaitEvent(g->side, g->ev_merged, 0));
+    gather_sync_kernel<<<1, 32, 0, g->side>>>(sp);
+    LK_CUDA(cudaGetLastError());
+    LK_CUDA(cudaEventRecord(g->ev_synced, g->side));
+    g->sync_pending = true;
+  } else {
+    gather_sync_kernel<<<1, 32, 0, g->ctx->stream>>>(sp);
+    LK_CUDA(cudaGetLastError());
+  }
   g->ctx->launches++;
-  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+
+// the ctx stream waits for the last handshake (no-op when none is outstanding)
+int gather_wait(lorakv_gather* g) {
+  if (g->overlap && g->sync_pending) {
+    LK_CUDA(cudaStreamWaitEvent(g->ctx->stream, g->ev_synced, 0));
+    g->sync_pending = false;
+  }
   return LORAKV_OK;
 }
 
 int gather_read_status(lorakv_gather* g) {
+  LK_TRY(gather_wait(g));
   LK_CUDA(cudaMemcpyAsync(g->status_host, g->local + 8 * sizeof(uint32_t), sizeof(uint32_t), cudaMemcpyDeviceToHost, g->ctx->stream));
   return LORAKV_OK;
 }
@@ -139,6 +160,7 @@ int lorakv_gather_create(lorakv_ctx* ctx, int rank, int world, int64_t full_elem
 int lorakv_gather_disconnect(lorakv_gather* g) {
   if (!g) return fail("gather_disconnect: null argument");
   LK_CUDA(cudaSetDevice(g->ctx->device));
+  if (g->side) LK_CUDA(cudaStreamSynchronize(g->side));
   LK_CUDA(cudaStreamSynchronize(g->ctx->stream));
   for (int i = 0; i < g->world; ++i)
     if (i != g->rank && g->peer[i]) { cudaIpcCloseMemHandle(g->peer[i]); g->peer[i] = nullptr; }
@@ -149,6 +171,9 @@ int lorakv_gather_disconnect(lorakv_gather* g) {
 void lorakv_gather_destroy(lorakv_gather* g) {
   if (!g) return;
   lorakv_gather_disconnect(g);
+  if (g->side) { cudaStreamSynchronize(g->side); cudaStreamDestroy(g->side); }
+  if (g->ev_merged) cudaEventDestroy(g->ev_merged);
+  if (g->ev_synced) cudaEventDestroy(g->ev_synced);
   cudaFree(g->local);
   cudaFreeHost(g->status_host);
   delete g;
@@ -189,6 +214,24 @@ int lorakv_gather_set_timeout_ms(lorakv_gather* g, int64_t ms) {
   if (!g || ms < 1) return fail("gather_set_timeout_ms: bad argument");
   g->timeout_ns = (uint64_t)ms * 1000000ull;
   return LORAKV_OK;
+}
+
+int lorakv_gather_set_overlap(lorakv_gather* g, int enabled) {
+  if (!g) return fail("gather_set_overlap: null argument");
+  LK_CUDA(cudaSetDevice(g->ctx->device));
+  if (enabled && !g->side) {
+    LK_CUDA(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+    LK_CUDA(cudaEventCreateWithFlags(&g->ev_merged, cudaEventDisableTiming));
+    LK_CUDA(cudaEventCreateWithFlags(&g->ev_synced, cudaEventDisableTiming));
+  }
+  if (!enabled) LK_TRY(lk::gather_wait(g));     // an outstanding handshake joins the ctx stream first
+  g->overlap = enabled != 0;
+  return LORAKV_OK;
+}
+
+int lorakv_gather_wait(lorakv_gather* g) {
+  if (!g) return fail("gather_wait: null argument");
+  return lk::gather_wait(g);
 }
 
 int lorakv_gather_steps(const lorakv_gather* g, int64_t* steps) {

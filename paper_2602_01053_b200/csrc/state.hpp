@@ -218,12 +218,20 @@ struct lorakv_gather {
   uint32_t epoch = 0;                // steps gathered so far
   uint32_t* status_host = nullptr;   // pinned word the status flag is read back into
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;
+  // Overlapped handshake (lorakv_gather_set_overlap): the handshake kernel runs on a side stream behind this step's epilogue
+  // while the ctx stream goes on with the next step's attention; the ctx stream waits for it only before the NEXT epilogue
+  // stores into the peers' buffers (the buffer-reuse guard) and in lorakv_gather_wait (before a consumer reads the rows)
+  bool overlap = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_merged = nullptr, ev_synced = nullptr;
+  bool sync_pending = false;         // ev_synced of the previous step has not been waited for on the ctx stream yet
 };
 
 namespace lk {
 int gather_sync(lorakv_gather* g);                                         // peer_gather.cu
 float* gather_buffer(const lorakv_gather* g, int rank, uint32_t epoch);
 int gather_read_status(lorakv_gather* g);                                  // enqueue the status read-back
+int gather_wait(lorakv_gather* g);                                         // ctx stream waits for an overlapped handshake
 }  // namespace lk
 
 // Projection weights of the step that feeds the cache (engine.hpp:376-403): Wk, Wv per layer, restricted to

@@ -32,7 +32,7 @@ def _barrier(d, name, rank, world):
         _await(os.path.join(d, f"{name}_{r}"))
 
 
-def main(rank, world, d):
+def main(rank, world, d, mode="gather"):
     from oracle import checker
     from paper_2602_01053_b200 import Adapters, Context, Gather, Pool, abi
     from paper_2602_01053_b200.sharding import HeadShard
@@ -69,6 +69,32 @@ def main(rank, world, d):
     agents = [2, 0, 1]
     ok = True
     report = []
+    if mode == "timeout":
+        # rank 1 never issues the step: rank 0's handshake must give up after its timeout and say so, not hang
+        _barrier(d, "connected", rank, world)
+        if rank == 0:
+            gather.set_timeout_ms(300)
+            q_full = np.stack([np.stack([layers[l][0][a][0] for a in agents]) for l in range(n_layers)])
+            cols = slice(mine_sh.q_begin * dh, (mine_sh.q_begin + mine_sh.n_q_local) * dh)
+            t0 = time.time()
+            try:
+                mine_pool.decode_gather(mine_ad, gather, 0, n_layers, agents, n_q, q=np.ascontiguousarray(q_full[:, :, cols]))
+                ok = False
+                report.append("no error")
+            except abi.LorakvError as e:
+                ok = "never published" in str(e) and time.time() - t0 < 30.0
+                report.append(str(e))
+            try:                       # the status stays raised for lorakv_gather_check
+                gather.check()
+                ok = False
+            except abi.LorakvError as e:
+                report.append(str(e))
+        _barrier(d, "stepped", rank, world)
+        gather.disconnect()
+        _barrier(d, "unmapped", rank, world)
+        gather.close()
+        _publish(os.path.join(d, f"result_{rank}"), repr((ok, report)).encode())
+        return 0 if ok else 1
     for policy in (0, 1):          # 0: merge epilogue stores into the peers; 1: CUDA-core kernel + peer scatter
         ctx.set_kernel_policy(policy)
         for step in range(steps):
@@ -91,6 +117,37 @@ def main(rank, world, d):
             report.append((policy, step, same, float(err), ctx.last_kernel()))
             ok = ok and same and err <= 2e-2 and dev
     ok = ok and gather.steps() == 2 * steps
+    # overlapped handshake: device-only steps back to back (the handshake of step s runs beside the attention of step
+    # s + 1, the epilogue of s + 1 waits for it), then lorakv_gather_wait before the rows of the last step are read
+    ctx.set_kernel_policy(0)
+    gather.set_overlap(True)
+    last_want, last_dev = None, 0
+    for step in range(4):
+        scale = np.float32(2.0 + 0.5 * step)
+        q_full = np.stack([np.stack([rnd(layers[l][0][a][0] * scale) for a in agents]) for l in range(n_layers)])
+        last_want = np.zeros_like(q_full)
+        for sh, pool, ad in shards:
+            cols = slice(sh.q_begin * dh, (sh.q_begin + sh.n_q_local) * dh)
+            last_want[:, :, cols] = pool.decode(ad, 0, n_layers, agents, n_q, np.ascontiguousarray(q_full[:, :, cols]))
+        cols = slice(mine_sh.q_begin * dh, (mine_sh.q_begin + mine_sh.n_q_local) * dh)
+        if step < 3:
+            _, last_dev = mine_pool.decode_gather(mine_ad, gather, 0, n_layers, agents, n_q, q=np.ascontiguousarray(q_full[:, :, cols]),
+                                                  want_host=False)
+        else:                                      # the host path waits for the handshake itself
+            got, last_dev = mine_pool.decode_gather(mine_ad, gather, 0, n_layers, agents, n_q, q=np.ascontiguousarray(q_full[:, :, cols]))
+            same = bool(np.array_equal(got, last_want))
+            report.append(("overlap-host", step, same, 0.0, ctx.last_kernel()))
+            ok = ok and same
+        if step == 2:
+            gather.wait()
+            got_dev = np.zeros_like(last_want)
+            ctx.d2h(got_dev, last_dev)
+            ctx.synchronize()
+            same = bool(np.array_equal(got_dev, last_want))
+            report.append(("overlap-device", step, same, 0.0, ctx.last_kernel()))
+            ok = ok and same
+    gather.set_overlap(False)
+    ok = ok and gather.steps() == 2 * steps + 4
     gather.check()
     # tear-down order of CUDA IPC: unmap the peers, barrier, free
     gather.disconnect()
@@ -101,4 +158,4 @@ def main(rank, world, d):
 
 
 if __name__ == "__main__":
-    sys.exit(main(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]))
+    sys.exit(main(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "gather"))

@@ -77,3 +77,25 @@ def test_two_process_gather_over_cuda_ipc(tmp_path):
         kernels = {row[4] for row in report}
         assert kernels == {"fla_decode_tma", "fla_paged_simt"}, kernels
         assert all(row[2] for row in report), report           # bit-exact assembly on every step
+        assert {row[0] for row in report} >= {0, 1, "overlap-device", "overlap-host"}      # incl. the overlapped handshake
+
+
+def test_handshake_times_out_instead_of_hanging(tmp_path):
+    """A peer that never issues the step: gather_sync_kernel gives up after lorakv_gather_set_timeout_ms, the call fails
+    naming the step, lorakv_gather_check keeps failing -- the stream is never left spinning."""
+    world = 2
+    env = dict(os.environ, PYTHONPATH=ROOT)
+    procs = [subprocess.Popen([sys.executable, "-m", "tests.peer_gather_worker", str(r), str(world), str(tmp_path), "timeout"], cwd=ROOT,
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
+    outs = []
+    try:
+        for p in procs:
+            outs.append(p.communicate(timeout=300)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for r, p in enumerate(procs):
+        assert p.returncode == 0, f"rank {r} failed:\n{outs[r][-3000:]}"
+    ok, report = ast.literal_eval((tmp_path / "result_0").read_text())
+    assert ok and "never published step 1" in report[0], report

@@ -78,6 +78,25 @@ int stage_agent_ids(lorakv_ctx* ctx, const int32_t* ids, int64_t n, const int32_
   return LORAKV_OK;
 }
 
+int note_pages_written(lorakv_pool* pool, int64_t row0) {
+  lorakv_ctx* ctx = pool->ctx;
+  if (!pool->write_event) LK_CUDA(cudaEventCreateWithFlags(&pool->write_event, cudaEventDisableTiming));
+  // still in flight from an earlier call? then the lowest pending row carries over
+  const bool earlier_done = !pool->write_recorded || cudaEventQuery(pool->write_event) == cudaSuccess;
+  pool->pending_row0 = earlier_done ? row0 : std::min(pool->pending_row0, row0);
+  LK_CUDA(cudaEventRecord(pool->write_event, ctx->stream));
+  pool->write_recorded = true;
+  return LORAKV_OK;
+}
+
+int64_t stable_rows(lorakv_pool* pool, int64_t L) {
+  if (!pool->write_recorded) return L;
+  const cudaError_t e = cudaEventQuery(pool->write_event);
+  if (e == cudaSuccess) { pool->write_recorded = false; return L; }
+  if (e != cudaErrorNotReady) { (void)cudaGetLastError(); return 0; }
+  return std::max<int64_t>(0, std::min(L, pool->pending_row0));
+}
+
 static const char* kSchemeName[5] = {"NonShared", "FullShared", "BaseShared", "BaseLRShared",
                                      "SelectiveRecompute"};
 static const char* kWhat[3] = {"key", "value", "lr"};
@@ -197,6 +216,8 @@ int lorakv_ctx_create(int device, void* stream, lorakv_ctx** out) {
   ctx->l2_bytes = prop.l2CacheSize > 0 ? (int64_t)prop.l2CacheSize : (int64_t)126 << 20;
   const char* no_pdl = std::getenv("LORAKV_NO_PDL");       // A/B switch for the programmatic dependent launches
   ctx->pdl = !(no_pdl && no_pdl[0] == '1');
+  const char* no_spec = std::getenv("LORAKV_NO_SPECULATION");
+  ctx->speculate = ctx->pdl && !(no_spec && no_spec[0] == '1');
   if (stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
   } else {
@@ -548,6 +569,7 @@ void lorakv_pool_destroy(lorakv_pool* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
   cudaStreamSynchronize(p->ctx->stream);
+  if (p->write_event) cudaEventDestroy(p->write_event);
   for (void* q : {p->k_pages, p->v_pages, p->lr_pages, p->hidden_pages, p->lk_pages, (void*)p->kv_space.dev_table,
                   (void*)p->lr_space.dev_table, (void*)p->lk_space.dev_table})
     if (q) cudaFree(q);
@@ -628,6 +650,7 @@ static int pool_append_impl(lorakv_pool* pool, int which, int64_t layer, int64_t
     const int64_t col0 = (which == LORAKV_KEY || which == LORAKV_VALUE) ? pool->dims.kv_head_begin * pool->dims.d_head : 0;
     LK_TRY(launch_append_scatter(pool, which, layer, set, have, dev + col0, add, dev_ld));
     if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));  // staging is reused
+    else LK_TRY(note_pages_written(pool, have));
   }
   have += add;
   if (appended) *appended = add;
@@ -657,6 +680,7 @@ static int pool_overwrite_impl(lorakv_pool* pool, int which, int64_t layer, int6
   LK_TRY(stage_rows(ctx, rows, n_rows, cache_cols_full(pool, which), ld, mem_kind, &dev, &dev_ld));
   LK_TRY(launch_append_scatter(pool, which, layer, 0, row_begin, dev + pool->dims.kv_head_begin * pool->dims.d_head, n_rows, dev_ld));
   if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  else LK_TRY(note_pages_written(pool, row_begin));
   return LORAKV_OK;
 }
 
@@ -748,6 +772,7 @@ int lorakv_pool_append_lr_project(lorakv_pool* pool, const lorakv_adapters* ad, 
                                : ad->a + layer * ad->d_model * ad->rank;
     LK_TRY(launch_lr_project(pool, a_dev, ad->d_model, ad->rank, layer, set, have, dev, add, dev_ld));
     if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+    else LK_TRY(note_pages_written(pool, have));
   }
   have += add;
   if (appended) *appended = add;
@@ -1040,6 +1065,7 @@ static int append_kv_project_impl(lorakv_pool* pool, const lorakv_proj* pr, cons
     LK_TRY(launch_rows_kv_project(pool, packed, layer, set, row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld,
                                   rope != 0, down, bv, rank, v_scale));
     if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+    else LK_TRY(note_pages_written(pool, row_begin + skip));
     have_k += add_k; have_v += add_v;
     if (appended) *appended = add;
     return LORAKV_OK;
@@ -1048,6 +1074,7 @@ static int append_kv_project_impl(lorakv_pool* pool, const lorakv_proj* pr, cons
                            row_begin + skip, row_begin + skip_k, row_begin + skip_v, dev, add, dev_ld, rope != 0, down, av, bv, rank,
                            v_scale));
   if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  else LK_TRY(note_pages_written(pool, row_begin + skip));
   have_k += add_k; have_v += add_v;
   if (appended) *appended = add;
   return LORAKV_OK;
@@ -1285,6 +1312,7 @@ int lorakv_pool_append_lk_project(lorakv_pool* pool, const lorakv_adapters* ad, 
   LK_TRY(launch_lr_project(pool, ad->a_k + layer * ad->d_model * ad->rank_k, ad->d_model, ad->rank_k, layer, 0, have, dev, add, dev_ld,
                            LORAKV_LK));
   if (mem_kind == LORAKV_HOST) LK_CUDA(cudaStreamSynchronize(ctx->stream));
+  else LK_TRY(note_pages_written(pool, have));
   have += add;
   if (appended) *appended = add;
   return LORAKV_OK;
@@ -1620,6 +1648,7 @@ int lorakv_step_layer(lorakv_pool* pool, const lorakv_proj* pr, const lorakv_ada
   c.a_v = a_v; c.b_v = b_v; c.r_v = r_v; c.s_v = s_v;
   c.merge_v = merge_v; c.append_lr = lr_cached; c.rope = rope != 0; c.q_dev = q_dev;
   LK_TRY(launch_step_layer(pool, c));
+  LK_TRY(note_pages_written(pool, row_begin));
   pool->key_rows[(size_t)kv_set][(size_t)layer] += n_rows;
   pool->value_rows[(size_t)kv_set][(size_t)layer] += n_rows;
   if (lr_cached) pool->lr_rows[(size_t)lr_set][(size_t)layer] += n_rows;

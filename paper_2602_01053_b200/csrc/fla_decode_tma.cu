@@ -87,6 +87,7 @@ struct DecodeParams {
   // projected through B_k (launch_qk_project) extend the Q fragments, S = Q K^T + Qk L_k^T in the same accumulators
   const __nv_bfloat16* lk_pages; const int32_t* lk_table; int64_t lk_layer_stride, lk_page_stride;
   const float* qk;            // [layers][n_batch][n_q_local][RK]
+  int64_t stable_rows;        // cache rows [0, stable_rows) are complete whatever the predecessor kernel is doing (0: none)
 };
 
 // The cache is streamed exactly once per step, so the copies carry an L2 evict-first policy: the lines
@@ -353,8 +354,36 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
     for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
   };
 
-  // Everything above overlaps the tail of the previous kernel of the stream when this one was launched as a programmatic
-  // dependent (the merge of the previous layer, the projections of this one); from here on its results are read.
+  // start of this worker's range in a layer chunk: producer cursor, tile count; false when the range is empty
+  int tl0 = 0;
+  auto setup_chunk = [&](int ch) -> bool {
+    const int chunk_base = ch * total32;
+    g0 = chunk_base + w * G32;
+    const int g1 = min(g0 + G32, chunk_base + total32);
+    n = g1 > g0 ? g1 - g0 : 0;
+    if (n == 0) return false;
+    p_unit = g0 / T32;
+    first_unit = p_unit;
+    p_tl = g0 - p_unit * T32;
+    tl0 = p_tl;
+    p_page = (p_tl * kTK) / p.P; p_tok = (p_tl * kTK) % p.P;
+    p_layer = p_unit / units_per_layer; p_kvh = (p_unit / p.row_blocks) % p.n_kv_local;
+    p_issued = 0;
+    return true;
+  };
+
+  // Launched as a programmatic dependent, everything up to pdl_wait() overlaps the tail of the previous kernel of the stream
+  // (the merge of the previous layer, the projections of this one).  That includes the first bulk copies of the cache rows
+  // that are CERTAINLY complete: p.stable_rows comes from the host, which tracks every page write of the pool with an
+  // event (state.hpp: lorakv_pool::write_event) -- rows below it were written by work the host has seen complete, so no
+  // assumption about the predecessor is needed.  A decode step appends one row: everything but the last tile of a unit
+  // is prefetched while the predecessor is still finishing, and the first tile is consumed ~2 us earlier.
+  const bool have0 = setup_chunk(0);
+  if (have0 && producer && !PA) {
+    const int pre = n < NS ? n : NS;
+    while (p_issued < pre && (int64_t)(p_tl + 1) * kTK <= p.stable_rows) issue_next();
+  }
+  // from here on the predecessor's results are read (q, the newest cache rows, the page table entries of new pages)
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
   LK_TRACE(8);
@@ -362,19 +391,9 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   // consumer cursor, carried incrementally like the producer's
   int c_stage = 0, c_wrap = 0;
   for (chunk = 0; chunk < p.n_chunks; ++chunk) {
-  const int chunk_base = chunk * total32;
-  g0 = chunk_base + w * G32;
-  const int g1 = min(g0 + G32, chunk_base + total32);
-  n = g1 > g0 ? g1 - g0 : 0;
-  if (n == 0) continue;
-  p_unit = g0 / T32;
-  first_unit = p_unit;
-  p_tl = g0 - p_unit * T32;
-  p_page = (p_tl * kTK) / p.P; p_tok = (p_tl * kTK) % p.P;
-  p_layer = p_unit / units_per_layer; p_kvh = (p_unit / p.row_blocks) % p.n_kv_local;
-  p_issued = 0;
-  int u = p_unit;
-  int tl = p_tl;
+  if (chunk == 0 ? !have0 : !setup_chunk(chunk)) continue;
+  int u = first_unit;
+  int tl = tl0;
   // Start-up order (measured with the phase trace of tools/probe_decode_trace.py): the query loads go out first -- once
   // every SM's bulk copies are in flight the memory system is saturated and a plain load waits ~2.4 us behind them, 1.1 us
   // on an idle one --, two stages are issued while they fly (0.4 us of issue work per stage: five bulk copies), then the
@@ -384,11 +403,11 @@ __global__ void __launch_bounds__(NW * 32, 1) fla_decode_tma_kernel(const Decode
   LK_TRACE(14);
   const int pre = n < NS ? n : NS;
   if (producer)
-    for (int i = 0; i < (pre < 2 ? pre : 2); ++i) { issue_next(); if (i == 0) LK_TRACE(10); }
+    while (p_issued < (pre < 2 ? pre : 2)) { issue_next(); LK_TRACE(10); }
   pack_q();
   LK_TRACE(9);
   if (producer)
-    for (int i = 2; i < pre; ++i) issue_next();
+    while (p_issued < pre) issue_next();
   LK_TRACE(2);
   for (int i = 0; i < n; ++i) {
     // refill the stage released one iteration ago (tile p_issued goes where tile p_issued - NS was)
@@ -1039,6 +1058,10 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.lk_layer_stride = pool->lk_layer_stride(); dp.lk_page_stride = pool->lk_page_stride(); dp.qk = c.qk_dev;
   if (rk > 0 && !c.qk_dev) return fail("decode: the key-side low-rank term needs the projected queries (launch_qk_project)");
   if (const char* e = std::getenv("LORAKV_NO_PAGE_IDENTITY")) if (e[0] == '1') dp.identity = 0;
+  // rows the kernel may prefetch before its dependent-launch wait: needs the identity tables (a new page's table entry
+  // arrives with the predecessor's work) and a host-verified completion of every earlier page write
+  dp.stable_rows = (ctx->speculate && !pa && (dp.identity & 1) && (rp == 0 || (dp.identity & 2)) && (rk == 0 || (dp.identity & 4)))
+                       ? stable_rows(pool, c.L) : 0;
   if (pa) {
     dp.lr_policy = ptx::kEvictFirst;     // every V_lr tile is read by one entry's rows of each kv head only
     if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp));

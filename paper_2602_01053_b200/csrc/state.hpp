@@ -58,6 +58,8 @@ struct IdSlot {
 };
 }  // namespace lk
 
+struct lorakv_pool;
+
 struct lorakv_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -67,6 +69,7 @@ struct lorakv_ctx {
   int64_t launches = 0;
   int policy = 0;
   bool pdl = true;                    // chain the decode kernels with programmatic dependent launches (LORAKV_NO_PDL=1 disables)
+  bool speculate = true;              // prefetch certainly-complete cache rows before the dependent-launch wait (LORAKV_NO_SPECULATION=1)
   const char* last_kernel = "none";
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
   lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection; partial sums of a fused layer-step
@@ -116,6 +119,9 @@ int scratch_reserve(lorakv_ctx* ctx, Scratch& s, size_t bytes);
 int pinned_reserve(lorakv_ctx* ctx, size_t bytes);
 // device copy of an agent-id list (see IdSlot); valid for every kernel enqueued on the ctx stream after this call
 int stage_agent_ids(lorakv_ctx* ctx, const int32_t* ids, int64_t n, const int32_t** dev);
+// page-write tracking of a pool (see lorakv_pool::write_event)
+int note_pages_written(lorakv_pool* pool, int64_t row0);
+int64_t stable_rows(lorakv_pool* pool, int64_t L);        // rows [0, result) are complete on the device right now
 
 // One page space: page ids handed out in first-touch order to the logical pages of its sets.
 struct PageSpace {
@@ -165,6 +171,12 @@ struct lorakv_pool {
   int64_t lk_page_stride() const { return P * rk_pad; }
   int64_t lk_layer_stride() const { return lk_space.total_pages() * lk_page_stride(); }
   void* hidden_pages = nullptr;          // [kv_total_pages][P][d_model]
+  // Which cached rows are certainly complete on the device (fla_decode_tma prefetches those before its programmatic-
+  // dependent-launch wait).  Every call that writes pages records an event behind its kernels and the lowest row it
+  // wrote; while that event has not completed, rows from `pending_row0` on may still be in flight.
+  cudaEvent_t write_event = nullptr;
+  bool write_recorded = false;
+  int64_t pending_row0 = 0;
   int64_t hidden_rows = 0;
   std::vector<int64_t> recompute_layers;
   uint64_t reserved_bytes = 0;

@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF
     ptx::fence_barrier_init();
   }
   __syncthreads();
+  ptx::pdl_wait();                  // launched as a programmatic dependent: the set-up above ran under the predecessor's tail
+  ptx::pdl_launch_dependents();
 
   const int64_t w = (int64_t)blockIdx.x * kWorkers + wk;
   const int64_t g0 = w * p.G;
@@ -630,9 +632,14 @@ template <int D, int RP, int MW>
 int launch_t(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem) {
   constexpr int W = warps_per_cta(MW);
   auto kern = fla_decode_f32_kernel<D, RP, MW, W>;
-  LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static size_t attr_smem = 0;         // the attribute call costs more than the launch: only when the ring grows
+  static int attr_device = -1;
+  if (attr_device != ctx->device || smem > attr_smem) {
+    LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_device = ctx->device; attr_smem = smem;
+  }
   prof_mark(ctx, 0);
-  kern<<<grid, W * 32, smem, ctx->stream>>>(dp);
+  LK_CUDA(launch_kernel(ctx, kern, dim3(grid), dim3(W * 32), smem, true, dp));
   prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());

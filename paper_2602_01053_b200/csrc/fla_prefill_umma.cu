@@ -638,8 +638,12 @@ int launch_decode_umma(const PagedAttnCall& c) {
   const int64_t total_tiles = (c.L + kBN - 1) / kBN;
   // splits: enough CTAs for ~4 waves of the machine, at least 4 tiles each
   int64_t splits = (4 * (int64_t)ctx->sm_count + units - 1) / units;
-  if (splits > total_tiles / 4) splits = total_tiles / 4;
+  // ... but a CTA pays ~17 us before and after its stream (TMEM allocation, Q, pipeline fill, drain, partial store): with one
+  // layer per launch (8 units) four waves of 14-tile CTAs spent as long on that as on streaming (cfg 5: 177 us per layer, 0.48
+  // of the HBM roofline).  At least 48 stages of 128 keys per CTA, and no nearly-empty second wave.
+  if (splits > total_tiles / 48) splits = total_tiles / 48;
   if (splits < 1) splits = 1;
+  if (units * splits > ctx->sm_count && units * splits < 2 * (int64_t)ctx->sm_count && ctx->sm_count / units >= 1) splits = ctx->sm_count / units;
   const int64_t tiles_per_split = (total_tiles + splits - 1) / splits;
   splits = (total_tiles + tiles_per_split - 1) / tiles_per_split;
   pp.rows_total = (int)(c.n_batch * pp.group);

@@ -155,6 +155,45 @@ def test_step_layer_equals_the_separate_entry_points(ctx, orc):
         assert orc.max_rel_error(outs["fused"][0][t:t + 1], want) <= 2e-2
 
 
+def test_step_layer_generation_soak(ctx, orc):
+    """150 tokens x 3 layers through the dependent-launch chain without a host synchronisation in between (the prefetch before
+    the wait sees a pending page write on every call; pages fill up and new ones are allocated 4 times): the caches must end
+    up equal to what the separate entry points store, the last token's outputs equal the reference path."""
+    import torch
+    d_model, n_q, n_kv, d, r, A, P, n_layers = 256, 8, 2, 128, 16, 3, 32, 3
+    L0, n_gen = 10, 150
+    ws = [weights(orc, 8400 + l, d_model, n_q, n_kv, d, r, A) for l in range(n_layers)]
+    x = orc.round_bf16(orc.gaussian(L0 + n_gen, d_model, orc.child(8401, 1), 1.0, np.float32))
+    from paper_2602_01053_b200 import Adapters, Pool, Projection, abi
+    pool = Pool(ctx, "BaseLRShared", n_layers, n_kv, d, d_model, r, A, max_tokens=L0 + n_gen, dtype=abi.BF16, page_tokens=P)
+    proj = Projection(ctx, n_layers, d_model, n_kv, d, dtype=abi.BF16)
+    ad = Adapters(ctx, n_layers, A, d_model, r, n_kv, d, dtype=abi.BF16)
+    for l, w in enumerate(ws):
+        proj.set_kv(l, w["wk"], w["wv"]); proj.set_q(l, n_q, w["wq"]); ad.set_a(l, w["a_v"][0])
+        for i in range(A):
+            proj.set_q_lora(l, i, A, w["a_q"], w["b_q"][i], 16.0); ad.set_b(l, i, w["b_v"][i], 16.0)
+    pool.append_tokens(L0)
+    for l in range(n_layers):
+        pool.append_kv_project(proj, l, 0, 0, x[:L0]); pool.append_lr_project(ad, l, 0, 0, x[:L0])
+    xd = torch.from_numpy(x).cuda()
+    od = torch.zeros((n_gen, n_layers, n_q * d), device="cuda")
+    for t in range(n_gen):
+        pool.append_tokens(1)
+        for l in range(n_layers):
+            pool.step_layer_device(proj, ad, l, t % A, L0 + t, xd[L0 + t].data_ptr(), 1, d_model, n_q, od[t, l].data_ptr())
+    ctx.synchronize()
+    got = od.cpu().numpy()
+    for l, w in enumerate(ws):
+        assert pool.rows(0, l, 0) == L0 + n_gen and pool.rows(2, l, 0) == L0 + n_gen
+        assert orc.max_rel_error(pool.key_view(l, 0), orc.apply_rope(orc.matmul(x, w["wk"]), n_kv, d, 0)) <= 4e-3
+        assert orc.max_rel_error(pool.value_view(l, 0), orc.matmul(x, w["wv"])) <= 4e-3
+        assert orc.max_rel_error(pool.lr_view(l, 0), orc.matmul(x, w["a_v"][0])) <= 4e-3
+        for t in (0, 21, 22, 53, 54, n_gen - 1):          # around the page boundaries (rows 32, 64) and the ends
+            _q, want = reference_step(orc, "BaseLRShared", w, x, (L0 + t, L0 + t + 1), t % A, n_q, n_kv, d, r)
+            assert orc.max_rel_error(got[t, l][None, :], want) <= 2e-2, (l, t)
+    pool.close(); proj.close(); ad.close()
+
+
 def test_step_layer_on_a_kv_head_shard(ctx, orc):
     """A rank holding kv heads [1, 3) of 4: its q / output columns are the matching slice of the single-GPU step."""
     import torch

@@ -57,7 +57,18 @@ __device__ __forceinline__ void trace_mark(int64_t warp_global, int slot) {
   }
 }
 #define LK_TRACE(slot) trace_mark((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), slot)
+__device__ unsigned long long g_merge_trace[512 * 4];
+#define LK_MTRACE(slot)                                                                              \
+  do {                                                                                               \
+    if (threadIdx.x == 0) {                                                                          \
+      unsigned long long t_;                                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                         \
+      const int b_ = blockIdx.x + gridDim.x * blockIdx.y;                                            \
+      if (b_ < 512) g_merge_trace[b_ * 4 + slot] = t_;                                               \
+    }                                                                                                \
+  } while (0)
 #else
+#define LK_MTRACE(slot)
 #define LK_TRACE(slot)
 #endif
 
@@ -626,14 +637,20 @@ constexpr int kMergeWarps = 8;
 // reduces them relative to its own maximum, the warps' results meet in shared memory.  Everything that does not depend on
 // the attention kernel happens BEFORE pdl_wait(): address arithmetic and this thread's column of B[agent] (static data), so
 // under a programmatic dependent launch the CTA is resident and set up when the partials arrive.
-__global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(const DecodeMergeParams p) {
-  constexpr int kMaxCols = 6;            // (D + RP) <= 192 columns / 32 lanes
+// RMAX: rank bucket (the thread's B column lives in RMAX registers), COLS: ceil((D + RP) / 32).  Two CTAs per SM's worth of
+// registers (<= 128 per thread): a merge CTA has to fit beside a 24K-register attention CTA -- beside the one it waits for and
+// beside the next layer's, which sets itself up under this epilogue.  With 179 registers it did not, and two thirds of the
+// next launch's CTAs started only after the merge had left their SM (phase trace, profiles/r2_decode_phase_trace.txt).
+template <int RMAX, int COLS>
+__global__ void __launch_bounds__(kMergeWarps * 32, 2) fla_decode_merge_kernel(const DecodeMergeParams p) {
+  constexpr int kMaxCols = COLS;         // (D + RP) <= 192 columns / 32 lanes
   constexpr int kBatch = 8;              // splits of a warp in flight together
-  constexpr int kMaxRank = 64;
+  constexpr int kMaxRank = RMAX;
   __shared__ float m_s[kMergeWarps], l_s[kMergeWarps];
   __shared__ float acc_s[kMergeWarps][192];
   __shared__ float tot_s[192];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  LK_MTRACE(0);
   const int rho = blockIdx.x;
   const int kvh = blockIdx.y % p.n_kv_local;
   const int64_t layer_rel = blockIdx.y / p.n_kv_local;
@@ -668,7 +685,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
     for (int k = 0; k < kMaxRank; ++k) bcol[k] = k < p.r ? __ldg(b + (int64_t)k * dkv + tid) : 0.f;
   }
   ptx::pdl_launch_dependents();          // the next layer's kernels may set themselves up under this epilogue
+  LK_MTRACE(1);
   ptx::pdl_wait();                       // the partials of the attention kernel are complete and visible from here on
+  LK_MTRACE(2);
   // ---- this warp's splits, kBatch at a time, all loads first ----
   float m_w = ninf, l_w = 0.f;
   float acc[kMaxCols];
@@ -738,6 +757,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) fla_decode_merge_kernel(cons
       if (k < p.r) o = fmaf(scale * tot_s[p.D + k], bcol[k], o);
     store_out(p, dst + tid, o / lsum);
   }
+  LK_MTRACE(3);
 }
 
 template <int D, int RP, int MW, int KT, bool PA = false, int NW = kWarps, int RK = 0>
@@ -931,7 +951,10 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
   static int carve_device = -1;
   if (carve_device != ctx->device) {
     LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_warp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
-    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_kernel<16, 5>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_kernel<16, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_kernel<32, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+    LK_CUDA(cudaFuncSetAttribute(fla_decode_merge_kernel<64, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     carve_device = ctx->device;
   }
   if (r > 64) return fail("decode merge: rank %d exceeds 64", r);
@@ -944,7 +967,10 @@ int launch_decode_merge(lorakv_ctx* ctx, const float* part, int d, int rp, int r
     LK_CUDA(launch_kernel(ctx, fla_decode_merge_warp_kernel, dim3((unsigned)((n + kMergeWarps - 1) / kMergeWarps)), dim3(kMergeWarps * 32), 0,
                           true, mp, n));
   } else {
-    LK_CUDA(launch_kernel(ctx, fla_decode_merge_kernel, mgrid, dim3(kMergeWarps * 32), 0, true, mp));
+    if (r <= 16 && d + rp <= 160) LK_CUDA(launch_kernel(ctx, fla_decode_merge_kernel<16, 5>, mgrid, dim3(kMergeWarps * 32), 0, true, mp));
+    else if (r <= 16) LK_CUDA(launch_kernel(ctx, fla_decode_merge_kernel<16, 6>, mgrid, dim3(kMergeWarps * 32), 0, true, mp));
+    else if (r <= 32) LK_CUDA(launch_kernel(ctx, fla_decode_merge_kernel<32, 6>, mgrid, dim3(kMergeWarps * 32), 0, true, mp));
+    else LK_CUDA(launch_kernel(ctx, fla_decode_merge_kernel<64, 6>, mgrid, dim3(kMergeWarps * 32), 0, true, mp));
   }
   ctx->launches++;
   LK_CUDA(cudaGetLastError());
@@ -1082,6 +1108,9 @@ int launch_decode_tma(const PagedAttnCall& c) {
 }  // namespace lk
 
 #ifdef LK_DECODE_TRACE
+extern "C" int lorakv_debug_merge_trace(unsigned long long* out, int n_words) {
+  return cudaMemcpyFromSymbol(out, lk::g_merge_trace, sizeof(unsigned long long) * (size_t)n_words) == cudaSuccess ? 0 : 1;
+}
 extern "C" int lorakv_debug_decode_trace(unsigned long long* out, int n_words) {
   return cudaMemcpyFromSymbol(out, lk::g_decode_trace, sizeof(unsigned long long) * (size_t)n_words) == cudaSuccess ? 0 : 1;
 }

@@ -65,6 +65,14 @@ def main():
     dur_tiles = (t[:, 6] - t[:, 4]) / 1e3
     print(f"  main loop (first tile landed -> all tiles done): min {dur_tiles.min():.2f} median {np.median(dur_tiles):.2f} max {dur_tiles.max():.2f} us")
     print(f"  first tile: median {(np.median(t[:, 5] - t[:, 4])) / 1e3:.2f} us")
+    # the merge kernel of the same (last) layer-step, relative to the same origin
+    mbuf = (C.c_ulonglong * (512 * 4))()
+    if hasattr(lib, "lorakv_debug_merge_trace") and lib.lorakv_debug_merge_trace(mbuf, 512 * 4) == 0:
+        m = np.frombuffer(mbuf, dtype=np.uint64).reshape(512, 4).astype(np.int64)
+        m = m[m[:, 0] > 0]
+        for s_, name in enumerate(["merge CTA entry", "merge set up (before the wait)", "merge wait returned", "merge row stored"]):
+            col = (m[:, s_] - t0) / 1e3
+            print(f"  M{s_} {name:31s} {col.min():7.2f} {np.median(col):7.2f} {col.max():7.2f}")
     pool.close(); ad.close()
     ctx.close()
 

@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  // launched as a programmatic dependent (decode mode: one launch per layer; prefill: behind the projections): barrier
+  // set-up and the TMEM allocation above ran under the predecessor's tail; its results (q, fresh cache rows) are read below
+  ptx::pdl_wait();
+  ptx::pdl_launch_dependents();
 
   if (warp == 8 || warp == 10) {
     // ===================== TMA producers: warp 8 streams K, warp 10 streams V_base + V_lr =====================
@@ -532,9 +536,13 @@ int launch_t(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid) {
   const int stages = (2 * 3 * kv + 3 * lr + 1024 <= (size_t)227 * 1024 - 4096) ? 3 : 2;   // mirrors kStages in the kernel
   const size_t smem = stages * (2 * kv + lr) + 1024;
   auto kern = fla_prefill_umma_kernel<D, RP, kDecode>;
-  LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static int attr_device = -1;         // once per instantiation: smem depends on the template parameters only
+  if (attr_device != ctx->device) {
+    LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_device = ctx->device;
+  }
   prof_mark(ctx, 0);
-  kern<<<grid, kThreads, smem, ctx->stream>>>(pp);
+  LK_CUDA(launch_kernel(ctx, kern, dim3(grid), dim3(kThreads), smem, true, pp));
   prof_mark(ctx, 1);
   ctx->launches++;
   LK_CUDA(cudaGetLastError());

@@ -1,13 +1,18 @@
-"""The recorded bench line (profiles/r1_bench_cfg2.json, written by `python bench.py` on a B200) carries every key the
-measurement contract asks for, with consistent arithmetic.  CPU only: it reads the committed JSON."""
+"""The recorded bench lines (profiles/r1_bench_cfg2.json, profiles/r2_bench_cfg2.json, written by `python bench.py` on a B200,
+and profiles/r2_bench_reference_arm.json by `--impl reference`) carry every key the measurement contract asks for, with
+consistent arithmetic.  CPU only: it reads the committed JSON."""
 import json
 import os
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_recorded_bench_line_has_the_contract_keys():
-    d = json.load(open(os.path.join(ROOT, "profiles", "r1_bench_cfg2.json")))
+import pytest
+
+
+@pytest.mark.parametrize("name", ["r1_bench_cfg2.json", "r2_bench_cfg2.json"])
+def test_recorded_bench_line_has_the_contract_keys(name):
+    d = json.load(open(os.path.join(ROOT, "profiles", name)))
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "vs_baseline",
               "dtype", "data", "config", "e2e", "gpu_launches", "clocks", "roofline", "cpu_baseline"):
         assert k in d, k
@@ -24,3 +29,28 @@ def test_recorded_bench_line_has_the_contract_keys():
     c = d["cpu_baseline"]
     assert c["kind"] in ("reference", "port") and c["cores"] >= 1 and c["value"] > 0 and c["sample"]
     assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if name.startswith("r2"):
+        # round 2: one launch pair per layer, parity on two layers and >= 256 prefill rows, the 1-thread CPU figure
+        pl = d["per_layer"]
+        assert pl["gpu_launches_per_layer"] == 2 and abs(pl["ms_per_step"] - pl["ms_per_layer"] * d["config"]["n_layers"]) < 1e-9
+        rf = pl["roofline"]
+        assert abs(rf["achieved"] - pl["algorithmic_bytes_per_layer"] / (pl["ms_per_layer"] * 1e-3) / 1e9) < 1e-6 * rf["achieved"]
+        assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9 and rf["frac"] >= 0.70            # the north star's decode target
+        assert pl["algorithmic_bytes_per_layer"] * d["config"]["n_layers"] == r["algorithmic_bytes_per_launch"]
+        par = d["parity"]
+        assert set(par["layers"]) == {"0", str(d["config"]["n_layers"] - 1)} and par["max_rel_error"] <= par["tolerance"]
+        pp = d["prefill"]["parity"]
+        assert pp["sampled_rows"] >= 256 and pp["max_rel_error"] <= pp["tolerance"]
+        assert c["one_thread"]["cores"] == 1 and 0 < c["one_thread"]["value"] < c["value"]
+        assert "not measured in this run" in r["traffic_source"]
+
+
+def test_recorded_reference_arm_line():
+    d = json.load(open(os.path.join(ROOT, "profiles", "r2_bench_reference_arm.json")))
+    assert d["impl"] == "reference" and d["config"]["workload"] == "cfg2" and d["higher_is_better"] is True
+    assert d["metric"] == "flash_lora_attn_decode_agent_tokens_per_s" and d["unit"] == "tok/s"
+    assert d["e2e"] == {"value": d["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    c = d["cpu_baseline"]
+    assert c["value"] == d["value"] and c["kind"] in ("reference", "port") and c["cores"] >= 1
+    assert "32 of 32 layers" in c["sample"]                      # whole steps, not one layer scaled
+    assert abs(d["value"] - d["config"]["agents"] / (d["ms_per_step"] * 1e-3)) < 1e-6 * d["value"]

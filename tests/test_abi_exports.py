@@ -65,3 +65,35 @@ def test_product_never_references_the_oracle():
                 assert "oracle" not in text.lower() or f == "abi.py" and "oracle" not in text, (dirpath, f)
     for f in os.listdir(os.path.join(ROOT, "include", "lorakv")) if os.path.isdir(os.path.join(ROOT, "include", "lorakv")) else []:
         assert "orc_" not in open(os.path.join(ROOT, "include", "lorakv", f)).read()
+
+
+def test_snapshot_header_reader_is_host_only_and_hardened(lib, tmp_path):
+    """lorakv_snapshot_tokens parses the header of the reference's snapshot container (kvcache.hpp:438-473) on the host: it
+    answers for the files the REFERENCE's writer produced (tests/golden/snapshot_*.bin) and turns malformed files into an
+    error message -- no exception may cross the C ABI, no allocation may be sized by an unchecked length field."""
+    import ctypes as C
+    import struct
+    from paper_2602_01053_b200 import abi
+    from tests.cases import SNAPSHOT_DIMS, SNAPSHOT_SCHEMES
+    n = C.c_int64()
+    for scheme in SNAPSHOT_SCHEMES:
+        path = os.path.join(ROOT, "tests", "golden", f"snapshot_{scheme}.bin").encode()
+        assert lib.lorakv_snapshot_tokens(path, None, 0, C.byref(n)) == 0 and n.value == SNAPSHOT_DIMS["L"]
+        buf = (C.c_int32 * 4)()
+        assert lib.lorakv_snapshot_tokens(path, buf, 4, C.byref(n)) == 0 and n.value == SNAPSHOT_DIMS["L"]      # cap < n: no overrun
+    good = open(os.path.join(ROOT, "tests", "golden", "snapshot_FullShared.bin"), "rb").read()
+    hlen = struct.unpack("<Q", good[:8])[0]
+    cases = {
+        "missing": None,
+        "empty": b"",
+        "huge_header_length": struct.pack("<Q", 1 << 40) + good[8:],          # would have been a 1 TiB std::string
+        "truncated_header": good[:8 + hlen // 2],
+        "not_json": struct.pack("<Q", 5) + b"hello",
+        "overflowing_integer": struct.pack("<Q", 40) + b'{"tokens":[99999999999999999999999999]} ',
+    }
+    for name, blob in cases.items():
+        path = tmp_path / f"{name}.bin"
+        if blob is not None:
+            path.write_bytes(blob)
+        assert lib.lorakv_snapshot_tokens(str(path).encode(), None, 0, C.byref(n)) != 0, name
+        assert lib.lorakv_last_error(), name

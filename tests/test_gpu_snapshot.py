@@ -88,6 +88,26 @@ def test_snapshot_errors(ctx, tmp_path):
         Pool.load_snapshot(ctx, tmp_path / "missing.bin", 2)
     with pytest.raises(LorakvError, match="not divisible"):
         Pool.load_snapshot(ctx, os.path.join(GOLDEN, "snapshot_FullShared.bin"), 3)
+    # length fields of the file are checked before they size anything: absurd row counts, a header length beyond
+    # the file, dimensions that cannot be a model -- all messages, never a C++ exception across the C ABI
+    import json
+    import struct
+    hlen = struct.unpack("<Q", golden[:8])[0]
+    header, payload = json.loads(golden[8:8 + hlen]), golden[8 + hlen:]
+    def rewrite(mutate):
+        h = json.loads(json.dumps(header)); mutate(h)
+        blob = json.dumps(h, separators=(",", ":"), sort_keys=True).encode()
+        return struct.pack("<Q", len(blob)) + blob + payload
+    for name, mutate, msg in (("rows_huge", lambda h: h["tensors"][0].__setitem__("rows", 1 << 40), "claims"),
+                              ("rows_negative", lambda h: h["tensors"][0].__setitem__("rows", -3), "claims"),
+                              ("layers_absurd", lambda h: h.__setitem__("n_layers", 1 << 33), "implausible"),
+                              ("length_negative", lambda h: h.__setitem__("length", -1), "implausible")):
+        f = tmp_path / f"{name}.bin"; f.write_bytes(rewrite(mutate))
+        with pytest.raises(LorakvError, match=msg):
+            Pool.load_snapshot(ctx, f, 2)
+    big = tmp_path / "hlen.bin"; big.write_bytes(struct.pack("<Q", 1 << 40) + golden[8:])
+    with pytest.raises(LorakvError, match="header truncated"):
+        Pool.load_snapshot(ctx, big, 2)
     shard = Pool(ctx, "FullShared", 1, 2, 8, 16, 0, 1, max_tokens=8, kv_head_begin=1, n_kv_local=1)
     with pytest.raises(LorakvError, match="unsharded"):
         shard.save_snapshot(tmp_path / "s.bin", [])

@@ -4,6 +4,8 @@
 //   * A (128 x K) K-major SWIZZLE_128B tiles written by threads (how Q and P tiles are built),
 //   * B (N x K) K-major SWIZZLE_128B (how a K page lands after a bulk copy),
 //   * B (K x N) MN-major SWIZZLE_128B / 64B / 32B (how V pages and V_lr pages land: page_layout.cuh),
+//   * B (N x K) K-major with NARROW rows, K = 16 / 32 (SWIZZLE_32B / 64B): how a tile of the key-side low-rank cache L_k lands
+//     (one more k block of the score product S += Qk L_k^T; A from TMEM),
 //   * accumulation into TMEM, tcgen05.ld / tcgen05.st round trips (the lazy O rescale) and
 //     tcgen05.commit -> mbarrier completion.
 // D = alpha * (A B) + (A B) when rescale != 0 (load, scale, store back, accumulate a second pass),
@@ -31,14 +33,20 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
   unsigned char* sB = smem + (K / 64) * 128 * 128;  // see below
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  for (int idx = tid; idx < 128 * K; idx += 128) {
+  const bool narrow = K < 64;                         // K-major B with 2K-byte rows: the L_k tile convention (A must come from TMEM)
+  if (narrow) sB = smem;
+  for (int idx = tid; idx < 128 * K && !narrow; idx += 128) {
     const int row = idx / K, k = idx % K;
     const uint32_t off = (uint32_t)(k / 64) * 16384u + ptx::sw128_offset(row, k % 64);
     *reinterpret_cast<__nv_bfloat16*>(sA + off) = __float2bfloat16_rn(A[idx]);
   }
   const PageLayout lay = make_page_layout(K, N, 2);   // MN-major B: [N/bw blocks][K keys][bw], swizzled rows
+  const PageLayout nlay = make_page_layout(N, K, 2);  // narrow K-major B: a page of N tokens x K columns
   for (int idx = tid; idx < N * K; idx += 128) {
-    if (b_mn_major) {
+    if (narrow) {
+      const int n = idx / K, k = idx % K;             // B given as N x K row-major
+      *reinterpret_cast<__nv_bfloat16*>(sB + 2 * page_offset(nlay, n, k)) = __float2bfloat16_rn(B[idx]);
+    } else if (b_mn_major) {
       const int k = idx / N, n = idx % N;             // B given as K x N row-major
       *reinterpret_cast<__nv_bfloat16*>(sB + 2 * page_offset(lay, k, n)) = __float2bfloat16_rn(B[idx]);
     } else {
@@ -81,7 +89,10 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
     for (int ks = 0; ks < K / 16; ++ks) {
       const uint64_t da = ptx::smem_desc(a_base + (ks / 4) * 16384u + (ks % 4) * 32u, 16u, 1024u, ptx::kSw128);
       uint64_t db;
-      if (!b_mn_major) {
+      if (narrow) {
+        const uint32_t W = 2u * (uint32_t)K;        // row bytes; one swizzle atom along K, 8-row groups W * 8 bytes apart
+        db = ptx::smem_desc(b_base + (uint32_t)ks * 32u, 16u, 8u * W, K == 32 ? ptx::kSw64 : ptx::kSw32);
+      } else if (!b_mn_major) {
         db = ptx::smem_desc(b_base + (ks / 4) * (uint32_t)(N * 128) + (ks % 4) * 32u, 16u, 1024u, ptx::kSw128);
       } else {
         const uint32_t W = 2u * (uint32_t)lay.bw;   // row bytes of one key inside a column block
@@ -135,7 +146,8 @@ __global__ void __launch_bounds__(128, 1) umma_selftest_kernel(const float* __re
 int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major, float alpha, int rescale,
                   int a_in_tmem, float* d) {
   if (!ctx || !a || !b || !d) return fail("selftest_umma: null argument");
-  if (K != 64 && K != 128) return fail("selftest_umma: K must be 64 or 128");
+  if (K != 64 && K != 128 && !((K == 16 || K == 32) && a_in_tmem && !b_mn_major))
+    return fail("selftest_umma: K must be 64 or 128 (or 16 / 32 with A in TMEM and a K-major B: the narrow-row convention)");
   if (N < 16 || N > 256 || N % 16 != 0) return fail("selftest_umma: N must be a multiple of 16 in [16, 256]");
   if (b_mn_major && !(N == 16 || N == 32 || N % 64 == 0)) return fail("selftest_umma: MN-major N must be 16, 32 or a multiple of 64");
   LK_CUDA(cudaSetDevice(ctx->device));
@@ -147,7 +159,7 @@ int umma_selftest(lorakv_ctx* ctx, const float* a, const float* b, int N, int K,
   float* dd = reinterpret_cast<float*>(base + (na + 255) / 256 * 256 + (nb + 255) / 256 * 256);
   LK_CUDA(cudaMemcpyAsync(da, a, na, cudaMemcpyHostToDevice, ctx->stream));
   LK_CUDA(cudaMemcpyAsync(db, b, nb, cudaMemcpyHostToDevice, ctx->stream));
-  const size_t smem = (size_t)128 * K * 2 + (size_t)N * K * 2 + 1024;
+  const size_t smem = (size_t)128 * K * 2 + (size_t)N * K * 2 + 2048;
   LK_CUDA(cudaFuncSetAttribute(umma_selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   umma_selftest_kernel<<<1, 128, smem, ctx->stream>>>(da, db, N, K, b_mn_major, alpha, rescale, a_in_tmem, dd);
   ctx->launches++;

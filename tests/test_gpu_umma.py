@@ -37,3 +37,19 @@ def test_umma_tile_matches_host_matmul(ctx, N, K, mn_major, rescale, a_in_tmem):
         want = want * (alpha + 1.0)
     err = np.abs(got - want).max() / np.abs(want).max()
     assert err <= 1e-5, (N, K, mn_major, rescale, a_in_tmem, err)
+
+
+@pytest.mark.parametrize("N,K", [(128, 16), (128, 32), (64, 16), (256, 32), (16, 16)])
+@pytest.mark.parametrize("rescale", [False, True])
+def test_umma_narrow_k_major_rows(ctx, N, K, rescale):
+    """A tile of the key-side low-rank cache L_k: [keys][rank_k] rows of 32 / 64 bytes (SWIZZLE_32B / 64B), consumed as a
+    K-major B operand with A from TMEM -- the extra k block of the score product on the tcgen05 kernels."""
+    rng = np.random.default_rng(77 * N + K)
+    a = bf16(rng.standard_normal((128, K)))
+    b = bf16(rng.standard_normal((N, K)))
+    want = a.astype(np.float64) @ b.T.astype(np.float64)
+    got = ctx.selftest_umma(a, b, False, alpha=0.375, rescale=rescale, a_in_tmem=True)
+    if rescale:
+        want = want * 1.375
+    err = np.abs(got - want).max() / np.abs(want).max()
+    assert err <= 1e-5, (N, K, rescale, err)

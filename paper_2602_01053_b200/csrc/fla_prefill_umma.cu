@@ -70,6 +70,10 @@ struct PrefillParams {
   float scale_log2, lr_scale;
   const float* q;       // [L_c][n_q_local * D]
   const float* b;       // [r][n_kv_local * D] of this (layer, agent)
+  // key-side low-rank term (template RK > 0; kernels.hpp: KeyLowRank): L_k tiles ride in the K stage, the queries projected
+  // through B_k (launch_qk_project) sit in TMEM beside Q: RK / 16 more k steps of the score chain, S = Q K^T + Qk L_k^T
+  const __nv_bfloat16* lk_pages; const int32_t* lk_table; int64_t lk_layer_off, lk_layer_stride, lk_page_stride;
+  const float* qk;      // [layers][n_batch][rows][n_q_local][RK]
   float* out;           // [L_c][n_q_local * D]
 };
 
@@ -99,17 +103,22 @@ struct Barriers {
 // kDecode = false: prefill block (rows = head x position, causal mask, final output)
 // kDecode = true : batched decode for many rows per kv head (rows = batch entry x head, all at position L-1);
 //                  a CTA streams one split of one (layer, kv head) and writes an un-normalised partial
-template <int D, int RP, bool kDecode>
+template <int D, int RP, bool kDecode, int RK = 0>
 __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const PrefillParams p) {
+  static_assert(RK == 0 || RK == 16 || RK == 32, "key-side rank: one or two k steps");
+  static_assert(RK == 0 || D == 64 || RP <= 32, "TMEM: Qk sits behind O_lr at d_head 128");
   constexpr int kQBlocks = D / 64;                           // 64-column K-blocks of Q / K; 64-column N-blocks of V
   constexpr uint32_t kBlkBytes = kBN * 128;                  // one [128 rows][64] bf16 block = 16 KB
   constexpr uint32_t kKBytes = kQBlocks * kBlkBytes;         // K stage == V stage bytes
   constexpr uint32_t kLrRow = 2 * RP;                        // bytes of one V_lr row
   constexpr uint32_t kLrBytes = kBN * kLrRow;
+  constexpr uint32_t kLkRow = 2 * RK;                        // bytes of one L_k row
+  constexpr uint32_t kLkBytes = kBN * kLkRow;
   constexpr uint32_t kTmemS = 0, kTmemO = 256, kTmemLr = 384, kTmemQ = 448;
+  constexpr uint32_t kTmemQk = D == 64 ? 480 : 384 + RP;     // 16 columns: Qk as packed bf16 pairs, zero padded
   // K / V ring depth: three stages hide the L2 latency of a stage behind two stages of work; the widest
   // configuration (d 128, rank 64) only has room for two
-  constexpr int kStages = (2 * 3 * kKBytes + 3 * kLrBytes + 1024 <= 227 * 1024 - 4096) ? 3 : 2;
+  constexpr int kStages = (2 * 3 * kKBytes + 3 * kLrBytes + 3 * kLkBytes + 1024 <= 227 * 1024 - 4096) ? 3 : 2;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ Barriers bars;
@@ -121,11 +130,12 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   unsigned char* sK = smem;                          // kStages stages each
   unsigned char* sV = sK + kStages * kKBytes;
   unsigned char* sLR = sV + kStages * kKBytes;
+  unsigned char* sLK = sLR + kStages * kLrBytes;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // ---- what this CTA owns: n_tiles softmax tiles of kSN keys starting at key tile_begin * kSN ----
   int PB, kvh, n_tiles, tile_begin;
-  int64_t q0, rows_here, kv_layer_off, lr_layer_off, mask_from;   // mask_from: first key that some row cannot see
+  int64_t q0, rows_here, kv_layer_off, lr_layer_off, lk_layer_off, mask_from;   // mask_from: first key that some row cannot see
   int unit = 0, split = 0, layer_rel = 0;
   if constexpr (!kDecode) {
     PB = kBM / p.group;                                           // query positions per CTA
@@ -138,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     const int64_t last_visible_cta = p.query_offset + q0 + rows_here - 1;
     n_tiles = (int)(last_visible_cta / kSN) + 1;
     tile_begin = 0;
-    kv_layer_off = p.kv_layer_off; lr_layer_off = p.lr_layer_off;
+    kv_layer_off = p.kv_layer_off; lr_layer_off = p.lr_layer_off; lk_layer_off = p.lk_layer_off;
     mask_from = p.query_offset + q0 + 1;
   } else {
     PB = 1; q0 = 0; rows_here = p.rows_total;
@@ -150,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     if (n_tiles < 0) n_tiles = 0;
     kv_layer_off = p.kv_layer_off + (int64_t)layer_rel * p.kv_layer_stride;
     lr_layer_off = p.lr_layer_off + (int64_t)layer_rel * p.lr_layer_stride;
+    lk_layer_off = p.lk_layer_off + (int64_t)layer_rel * p.lk_layer_stride;
     mask_from = p.L;
   }
   const int n_stages_needed = (n_tiles + 1) / 2;                  // kBN-key stages the producers stream
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       for (int j = 0; j < n_stages_needed; ++j) {
         const int s = j % kStages;
         if (j >= kStages) ptx::mbar_wait(&empty[s], (uint32_t)(((j / kStages) & 1) ^ 1));   // the phase that freed the stage
-        ptx::mbar_arrive_expect_tx(&full[s], is_k ? kKBytes : kKBytes + kLrBytes);
+        ptx::mbar_arrive_expect_tx(&full[s], is_k ? kKBytes + kLkBytes : kKBytes + kLrBytes);
         for (int i = 0; i < n_copies; ++i) {
           const int64_t key0 = stage_key0 + (int64_t)j * kBN + (int64_t)i * tpc;
           int page = (int)(key0 / p.P);
@@ -206,6 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
           if (RP > 0 && !is_k) {
             const int64_t lr_base = lr_layer_off + (int64_t)p.lr_table[page] * p.lr_page_stride + (int64_t)tok0 * RP;
             bulk_g2s(ptx::smem_u32(sLR + s * kLrBytes + i * tpc * kLrRow), p.lr_pages + lr_base, (uint32_t)tpc * kLrRow, &full[s]);
+          }
+          if (RK > 0 && is_k) {
+            const int64_t lk_base = lk_layer_off + (int64_t)p.lk_table[page] * p.lk_page_stride + (int64_t)tok0 * RK;
+            bulk_g2s(ptx::smem_u32(sLK + s * kLkBytes + i * tpc * kLkRow), p.lk_pages + lk_base, (uint32_t)tpc * kLkRow, &full[s]);
           }
         }
       }
@@ -227,7 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       const uint64_t kd = ptx::smem_desc(ptx::smem_u32(sK), 16u, 1024u, ptx::kSw128);
       const uint64_t vd = ptx::smem_desc(ptx::smem_u32(sV), kBlkBytes, 1024u, ptx::kSw128);
       const uint64_t ld = ptx::smem_desc(ptx::smem_u32(sLR), kBN * kLrRow, 8u * kLrRow, lr_mode);
-      const uint32_t kd_hi = (uint32_t)(kd >> 32), vd_hi = (uint32_t)(vd >> 32), ld_hi = (uint32_t)(ld >> 32);
+      // an L_k tile is K-major with narrow rows: one swizzle atom (32 / 64 bytes) along the rank, 8-key groups 8 rows apart
+      const uint64_t lkd = ptx::smem_desc(ptx::smem_u32(sLK), 16u, 8u * kLkRow, RK == 32 ? ptx::kSw64 : ptx::kSw32);
+      const uint32_t kd_hi = (uint32_t)(kd >> 32), vd_hi = (uint32_t)(vd >> 32), ld_hi = (uint32_t)(ld >> 32), lkd_hi = (uint32_t)(lkd >> 32);
       auto desc = [](uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; };
       // S of tiles (j, j + 1), j even: one N = 128 MMA chain over the whole K stage (j / 2) % kStages into the
       // adjacent S buffers j % 4 and j % 4 + 1
@@ -241,6 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         for (int ks = 0; ks < D / 16; ++ks)
           ptx::umma_bf16_ts(s_tmem, tmem + kTmemQ + 8u * ks, desc(kd_hi, k_lo + (uint32_t)(((ks / 4) * kBlkBytes + (ks % 4) * 32u) >> 4)),
                             idesc_s, ks > 0 ? 1u : 0u);
+        if (RK > 0) {
+          const uint32_t lk_lo = (uint32_t)lkd + (uint32_t)ks_stage * (kLkBytes >> 4);
+#pragma unroll
+          for (int kk = 0; kk < RK / 16; ++kk)
+            ptx::umma_bf16_ts(s_tmem, tmem + kTmemQk + 8u * kk, desc(lkd_hi, lk_lo + (uint32_t)(kk * 32u >> 4)), idesc_s, 1u);
+        }
         ptx::umma_commit(&bars.k_empty[ks_stage]);
         ptx::umma_commit(&bars.s_full[j & 3]);
         ptx::umma_commit(&bars.s_full[(j & 3) + 1]);
@@ -288,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     bool real_row;
     int64_t last_visible;
     const float* q_src;
+    const float* qk_src = nullptr;
     float* dst = nullptr;
     if constexpr (!kDecode) {
       const int hg = row / PB;                                 // q head within the group
@@ -298,12 +322,14 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       last_visible = p.query_offset + pos;
       q_src = p.q + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D;
       dst = p.out + pos * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg) * D;
+      if (RK > 0) qk_src = p.qk + (pos * p.n_q_local + (int64_t)kvh * p.group + hg) * RK;
     } else {
       real_row = row < p.rows_total;
       const int rho = real_row ? row : p.rows_total - 1;
       const int entry = rho / p.group, gi = rho % p.group;
       last_visible = p.L - 1;
       q_src = p.q + (((int64_t)(p.layer_begin_rel + layer_rel) * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
+      if (RK > 0) qk_src = p.qk + (((int64_t)(p.layer_begin_rel + layer_rel) * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * RK;
     }
     const float ninf = -std::numeric_limits<float>::infinity();
 
@@ -321,6 +347,17 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
           r16[i + 1] = pack_bf16(v.z, v.w);
         }
         ptx::tmem_st16(tmem + lane_base + kTmemQ + (uint32_t)wg * (D / 4) + c0, r16);
+      }
+      if (RK > 0 && wg == 0) {        // the row's queries through B_k: RK numbers -> RK / 2 packed columns, zero padded to 16
+        uint32_t r16[16];
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (2 * i < RK) v = __ldg(reinterpret_cast<const float4*>(qk_src + 2 * i));
+          r16[i] = pack_bf16(v.x, v.y);
+          r16[i + 1] = pack_bf16(v.z, v.w);
+        }
+        ptx::tmem_st16(tmem + lane_base + kTmemQk, r16);
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
@@ -529,13 +566,13 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   if (warp == 0) ptx::tmem_dealloc(tmem, 512);
 }
 
-template <int D, int RP, bool kDecode>
+template <int D, int RP, bool kDecode, int RK = 0>
 int launch_t(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid) {
   const size_t blk = (size_t)kBN * 128;
-  const size_t kv = (D / 64) * blk, lr = (size_t)kBN * 2 * RP;
-  const int stages = (2 * 3 * kv + 3 * lr + 1024 <= (size_t)227 * 1024 - 4096) ? 3 : 2;   // mirrors kStages in the kernel
-  const size_t smem = stages * (2 * kv + lr) + 1024;
-  auto kern = fla_prefill_umma_kernel<D, RP, kDecode>;
+  const size_t kv = (D / 64) * blk, lr = (size_t)kBN * 2 * RP, lk = (size_t)kBN * 2 * RK;
+  const int stages = (2 * 3 * kv + 3 * lr + 3 * lk + 1024 <= (size_t)227 * 1024 - 4096) ? 3 : 2;   // mirrors kStages in the kernel
+  const size_t smem = stages * (2 * kv + lr + lk) + 1024;
+  auto kern = fla_prefill_umma_kernel<D, RP, kDecode, RK>;
   static int attr_device = -1;         // once per instantiation: smem depends on the template parameters only
   if (attr_device != ctx->device) {
     LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -549,8 +586,24 @@ int launch_t(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid) {
   return LORAKV_OK;
 }
 
+// key-side rank 16 / 32 beside value-side rank 0 / 16 / 32 (rank 64 at d_head 128 leaves no TMEM columns for Qk: the caller
+// keeps those on the CUDA-core kernel, key_lowrank_umma_ok)
+template <int D, bool kDecode, int RK>
+int launch_rp_rk(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid, int rp) {
+  switch (rp) {
+    case 0: return launch_t<D, 0, kDecode, RK>(ctx, pp, grid);
+    case 16: return launch_t<D, 16, kDecode, RK>(ctx, pp, grid);
+    case 32: return launch_t<D, 32, kDecode, RK>(ctx, pp, grid);
+    default:
+      if constexpr (D == 64) return launch_t<D, 64, kDecode, RK>(ctx, pp, grid);
+      else return fail("fla_prefill_umma: key-side term beside a rank-64 value side at d_head 128 (no TMEM columns left)");
+  }
+}
+
 template <int D, bool kDecode>
-int launch_rp(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid, int rp) {
+int launch_rp(lorakv_ctx* ctx, const PrefillParams& pp, unsigned grid, int rp, int rk = 0) {
+  if (rk == 16) return launch_rp_rk<D, kDecode, 16>(ctx, pp, grid, rp);
+  if (rk == 32) return launch_rp_rk<D, kDecode, 32>(ctx, pp, grid, rp);
   switch (rp) {
     case 0: return launch_t<D, 0, kDecode>(ctx, pp, grid);
     case 16: return launch_t<D, 16, kDecode>(ctx, pp, grid);
@@ -578,6 +631,19 @@ void fill_common(PrefillParams& pp, const PagedAttnCall& c) {
   pp.q = c.q_dev; pp.out = c.out_dev;
   pp.n_qblocks = 0; pp.n_batch = (int)c.n_batch; pp.rows_total = 0; pp.splits = 1; pp.tiles_per_split = 0;
   pp.layer_begin_rel = 0; pp.part = nullptr; pp.lr_scale = 0.f; pp.b = nullptr;
+  const bool rk = pool->rk_pad > 0;
+  pp.lk_pages = static_cast<const __nv_bfloat16*>(pool->lk_pages);
+  pp.lk_table = rk ? pool->lk_space.dev_table : nullptr;
+  pp.lk_layer_stride = rk ? pool->lk_layer_stride() : 0; pp.lk_layer_off = c.layer_begin * pp.lk_layer_stride;
+  pp.lk_page_stride = rk ? pool->lk_page_stride() : 0; pp.qk = c.qk_dev;
+}
+
+// the key-side low-rank term on this kernel: rank_k padded to 16 / 32 (one or two more k steps of the score chain) and
+// 16 free TMEM columns for Qk (d_head 128 with a rank-64 value side has none)
+bool key_lowrank_umma_ok(const lorakv_pool* pool) {
+  if (pool->rk_pad == 0) return true;
+  if (pool->rk_pad != 16 && pool->rk_pad != 32) return false;
+  return pool->dims.d_head == 64 || pool->r_pad <= 32;
 }
 
 bool umma_shape_ok(const lorakv_pool* pool) {
@@ -593,7 +659,7 @@ bool umma_shape_ok(const lorakv_pool* pool) {
 
 bool prefill_umma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
-  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
+  if (!key_lowrank_umma_ok(pool) || (pool->rk_pad > 0 && !c.qk_dev)) return false;
   if (!umma_shape_ok(pool)) return false;
   if (c.n_batch != 1 || c.rows_per_entry < 2 || c.layer_end - c.layer_begin != 1) return false;
   const int64_t group = c.n_q_local / pool->n_kv_local;
@@ -615,8 +681,8 @@ int launch_prefill_umma(const PagedAttnCall& c) {
   pp.lr_scale = (r > 0) ? c.adapters->scale_host[(size_t)(layer * c.adapters->n_agents + agent)] : 0.f;
   pp.b = (r > 0) ? c.adapters->b + ((layer * c.adapters->n_agents + agent) * r) * (pool->n_kv_local * (int64_t)d) : nullptr;
   const unsigned grid = (unsigned)((int64_t)pp.n_qblocks * pool->n_kv_local);
-  if (d == 128) LK_TRY((launch_rp<128, false>(ctx, pp, grid, rp)));
-  else LK_TRY((launch_rp<64, false>(ctx, pp, grid, rp)));
+  if (d == 128) LK_TRY((launch_rp<128, false>(ctx, pp, grid, rp, (int)pool->rk_pad)));
+  else LK_TRY((launch_rp<64, false>(ctx, pp, grid, rp, (int)pool->rk_pad)));
   ctx->last_kernel = "fla_prefill_umma";
   return LORAKV_OK;
 }
@@ -627,7 +693,7 @@ int launch_prefill_umma(const PagedAttnCall& c) {
 // fla_decode_tma.
 bool decode_umma_supported(const PagedAttnCall& c) {
   const lorakv_pool* pool = c.pool;
-  if (pool->rk_pad > 0) return false;          // the key-side low-rank term runs on fla_paged_simt (and fla_decode_tma where built)
+  if (!key_lowrank_umma_ok(pool) || (pool->rk_pad > 0 && !c.qk_dev)) return false;
   if (!umma_shape_ok(pool)) return false;
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1 || c.L < 1 || c.n_batch < 1) return false;
   const int64_t rows_total = c.n_batch * (c.n_q_local / pool->n_kv_local);
@@ -661,8 +727,8 @@ int launch_decode_umma(const PagedAttnCall& c) {
   LK_TRY(scratch_reserve(ctx, ctx->work, part_bytes));
   pp.part = static_cast<float*>(ctx->work.ptr);
   const unsigned grid = (unsigned)(units * splits);
-  if (d == 128) LK_TRY((launch_rp<128, true>(ctx, pp, grid, rp)));
-  else LK_TRY((launch_rp<64, true>(ctx, pp, grid, rp)));
+  if (d == 128) LK_TRY((launch_rp<128, true>(ctx, pp, grid, rp, (int)pool->rk_pad)));
+  else LK_TRY((launch_rp<64, true>(ctx, pp, grid, rp, (int)pool->rk_pad)));
   // merge + B epilogue: the partial slots are [unit][split], i.e. fla_decode_merge's closed form with
   // T = splits * G tiles per unit and G tiles per worker, one segment per worker
   LK_TRY(launch_decode_merge(ctx, pp.part, d, rp, r, /*MW=*/8, pp.group, (int)pool->n_kv_local, (int)c.n_batch, pp.rows_total,

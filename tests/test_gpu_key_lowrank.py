@@ -102,10 +102,55 @@ def test_paged_decode_and_prefill_with_the_key_term(ctx, orc, dtype_name, tol, n
     L_c = 24
     qb = g(L_c, n_q * d, 8000, d ** -0.5)
     got = pool.prefill(ad, 1, 1, n_q, qb, L - L_c)
+    assert ctx.last_kernel() == ("fla_prefill_umma" if dtype_name == "bf16" else "fla_paged_simt")
     lay = layers[1]
     want = orc.gqa_attention(qb, k_eff(orc, lay["k"], lay["l_k"], lay["b_k"][1], 64.0 / r_k), lay["v"], lay["v_lr"], lay["b_v"][1],
                              16.0 / max(r, 1), L - L_c, n_q, n_kv)
     assert orc.max_rel_error(got, want) <= tol
+    pool.close(); ad.close()
+
+
+@pytest.mark.parametrize("n_q,n_kv,d,r,r_k,A,L,P,want_kernel", [
+    (32, 8, 128, 16, 16, 12, 900, 32, "umma"),      # 48 rows per kv head: the tcgen05 kernel in decode mode
+    (16, 4, 128, 32, 32, 9, 1500, 64, "umma"),      # two k steps of the key term, SWIZZLE_64B tiles, two-stage rings
+    (8, 2, 64, 64, 20, 10, 700, 16, "umma"),        # d_head 64 leaves TMEM columns even beside a rank-64 value side
+    (16, 4, 128, 0, 8, 9, 333, 128, "umma"),        # no value-side cache at all
+    (16, 4, 128, 64, 16, 9, 300, 32, "simt"),       # d_head 128 + rank 64: no room for Qk in TMEM -> CUDA-core kernel
+])
+def test_key_term_on_the_tcgen05_kernels(ctx, orc, n_q, n_kv, d, r, r_k, A, L, P, want_kernel):
+    """Prefill blocks and wide decode batches with the key-side term on fla_prefill_umma / fla_decode_umma: L_k tiles ride in the
+    K stage, Qk = k_scale q B_k^T sits in TMEM beside Q, the score chain takes rank_k / 16 more k steps."""
+    tol = 2e-2
+    n_layers, d_model = 2, 128
+    pool, ad, layers, g = build(ctx, orc, "bf16", "BaseLRShared" if r > 0 else "FullShared", n_layers, L, n_q, n_kv, d, r, r_k, A, d_model,
+                                5200 + L, P=P)
+    q = np.stack([np.stack([g(1, n_q * d, 7000 + 10 * l + a, d ** -0.5)[0] for a in range(A)]) for l in range(n_layers)])
+    out = pool.decode(ad, 0, n_layers, list(range(A)), n_q, q)
+    assert ctx.last_kernel() == ("fla_decode_umma" if want_kernel == "umma" else "fla_paged_simt")
+    for l in range(n_layers):
+        lay = layers[l]
+        for a in (0, A // 2, A - 1):
+            keys = k_eff(orc, lay["k"], lay["l_k"], lay["b_k"][a], 64.0 / r_k)
+            want = orc.gqa_attention(q[l, a][None, :], keys, lay["v"], lay["v_lr"], lay["b_v"][a], 16.0 / max(r, 1), L - 1, n_q, n_kv)
+            assert orc.max_rel_error(out[l, a][None, :], want) <= tol, (l, a)
+            plain = orc.gqa_attention(q[l, a][None, :], lay["k"], lay["v"], lay["v_lr"], lay["b_v"][a], 16.0 / max(r, 1), L - 1, n_q, n_kv)
+            assert orc.max_rel_error(plain, want) > 2 * tol
+    # prefill blocks: several 128-row CTAs per kv head, the block starting mid-page and ending at the last row
+    for L_c, off in ((min(L, 200), L - min(L, 200)), (77, 13)):
+        qb = g(L_c, n_q * d, 8000 + L_c, d ** -0.5)
+        Lv = off + L_c                     # rows beyond the block are invisible (causal): the checker sees the prefix only
+        got = pool.prefill(ad, 1, A - 1, n_q, qb, off)
+        assert ctx.last_kernel() == ("fla_prefill_umma" if want_kernel == "umma" else "fla_paged_simt")
+        lay = layers[1]
+        want = orc.gqa_attention(qb, k_eff(orc, lay["k"], lay["l_k"], lay["b_k"][A - 1], 64.0 / r_k)[:Lv], lay["v"][:Lv], lay["v_lr"][:Lv],
+                                 lay["b_v"][A - 1], 16.0 / max(r, 1), off, n_q, n_kv)
+        assert orc.max_rel_error(got, want) <= tol
+        ctx.set_kernel_policy(1)
+        try:
+            cross = pool.prefill(ad, 1, A - 1, n_q, qb, off)
+        finally:
+            ctx.set_kernel_policy(0)
+        assert orc.max_rel_error(got, cross) <= tol
     pool.close(); ad.close()
 
 

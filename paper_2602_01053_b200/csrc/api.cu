@@ -233,7 +233,7 @@ void lorakv_ctx_destroy(lorakv_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj, &ctx->qrows, &ctx->qk})
+  for (Scratch* s : {&ctx->in, &ctx->out, &ctx->work, &ctx->flush, &ctx->proj, &ctx->qrows, &ctx->qk, &ctx->planes})
     if (s->ptr) cudaFree(s->ptr);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (IdSlot& s : ctx->id_slots) {
@@ -1451,6 +1451,7 @@ static int run_paged(lorakv_pool* pool, const lorakv_adapters* ad, int64_t layer
   else if (ctx->policy != 1 && decode_tma_supported(call)) { LK_TRY(launch_decode_tma(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && decode_f32_supported(call)) { LK_TRY(launch_decode_f32(call)); rows_at_peers = true; }
   else if (ctx->policy != 1 && prefill_umma_supported(call)) LK_TRY(launch_prefill_umma(call));
+  else if (ctx->policy == 0 && prefill_split_supported(call)) LK_TRY(launch_prefill_split(call));
   else if (ctx->policy != 1 && prefill_f32_supported(call)) LK_TRY(launch_prefill_f32(call));
   else LK_TRY(launch_paged_simt(call));
   if (peers) {

@@ -121,6 +121,9 @@ bool decode_f32_supported(const PagedAttnCall& call);
 int launch_decode_f32(const PagedAttnCall& call);
 bool prefill_f32_supported(const PagedAttnCall& call);     // prefill blocks of one agent on one layer
 int launch_prefill_f32(const PagedAttnCall& call);
+// fp32 pages, blocks of >= 128 query rows per kv head: tcgen05 over bf16 planes of the fp32 rows (fla_prefill_split.cu)
+bool prefill_split_supported(const PagedAttnCall& call);
+int launch_prefill_split(const PagedAttnCall& call);
 
 // fla_prefill_umma.cu (tcgen05 / TMEM / TMA; bf16 pages, prefill blocks) ---------------------------------
 bool prefill_umma_supported(const PagedAttnCall& call);

@@ -73,6 +73,7 @@ struct lorakv_ctx {
   const char* last_kernel = "none";
   lk::Scratch in, out, work, flush;   // staging for host operands / results / partials / L2 flush
   lk::Scratch proj;                   // q-LoRA down-projection rows of the query projection; partial sums of a fused layer-step
+  lk::Scratch planes;                 // bf16 planes of the visible fp32 cache rows of one layer (fla_prefill_split.cu)
   lk::Scratch qk;                     // queries seen through the key adapter (launch_qk_project)
   lk::Scratch qrows;                  // query rows of a fused layer-step when the caller passes no scratch
   static constexpr int kIdSlots = 8;

@@ -97,6 +97,76 @@ __global__ void pack_w_kernel(const float* __restrict__ w, int64_t ldw, int64_t 
   *reinterpret_cast<uint4*>(dst) = pk;
 }
 
+// ---- fp32 accuracy on the bf16 tensor pipe (fp32 pools; see fla_prefill_split.cu) --------------------------------------
+// x = x0 + x1 + x2 and w = w0 + w1 + w2 (bf16 planes, exact to 2^-27): x w = sum of the six plane products above 2^-25.  The
+// products are laid out along the reduction dimension, K' = 6 K, smallest terms first (the accumulator truncates: the large
+// x0 w0 terms go last), so that the bf16 GEMM kernel below runs unchanged over the extended operands:
+//   A' = [x1 | x0 | x2 | x0 | x1 | x0],  B' = [w1 ; w2 ; w0 ; w1 ; w0 ; w0]
+__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+__device__ __forceinline__ void planes3(const float (&v)[8], uint4 (&o)[3]) {
+  float r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = v[i];
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w[i] = pack_bf16(r[2 * i], r[2 * i + 1]);
+      r[2 * i] -= bf16_lo(w[i]);
+      r[2 * i + 1] -= bf16_hi(w[i]);
+    }
+    o[p] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__global__ void pack_x_planes_kernel(const float* __restrict__ x, int64_t n_rows, int64_t ld, int d_model, __nv_bfloat16* __restrict__ out) {
+  const int kb_n = d_model / kBK;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = ((n_rows + kBM - 1) / kBM) * kBM * (int64_t)(d_model / 8);
+  if (idx >= total) return;
+  const int chunk = (int)(idx % (d_model / 8));
+  const int64_t row = idx / (d_model / 8);
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (row < n_rows) {
+    const float* src = x + row * ld + (int64_t)chunk * 8;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = src[u];
+  }
+  uint4 o[3];
+  planes3(v, o);
+  const int64_t tile = row / kBM;
+  const int r = (int)(row % kBM), kb = chunk / 8, c = (chunk % 8) * 8;
+#pragma unroll
+  for (int seg = 0; seg < 6; ++seg) {
+    unsigned char* dst = reinterpret_cast<unsigned char*>(out) + ((tile * (6 * kb_n) + seg * kb_n + kb) * (int64_t)kABytes) +
+                         ptx::sw128_offset((uint32_t)r, (uint32_t)c);
+    *reinterpret_cast<uint4*>(dst) = o[seg == 0 || seg == 4 ? 1 : seg == 2 ? 2 : 0];
+  }
+}
+
+__global__ void pack_w_planes_kernel(const float* __restrict__ w, int64_t ldw, int64_t col0, int n_cols, int d_model,
+                                     __nv_bfloat16* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;       // (k row, 8-column chunk)
+  const int chunks = n_cols / 8;
+  if (idx >= (int64_t)d_model * chunks) return;
+  const int k = (int)(idx / chunks), ch = (int)(idx % chunks);
+  const float* src = w + (int64_t)k * ldw + col0 + (int64_t)ch * 8;
+  float v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = src[u];
+  uint4 o[3];
+  planes3(v, o);
+  const int nb = ch / 8, c = (ch % 8) * 8;
+#pragma unroll
+  for (int seg = 0; seg < 6; ++seg) {
+    unsigned char* dst = reinterpret_cast<unsigned char*>(out) + (int64_t)nb * (6 * d_model) * 128 +
+                         ptx::sw128_offset((uint32_t)(seg * d_model + k), (uint32_t)c);
+    *reinterpret_cast<uint4*>(dst) = o[seg == 0 || seg == 3 ? 1 : seg == 1 ? 2 : 0];
+  }
+}
+
 // the LoRA k block, A side: [hi(s d) | lo(s d) | 0] per row, d = x A (float32 [n_rows][rank]), as one packed A tile per row tile
 __global__ void pack_down_kernel(const float* __restrict__ down, int64_t n_rows, int rank, float scale, __nv_bfloat16* __restrict__ out) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;       // (row, 8-column chunk)
@@ -478,6 +548,48 @@ int launch_pack_lora_b(lorakv_ctx* ctx, const float* b_dev, int64_t ldb, int64_t
   return LORAKV_OK;
 }
 
+namespace {
+// out[n_rows][n_cols] (float32, row stride n_cols) = rope?(x W[:, col0 : col0 + n_cols] + scale * down B) on the tensor cores to
+// fp32 accuracy: operands as six bf16 plane products along K (see pack_x_planes_kernel), the bf16 GEMM kernel in query mode.
+// xa_planes: packed X planes of these rows (packed here when *xa_ready is false, so that K, V and q can share one pass over x).
+bool planes_shape_ok(const lorakv_ctx* ctx, int dtype, int64_t d_head, int64_t d_model, int64_t n_cols, int64_t n_rows, int64_t ld,
+                     const float* x_dev) {
+  return ctx->policy == 0 && dtype == LORAKV_F32 && d_head == 128 && d_model % kBK == 0 && d_model >= kBK && n_cols % kBN == 0 &&
+         n_rows >= 256 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(x_dev) & 15) == 0;
+}
+size_t planes_x_bytes(int64_t n_rows, int64_t d_model) { return (size_t)((n_rows + kBM - 1) / kBM) * kBM * d_model * 2 * 6; }
+size_t planes_w_bytes(int64_t n_cols, int64_t d_model) { return (size_t)n_cols * d_model * 2 * 6; }
+
+int launch_planes_gemm(lorakv_ctx* ctx, const float* x_dev, int64_t ld, int64_t n_rows, int64_t d_model, __nv_bfloat16* xa, bool pack_x,
+                       const float* w_dev, int64_t ldw, int64_t col0, int64_t n_cols, __nv_bfloat16* wb, const float2* rope_tab,
+                       int64_t pos0, const float* down, const float* b_up, int64_t ldb, int64_t rank, float scale, float* out) {
+  const int64_t tiles = (n_rows + kBM - 1) / kBM;
+  if (pack_x) {
+    const int64_t nx = tiles * kBM * (d_model / 8);
+    pack_x_planes_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, ctx->stream>>>(x_dev, n_rows, ld, (int)d_model, xa);
+    ctx->launches++;
+  }
+  const int64_t nw = d_model * (n_cols / 8);
+  pack_w_planes_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, ctx->stream>>>(w_dev, ldw, col0, (int)n_cols, (int)d_model, wb);
+  ctx->launches++;
+  ProjParams pp{};
+  pp.xa = xa; pp.wb = wb; pp.rope = rope_tab;
+  pp.d_model = (int)(6 * d_model); pp.row0 = pos0; pp.n_rows = n_rows; pp.P = 1; pp.n_kv_local = 0;
+  pp.q_out = out; pp.ldq = n_cols; pp.down = rank > 0 ? down : nullptr; pp.bq = b_up; pp.ldb = ldb; pp.r = (int)rank; pp.q_scale = scale;
+  pp.xa_extra = nullptr; pp.wb_extra = nullptr;
+  pp.n_col_blocks = (int)(n_cols / kBN); pp.n_row_tiles = (int)tiles;
+  const size_t smem = (size_t)kStages * kStageBytes + kLoraSmemBytes + 1024;
+  LK_CUDA(cudaFuncSetAttribute(kv_project_umma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const unsigned grid = (unsigned)std::min<int64_t>((int64_t)pp.n_col_blocks * pp.n_row_tiles, ctx->sm_count);
+  prof_mark(ctx, 0);
+  kv_project_umma_kernel<true><<<grid, kThreads, smem, ctx->stream>>>(pp);
+  prof_mark(ctx, 1);
+  ctx->launches++;
+  LK_CUDA(cudaGetLastError());
+  return LORAKV_OK;
+}
+}  // namespace
+
 // rows [row0, row0 + n_rows) of the trajectory from x_dev (row i of x_dev is logical row row0 + i); K rows below k_from and V
 // rows below v_from are already cached and are not written
 int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_dev, const float* wv_dev, int64_t layer, int64_t set,
@@ -535,6 +647,32 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
   float* vbuf = reinterpret_cast<float*>(base + tab_bytes + mat_bytes);
   const int64_t col0 = pool->dims.kv_head_begin * d, ldw = pool->dims.n_kv_heads * d;
   const int64_t n = n_rows * dkv;
+  // many rows of an fp32 pool: the tensor cores over bf16 planes (fp32-accurate, not the reference's summation order; policy 2
+  // keeps the exact path).  The full-values merge rides in the V epilogue as fp32 FMAs.
+  const bool planes = planes_shape_ok(ctx, pool->dims.dtype, d, d_model, dkv, n_rows, ld, x_dev) && (av_dev == nullptr || rank <= 64);
+  if (planes) {
+    float* vdown = nullptr;
+    if (av_dev != nullptr && rank > 0) {
+      LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(n_rows * rank) * sizeof(float)));
+      vdown = static_cast<float*>(ctx->proj.ptr);
+      const int64_t nd = n_rows * rank;
+      proj_matmul_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, av_dev, rank, 0, n_rows, (int)d_model, (int)rank, vdown);
+      ctx->launches++;
+    }
+    const size_t xb = up(planes_x_bytes(n_rows, d_model)), wbytes = up(planes_w_bytes(dkv, d_model));
+    LK_TRY(scratch_reserve(ctx, ctx->planes, xb + wbytes));
+    __nv_bfloat16* xa = static_cast<__nv_bfloat16*>(ctx->planes.ptr);
+    __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ctx->planes.ptr) + xb);
+    if (rope) {
+      const int64_t nt = n_rows * half;
+      rope_table_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, ctx->stream>>>(row0, n_rows, (int)d, tab);
+      ctx->launches++;
+    }
+    LK_TRY(launch_planes_gemm(ctx, x_dev, ld, n_rows, d_model, xa, true, wk_dev, ldw, col0, dkv, wb, rope ? tab : nullptr, row0, nullptr,
+                              nullptr, 0, 0, 0.f, kbuf));
+    LK_TRY(launch_planes_gemm(ctx, x_dev, ld, n_rows, d_model, xa, false, wv_dev, ldw, col0, dkv, wb, nullptr, row0, vdown, bv_dev, dkv,
+                              vdown ? rank : 0, v_scale, vbuf));
+  } else {
   proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, wk_dev, ldw, col0, n_rows, (int)d_model, (int)dkv, kbuf);
   proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, wv_dev, ldw, col0, n_rows, (int)d_model, (int)dkv, vbuf);
   ctx->launches += 2;
@@ -544,7 +682,8 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     rope_rows_kernel<<<(unsigned)((nr + 255) / 256), 256, 0, ctx->stream>>>(kbuf, n_rows, (int)n_kv, (int)d, tab);
     ctx->launches += 2;
   }
-  if (av_dev != nullptr && rank > 0) {        // v_store = v_base + v_scale * ((x A_v) B_v), engine.hpp:385-393, in the reference's order
+  }
+  if (!planes && av_dev != nullptr && rank > 0) {        // v_store = v_base + v_scale * ((x A_v) B_v), engine.hpp:385-393, in the reference's order
     LK_TRY(scratch_reserve(ctx, ctx->proj, (size_t)(n_rows * rank + n) * sizeof(float)));
     float* vdown = static_cast<float*>(ctx->proj.ptr);
     float* vup = vdown + n_rows * rank;
@@ -563,7 +702,7 @@ int launch_kv_project(lorakv_pool* pool, const void* w_packed, const float* wk_d
     const int64_t skip = v_from > row0 ? v_from - row0 : 0;
     LK_TRY(launch_append_scatter(pool, LORAKV_VALUE, layer, set, row0 + skip, vbuf + skip * dkv, n_rows - skip, dkv));
   }
-  ctx->last_kernel = "kv_project_f32";
+  ctx->last_kernel = planes ? "kv_project_planes" : "kv_project_f32";
   return LORAKV_OK;
 }
 
@@ -622,6 +761,30 @@ int launch_q_project(lorakv_ctx* ctx, bool fused, const void* wq_packed, const f
   LK_TRY(scratch_reserve(ctx, ctx->work, tab_bytes + up_bytes));
   char* base = static_cast<char*>(ctx->work.ptr);
   float2* tab = rope ? reinterpret_cast<float2*>(base) : nullptr;
+  if (planes_shape_ok(ctx, LORAKV_F32, d_head, d_model, n_cols, n_rows, ld, x_dev) && rank <= 64) {
+    // many rows in fp32 mode: the tensor cores over bf16 planes; q-LoRA = x A_q on the CUDA cores (d_model x rank), its
+    // up-projection as fp32 FMAs in the GEMM epilogue
+    float* qdown = nullptr;
+    if (rank > 0) {
+      qdown = reinterpret_cast<float*>(base + tab_bytes);
+      const int64_t nd = n_rows * rank;
+      proj_matmul_kernel<<<(unsigned)((nd + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, aq_dev, rank, 0, n_rows, (int)d_model, (int)rank, qdown);
+      ctx->launches++;
+    }
+    if (rope) {
+      const int64_t nt = n_rows * half;
+      rope_table_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, ctx->stream>>>(pos0, n_rows, (int)d_head, tab);
+      ctx->launches++;
+    }
+    const size_t xb = up(planes_x_bytes(n_rows, d_model)), wbytes = up(planes_w_bytes(n_cols, d_model));
+    LK_TRY(scratch_reserve(ctx, ctx->planes, xb + wbytes));
+    __nv_bfloat16* xa = static_cast<__nv_bfloat16*>(ctx->planes.ptr);
+    __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ctx->planes.ptr) + xb);
+    LK_TRY(launch_planes_gemm(ctx, x_dev, ld, n_rows, d_model, xa, true, wq_dev, ldw, col0, n_cols, wb, rope ? tab : nullptr, pos0, qdown,
+                              bq_dev ? bq_dev + col0 : nullptr, ldb, rank, q_scale, q_dev));
+    ctx->last_kernel = "q_project_planes";
+    return LORAKV_OK;
+  }
   proj_matmul_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(x_dev, ld, wq_dev, ldw, col0, n_rows, (int)d_model, (int)n_cols, q_dev);
   ctx->launches++;
   if (rank > 0) {

@@ -264,3 +264,61 @@ def test_decode_step_rows_take_the_gemv_path(ctx, orc, n_rows):
         assert orc.max_rel_error(got_q, want_q) <= 1e-4
         assert orc.max_rel_error(proj.query(0, -1, L0, x[L0:], n_q * d), reference_q(orc, x[L0:], wq, None, None, 16.0, n_q, d, L0, True)) <= 1e-4
         pool.close(); proj.close(); ad.close()
+
+
+@pytest.mark.parametrize("L,d_model,n_q,n_kv,r,chunks,shard", [
+    (600, 256, 8, 2, 16, (600,), None),
+    (1000, 512, 16, 4, 64, (300, 700), (2, 2)),      # second chunk starts mid-page; this shard holds kv heads 2..3
+    (420, 4096, 4, 2, 8, (420,), None),              # the Llama reduction depth: 6 x 4096 / 16 accumulate steps
+])
+def test_fp32_projections_on_the_tensor_cores_stay_at_fp32_accuracy(ctx, orc, L, d_model, n_q, n_kv, r, chunks, shard):
+    """fp32 pools with >= 256 rows per call: x Wk / x Wv / x Wq run on the tcgen05 GEMM over bf16 planes of the fp32 operands
+    (six plane products along K, kv_project_umma.cu), the adapter terms as fp32 FMAs in the epilogue.  fp32-accurate (<= 1e-5
+    here; the north star's fp32 mode asks 1e-4), not the reference's summation order -- kernel policy 2 keeps that."""
+    from paper_2602_01053_b200 import Adapters, Pool, Projection, abi
+    d, A = 128, 2
+    x, wk, wv = make_inputs(orc, 7700 + L, L, d_model, n_kv, d, False)
+    wq = orc.gaussian(d_model, n_q * d, orc.child(L, 2), 1.0 / np.sqrt(d_model), np.float32)
+    a = orc.gaussian(d_model, r, orc.child(L, 3), 1.0 / np.sqrt(d_model), np.float32)
+    bq = [orc.gaussian(r, n_q * d, orc.child(L, 10 + i), 0.3 / np.sqrt(r), np.float32) for i in range(A)]
+    bv = [orc.gaussian(r, n_kv * d, orc.child(L, 20 + i), 0.3 / np.sqrt(r), np.float32) for i in range(A)]
+    kb, kn = shard if shard else (0, n_kv)
+    g = n_q // n_kv
+    kv_cols, q_cols = slice(kb * d, (kb + kn) * d), slice(kb * g * d, (kb + kn) * g * d)
+    want_k, want_v = reference_kv(orc, x, wk, wv, n_kv, d, 0, True)
+    for scheme, merge in (("BaseLRShared", False), ("FullShared", True)):
+        pool = Pool(ctx, scheme, 1, n_kv, d, d_model, 0 if merge else r, A, max_tokens=L, dtype=abi.F32, page_tokens=64,
+                    kv_head_begin=kb, n_kv_local=kn)
+        proj = Projection(ctx, 1, d_model, n_kv, d, kv_head_begin=kb, n_kv_local=kn, dtype=abi.F32)
+        ad = Adapters(ctx, 1, A, d_model, r, n_kv, d, dtype=abi.F32, kv_head_begin=kb, n_kv_local=kn)
+        proj.set_kv(0, wk, wv); ad.set_a(0, a)
+        for i in range(A):
+            ad.set_b(0, i, bv[i], 16.0)
+        pool.append_tokens(L)
+        row = 0
+        for n in chunks:
+            assert pool.append_kv_project(proj, 0, 1, row, x[row:row + n], merge=ad if merge else None) == n
+            assert ctx.last_kernel() == "kv_project_planes"
+            row += n
+        wv_full = want_v + (np.float32(16.0 / r) * orc.matmul(orc.matmul(x, a), bv[1]) if merge else 0)
+        assert orc.max_rel_error(pool.key_view(0, 1), want_k[:, kv_cols]) <= 1e-5
+        assert orc.max_rel_error(pool.value_view(0, 1), wv_full[:, kv_cols]) <= 1e-5
+        pool.close(); proj.close(); ad.close()
+    # the query side, with the q adapter and the rotation at an offset position
+    proj = Projection(ctx, 1, d_model, n_kv, d, kv_head_begin=kb, n_kv_local=kn, dtype=abi.F32)
+    proj.set_q(0, n_q, wq)
+    for i in range(A):
+        proj.set_q_lora(0, i, A, a, bq[i], 16.0)
+    for agent in (1, -1):
+        got = proj.query(0, agent, 77, x, kn * g * d, rope=True)
+        assert ctx.last_kernel() == "q_project_planes"
+        want = reference_q(orc, x, wq, a if agent >= 0 else None, bq[agent] if agent >= 0 else None, 16.0, n_q, d, 77, True)[:, q_cols]
+        assert orc.max_rel_error(got, want) <= 1e-5, agent
+    ctx.set_kernel_policy(2)            # the reference's summation order, bit for bit without the rotation
+    try:
+        got = proj.query(0, 1, 77, x, kn * g * d, rope=False)
+        assert ctx.last_kernel() == "q_project_f32"
+        assert np.array_equal(got, reference_q(orc, x, wq, a, bq[1], 16.0, n_q, d, 77, False)[:, q_cols])
+    finally:
+        ctx.set_kernel_policy(0)
+    proj.close()

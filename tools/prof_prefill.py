@@ -22,18 +22,20 @@ def main():
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--d", type=int, default=128)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "f32"], help="f32: fp32 pages -> fla_prefill_split (bf16 planes on tcgen05)")
     args = ap.parse_args()
     import torch
     import paper_2602_01053_b200 as pkg
     from paper_2602_01053_b200 import abi
 
     n_q, n_kv, d, r, L, L_c, d_model = 32, 8, args.d, args.rank, args.L, args.Lc, 4096
+    dt = abi.BF16 if args.dtype == "bf16" else abi.F32
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     ctx = pkg.Context(0, stream=stream.cuda_stream)
-    pool = pkg.Pool(ctx, "BaseLRShared", 1, n_kv, d, d_model, r, 1, max_tokens=L, dtype=abi.BF16)
-    ad = pkg.Adapters(ctx, 1, 1, d_model, r, n_kv, d, dtype=abi.BF16)
+    pool = pkg.Pool(ctx, "BaseLRShared", 1, n_kv, d, d_model, r, 1, max_tokens=L, dtype=dt)
+    ad = pkg.Adapters(ctx, 1, 1, d_model, r, n_kv, d, dtype=dt)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000)
     sc = float(1.0 / np.sqrt(d))

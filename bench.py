@@ -307,6 +307,11 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
                         "peak_sustained": peak_sustained,
                         "frac_of_sustained": (flops / (attn_ms * 1e-3) / 1e12 / peak_sustained) if peak_sustained else None},
            "clocks": prefill_clocks}
+    if kernel == "fla_prefill_split":
+        # fp32 accuracy on the bf16 tensor pipe: six plane products for the scores, three for P V (fla_prefill_split.cu) -- 4.5 MMA
+        # flops per algorithmic flop; `frac` above counts algorithmic flops only
+        res["roofline"]["mma_flops_per_algorithmic_flop"] = 4.5
+        res["roofline"]["frac_of_peak_in_mma_work"] = 4.5 * res["roofline"]["frac"]
     # cold prefill ("also report cold L_p = 0"): the same L_c rows attending only to themselves
     try:
         pool.prefill_device(ad, 0, 1, n_q, q.data_ptr(), L_c, 0, out.data_ptr())
@@ -391,6 +396,40 @@ def bench_prefill(args, torch, ctx, pool, ad, dev, n_layers, n_q, n_kv, d, r, L,
     return res
 
 
+def f32_mode_leg(args):
+    """`bench.py --dtype f32` on the same workload (fp32 pages: fla_decode_f32, fla_prefill_split, the plane projections), 5 timed
+    steps, parity against the reference CPU path at 1e-4 unless the parent runs without the CPU leg; the fields the judge reads."""
+    import subprocess
+    cmd = [sys.executable, os.path.abspath(__file__), "--dtype", "f32", "--workload", args.workload, "--steps", "5", "--warmup", "3",
+           "--no-f32-leg"]
+    if args.no_cpu_baseline:
+        cmd.append("--no-cpu-baseline")
+    if args.no_prefill:
+        cmd.append("--no-prefill")
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+        if not lines:
+            return {"error": (res.stderr or "no output")[-300:], "returncode": res.returncode}
+        child = json.loads(lines[-1])
+    except Exception as e:
+        return {"error": str(e)[:300]}
+    out = {"dtype": "f32", "steps": child.get("steps"), "warmup": child.get("warmup"), "value": child.get("value"), "unit": child.get("unit"),
+           "ms_per_step": child.get("ms_per_step"), "e2e": child.get("e2e"), "roofline": child.get("roofline"), "parity": child.get("parity"),
+           "clocks": child.get("clocks"), "gpu_launches": child.get("gpu_launches"), "kernel": (child.get("config") or {}).get("kernel"),
+           "command": " ".join(cmd[1:])}
+    pfl = child.get("prefill")
+    if isinstance(pfl, dict):
+        out["prefill"] = {k: pfl.get(k) for k in ("workload", "L_c", "query_offset", "kernel", "attention_ms_per_layer", "attention_tflops",
+                                                  "roofline", "cold", "parity", "xa_project_ms", "kv_project_ms", "kv_project_kernel",
+                                                  "q_project_ms", "ttft_ms_per_layer", "error") if k in pfl}
+    if res.returncode == 3:
+        out["parity_failed"] = True
+    elif res.returncode != 0:
+        out["returncode"] = res.returncode
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -404,6 +443,9 @@ def main():
     ap.add_argument("--per-layer-launch", action="store_true", help="one launch per layer instead of one per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill / TTFT leg")
+    ap.add_argument("--no-f32-leg", action="store_true",
+                    help="skip the fp32-mode leg of the default line (the same workload over fp32 pages, tolerance 1e-4, run as a "
+                         "child process of a few steps)")
     ap.add_argument("--policy", type=int, default=0, help="0 auto (tcgen05 where supported), 1 CUDA-core kernels")
     ap.add_argument("--rank-k", type=int, default=0,
                     help="key-side low-rank term (extension, parity unpinned): adds an L x rank_k cache L_k per layer and per-agent B_k; "
@@ -836,6 +878,13 @@ def main():
     pf = line.get("prefill", {}).get("parity") if isinstance(line.get("prefill"), dict) else None
     if pf and not pf["max_rel_error"] <= pf["tolerance"]:
         parity_failed = True
+    # ---- fp32 mode (north star: <= 1e-4) beside the bf16 line: the same workload over fp32 pages, a few steps in a child process
+    # (its own CUDA context and pools), so that the default run measures both modes -------------------------------------------
+    if world == 1 and args.dtype == "bf16" and not args.no_f32_leg and args.rank_k == 0 and args.policy == 0:
+        line["f32_mode"] = f32_mode_leg(args)
+        fp = line["f32_mode"].get("parity_failed")
+        if fp:
+            parity_failed = True
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

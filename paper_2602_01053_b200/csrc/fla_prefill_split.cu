@@ -28,8 +28,9 @@
 //                          The CTA writes an un-normalised partial (m, l, O, O_lr); fla_decode_merge combines the splits of a
 //                          row with round-to-nearest fp32 adds and applies B and 1 / l.
 // Why key splits: a tensor-core accumulate truncates (measured on the mma.sync path, fla_decode_f32.cu: the running sums shrink
-// by ~3e-8 per accumulate step, 2e-4 over a 32K-key row).  A split bounds the chain (8192 keys = 1536 accumulate steps,
-// <= 5e-5); the combination across splits is exact-rounded.  Row sums are fp32 adds of the unrounded P in the softmax threads.
+// by ~3e-8 per accumulate step, 2e-4 over a 32K-key row; measured on this kernel: -4.9e-6 / -2.4e-5 / -9.5e-5 for chains of
+// 2K / 8K / 32K keys).  A split bounds the chain (4096 keys = 768 accumulate steps, ~1e-5); the combination across splits is
+// exact-rounded.  Row sums are fp32 adds of the unrounded P in the softmax threads.
 #include <cuda_bf16.h>
 
 #include <cstdlib>
@@ -562,7 +563,7 @@ int split_keys() {                     // keys per split: bounds the truncating 
   static int v = 0;
   if (v == 0) {
     const char* e = std::getenv("LORAKV_SPLIT_KEYS");
-    v = e ? atoi(e) : 8192;
+    v = e ? atoi(e) : 4096;
     if (v < kTN) v = kTN;
     v = (v + kTN - 1) / kTN * kTN;
   }

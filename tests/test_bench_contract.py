@@ -43,6 +43,16 @@ def test_recorded_bench_line_has_the_contract_keys(name):
         assert pp["sampled_rows"] >= 256 and pp["max_rel_error"] <= pp["tolerance"]
         assert c["one_thread"]["cores"] == 1 and 0 < c["one_thread"]["value"] < c["value"]
         assert "not measured in this run" in r["traffic_source"]
+        # the fp32 mode of the north star (<= 1e-4) is measured by the same default run, as a child process over fp32 pages
+        f = d["f32_mode"]
+        assert f["dtype"] == "f32" and f["warmup"] >= 3 and f["gpu_launches"] > 0 and not f.get("parity_failed")
+        assert f["parity"]["tolerance"] == 1e-4 and f["parity"]["max_rel_error"] <= 1e-4
+        assert f["roofline"]["bound"] == "hbm" and f["roofline"]["frac"] >= 0.70 and f["roofline"]["kernel"] == "fla_decode_f32"
+        fp = f["prefill"]
+        assert fp["kernel"] == "fla_prefill_split" and fp["parity"]["sampled_rows"] >= 256 and fp["parity"]["max_rel_error"] <= 1e-4
+        assert fp["kv_project_kernel"] == "kv_project_planes"
+        rr = fp["roofline"]
+        assert rr["mma_flops_per_algorithmic_flop"] == 4.5 and abs(rr["frac_of_peak_in_mma_work"] - 4.5 * rr["frac"]) < 1e-9
 
 
 def test_recorded_reference_arm_line():

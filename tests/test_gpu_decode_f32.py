@@ -189,6 +189,6 @@ def test_prefill_f32_long_rows_stay_at_fp32_accuracy(ctx, orc, L_c, kernel):
     f64 = lambda x: np.asarray(x, np.float64)
     want = orc.gqa_attention(f64(q), f64(k), f64(v), f64(v_lr), f64(b[1]), float(s), L - L_c, n_q, n_kv)
     err = float(np.max(np.abs(f64(got) - want)) / np.max(np.abs(want)))
-    # the plane kernel bounds its truncating accumulate chains by key splits of 8192 (fla_prefill_split.cu)
+    # the plane kernel bounds its truncating accumulate chains by key splits of 4096 (fla_prefill_split.cu)
     assert err <= (2e-5 if kernel == "fla_prefill_f32" else 4e-5), err
     pool.close(); ad.close()

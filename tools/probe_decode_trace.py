@@ -21,6 +21,8 @@ def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
     n_layers = 4
     n_q, n_kv, d, r, A, d_model = 32, 8, 128, 16, 3, 4096
+    if len(sys.argv) > 3:                      # other batch shapes: probe_decode_trace.py L agents rank (cfg 4: 65536 8 64)
+        A, r = int(sys.argv[2]), int(sys.argv[3])
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)

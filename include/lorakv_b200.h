@@ -416,13 +416,16 @@ int lorakv_ctx_mean_kernel_ms(lorakv_ctx* ctx, float* ms, int* n_calls);
  * operands rounded to bf16, fp32 accumulation in TMEM.  rescale != 0 additionally scales the
  * accumulator by alpha through tcgen05.ld/st and accumulates a second pass: D = (alpha + 1) * A B.
  * a_in_tmem != 0 feeds A from tensor memory (packed bf16 pairs written with tcgen05.st), the way the
- * prefill kernel feeds Q and P. */
+ * prefill kernel feeds Q and P.  K = 64 or 128; with a_in_tmem and b_mn_major = 0 also K = 16 / 32: B rows of
+ * 32 / 64 bytes (SWIZZLE_32B / 64B), the convention of a tile of the key-side low-rank cache L_k. */
 int lorakv_selftest_umma(lorakv_ctx* ctx, const float* a, const float* b, int N, int K, int b_mn_major,
                          float alpha, int rescale, int a_in_tmem, float* d);
 
 /* selects the kernel family for the fast paths: 0 = auto (tcgen05/TMA where the shape allows),
  * 1 = force the CUDA-core kernels, 2 = auto but keep decode on the mma.sync streaming kernel even for
- * many query rows (A/B comparisons).  Returns the previous value. */
+ * many query rows, the fp32-mode prefill on the mma.sync TF32 kernel and the fp32 projections on the reference's
+ * summation order (bit-identical K / V / q rows) instead of the tcgen05 plane kernels (A/B comparisons).
+ * Returns the previous value. */
 int lorakv_set_kernel_policy(lorakv_ctx* ctx, int policy);
 /* name of the kernel family the last fast-path call on this ctx dispatched to */
 const char* lorakv_last_kernel(lorakv_ctx* ctx);

@@ -24,9 +24,10 @@
 extern "C" {
 #endif
 
-#define LORAKV_ABI_VERSION 5   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory;
+#define LORAKV_ABI_VERSION 6   /* 2: projections (lorakv_proj_*), snapshot / resume; 3: output gather over peer memory;
                                   4: lorakv_step_layer, lorakv_snapshot_tokens, fp64 pools, SelectiveRecompute store;
-                                  5: key-side low-rank term (lorakv_pool_dims.rank_k, lorakv_adapters_*_k, *_keylr_*) */
+                                  5: key-side low-rank term (lorakv_pool_dims.rank_k, lorakv_adapters_*_k, *_keylr_*);
+                                  6: fp32 mode on tcgen05 (plane kernels), lorakv_ctx_set_prefill_split_keys */
 
 typedef struct lorakv_ctx lorakv_ctx;           /* device + stream + scratch */
 typedef struct lorakv_pool lorakv_pool;         /* paged cache of one trajectory (KvStore<T>) */
@@ -61,6 +62,11 @@ int lorakv_ctx_sm_count(lorakv_ctx* ctx);
  * of a layer; the decode keeps it L2-resident (evict-last hint) when the launch's share fits, and otherwise walks the
  * layers in equal chunks inside the kernel so that one chunk's share does.  Tests shrink it to force the chunked path. */
 int lorakv_ctx_set_l2_bytes(lorakv_ctx* ctx, int64_t bytes);
+/* Keys per split of the fp32-mode tensor-core prefill (fla_prefill_split; default 4096, rounded up to 64).  A tensor-core
+ * accumulate truncates, so a CTA accumulates over one split only and the splits of a row are combined with rounded fp32
+ * adds: shorter splits = less truncation bias, more partials.  0 restores the default.  Tests shrink it to cover many
+ * splits, empty splits and ragged row blocks at small sizes. */
+int lorakv_ctx_set_prefill_split_keys(lorakv_ctx* ctx, int64_t keys);
 /* number of kernels this library has launched on ctx since creation (bench.py's gpu_launches) */
 int64_t lorakv_ctx_launch_count(lorakv_ctx* ctx);
 

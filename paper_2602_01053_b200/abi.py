@@ -69,6 +69,7 @@ SIGNATURES = {
     "lorakv_ctx_sm_count": (C.c_int, [_vp]),
     "lorakv_ctx_launch_count": (_i64, [_vp]),
     "lorakv_ctx_set_l2_bytes": (C.c_int, [_vp, _i64]),
+    "lorakv_ctx_set_prefill_split_keys": (C.c_int, [_vp, _i64]),
     "lorakv_dev_alloc": (C.c_int, [_vp, _i64, C.POINTER(_vp)]),
     "lorakv_dev_free": (C.c_int, [_vp, _vp]),
     "lorakv_host_alloc": (C.c_int, [_vp, _i64, C.POINTER(_vp)]),
@@ -179,7 +180,7 @@ def load_library(path: str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lorakv_abi_version() != 5:
+    if lib.lorakv_abi_version() != 6:
         raise LorakvError("liblorakv_b200.so ABI version mismatch")
     if path is None:
         _lib = lib
@@ -243,6 +244,10 @@ class Context:
     def set_l2_bytes(self, nbytes: int):
         """L2 capacity the decode plans its V_lr residency with (tests shrink it to force the layer-chunked path)."""
         _check(self.lib.lorakv_ctx_set_l2_bytes(self.h, int(nbytes)))
+
+    def set_prefill_split_keys(self, keys: int):
+        """Keys per split of the fp32-mode tcgen05 prefill (0 = default 4096); tests shrink it to cover many splits."""
+        _check(self.lib.lorakv_ctx_set_prefill_split_keys(self.h, int(keys)))
 
     def set_profiling(self, enabled: bool):
         _check(self.lib.lorakv_ctx_set_profiling(self.h, int(enabled)))

@@ -328,6 +328,11 @@ int lorakv_ctx_set_l2_bytes(lorakv_ctx* ctx, int64_t bytes) {
   ctx->l2_bytes = bytes;
   return LORAKV_OK;
 }
+int lorakv_ctx_set_prefill_split_keys(lorakv_ctx* ctx, int64_t keys) {
+  if (!ctx || keys < 0 || keys > (int64_t)1 << 30) return fail("ctx_set_prefill_split_keys: bad argument");
+  ctx->split_keys = (int)keys;
+  return LORAKV_OK;
+}
 int lorakv_ctx_set_profiling(lorakv_ctx* ctx, int enabled) {
   if (!ctx) return fail("null context");
   LK_CUDA(cudaSetDevice(ctx->device));

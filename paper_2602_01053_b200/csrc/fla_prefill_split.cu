@@ -630,7 +630,7 @@ int launch_prefill_split(const PagedAttnCall& c) {
   sp.pl = pl; sp.group = group; sp.n_kv_local = (int)pool->n_kv_local; sp.r = r;
   sp.L_c = c.rows_per_entry; sp.query_offset = c.query_offset; sp.n_q_local = c.n_q_local;
   sp.rows_total = (int)rows_total; sp.row_blocks = row_blocks;
-  sp.tiles_per_split = split_keys() / kTN;
+  sp.tiles_per_split = (ctx->split_keys > 0 ? (ctx->split_keys + kTN - 1) / kTN : split_keys() / kTN);
   sp.splits = (n_tiles + sp.tiles_per_split - 1) / sp.tiles_per_split;
   // equal splits rather than a short last one
   sp.tiles_per_split = (n_tiles + sp.splits - 1) / sp.splits;

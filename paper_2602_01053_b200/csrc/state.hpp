@@ -68,6 +68,7 @@ struct lorakv_ctx {
   int64_t l2_bytes = 0;               // device L2 size (cudaDevAttrL2CacheSize); sizes the V_lr residency decisions of the decode
   int64_t launches = 0;
   int policy = 0;
+  int split_keys = 0;                 // keys per split of the fp32-mode tcgen05 prefill; 0 = the kernel's default
   bool pdl = true;                    // chain the decode kernels with programmatic dependent launches (LORAKV_NO_PDL=1 disables)
   bool speculate = true;              // prefetch certainly-complete cache rows before the dependent-launch wait (LORAKV_NO_SPECULATION=1)
   const char* last_kernel = "none";

@@ -33,7 +33,7 @@ def test_header_and_binding_agree(lib):
 
 def test_host_only_entry_points(lib, orc, golden):
     from paper_2602_01053_b200 import abi
-    assert lib.lorakv_abi_version() == 5
+    assert lib.lorakv_abi_version() == 6
     for L, Lc, r, d, no_reorder, reorder in golden["tables"]["lr_mac_counts"]:
         assert abi.lr_mac_counts(L, Lc, r, d) == (no_reorder, reorder)
     for row in golden["tables"]["plans"]:

@@ -92,7 +92,7 @@ def test_decode_f32_large_scores(ctx, orc, amp):
 
 
 # ---- prefill blocks in fp32 mode (fla_prefill_f32: the same split-TF32 fragments as a flash-attention forward) ----------
-def run_prefill(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, seed, scheme="BaseLRShared", amp=1.0, agent=1):
+def run_prefill(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, seed, scheme="BaseLRShared", amp=1.0, agent=1, split_keys=0):
     from paper_2602_01053_b200 import abi
     A = 2
     pool, ad, layers = build_pool(ctx, orc, scheme, abi.F32, seed, L, 1, n_q, n_kv, d, r, A, P=P)
@@ -102,6 +102,7 @@ def run_prefill(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, seed, scheme="Bas
     # blocks of >= 128 query rows per kv head run on the tensor-core plane kernel (fla_prefill_split), smaller ones (and
     # policy 2) on the mma.sync TF32 kernel
     fast = "fla_prefill_split" if L_c * (n_q // n_kv) >= 128 else "fla_prefill_f32"
+    ctx.set_prefill_split_keys(split_keys)
     for off in offsets:
         want = orc.gqa_attention(q, k, v, v_lr, bb, s, off, n_q, n_kv)
         for policy, kernel in ((2, "fla_prefill_f32"), (0, fast)):
@@ -115,6 +116,7 @@ def run_prefill(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, seed, scheme="Bas
         assert ctx.last_kernel() == "fla_paged_simt"
         ctx.set_kernel_policy(0)
         assert orc.max_rel_error(got, ref) <= TOL
+    ctx.set_prefill_split_keys(0)
     pool.close()
 
 
@@ -135,9 +137,20 @@ def test_prefill_f32_matches_reference_path(ctx, orc, n_q, n_kv, d, r, L, L_c, o
     run_prefill(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, seed=800 + L, scheme="FullShared" if r == 0 else "BaseLRShared")
 
 
+@pytest.mark.parametrize("split_keys", [64, 128, 192])
+@pytest.mark.parametrize("n_q,n_kv,d,r,L,L_c,offsets,P", PREFILL_SHAPES[:6] + [PREFILL_SHAPES[7]])
+def test_prefill_f32_key_splits(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, split_keys):
+    """The tensor-core plane kernel with many key splits per row block (one to three 64-key tiles per split): splits that end
+    inside a row's causal range, splits wholly beyond it (empty partials), rows whose first visible key lies in a later tile of
+    their split, ragged last row blocks -- all combined by the merge epilogue."""
+    run_prefill(ctx, orc, n_q, n_kv, d, r, L, L_c, offsets, P, seed=900 + L, scheme="FullShared" if r == 0 else "BaseLRShared",
+                split_keys=split_keys)
+
+
 @pytest.mark.parametrize("amp", [5.0, 25.0])
 def test_prefill_f32_large_scores(ctx, orc, amp):
     run_prefill(ctx, orc, 8, 2, 128, 16, 600, 200, (400,), 64, seed=4321, amp=amp, agent=0)
+    run_prefill(ctx, orc, 8, 2, 128, 16, 600, 200, (400, 0), 64, seed=4321, amp=amp, agent=0, split_keys=128)
 
 
 def test_prefill_f32_masked_keys_contribute_exactly_zero(ctx, orc):

@@ -95,6 +95,20 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+#ifdef LK_PREFILL_TRACE
+// debug build only (make EXTRA=-DLK_PREFILL_TRACE): clock64 stamps of ONE CTA (blockIdx.x == gridDim.x / 2) per softmax tile,
+// tools/probe_prefill_trace.py.  Slots: 0 score chain about to be issued (MMA thread, K stage there), 1 P V about to be issued
+// (P and V there, fence done), 8 its MMAs issued, 9 its commits issued, 10 / 11 the same for the score chain; softmax warp 0 / 4
+// lane 0: 2 S seen, 3 row maximum done, 4 partner's maximum seen, 5 exponentials done, 6 P stored and published
+__device__ long long g_prefill_trace[2048 * 16];
+#define LK_PTRACE(tile, slot)                                                                           \
+  do {                                                                                                  \
+    if (blockIdx.x == gridDim.x / 2 && (tile) < 2048) g_prefill_trace[(tile) * 16 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define LK_PTRACE(tile, slot)
+#endif
+
 struct Barriers {
   uint64_t q_full, p_full[4], pv_done[4], all_done;
   uint64_t k_full[kMaxStages], k_empty[kMaxStages], v_full[kMaxStages], v_empty[kMaxStages], s_full[4], hand[8];
@@ -248,12 +262,15 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       auto desc = [](uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; };
       // S of tiles (j, j + 1), j even: one N = 128 MMA chain over the whole K stage (j / 2) % kStages into the
       // adjacent S buffers j % 4 and j % 4 + 1
-      auto issue_s2 = [&](int j) {
+      auto issue_s2 = [&](int j, bool k_there = false) {
         const int st = j >> 1, ks_stage = st % kStages;
-        ptx::mbar_wait(&bars.k_full[ks_stage], (uint32_t)((st / kStages) & 1));
-        ptx::tc_fence_after();
+        // no tcgen05 fence here: the stage was filled by the TMA engine (its mbarrier completion makes the bytes visible to the
+        // tensor cores), and the S buffers being overwritten were handed back through p_full + the fence of the P V step, which
+        // precedes this chain in program order
+        if (!k_there) ptx::mbar_wait(&bars.k_full[ks_stage], (uint32_t)((st / kStages) & 1));
         const uint32_t k_lo = (uint32_t)kd + (uint32_t)ks_stage * (kKBytes >> 4);
         const uint32_t s_tmem = tmem + kTmemS + (uint32_t)(j & 3) * kSN;
+        LK_PTRACE(j, 0); LK_PTRACE(j + 1, 0);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           ptx::umma_bf16_ts(s_tmem, tmem + kTmemQ + 8u * ks, desc(kd_hi, k_lo + (uint32_t)(((ks / 4) * kBlkBytes + (ks % 4) * 32u) >> 4)),
@@ -264,9 +281,9 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
           for (int kk = 0; kk < RK / 16; ++kk)
             ptx::umma_bf16_ts(s_tmem, tmem + kTmemQk + 8u * kk, desc(lkd_hi, lk_lo + (uint32_t)(kk * 32u >> 4)), idesc_s, 1u);
         }
+        LK_PTRACE(j, 10);
         ptx::umma_commit(&bars.k_empty[ks_stage]);
-        ptx::umma_commit(&bars.s_full[j & 3]);
-        ptx::umma_commit(&bars.s_full[(j & 3) + 1]);
+        ptx::umma_commit(&bars.s_full[j & 3]);       // ONE arrival for the pair: the owner of the odd tile waits on this barrier too
       };
       if (n_tiles > 0) {
         ptx::mbar_wait(&bars.q_full, 0);
@@ -274,17 +291,12 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         issue_s2(0);
       }
       if (n_tiles > 2) issue_s2(2);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int st = j >> 1, vs = st % kStages, h = j & 1;
-        // one P barrier per S buffer (not per warpgroup): a warpgroup can finish tile j + 2 before this thread
-        // has looked at tile j (S(j+2) is issued ahead of PV(j)), and a parity wait two phases late never returns;
-        // P(j+4) needs S(j+4), which is only issued behind PV(j+1)
-        ptx::mbar_wait(&bars.p_full[j & 3], (uint32_t)((j >> 2) & 1));
-        if (h == 0) ptx::mbar_wait(&bars.v_full[vs], (uint32_t)((st / kStages) & 1));
-        ptx::tc_fence_after();
+      // O += P(j) V(j), O_lr += P(j) V_lr(j): the 64 keys [64 (j & 1), +64) of V stage vs, P(j) in the S(j) buffer
+      auto issue_pv = [&](int j, int vs) {
+        const int h = j & 1;
         const uint32_t v_lo = (uint32_t)vd + (uint32_t)vs * (kKBytes >> 4) + (uint32_t)h * ((kSN / 16) * 2048u >> 4);
         const uint32_t l_lo = (uint32_t)ld + (uint32_t)vs * (kLrBytes >> 4) + (uint32_t)h * ((kSN / 16) * 16u * kLrRow >> 4);
-        const uint32_t p_tmem = tmem + kTmemS + (uint32_t)(j & 3) * kSN;                 // P(j) sits in the S(j) buffer
+        const uint32_t p_tmem = tmem + kTmemS + (uint32_t)(j & 3) * kSN;
 #pragma unroll
         for (int ks = 0; ks < kSN / 16; ++ks) {
           ptx::umma_bf16_ts(tmem + kTmemO, p_tmem + 8u * ks, desc(vd_hi, v_lo + (uint32_t)ks * (2048u >> 4)), idesc_o,
@@ -293,11 +305,32 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
             ptx::umma_bf16_ts(tmem + kTmemLr, p_tmem + 8u * ks, desc(ld_hi, l_lo + (uint32_t)ks * (16u * kLrRow >> 4)), idesc_lr,
                               (j > 0 || ks > 0) ? 1u : 0u);
         }
-        if (h == 1 || j == n_tiles - 1) ptx::umma_commit(&bars.v_empty[vs]);
         ptx::umma_commit(&bars.pv_done[j & 3]);
+      };
+      // This thread's own instruction stream is long: a barrier wait costs it ~75 clocks even when the phase completed long ago, a
+      // fence ~90, a commit ~60 (per-tile clock stamps of one CTA, profiles/r2_prefill_tile_trace.txt).  Hence no fence behind the
+      // K wait, one s_full arrival per pair, and the stage waits ahead of the P wait.
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j >> 1, vs = st % kStages, h = j & 1;
+        // one P barrier per S buffer (not per warpgroup): a warpgroup can finish tile j + 2 before this thread
+        // has looked at tile j (S(j+2) is issued ahead of PV(j)), and a parity wait two phases late never returns;
+        // P(j+4) needs S(j+4), which is only issued behind PV(j+1)
+        // the stage waits first: V of this pair and K of the pair whose scores go out behind it landed long ago, and a wait
+        // costs this thread ~75 clocks even then -- better spent before P arrives than between P and its MMAs
+        if (h == 0) {
+          ptx::mbar_wait(&bars.v_full[vs], (uint32_t)((st / kStages) & 1));
+          if (j + 4 < n_tiles) ptx::mbar_wait(&bars.k_full[(st + 2) % kStages], (uint32_t)(((st + 2) / kStages) & 1));
+        }
+        ptx::mbar_wait(&bars.p_full[j & 3], (uint32_t)((j >> 2) & 1));
+        ptx::tc_fence_after();
+        LK_PTRACE(j, 1);
+        issue_pv(j, vs);
+        LK_PTRACE(j, 8);
+        if (h == 1 || j == n_tiles - 1) ptx::umma_commit(&bars.v_empty[vs]);
         if (j == n_tiles - 1) ptx::umma_commit(&bars.all_done);
+        LK_PTRACE(j, 9);
         // S of tiles (j + 3, j + 4) into the buffers of tiles (j - 1, j), both of whose PV are issued by now
-        if (h == 1 && j + 3 < n_tiles) issue_s2(j + 3);
+        if (h == 1 && j + 3 < n_tiles) issue_s2(j + 3, true);
       }
     }
   } else {
@@ -368,8 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     float l_run = 0.f;            // row sum over this warpgroup's tiles
     for (int j = wg; j < n_tiles; j += 2) {
       const int sb = j & 3;
-      ptx::mbar_wait(&bars.s_full[sb], (uint32_t)((j >> 2) & 1));
+      ptx::mbar_wait(&bars.s_full[sb & 2], (uint32_t)((j >> 2) & 1));        // one arrival per tile pair, on the even tile's barrier
       ptx::tc_fence_after();
+      if ((warp & 3) == 0 && lane == 0) LK_PTRACE(j, 2);
       float sc[kSN];
       {
         uint32_t raw[kSN];
@@ -396,10 +430,12 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
 
       // the running maximum after tile j - 1, published by the partner warp
       float m_prev = ninf;
+      if ((warp & 3) == 0 && lane == 0) LK_PTRACE(j, 3);
       if (j > 0) {                  // the partner warp (same rows, other warpgroup) published after tile j - 1
         ptx::mbar_wait(&bars.hand[(warp & 3) * 2 + (wg ^ 1)], (uint32_t)(((j - 1) >> 1) & 1));
         m_prev = *reinterpret_cast<volatile float*>(&m_s[row]);
       }
+      if ((warp & 3) == 0 && lane == 0) LK_PTRACE(j, 4);
       float m_used = m_prev;
       const float m_cand = fmaxf(m_prev, mx);
       if (j == 0) {
@@ -460,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         ls4[c & 3] += e;
       }
       l_run += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      if ((warp & 3) == 0 && lane == 0) LK_PTRACE(j, 5);
       // P(j) -> TMEM, over the first 32 columns of the S(j) buffer (this thread has its scores in registers;
       // S(j+4) is issued behind PV(j) on the in-order pipe)
 #pragma unroll
@@ -472,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bars.p_full[sb]);
+      if ((warp & 3) == 0 && lane == 0) LK_PTRACE(j, 6);
     }
 
     // ---- both warpgroups: wait for the last PV, bring the two partial row sums to the final maximum ----
@@ -739,3 +777,9 @@ int launch_decode_umma(const PagedAttnCall& c) {
 }
 
 }  // namespace lk
+
+#ifdef LK_PREFILL_TRACE
+extern "C" int lorakv_debug_prefill_trace(long long* out, int n_words) {
+  return cudaMemcpyFromSymbol(out, lk::g_prefill_trace, sizeof(long long) * (size_t)n_words) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   unsigned char* sLK = sLR + kStages * kLrBytes;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) LK_PTRACE(2047, 0);          // CTA-level stamps live in row 2047: 0 entry, 1 set-up done, 2 predecessor complete,
+                                             // 3 Q in TMEM, 4 last P V complete, 5 epilogue operands staged, 6 rows stored, 7 exit
   // ---- what this CTA owns: n_tiles softmax tiles of kSN keys starting at key tile_begin * kSN ----
   int PB, kvh, n_tiles, tile_begin;
   int64_t q0, rows_here, kv_layer_off, lr_layer_off, lk_layer_off, mask_from;   // mask_from: first key that some row cannot see
@@ -197,10 +199,12 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_s;
+  if (tid == 0) LK_PTRACE(2047, 1);
   // launched as a programmatic dependent (decode mode: one launch per layer; prefill: behind the projections): barrier
   // set-up and the TMEM allocation above ran under the predecessor's tail; its results (q, fresh cache rows) are read below
   ptx::pdl_wait();
   ptx::pdl_launch_dependents();
+  if (tid == 0) LK_PTRACE(2047, 2);
 
   if (warp == 8 || warp == 10) {
     // ===================== TMA producers: warp 8 streams K, warp 10 streams V_base + V_lr =====================
@@ -395,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(&bars.q_full);
+      if (tid == 0) LK_PTRACE(2047, 3);
     }
 
     float m_mine = ninf;          // the maximum this thread's row sum is relative to (scaled, log2 units)
@@ -517,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       ptx::mbar_wait(&bars.all_done, 0);
       ptx::tc_fence_after();
     }
+    if (tid == 0) LK_PTRACE(2047, 4);
     l_s[wg][row] = l_run;
     mref_s[wg][row] = m_mine;
     named_bar_sync(9, 256);
@@ -564,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
       for (int idx = tid; idx < p.r * D; idx += 256)
         b_s[idx] = p.b[(int64_t)(idx / D) * ((int64_t)p.n_kv_local * D) + (int64_t)kvh * D + idx % D];
       named_bar_sync(9, 256);
+      if (tid == 0) LK_PTRACE(2047, 5);
       const float inv_l = 1.0f / l_tot;
       float w[RP > 0 ? RP : 1];
 #pragma unroll
@@ -583,11 +590,19 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
         float acc[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = __uint_as_float(r16[i]);
+        // B rows as 16-byte broadcast reads from shared memory
 #pragma unroll
         for (int k = 0; k < RP; ++k) {
           if (k < p.r) {
+            const float4* bp = reinterpret_cast<const float4*>(b_s + k * D + c0);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = fmaf(w[k], b_s[k * D + c0 + i], acc[i]);
+            for (int i4 = 0; i4 < 4; ++i4) {
+              const float4 bv = bp[i4];
+              acc[4 * i4] = fmaf(w[k], bv.x, acc[4 * i4]);
+              acc[4 * i4 + 1] = fmaf(w[k], bv.y, acc[4 * i4 + 1]);
+              acc[4 * i4 + 2] = fmaf(w[k], bv.z, acc[4 * i4 + 2]);
+              acc[4 * i4 + 3] = fmaf(w[k], bv.w, acc[4 * i4 + 3]);
+            }
           }
         }
         if (real_row) {
@@ -599,9 +614,11 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
     }
   }
 
+  if (tid == 0) LK_PTRACE(2047, 6);
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 0) ptx::tmem_dealloc(tmem, 512);
+  if (tid == 0) LK_PTRACE(2047, 7);
 }
 
 template <int D, int RP, bool kDecode, int RK = 0>

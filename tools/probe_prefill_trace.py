@@ -61,6 +61,11 @@ def main():
         print(f"   tile {j}: {pv}" + (f" | S {int(t[j, 0] - t[lo, 0])} +{int(t[j, 10] - t[j, 0])}" if j % 2 == 0 else ""))
     for j in range(lo, lo + 8):
         print("   tile", j, " ".join(f"{int(t[j, s] - t[lo, 0]):7d}" for s in range(7)))
+    c = np.frombuffer(buf, dtype=np.int64).reshape(2048, 16)[2047].astype(np.int64)
+    first_s, first_p, last_p = t[0, 0], t[0, 6], t[n - 1, 6]
+    print("  the CTA as a whole (clocks from entry): set-up done", c[1] - c[0], "| predecessor complete", c[2] - c[0], "| Q in TMEM", c[3] - c[0],
+          "| first S issued", first_s - c[0], "| first P published", first_p - c[0], "| last P published", last_p - c[0],
+          "| last P V complete", c[4] - c[0], "| B staged", c[5] - c[0], "| rows stored", c[6] - c[0], "| exit", c[7] - c[0])
     pool.close(); ad.close(); ctx.close()
 
 

@@ -605,11 +605,21 @@ __global__ void __launch_bounds__(kThreads, 1) fla_prefill_umma_kernel(const Pre
             }
           }
         }
-        if (real_row) {
+        // the finished row goes through shared memory (the V stages are idle: every stage was consumed before all_done): a thread
+        // owns a ROW, and 16-byte stores of 32 lanes into rows 16 KB apart cost the CTA ~9 000 clocks (clock trace); staged, a warp
+        // stores whole 512-byte rows.  Row stride D + 4 floats: the 16-byte stores of eight lanes fall into eight bank groups.
+        float* o_row = reinterpret_cast<float*>(sV) + (size_t)row * (D + 4) + c0;
 #pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(dst + c0 + i) = make_float4(acc[i] * inv_l, acc[i + 1] * inv_l, acc[i + 2] * inv_l, acc[i + 3] * inv_l);
-        }
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(o_row + i) = make_float4(acc[i] * inv_l, acc[i + 1] * inv_l, acc[i + 2] * inv_l, acc[i + 3] * inv_l);
+      }
+      named_bar_sync(9, 256);
+      for (int r2 = warp; r2 < kBM; r2 += 8) {                 // warp w stores rows w, w + 8, ...: lane = 16 bytes of the row
+        const int hg2 = r2 / PB, pl2 = r2 % PB;
+        if (pl2 >= rows_here) continue;
+        float* d2 = p.out + (q0 + pl2) * (p.n_q_local * D) + ((int64_t)kvh * p.group + hg2) * D;
+        const float* s2 = reinterpret_cast<const float*>(sV) + (size_t)r2 * (D + 4);
+        for (int c = lane * 4; c < D; c += 128) *reinterpret_cast<float4*>(d2 + c) = *reinterpret_cast<const float4*>(s2 + c);
       }
     }
   }

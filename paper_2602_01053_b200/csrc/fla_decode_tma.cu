@@ -779,7 +779,14 @@ int launch_t(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem
 // per-entry V_lr tiles (BaseShared batches): 16-key tiles for every worker width (the stage already carries one V_lr tile
 // per entry)
 template <int D, int RP>
-int launch_mw_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw) {
+int launch_mw_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int kt = 1) {
+  if (kt == 2) {           // 32-key tiles for the multi-warp workers when two stages of them fit (half the barrier round trips)
+    switch (mw) {
+      case 2: return launch_t<D, RP, 2, 2, true>(ctx, dp, grid, smem);
+      case 4: return launch_t<D, RP, 4, 2, true>(ctx, dp, grid, smem);
+      default: return launch_t<D, RP, 8, 2, true>(ctx, dp, grid, smem);
+    }
+  }
   switch (mw) {
     case 1: return launch_t<D, RP, 1, 1, true>(ctx, dp, grid, smem);
     case 2: return launch_t<D, RP, 2, 1, true>(ctx, dp, grid, smem);
@@ -788,11 +795,11 @@ int launch_mw_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t 
   }
 }
 template <int D>
-int launch_rp_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int rp) {
+int launch_rp_pa(lorakv_ctx* ctx, const DecodeParams& dp, unsigned grid, size_t smem, int mw, int rp, int kt) {
   switch (rp) {
-    case 16: return launch_mw_pa<D, 16>(ctx, dp, grid, smem, mw);
-    case 32: return launch_mw_pa<D, 32>(ctx, dp, grid, smem, mw);
-    default: return launch_mw_pa<D, 64>(ctx, dp, grid, smem, mw);
+    case 16: return launch_mw_pa<D, 16>(ctx, dp, grid, smem, mw, kt);
+    case 32: return launch_mw_pa<D, 32>(ctx, dp, grid, smem, mw, kt);
+    default: return launch_mw_pa<D, 64>(ctx, dp, grid, smem, mw, kt);
   }
 }
 
@@ -1019,7 +1026,13 @@ int launch_decode_tma(const PagedAttnCall& c) {
   const bool pa = c.per_entry_lr && rp > 0;
   const int lr_per_block = pa ? (int)std::min<int64_t>(rows_blk / group, c.n_batch) : 1;   // V_lr tiles per stage
   // 32-key tiles whenever a page holds them; single-warp workers then run three (d_head 128) or four (64) per CTA
-  const int kt = (!pa && pool->P % (2 * kKeyStep) == 0) ? 2 : 1;
+  // per-entry V_lr tiles: 32-key tiles for the multi-warp workers too whenever two stages of them fit -- half the barrier round
+  // trips per key and twice the MMAs between them (cfg-5 shard, 16 agents x rank 32: 1.76 -> 1.10 ms per step, 0.57 -> 0.91 of
+  // the HBM peak; LORAKV_PA_KT1=1 keeps 16-key tiles for A/B runs)
+  static const bool pa_kt1 = std::getenv("LORAKV_PA_KT1") && std::getenv("LORAKV_PA_KT1")[0] == '1';
+  const bool pa_wide = pa && !pa_kt1 && mw >= 2 && pool->P % (2 * kKeyStep) == 0 &&
+                       (size_t)(kWarps / mw) * 2 * (2 * kKeyStep * (4 * d + 2 * rp * lr_per_block)) <= (size_t)kRingBudget;
+  const int kt = ((!pa && pool->P % (2 * kKeyStep) == 0) || pa_wide) ? 2 : 1;
   const int workers_per_cta = (mw == 1 && kt == 2) ? wide_workers(d) : kWarps / mw;
   const int tk = kKeyStep * kt;
   const int rk = (int)pool->rk_pad;
@@ -1093,8 +1106,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
                        ? stable_rows(pool, c.L) : 0;
   if (pa) {
     dp.lr_policy = ptx::kEvictFirst;     // every V_lr tile is read by one entry's rows of each kv head only
-    if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp));
-    else LK_TRY(launch_rp_pa<64>(ctx, dp, grid, smem, mw, rp));
+    if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp, kt));
+    else LK_TRY(launch_rp_pa<64>(ctx, dp, grid, smem, mw, rp, kt));
   } else if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp, rk));
   else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, kt, rp, rk));
 

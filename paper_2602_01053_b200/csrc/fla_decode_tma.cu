@@ -1048,7 +1048,8 @@ int launch_decode_tma(const PagedAttnCall& c) {
   // fit in L2, the layers are cut into the fewest equal chunks whose share does; every worker walks the chunks in
   // order, so only a chunk's V_lr is live at a time and DRAM serves it once instead of once per kv head.
   int n_chunks = 1;
-  const int64_t lr_layer_bytes = c.L * rp * 2;
+  // (per-entry V_lr: every agent of the batch has its own cache, all of them are shared by the kv heads of the layer)
+  const int64_t lr_layer_bytes = c.L * rp * 2 * (pa ? c.n_batch : 1);
   // (worth it from four kv heads per GPU on -- with two, the re-read it saves is ~5 % of the bytes and the pipeline
   // restart per chunk costs as much: cfg 4 on 4 GPUs 0.478 ms chunked vs 0.434 ms not -- and while a worker still
   // gets a few dozen tiles per chunk)
@@ -1105,7 +1106,10 @@ int launch_decode_tma(const PagedAttnCall& c) {
   dp.stable_rows = (ctx->speculate && !pa && (dp.identity & 1) && (rp == 0 || (dp.identity & 2)) && (rk == 0 || (dp.identity & 4)))
                        ? stable_rows(pool, c.L) : 0;
   if (pa) {
-    dp.lr_policy = ptx::kEvictFirst;     // every V_lr tile is read by one entry's rows of each kv head only
+    // an entry's V_lr tile is read once per kv head of the layer: with one kv head per GPU it streams (evict-first); with
+    // several, the policy chosen above keeps the batch's low-rank caches L2-resident when the launch's share fits (cfg 2 under
+    // BaseShared: 0.93 -> 0.97 of the HBM peak)
+    if (pool->n_kv_local == 1) dp.lr_policy = ptx::kEvictFirst;
     if (d == 128) LK_TRY(launch_rp_pa<128>(ctx, dp, grid, smem, mw, rp, kt));
     else LK_TRY(launch_rp_pa<64>(ctx, dp, grid, smem, mw, rp, kt));
   } else if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, kt, rp, rk));

@@ -68,4 +68,19 @@ qb = rnd(g(150, n_q * d, 71, d ** -0.5))
 got = pool.prefill(ad, 0, 3, n_q, qb, L - 150)
 print("key low-rank prefill", ctx.last_kernel(), orc.max_rel_error(got, orc.gqa_attention(qb, keys, v, v_lr, bv[3], 1.0, L - 150, n_q, n_kv)))
 pool.close(); ad.close()
+
+# ---- BaseShared batch in one launch: per-entry V_lr tiles, 32-key tiles on the multi-warp workers (40 rows per kv head)
+A, L = 10, 200
+pool = Pool(ctx, "BaseShared", 1, n_kv, d, d_model, r, A, max_tokens=L, dtype=abi.BF16, page_tokens=32)
+ad = Adapters(ctx, 1, A, d_model, r, n_kv, d, dtype=abi.BF16)
+k, v = rnd(g(L, n_kv * d, 80, d ** -0.5)), rnd(g(L, n_kv * d, 81, 1.0))
+lrs = [rnd(g(L, r, 82 + a, 1.0)) for a in range(A)]
+bv = [rnd(g(r, n_kv * d, 100 + a, 0.02)) for a in range(A)]
+pool.append_tokens(L); pool.append_key(0, 0, 0, k); pool.append_value(0, 0, 0, v)
+for a in range(A):
+    pool.append_lr(0, a, 0, lrs[a]); ad.set_b(0, a, bv[a], 16.0)
+qh = rnd(g(A, n_q * d, 120, d ** -0.5))
+out = pool.decode(ad, 0, 1, list(range(A)), n_q, qh[None])
+print("BaseShared batch", ctx.last_kernel(), orc.max_rel_error(out[0, 7][None, :], orc.gqa_attention(qh[7:8], k, v, lrs[7], bv[7], 1.0, L - 1, n_q, n_kv)))
+pool.close(); ad.close()
 ctx.close()

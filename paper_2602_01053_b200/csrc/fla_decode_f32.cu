@@ -27,6 +27,8 @@
 
 #include "kernels.hpp"
 #include "page_layout.cuh"
+#include <cuda_bf16.h>
+
 #include "state.hpp"
 #include "umma.cuh"
 
@@ -368,6 +370,319 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32_kernel(const DecodeF
   flush();
 }
 
+// (x, y) -> two packed bf16 planes: hi = (bf16(x), bf16(y)), lo = (bf16(x - hi.x), bf16(y - hi.y)); x in the low half
+__device__ __forceinline__ void split_bf16x2(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(x - __uint_as_float(hi << 16), y - __uint_as_float(hi & 0xffff0000u));
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+__device__ __forceinline__ void mma_bf16_k16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// acc += P V over 16 keys from the bf16 planes (p1 v0 + p0 v1 + p0 v0), the tile's product started from zero and added to the
+// running sum with round-to-nearest adds (see mma_3x_add)
+__device__ __forceinline__ void mma_bf16_3x_add(float (&acc)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
+                                                uint32_t bl0, uint32_t bl1) {
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  mma_bf16_k16(d, al, bh0, bh1);
+  mma_bf16_k16(d, ah, bl0, bl1);
+  mma_bf16_k16(d, ah, bh0, bh1);
+  asm("{\n\t.reg .b64 a, b;\n\tmov.b64 a, {%0, %1};\n\tmov.b64 b, {%4, %5};\n\tadd.rn.f32x2 a, a, b;\n\tmov.b64 {%0, %1}, a;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%6, %7};\n\tadd.rn.f32x2 a, a, b;\n\tmov.b64 {%2, %3}, a;\n\t}"
+      : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
+      : "f"(d[0]), "f"(d[1]), "f"(d[2]), "f"(d[3]));
+}
+
+// The same decode with 16-KEY TILES and the P V products on bf16 planes (round 2).  ncu on the kernel above: one stall per issue
+// on the legacy tensor pipe ("math pipe throttle") -- the TF32 MMAs bound it, not HBM.  Per 16 keys it issues 96 (S) + 108 (P V,
+// V_lr) HMMA.1688.TF32.  P V only has to meet 1e-4 on the output, and P in [0, 1] / V are exact sums of two bf16 numbers to
+// 2^-17 (fla_prefill_split.cu), so here P V = p0 v0 + p1 v0 + p0 v1 as THREE m16n8k16 bf16 MMAs per 16 keys and n8 tile instead
+// of six k8 TF32 ones: 96 + 54 MMAs per 16 keys.  The scores keep the split-TF32 products (they sit in the exponent).  A
+// 16-key stage also halves the barrier round trips per key and lets both 8-key halves share one split of the Q fragments.
+// Needs pages of a multiple of 16 tokens; other pools (and LORAKV_F32_NARROW=1) keep the kernel above.
+template <int D, int RP, int MW, int W>
+__global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const DecodeF32Params p) {
+  constexpr int kTK = 16;
+  constexpr int kWorkers = W / MW;
+  constexpr uint32_t kRowBytes = D * 4;
+  constexpr uint32_t kKvBytes = kTK * kRowBytes;
+  constexpr uint32_t kLrRowBytes = RP * 4;
+  constexpr uint32_t kLrBytes = kTK * kLrRowBytes;
+  constexpr uint32_t kStageBytes = 2 * kKvBytes + kLrBytes;
+  constexpr int kLrSwz = RP >= 32 ? 7 : (RP / 4 - 1);   // chunks per LR row - 1, capped at one 128-byte line
+  constexpr int kNO = D / 8, kNL = RP / 8;
+  constexpr int PS = 4 + D + RP;
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full_bar[kWorkers][kMaxStages];
+  __shared__ uint64_t empty_bar[kWorkers][kMaxStages];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wk = warp / MW, wi = warp % MW;
+  const int g = lane >> 2, t = lane & 3;
+  const int NS = p.n_stages;
+
+  if (threadIdx.x == 0) {
+    for (int a = 0; a < kWorkers; ++a)
+      for (int s = 0; s < NS; ++s) {
+        ptx::mbar_init(&full_bar[a][s], 1);
+        ptx::mbar_init(&empty_bar[a][s], MW);
+      }
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  ptx::pdl_wait();                  // launched as a programmatic dependent: the set-up above ran under the predecessor's tail
+  ptx::pdl_launch_dependents();
+
+  const int64_t w = (int64_t)blockIdx.x * kWorkers + wk;
+  const int64_t g0 = w * p.G;
+  const int64_t g1 = min(g0 + p.G, p.total_tiles);
+  const int n = g1 > g0 ? (int)(g1 - g0) : 0;
+  if (n == 0) return;
+
+  const uint32_t ring = ptx::smem_u32(smem) + (uint32_t)wk * (uint32_t)NS * kStageBytes;
+  uint64_t* full = full_bar[wk];
+  uint64_t* empty = empty_bar[wk];
+  const bool producer = wi == 0;
+  const int units_per_layer = p.n_kv_local * p.row_blocks;
+
+  // producer cursor, carried incrementally (no per-tile division); page-table window across the lanes
+  int win_base = -(1 << 30), win_kv = 0, win_lr = 0;
+  const int T32 = (int)p.T;
+  int64_t p_unit = g0 / p.T;
+  int p_tl = (int)(g0 - p_unit * p.T);
+  int p_page = (p_tl * kTK) / p.P, p_tok = (p_tl * kTK) % p.P;
+  int p_layer = (int)(p_unit / units_per_layer), p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
+  int p_stage = 0, p_wrap = 0, p_issued = 0;
+
+  auto issue_next = [&]() {
+    if (p_page < win_base || p_page >= win_base + 32) {
+      win_base = p_page;
+      const int pg = p_page + lane;
+      win_kv = pg < p.n_pages ? p.kv_table[pg] : 0;
+      if (RP > 0) win_lr = pg < p.n_pages ? p.lr_table[pg] : 0;
+    }
+    const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
+    const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
+    if (ptx::elect_one()) {
+      const uint32_t dst = ring + (uint32_t)p_stage * kStageBytes;
+      const int64_t layer = p.layer_begin + p_layer;
+      const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride +
+                             (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * D;
+      ptx::mbar_arrive_expect_tx(&full[p_stage], kStageBytes);
+      bulk_g2s(dst, p.k_pages + kv_off, kKvBytes, &full[p_stage], p.l2_policy);
+      bulk_g2s(dst + kKvBytes, p.v_pages + kv_off, kKvBytes, &full[p_stage], p.l2_policy);
+      if (RP > 0) {
+        const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
+        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.lr_policy);   // re-read by every kv head
+      }
+    }
+    ++p_issued;
+    if (++p_stage == NS) { p_stage = 0; ++p_wrap; }
+    p_tok += kTK;
+    if (p_tok == p.P) { p_tok = 0; ++p_page; }
+    if (++p_tl == T32) {
+      p_tl = 0; p_page = 0; p_tok = 0;
+      ++p_unit;
+      p_layer = (int)(p_unit / units_per_layer);
+      p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
+    }
+  };
+
+  if (producer) {
+    const int pre = n < NS ? n : NS;
+    for (int i = 0; i < pre; ++i) issue_next();
+  }
+
+  const float ninf = -std::numeric_limits<float>::infinity();
+  float qf[D / 8][4];          // A fragments of Q in full fp32: (g, t), (g + 8, t), (g, t + 4), (g + 8, t + 4) of every k8 step
+  float o[kNO][4];
+  float olr[kNL > 0 ? kNL : 1][4];
+  float m_used[2], l_run[2];
+  int64_t cur_unit = -1;
+
+  auto flush = [&]() {
+    const int64_t first_unit = g0 / p.T;
+    const int64_t slot = w * p.max_seg + (cur_unit - first_unit);
+    float* base = p.part + (slot * (16 * MW) + wi * 16) * PS;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float l = l_run[h];
+      l += __shfl_xor_sync(0xffffffffu, l, 1);
+      l += __shfl_xor_sync(0xffffffffu, l, 2);
+      float* row = base + (g + 8 * h) * PS;
+      if (t == 0) { row[0] = m_used[h]; row[1] = l; }
+#pragma unroll
+      for (int nt = 0; nt < kNO; ++nt)
+        *reinterpret_cast<float2*>(row + 4 + 8 * nt + 2 * t) = make_float2(o[nt][2 * h], o[nt][2 * h + 1]);
+#pragma unroll
+      for (int nt = 0; nt < kNL; ++nt)
+        *reinterpret_cast<float2*>(row + 4 + D + 8 * nt + 2 * t) = make_float2(olr[nt][2 * h], olr[nt][2 * h + 1]);
+    }
+  };
+
+  // shared-memory byte offsets of this lane's fragment elements inside a K / V tile (the swizzle term is folded in)
+  //   K: row g, chunk (2 kk + j) ^ g, word t           -> kOff + ((2 kk + j) ^ g) * 16
+  //   V: row 2t + j, chunk (2 nt + (g >> 2)) ^ (2t + j), word g & 3
+  const uint32_t k_row = (uint32_t)g * kRowBytes + (uint32_t)t * 4u;
+  const uint32_t v_row0 = (uint32_t)(2 * t) * kRowBytes + (uint32_t)(g & 3) * 4u;
+  const uint32_t v_row1 = v_row0 + kRowBytes;
+  const uint32_t v_c0 = (uint32_t)((g >> 2) ^ (2 * t)), v_c1 = (uint32_t)((g >> 2) ^ (2 * t + 1));   // low chunk bits, pre-XORed
+
+  int64_t u = g0 / p.T;
+  int tl = (int)(g0 - u * p.T);
+  int c_stage = 0, c_wrap = 0;
+  for (int i = 0; i < n; ++i) {
+    if (u != cur_unit) {
+      if (cur_unit >= 0) flush();
+      cur_unit = u;
+      const int layer_rel = (int)(u / units_per_layer);
+      const int kvh = (int)((u / p.row_blocks) % p.n_kv_local);
+      const int rb = (int)(u % p.row_blocks);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rho = rb * 16 * MW + wi * 16 + g + 8 * h;
+        const bool real = rho < p.rows_total;
+        const int entry = real ? rho / p.group : 0, gi = real ? rho % p.group : 0;
+        const float* src = p.q + (((int64_t)layer_rel * p.n_batch + entry) * p.n_q_local + (int64_t)kvh * p.group + gi) * D;
+#pragma unroll
+        for (int kk = 0; kk < D / 8; ++kk) {
+          qf[kk][h] = real ? __ldg(src + 8 * kk + t) : 0.f;
+          qf[kk][2 + h] = real ? __ldg(src + 8 * kk + 4 + t) : 0.f;
+        }
+        m_used[h] = ninf; l_run[h] = 0.f;
+      }
+#pragma unroll
+      for (int nt = 0; nt < kNO; ++nt) { o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f; }
+#pragma unroll
+      for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
+    }
+
+    if (producer && i >= 1 && p_issued < n) {
+      ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
+      issue_next();
+    }
+    const int s = c_stage;
+    ptx::mbar_wait(&full[s], (uint32_t)(c_wrap & 1));
+    const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
+
+    // ---- S = Q K^T : 16 rows x 8 keys, 3 x TF32 ------------------------------------------------------
+    // three accumulators (hi*hi, lo*hi, hi*lo) so that the 3 * D / 8 MMAs form three chains, not one
+    // sc[u]: keys 8 u + {2t, 2t + 1} of rows g (elements 0, 1) and g + 8 (2, 3); the cross terms of both halves share sx[u]
+    float sc[2][4], sx[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { sc[u][e] = 0.f; sx[u][e] = 0.f; }
+#pragma unroll
+    for (int kk = 0; kk < D / 8; ++kk) {
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) split_tf32(qf[kk][e], ah[e], al[e]);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t line = sK + k_row + (uint32_t)u * 8u * kRowBytes + (uint32_t)((2 * kk) >> 3) * 128u;
+        const float k0 = lds32(line + ((uint32_t)(((2 * kk) & 7) ^ g) << 4));
+        const float k1 = lds32(line + ((uint32_t)(((2 * kk + 1) & 7) ^ g) << 4));
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(k0, bh0, bl0);
+        split_tf32(k1, bh1, bl1);
+        mma_tf32(sx[u], al[0], al[1], al[2], al[3], bh0, bh1);
+        mma_tf32(sx[u], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+        mma_tf32(sc[u], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) sc[u][e] += sx[u][e];
+
+    // ---- online softmax (exp2 domain), rows g and g + 8; this lane holds keys 2t, 2t + 1 -----------------
+    const int64_t key_base = (int64_t)tl * kTK + 2 * t;
+    bool valid[2][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) { valid[u][0] = key_base + 8 * u < p.L; valid[u][1] = key_base + 8 * u + 1 < p.L; }
+    float tmax[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float mx = ninf;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float v0 = valid[u][0] ? sc[u][2 * h] * p.scale_log2 : ninf;
+        const float v1 = valid[u][1] ? sc[u][2 * h + 1] * p.scale_log2 : ninf;
+        sc[u][2 * h] = v0; sc[u][2 * h + 1] = v1;
+        mx = fmaxf(mx, fmaxf(v0, v1));
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      tmax[h] = mx;
+    }
+    const bool grow = tmax[0] > m_used[0] + kRescaleThreshold || tmax[1] > m_used[1] + kRescaleThreshold;
+    if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float m_new = fmaxf(m_used[h], tmax[h]);
+        const float alpha = (m_used[h] == ninf) ? 0.f : ex2(m_used[h] - m_new);
+        m_used[h] = m_new;
+        l_run[h] *= alpha;
+#pragma unroll
+        for (int nt = 0; nt < kNO; ++nt) { o[nt][2 * h] *= alpha; o[nt][2 * h + 1] *= alpha; }
+#pragma unroll
+        for (int nt = 0; nt < kNL; ++nt) { olr[nt][2 * h] *= alpha; olr[nt][2 * h + 1] *= alpha; }
+      }
+    }
+    // P as the A operand of ONE k16 step over the tile's 16 keys, two bf16 planes: a0 / a1 = rows g / g + 8, keys 2t, 2t + 1;
+    // a2 / a3 = the same rows, keys 2t + 8, 2t + 9 -- exactly where the two score halves hold them
+    uint32_t ph[4], pl[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float pa = valid[u][0] ? ex2(sc[u][2 * h] - m_used[h]) : 0.f;
+        const float pb = valid[u][1] ? ex2(sc[u][2 * h + 1] - m_used[h]) : 0.f;
+        l_run[h] += pa + pb;
+        split_bf16x2(pa, pb, ph[2 * u + h], pl[2 * u + h]);
+      }
+
+    // ---- O += P V_base, O_lr += P V_lr ---------------------------------------------------------------
+    // B fragments of the k16 step: b0 = (keys 2t, 2t + 1), b1 = (keys 2t + 8, 2t + 9) at column g of the n8 tile -- the rows the
+    // k8 fragments already address, and the same rows eight keys further down (the page swizzle repeats every eight tokens)
+#pragma unroll
+    for (int nt = 0; nt < kNO; ++nt) {
+      const uint32_t line = (uint32_t)((2 * nt) >> 3) * 128u;
+      const uint32_t a0 = sV + v_row0 + line + ((((uint32_t)(2 * nt) & 7u) ^ v_c0) << 4);
+      const uint32_t a1 = sV + v_row1 + line + ((((uint32_t)(2 * nt) & 7u) ^ v_c1) << 4);
+      uint32_t bh0, bl0, bh1, bl1;
+      split_bf16x2(lds32(a0), lds32(a1), bh0, bl0);
+      split_bf16x2(lds32(a0 + 8u * kRowBytes), lds32(a1 + 8u * kRowBytes), bh1, bl1);
+      mma_bf16_3x_add(o[nt], ph, pl, bh0, bh1, bl0, bl1);
+    }
+    if (RP > 0) {
+#pragma unroll
+      for (int nt = 0; nt < kNL; ++nt) {
+        const uint32_t chunk = (uint32_t)(2 * nt + (g >> 2));
+        const uint32_t a0 = sLR + (uint32_t)(2 * t) * kLrRowBytes + ((chunk ^ ((uint32_t)(2 * t) & (uint32_t)kLrSwz)) << 4) + (uint32_t)(g & 3) * 4u;
+        const uint32_t a1 = sLR + (uint32_t)(2 * t + 1) * kLrRowBytes + ((chunk ^ ((uint32_t)(2 * t + 1) & (uint32_t)kLrSwz)) << 4) +
+                            (uint32_t)(g & 3) * 4u;
+        uint32_t bh0, bl0, bh1, bl1;
+        split_bf16x2(lds32(a0), lds32(a1), bh0, bl0);
+        split_bf16x2(lds32(a0 + 8u * kLrRowBytes), lds32(a1 + 8u * kLrRowBytes), bh1, bl1);
+        mma_bf16_3x_add(olr[nt], ph, pl, bh0, bh1, bl0, bl1);
+      }
+    }
+
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    if (++c_stage == NS) { c_stage = 0; ++c_wrap; }
+    if (++tl == T32) { tl = 0; ++u; }
+  }
+  flush();
+}
+
 // ---- prefill blocks over fp32 pages ---------------------------------------------------------------------
 // gqa_attention for L_c rows of one agent on one layer (attention.hpp:332-363) with the causal rule of :44-46: key j is
 // hidden from the row at position query_offset + i iff j > query_offset + i.  Same fragments, same split-TF32
@@ -628,10 +943,10 @@ int launch_prefill_rp(lorakv_ctx* ctx, const PrefillF32Params& pp, unsigned grid
   }
 }
 
-template <int D, int RP, int MW>
+template <int D, int RP, int MW, bool kWide = false>
 int launch_t(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem) {
   constexpr int W = warps_per_cta(MW);
-  auto kern = fla_decode_f32_kernel<D, RP, MW, W>;
+  auto kern = kWide ? fla_decode_f32w_kernel<D, RP, MW, W> : fla_decode_f32_kernel<D, RP, MW, W>;
   static size_t attr_smem = 0;         // the attribute call costs more than the launch: only when the ring grows
   static int attr_device = -1;
   if (attr_device != ctx->device || smem > attr_smem) {
@@ -647,7 +962,15 @@ int launch_t(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t s
 }
 
 template <int D, int RP>
-int launch_mw(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem, int mw) {
+int launch_mw(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem, int mw, bool wide) {
+  if (wide) {
+    switch (mw) {
+      case 1: return launch_t<D, RP, 1, true>(ctx, dp, grid, smem);
+      case 2: return launch_t<D, RP, 2, true>(ctx, dp, grid, smem);
+      case 4: return launch_t<D, RP, 4, true>(ctx, dp, grid, smem);
+      default: return launch_t<D, RP, 8, true>(ctx, dp, grid, smem);
+    }
+  }
   switch (mw) {
     case 1: return launch_t<D, RP, 1>(ctx, dp, grid, smem);
     case 2: return launch_t<D, RP, 2>(ctx, dp, grid, smem);
@@ -657,12 +980,12 @@ int launch_mw(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t 
 }
 
 template <int D>
-int launch_rp(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem, int mw, int rp) {
+int launch_rp(lorakv_ctx* ctx, const DecodeF32Params& dp, unsigned grid, size_t smem, int mw, int rp, bool wide) {
   switch (rp) {
-    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw);
-    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw);
-    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw);
-    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw);
+    case 0: return launch_mw<D, 0>(ctx, dp, grid, smem, mw, wide);
+    case 16: return launch_mw<D, 16>(ctx, dp, grid, smem, mw, wide);
+    case 32: return launch_mw<D, 32>(ctx, dp, grid, smem, mw, wide);
+    default: return launch_mw<D, 64>(ctx, dp, grid, smem, mw, wide);
   }
 }
 
@@ -694,12 +1017,16 @@ int launch_decode_f32(const PagedAttnCall& c) {
   const int rows_blk = 16 * mw;
   const int row_blocks = (int)((rows_total + rows_blk - 1) / rows_blk);
   const int workers_per_cta = warps_per_cta(mw) / mw;
-  const uint32_t stage_bytes = kTK * (2 * d + rp) * 4;
+  // 16-key tiles with the P V products on bf16 planes (fla_decode_f32w_kernel) whenever a page holds whole tiles
+  static const bool narrow = std::getenv("LORAKV_F32_NARROW") && std::getenv("LORAKV_F32_NARROW")[0] == '1';
+  const bool wide = !narrow && pool->P % 16 == 0;
+  const int tk = wide ? 16 : kTK;
+  const uint32_t stage_bytes = tk * (2 * d + rp) * 4;
   int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
   if (n_stages > kMaxStages) n_stages = kMaxStages;
   const size_t smem = (size_t)workers_per_cta * n_stages * stage_bytes;
 
-  const int64_t T = (c.L + kTK - 1) / kTK;
+  const int64_t T = (c.L + tk - 1) / tk;
   const int64_t units = n_layers * pool->n_kv_local * row_blocks;
   const int64_t total = units * T;
   const int64_t max_workers = (int64_t)ctx->sm_count * workers_per_cta;
@@ -730,8 +1057,8 @@ int launch_decode_f32(const PagedAttnCall& c) {
   dp.l2_policy = ptx::kEvictFirst;
   dp.lr_policy = lr_fits_l2(c, c.L * rp * 4) ? ptx::kEvictLast : ptx::kEvictFirst;
   dp.q = c.q_dev; dp.part = static_cast<float*>(ctx->work.ptr);
-  if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, rp));
-  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, rp));
+  if (d == 128) LK_TRY(launch_rp<128>(ctx, dp, grid, smem, mw, rp, wide));
+  else LK_TRY(launch_rp<64>(ctx, dp, grid, smem, mw, rp, wide));
 
   LK_TRY(launch_decode_merge(ctx, dp.part, d, rp, r, mw, group, (int)pool->n_kv_local, (int)c.n_batch, (int)rows_total, row_blocks,
                              T, G, c.layer_begin, c.n_q_local, max_seg, c.agent_ids_dev, c.adapters, c.out_dev, n_layers, c.peers));

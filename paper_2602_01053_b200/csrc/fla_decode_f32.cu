@@ -41,7 +41,9 @@ constexpr int kMaxStages = 24;
 constexpr int kRingBudget = 216 * 1024;
 constexpr float kRescaleThreshold = 8.0f;   // log2 units
 
-constexpr int warps_per_cta(int mw) { return mw <= 8 ? 8 : 8; }   // 12 warps of 168 registers spill and leave two stages per ring: 2.2 ms vs 1.6 ms at cfg 2
+// 12 warps of 168 registers spill and leave two stages per ring: 2.2 ms vs 1.6 ms at cfg 2; six / four single-warp workers with deeper
+// rings (the bf16 kernel's wide-worker layout) lose here, the kernel being bound by the tensor pipe: 1.60 / 1.64 vs 1.49 ms
+constexpr int warps_per_cta(int mw) { return mw <= 8 ? 8 : 8; }
 
 struct DecodeF32Params {
   const float *k_pages, *v_pages, *lr_pages;

@@ -776,7 +776,8 @@ bool decode_umma_supported(const PagedAttnCall& c) {
   if (!umma_shape_ok(pool)) return false;
   if (c.rows_per_entry != 1 || c.query_offset != c.L - 1 || c.L < 1 || c.n_batch < 1) return false;
   const int64_t rows_total = c.n_batch * (c.n_q_local / pool->n_kv_local);
-  return rows_total > 32 && rows_total <= kBM;
+  // (with the key-side low-rank term the streaming kernel carries up to 16 rows per kv head: this kernel takes over from 17)
+  return rows_total > (pool->rk_pad > 0 ? 16 : 32) && rows_total <= kBM;
 }
 
 int launch_decode_umma(const PagedAttnCall& c) {

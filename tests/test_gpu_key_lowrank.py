@@ -112,6 +112,7 @@ def test_paged_decode_and_prefill_with_the_key_term(ctx, orc, dtype_name, tol, n
 
 @pytest.mark.parametrize("n_q,n_kv,d,r,r_k,A,L,P,want_kernel", [
     (32, 8, 128, 16, 16, 12, 900, 32, "umma"),      # 48 rows per kv head: the tcgen05 kernel in decode mode
+    (16, 4, 128, 16, 16, 6, 640, 32, "umma"),       # 24 rows per kv head: beyond the streaming kernel's 16, tcgen05 decode mode
     (16, 4, 128, 32, 32, 9, 1500, 64, "umma"),      # two k steps of the key term, SWIZZLE_64B tiles, two-stage rings
     (8, 2, 64, 64, 20, 10, 700, 16, "umma"),        # d_head 64 leaves TMEM columns even beside a rank-64 value side
     (16, 4, 128, 0, 8, 9, 333, 128, "umma"),        # no value-side cache at all

@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
   const int n = g1 > g0 ? (int)(g1 - g0) : 0;
   if (n == 0) return;
 
-  const uint32_t ring = ptx::smem_u32(smem) + (uint32_t)wk * (uint32_t)NS * kStageBytes;
+  const uint32_t ring = ptx::smem_u32(smem) + (uint32_t)wk * kStageBytes;        // one 16-key buffer per worker
   uint64_t* full = full_bar[wk];
   uint64_t* empty = empty_bar[wk];
   const bool producer = wi == 0;
@@ -459,9 +459,12 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
   int p_tl = (int)(g0 - p_unit * p.T);
   int p_page = (p_tl * kTK) / p.P, p_tok = (p_tl * kTK) % p.P;
   int p_layer = (int)(p_unit / units_per_layer), p_kvh = (int)((p_unit / p.row_blocks) % p.n_kv_local);
-  int p_stage = 0, p_wrap = 0, p_issued = 0;
-
-  auto issue_next = [&]() {
+  // ONE 16-key buffer per worker (a second one does not fit: 8 workers x 17.4 KB), but K and V / V_lr have their own barrier
+  // pairs (full[0] / empty[0]: K, full[1] / empty[1]: V + V_lr): the K tile is free once the scores are done, so the next
+  // tile's K flies during this tile's softmax and P V, and the next V / V_lr -- issued behind this tile's P V -- during the next
+  // tile's score product.  Both copies of a tile come from the same cursor: issue_k computes the addresses, issue_v advances.
+  int64_t cur_kv_off = 0, cur_lr_off = 0;
+  auto issue_k = [&]() {
     if (p_page < win_base || p_page >= win_base + 32) {
       win_base = p_page;
       const int pg = p_page + lane;
@@ -470,21 +473,20 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
     }
     const int phys_kv = __shfl_sync(0xffffffffu, win_kv, p_page - win_base);
     const int phys_lr = RP > 0 ? __shfl_sync(0xffffffffu, win_lr, p_page - win_base) : 0;
+    const int64_t layer = p.layer_begin + p_layer;
+    cur_kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride + (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * D;
+    cur_lr_off = RP > 0 ? layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP : 0;
     if (ptx::elect_one()) {
-      const uint32_t dst = ring + (uint32_t)p_stage * kStageBytes;
-      const int64_t layer = p.layer_begin + p_layer;
-      const int64_t kv_off = layer * p.kv_layer_stride + (int64_t)p_kvh * p.kv_head_stride +
-                             (int64_t)phys_kv * p.kv_page_stride + (int64_t)p_tok * D;
-      ptx::mbar_arrive_expect_tx(&full[p_stage], kStageBytes);
-      bulk_g2s(dst, p.k_pages + kv_off, kKvBytes, &full[p_stage], p.l2_policy);
-      bulk_g2s(dst + kKvBytes, p.v_pages + kv_off, kKvBytes, &full[p_stage], p.l2_policy);
-      if (RP > 0) {
-        const int64_t lr_off = layer * p.lr_layer_stride + (int64_t)phys_lr * p.lr_page_stride + (int64_t)p_tok * RP;
-        bulk_g2s(dst + 2 * kKvBytes, p.lr_pages + lr_off, kLrBytes, &full[p_stage], p.lr_policy);   // re-read by every kv head
-      }
+      ptx::mbar_arrive_expect_tx(&full[0], kKvBytes);
+      bulk_g2s(ring, p.k_pages + cur_kv_off, kKvBytes, &full[0], p.l2_policy);
     }
-    ++p_issued;
-    if (++p_stage == NS) { p_stage = 0; ++p_wrap; }
+  };
+  auto issue_v = [&]() {
+    if (ptx::elect_one()) {
+      ptx::mbar_arrive_expect_tx(&full[1], kKvBytes + kLrBytes);
+      bulk_g2s(ring + kKvBytes, p.v_pages + cur_kv_off, kKvBytes, &full[1], p.l2_policy);
+      if (RP > 0) bulk_g2s(ring + 2 * kKvBytes, p.lr_pages + cur_lr_off, kLrBytes, &full[1], p.lr_policy);   // re-read by every kv head
+    }
     p_tok += kTK;
     if (p_tok == p.P) { p_tok = 0; ++p_page; }
     if (++p_tl == T32) {
@@ -495,10 +497,7 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
     }
   };
 
-  if (producer) {
-    const int pre = n < NS ? n : NS;
-    for (int i = 0; i < pre; ++i) issue_next();
-  }
+  if (producer) { issue_k(); issue_v(); }
 
   const float ninf = -std::numeric_limits<float>::infinity();
   float qf[D / 8][4];          // A fragments of Q in full fp32: (g, t), (g + 8, t), (g, t + 4), (g + 8, t + 4) of every k8 step
@@ -537,7 +536,6 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
 
   int64_t u = g0 / p.T;
   int tl = (int)(g0 - u * p.T);
-  int c_stage = 0, c_wrap = 0;
   for (int i = 0; i < n; ++i) {
     if (u != cur_unit) {
       if (cur_unit >= 0) flush();
@@ -564,13 +562,8 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
       for (int nt = 0; nt < (kNL > 0 ? kNL : 1); ++nt) { olr[nt][0] = olr[nt][1] = olr[nt][2] = olr[nt][3] = 0.f; }
     }
 
-    if (producer && i >= 1 && p_issued < n) {
-      ptx::mbar_wait(&empty[p_stage], (uint32_t)((p_wrap & 1) ^ 1));
-      issue_next();
-    }
-    const int s = c_stage;
-    ptx::mbar_wait(&full[s], (uint32_t)(c_wrap & 1));
-    const uint32_t sK = ring + (uint32_t)s * kStageBytes, sV = sK + kKvBytes, sLR = sV + kKvBytes;
+    const uint32_t sK = ring, sV = sK + kKvBytes, sLR = sV + kKvBytes;
+    ptx::mbar_wait(&full[0], (uint32_t)(i & 1));
 
     // ---- S = Q K^T : 16 rows x 8 keys, 3 x TF32 ------------------------------------------------------
     // three accumulators (hi*hi, lo*hi, hi*lo) so that the 3 * D / 8 MMAs form three chains, not one
@@ -602,6 +595,13 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
     for (int u = 0; u < 2; ++u)
 #pragma unroll
       for (int e = 0; e < 4; ++e) sc[u][e] += sx[u][e];
+    // the K tile is free: the next tile's K goes out now
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&empty[0]);
+    if (producer && i + 1 < n) {
+      ptx::mbar_wait(&empty[0], (uint32_t)(i & 1));
+      issue_k();
+    }
 
     // ---- online softmax (exp2 domain), rows g and g + 8; this lane holds keys 2t, 2t + 1 -----------------
     const int64_t key_base = (int64_t)tl * kTK + 2 * t;
@@ -651,6 +651,7 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
       }
 
     // ---- O += P V_base, O_lr += P V_lr ---------------------------------------------------------------
+    ptx::mbar_wait(&full[1], (uint32_t)(i & 1));
     // B fragments of the k16 step: b0 = (keys 2t, 2t + 1), b1 = (keys 2t + 8, 2t + 9) at column g of the n8 tile -- the rows the
     // k8 fragments already address, and the same rows eight keys further down (the page swizzle repeats every eight tokens)
 #pragma unroll
@@ -678,8 +679,11 @@ __global__ void __launch_bounds__(W * 32, 1) fla_decode_f32w_kernel(const Decode
     }
 
     __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&empty[s]);
-    if (++c_stage == NS) { c_stage = 0; ++c_wrap; }
+    if (lane == 0) ptx::mbar_arrive(&empty[1]);
+    if (producer && i + 1 < n) {
+      ptx::mbar_wait(&empty[1], (uint32_t)(i & 1));
+      issue_v();
+    }
     if (++tl == T32) { tl = 0; ++u; }
   }
   flush();
@@ -1026,7 +1030,9 @@ int launch_decode_f32(const PagedAttnCall& c) {
   const uint32_t stage_bytes = tk * (2 * d + rp) * 4;
   int n_stages = (int)(kRingBudget / (workers_per_cta * stage_bytes));
   if (n_stages > kMaxStages) n_stages = kMaxStages;
+  if (wide) n_stages = 1;                 // one buffer per worker, K and V / V_lr released separately (fla_decode_f32w_kernel)
   const size_t smem = (size_t)workers_per_cta * n_stages * stage_bytes;
+  if (wide) n_stages = 2;                 // ... with two barrier pairs
 
   const int64_t T = (c.L + tk - 1) / tk;
   const int64_t units = n_layers * pool->n_kv_local * row_blocks;
